@@ -1,0 +1,278 @@
+// ref_shim.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" wrapper over the UNMODIFIED reference library (pkrr_core sources under
+// /root/reference/proj/src, compiled in place by oracle/Makefile into
+// oracle/_ref/libpkrr_ref.so).  It lets the Python tests pin the C restatement
+// (oracle/pkrr_oracle.c) against the reference itself and lets bench.py time the
+// reference CPU path (`--impl reference`, cpu_baseline kind "reference").
+// Dense row-major inputs are turned into dense reference Datasets (indices 0..d-1,
+// as standardize() emits them, dataset.cpp:183-193).
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "pkrr/clustering.hpp"
+#include "pkrr/kernel.hpp"
+#include "pkrr/rng.hpp"
+#include "pkrr/solver.hpp"
+#include "pkrr/strategies.hpp"
+
+using namespace pkrr;
+
+namespace {
+
+thread_local std::string g_err;
+
+Dataset dense(const double* X, const double* y, int64_t n, int64_t d) {
+  Dataset ds;
+  ds.d = static_cast<std::size_t>(d);
+  std::vector<int> idx(d);
+  for (int64_t j = 0; j < d; ++j) idx[j] = static_cast<int>(j);
+  ds.col.reserve(n * d);
+  ds.val.reserve(n * d);
+  for (int64_t i = 0; i < n; ++i)
+    ds.add_row(idx, std::span<const double>(X + i * d, d), y ? y[i] : 0.0);
+  ds.d = static_cast<std::size_t>(d);
+  return ds;
+}
+
+KernelSpec gauss(double sigma) {
+  KernelSpec s;
+  s.kind = KernelKind::gaussian;
+  s.sigma = sigma;
+  return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+uint64_t ref_sub_seed(uint64_t seed, const char* tag) { return sub_seed(seed, tag); }
+
+void ref_rng_stream(uint64_t seed, int64_t count, double* normals, uint64_t* belows,
+                    uint64_t below_n) {
+  Rng a(seed);
+  for (int64_t i = 0; i < count; ++i) normals[i] = a.normal();
+  Rng b(seed);
+  for (int64_t i = 0; i < count; ++i) belows[i] = b.below(below_n);
+}
+
+void ref_random_permutation(uint64_t seed, int64_t n, uint64_t* perm) {
+  Rng r(seed);
+  const auto p = random_permutation(static_cast<std::size_t>(n), r);
+  for (int64_t i = 0; i < n; ++i) perm[i] = p[i];
+}
+
+int ref_gram_sym(const double* X, int64_t m, int64_t d, double sigma, double* K) {
+  try {
+    const Dataset ds = dense(X, nullptr, m, d);
+    const Matrix G = gram(gauss(sigma), ds, ds);
+    std::memcpy(K, G.a.data(), sizeof(double) * m * m);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+int ref_gram_cross(const double* A, int64_t na, const double* B, int64_t nb, int64_t d,
+                   double sigma, double* K) {
+  try {
+    const Dataset a = dense(A, nullptr, na, d);
+    const Dataset b = dense(B, nullptr, nb, d);
+    const Matrix G = gram(gauss(sigma), a, b);
+    std::memcpy(K, G.a.data(), sizeof(double) * na * nb);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// Returns 0 ok, 2 NPD (pivot written), 1 other error.
+int ref_cholesky(const double* A, int64_t m, double* L, int64_t* pivot) {
+  try {
+    Matrix M(m, m);
+    std::memcpy(M.a.data(), A, sizeof(double) * m * m);
+    const CholeskyFactor F = cholesky(std::move(M));
+    std::memcpy(L, F.L.a.data(), sizeof(double) * m * m);
+    return 0;
+  } catch (const NotPositiveDefinite& e) {
+    if (pivot) *pivot = static_cast<int64_t>(e.pivot);
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+void ref_solve_spd(const double* L, int64_t m, const double* b, double* x) {
+  CholeskyFactor F;
+  F.L = Matrix(m, m);
+  std::memcpy(F.L.a.data(), L, sizeof(double) * m * m);
+  const auto r = solve_spd(F, std::span<const double>(b, m));
+  std::memcpy(x, r.data(), sizeof(double) * m);
+}
+
+int ref_train_krr(const double* X, const double* y, int64_t m, int64_t d, double sigma,
+                  double lambda, double* alpha, double* residual, int64_t* pivot) {
+  try {
+    const Dataset ds = dense(X, y, m, d);
+    const KrrModel model = train_krr(ds, gauss(sigma), lambda);
+    std::memcpy(alpha, model.alpha.data(), sizeof(double) * m);
+    if (residual) *residual = model.residual_ratio;
+    return 0;
+  } catch (const NotPositiveDefinite& e) {
+    if (pivot) *pivot = static_cast<int64_t>(e.pivot);
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// KrrModel::predict over q query rows (model trained by train_krr).
+int ref_train_predict(const double* X, const double* y, int64_t m, int64_t d, double sigma,
+                      double lambda, const double* Q, int64_t q, double* out) {
+  try {
+    const Dataset ds = dense(X, y, m, d);
+    const KrrModel model = train_krr(ds, gauss(sigma), lambda);
+    const Dataset qs = dense(Q, nullptr, q, d);
+    for (int64_t j = 0; j < q; ++j) out[j] = model.predict(qs.row(j));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+static void copy_clustering(const Clustering& c, int32_t* membership, double* centers,
+                            int64_t* sizes, int64_t d) {
+  for (std::size_t i = 0; i < c.membership.size(); ++i) membership[i] = c.membership[i];
+  for (int j = 0; j < c.k; ++j) {
+    std::memcpy(centers + j * d, c.centers[j].data(), sizeof(double) * d);
+    sizes[j] = static_cast<int64_t>(c.sizes[j]);
+  }
+}
+
+int ref_kmeans(const double* X, int64_t n, int64_t d, int k, uint64_t seed, double threshold,
+               int max_iters, int32_t* membership, double* centers, int64_t* sizes,
+               int* iterations, double* wcss) {
+  try {
+    const Dataset ds = dense(X, nullptr, n, d);
+    KMeansParams p;
+    p.threshold = threshold;
+    p.max_iters = max_iters;
+    KMeansDiag diag;
+    const Clustering c = kmeans(ds, k, seed, p, &diag);
+    copy_clustering(c, membership, centers, sizes, d);
+    if (iterations) *iterations = diag.iterations;
+    if (wcss)
+      for (std::size_t i = 0; i < diag.wcss.size(); ++i) wcss[i] = diag.wcss[i];
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+int ref_kbalance(const double* X, int64_t n, int64_t d, int k, uint64_t seed, double threshold,
+                 int max_iters, int recompute, int32_t* membership, double* centers,
+                 int64_t* sizes) {
+  try {
+    const Dataset ds = dense(X, nullptr, n, d);
+    KMeansParams p;
+    p.threshold = threshold;
+    p.max_iters = max_iters;
+    p.recompute_centers = recompute != 0;
+    const Clustering c = kbalance(ds, k, seed, p);
+    copy_clustering(c, membership, centers, sizes, d);
+    return 0;
+  } catch (const std::logic_error& e) {
+    g_err = e.what();
+    return 4;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+int ref_nearest_center(const double* centers, int k, int64_t d, const double* x) {
+  std::vector<std::vector<double>> c(k);
+  for (int j = 0; j < k; ++j) c[j].assign(centers + j * d, centers + (j + 1) * d);
+  const Dataset q = dense(x, nullptr, 1, d);
+  return nearest_center(c, q.row(0));
+}
+
+// make_partition: part id per row, centers (p*d) when defined. Returns p or -1.
+int64_t ref_make_partition(int kind, const double* X, int64_t n, int64_t d, int64_t p,
+                           uint64_t seed, int32_t* part_of, double* centers) {
+  try {
+    const Dataset ds = dense(X, nullptr, n, d);
+    const PartitionSet ps = make_partition(static_cast<StrategyKind>(kind), ds, p, seed);
+    for (std::size_t t = 0; t < ps.p; ++t)
+      for (std::size_t i : ps.parts[t]) part_of[i] = static_cast<int32_t>(t);
+    if (ps.has_centers() && centers)
+      for (std::size_t t = 0; t < ps.p; ++t)
+        std::memcpy(centers + t * d, ps.centers[t].data(), sizeof(double) * d);
+    return static_cast<int64_t>(ps.p);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// grid_search through the reference's public API.  Returns best index, -1 when
+// no cell succeeded, -2 on error.
+int64_t ref_grid_search(int kind, const double* Xtr, const double* ytr, int64_t n, int64_t d,
+                        const double* Xte, const double* yte, int64_t t, int64_t p,
+                        const double* lambdas, int64_t nl, const double* sigmas, int64_t ns,
+                        uint64_t seed, int64_t workers, double* cell_mse, uint8_t* cell_failed,
+                        double* cell_residual) {
+  try {
+    const Dataset train = dense(Xtr, ytr, n, d);
+    const Dataset test = dense(Xte, yte, t, d);
+    GridOptions opt;
+    opt.workers = static_cast<std::size_t>(workers < 1 ? 1 : workers);
+    const GridResult r =
+        grid_search(static_cast<StrategyKind>(kind), train, test, p,
+                    std::span<const double>(lambdas, nl), std::span<const double>(sigmas, ns),
+                    seed, opt);
+    for (std::size_t c = 0; c < r.cells.size(); ++c) {
+      cell_mse[c] = r.cells[c].mse;
+      cell_failed[c] = r.cells[c].failed ? 1 : 0;
+      cell_residual[c] = r.cells[c].max_residual;
+    }
+    return r.has_best() ? static_cast<int64_t>(r.best_index) : -1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -2;
+  }
+}
+
+// train_partitions + predict_nearest (the 4-stage API path, strategies.cpp:104-149)
+int ref_train_predict_nearest(int kind, const double* Xtr, const double* ytr, int64_t n,
+                              int64_t d, int64_t p, uint64_t seed, double sigma, double lambda,
+                              int64_t workers, const double* Q, int64_t q, double* out) {
+  try {
+    const Dataset train = dense(Xtr, ytr, n, d);
+    const PartitionSet ps = make_partition(static_cast<StrategyKind>(kind), train, p, seed);
+    const TrainedPartitions tp =
+        train_partitions(ps, train, gauss(sigma), lambda, static_cast<std::size_t>(workers));
+    const Dataset qs = dense(Q, nullptr, q, d);
+    for (int64_t j = 0; j < q; ++j) out[j] = predict_nearest(tp.models, ps.centers, qs.row(j));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+}  // extern "C"
