@@ -1,0 +1,226 @@
+/*
+ * pkrr_gpu.h -- C ABI of the B200 (sm_100a) partitioned Gaussian KRR engine.
+ *
+ * Drop-in boundary for the reference library's hot path (arxiv 1805.00569
+ * reference, /root/reference/proj).  The reference exposes a plain C++ API
+ * (no FFI); every entry point below replaces one reference function, cited as
+ * file:line, with the same argument meaning and the same error semantics
+ * expressed as status codes.  A header-only C++ adapter with the reference's own
+ * signatures (pkrr::gpu::gram, cholesky, train_krr, kmeans, make_partition,
+ * grid_search, ...) sits on top of this ABI: include/pkrr_gpu.hpp.
+ *
+ * Conventions
+ *  - Matrices are dense row-major FP64 (the reference's Matrix, matrix.hpp:9-28;
+ *    its Dataset rows are dense after standardize, dataset.cpp:183-193).
+ *  - Every array argument may be a HOST or a DEVICE pointer; the engine detects
+ *    which (cudaPointerGetAttributes) and copies only what it must.
+ *  - Return value: PKRRGPU_OK (0) or an error status; pkrrgpu_last_error()
+ *    returns the message of the last failure on the calling thread.
+ *  - Calls on one context are serialised by the caller (like the reference,
+ *    which has no globals; runtime.hpp:66-112).
+ */
+#ifndef PKRR_GPU_H
+#define PKRR_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  NPD mirrors NotPositiveDefinite (solver.hpp:17-21); INVALID
+ * mirrors std::invalid_argument; LOGIC mirrors kbalance's logic_error
+ * (clustering.cpp:172). */
+enum pkrrgpu_status {
+  PKRRGPU_OK = 0,
+  PKRRGPU_INVALID = 1,
+  PKRRGPU_NPD = 2,
+  PKRRGPU_CUDA = 3,
+  PKRRGPU_LOGIC = 4
+};
+
+/* StrategyKind, same order as strategies.hpp:21. */
+enum pkrrgpu_strategy {
+  PKRRGPU_EXACT = 0,
+  PKRRGPU_DCKRR = 1,
+  PKRRGPU_KKRR = 2,
+  PKRRGPU_KKRR2 = 3,
+  PKRRGPU_KKRR3 = 4,
+  PKRRGPU_BKRR = 5,
+  PKRRGPU_BKRR2 = 6,
+  PKRRGPU_BKRR3 = 7
+};
+
+typedef struct pkrrgpu_ctx pkrrgpu_ctx;
+
+/* Engine on one CUDA device (one process per GPU; multi-GPU = one context per
+ * rank, see pkrrgpu_grid_args.rank/world). */
+int pkrrgpu_create(int device, pkrrgpu_ctx** out);
+void pkrrgpu_destroy(pkrrgpu_ctx* ctx);
+const char* pkrrgpu_last_error(void);
+/* Kernel launches made by this context since creation (evidence counter). */
+int64_t pkrrgpu_launch_count(const pkrrgpu_ctx* ctx);
+const char* pkrrgpu_version(void);
+
+/* ---- kernel (kernel.hpp:40-44) ------------------------------------------ */
+
+/* gram(spec{gaussian, sigma}, A, B) -- kernel.cpp:81-132.  When A == B (same
+ * pointer, na == nb) the symmetric path is used: unit diagonal, bitwise
+ * symmetric result (kernel.cpp:107-119).  K is na x nb. */
+int pkrrgpu_gram(pkrrgpu_ctx* ctx, const double* A, int64_t na, const double* B, int64_t nb,
+                 int64_t d, double sigma, double* K);
+
+/* assemble_system(K, lambda, mult) -- kernel.cpp:134-141: A = K + lambda*mult*I. */
+int pkrrgpu_assemble(pkrrgpu_ctx* ctx, const double* K, int64_t m, double lambda, int64_t mult,
+                     double* A);
+
+/* ---- solver (solver.hpp:29-53) ------------------------------------------- */
+
+/* cholesky(A) -- solver.cpp:13-44.  L lower with zero strict upper triangle.
+ * PKRRGPU_NPD: *npd_pivot = first column j whose pivot is !(> 0). */
+int pkrrgpu_cholesky(pkrrgpu_ctx* ctx, const double* A, int64_t m, double* L,
+                     int64_t* npd_pivot);
+
+/* solve_spd(F, b) -- solver.cpp:46-72: L L^T x = b. */
+int pkrrgpu_solve_spd(pkrrgpu_ctx* ctx, const double* L, int64_t m, const double* b, double* x);
+
+/* train_krr(data, spec, lambda) -- solver.cpp:89-125: alpha (m) and the
+ * residual ratio ||(K + lambda m I) alpha - y|| / ||y|| (solver.cpp:103-119). */
+int pkrrgpu_train_krr(pkrrgpu_ctx* ctx, const double* X, const double* y, int64_t m, int64_t d,
+                      double sigma, double lambda, double* alpha, double* residual,
+                      int64_t* npd_pivot);
+
+/* KrrModel::predict over q queries -- solver.cpp:74-87:
+ * out[j] = sum_i alpha_i k(S_i, Q_j). */
+int pkrrgpu_predict(pkrrgpu_ctx* ctx, const double* S, const double* alpha, int64_t m, int64_t d,
+                    double sigma, const double* Q, int64_t q, double* out);
+
+/* ---- clustering (clustering.hpp:33-45) ----------------------------------- */
+
+/* kmeans -- clustering.cpp:53-138 (uniform distinct-sample init from
+ * Rng(seed), Lloyd, empty-cluster reseed).  Labels are bit-exact with the
+ * reference: same distance arithmetic, same tie rule, order-preserving means. */
+int pkrrgpu_kmeans(pkrrgpu_ctx* ctx, const double* X, int64_t n, int64_t d, int k, uint64_t seed,
+                   double threshold, int max_iters, int32_t* membership, double* centers,
+                   int64_t* sizes, int* iterations);
+
+/* kbalance -- clustering.cpp:140-180 (k-means warm start, then the capacity
+ * scan replayed exactly in parallel). */
+int pkrrgpu_kbalance(pkrrgpu_ctx* ctx, const double* X, int64_t n, int64_t d, int k,
+                     uint64_t seed, double threshold, int max_iters, int recompute,
+                     int32_t* membership, double* centers, int64_t* sizes);
+
+/* nearest_center for q rows -- clustering.cpp:182-195. */
+int pkrrgpu_nearest_center(pkrrgpu_ctx* ctx, const double* centers, int k, int64_t d,
+                           const double* Q, int64_t q, int32_t* out);
+
+/* ---- strategies (strategies.hpp:40-120) --------------------------------- */
+
+/* make_partition -- strategies.cpp:64-102 (default KMeansParams, :93-96).
+ * part_of[n] = part of each train row; order[n] = rows part by part in
+ * within-part order; centers[p*d] for k-means / k-balance (may be NULL);
+ * *p_out = effective number of parts (1 for exact). */
+int pkrrgpu_make_partition(pkrrgpu_ctx* ctx, int strategy, const double* X, int64_t n, int64_t d,
+                           int64_t p, uint64_t seed, int32_t* part_of, int64_t* order,
+                           double* centers, int64_t* p_out);
+
+/* Trained per-part models (TrainedPartitions, strategies.hpp:44-47), resident
+ * in device memory. */
+typedef struct pkrrgpu_models pkrrgpu_models;
+
+/* train_partitions -- strategies.cpp:104-133.  On NPD the status is
+ * PKRRGPU_NPD, *failed_part = the first failing part, *npd_pivot its column. */
+int pkrrgpu_train_partitions(pkrrgpu_ctx* ctx, int strategy, const double* X, const double* y,
+                             int64_t n, int64_t d, int64_t p, uint64_t seed, double sigma,
+                             double lambda, pkrrgpu_models** out, int64_t* failed_part,
+                             int64_t* npd_pivot);
+int64_t pkrrgpu_models_count(const pkrrgpu_models* models);
+int64_t pkrrgpu_models_size(const pkrrgpu_models* models, int64_t part);
+int pkrrgpu_models_alpha(const pkrrgpu_models* models, int64_t part, double* alpha);
+int pkrrgpu_models_residual(const pkrrgpu_models* models, int64_t part, double* residual);
+void pkrrgpu_models_free(pkrrgpu_models* models);
+
+/* predict_nearest -- strategies.cpp:142-149 (route by nearest_center, then the
+ * chosen model's KrrModel::predict), batched over q queries. */
+int pkrrgpu_predict_nearest(pkrrgpu_ctx* ctx, const pkrrgpu_models* models, const double* Q,
+                            int64_t q, double* out);
+
+/* grid_search -- strategies.cpp:343-507 (reference signature).  Cells are
+ * lambda-major (li * n_sigmas + si, :405).  best_index = first strict minimum
+ * over non-failed cells (:499-505), -1 when every cell failed. */
+int pkrrgpu_grid_search(pkrrgpu_ctx* ctx, int strategy, const double* X_train,
+                        const double* y_train, int64_t n, int64_t d, const double* X_test,
+                        const double* y_test, int64_t t, int64_t p, const double* lambdas,
+                        int64_t n_lambdas, const double* sigmas, int64_t n_sigmas, uint64_t seed,
+                        double* cell_mse, uint8_t* cell_failed, double* cell_residual,
+                        int64_t* best_index);
+
+/* Extended grid: adds a held-out evaluation set scored for every cell, explicit
+ * k-means parameters, and part sharding for one-process-per-GPU runs. */
+typedef struct {
+  int strategy;
+  const double* X_train;
+  const double* y_train;
+  int64_t n;
+  int64_t d;
+  const double* X_test; /* selection set (the reference's "test" argument) */
+  const double* y_test;
+  int64_t t;
+  const double* X_eval; /* optional held-out set; NULL/0 = none */
+  const double* y_eval;
+  int64_t t_eval;
+  int64_t p;
+  const double* lambdas;
+  int64_t n_lambdas;
+  const double* sigmas;
+  int64_t n_sigmas;
+  uint64_t seed;
+  double km_threshold; /* used when km_max_iters > 0; else reference defaults 0.01/100 */
+  int km_max_iters;
+  int rank;  /* parts t with t % world == rank are trained by this context */
+  int world; /* 1 = single process */
+} pkrrgpu_grid_args;
+
+typedef struct {
+  /* per cell [n_lambdas * n_sigmas]; combined over parts only when world == 1 */
+  double* cell_mse;
+  uint8_t* cell_failed;
+  double* cell_residual;
+  double* cell_eval_mse; /* optional */
+  int64_t best_index;
+  /* per (cell, part) [ncell * p], filled for the parts this rank trained; the
+   * multi-rank combine sums them in part order (deterministic, GPU-count
+   * independent).  All optional. */
+  double* part_sse;
+  double* part_eval_sse;
+  uint8_t* part_failed;
+  double* part_residual;
+  int64_t* part_test_count;  /* [p] test rows routed to each part */
+  int64_t* part_eval_count;  /* [p] */
+  /* partition + best-cell predictions, optional */
+  int32_t* part_of;      /* [n] */
+  double* centers;       /* [p*d] */
+  int64_t* part_sizes;   /* [p] */
+  double* best_pred;     /* [t] (world == 1) */
+  double* best_eval_pred;/* [t_eval] (world == 1) */
+  int64_t p_effective;
+  /* algorithmic FP64 work done by this rank (SURVEY 8(d) accounting) */
+  double flops_chol;
+  double flops_gram;
+  double flops_other;
+} pkrrgpu_grid_out;
+
+int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* args,
+                           pkrrgpu_grid_out* out);
+
+/* ---- timing hooks (bench / profiling only) ------------------------------- */
+
+/* Device time (ms, CUDA events on the engine's streams) spent in the last
+ * grid call by phase: [0] partition, [1] train (gram + Cholesky + solves),
+ * [2] predict + reduce, [3] total.  Cholesky-only time in [4]. */
+int pkrrgpu_last_timings(const pkrrgpu_ctx* ctx, double* ms, int n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PKRR_GPU_H */

@@ -1,0 +1,495 @@
+"""paper_1805_00569_b200 -- B200 (sm_100a) engine for partitioned Gaussian KRR.
+
+Python mirror of the reference library's hot-path API (arxiv 1805.00569
+reference, proj/include/pkrr/*.hpp) over the C ABI in include/pkrr_gpu.h.
+Names, argument meaning and error behaviour follow the reference:
+
+    gram(X, Y, sigma)                      kernel.hpp:40  (X is Y -> symmetric path)
+    assemble_system(K, lam, m)             kernel.hpp:44
+    cholesky(A) -> L                       solver.hpp:29  (raises NotPositiveDefinite)
+    solve_spd(L, b)                        solver.hpp:32
+    train_krr(X, y, sigma, lam) -> KrrModel solver.hpp:52
+    kmeans / kbalance / nearest_center     clustering.hpp:33-45
+    make_partition                         strategies.hpp:40
+    train_partitions / predict_nearest     strategies.hpp:50-58
+    mse                                    strategies.hpp:64
+    grid_search -> GridResult              strategies.hpp:117
+
+Every call runs on the GPU through libpkrr_gpu.so; there is no CPU fallback.
+Arrays may be numpy (host) or torch CUDA tensors (device pointers are passed
+through without copies).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpkrr_gpu.so")
+
+STRATEGIES = {"exact": 0, "dckrr": 1, "kkrr": 2, "kkrr2": 3, "kkrr3": 4, "bkrr": 5, "bkrr2": 6, "bkrr3": 7}
+OK, INVALID, NPD, CUDA, LOGIC = 0, 1, 2, 3, 4
+
+_d = C.POINTER(C.c_double)
+_i32 = C.POINTER(C.c_int32)
+_i64 = C.POINTER(C.c_int64)
+_u8 = C.POINTER(C.c_uint8)
+
+
+class NotPositiveDefinite(RuntimeError):
+    """solver.hpp:17-21: a pivot was not strictly positive."""
+
+    def __init__(self, pivot, msg=""):
+        super().__init__(msg or f"matrix not positive definite: pivot {pivot}")
+        self.pivot = int(pivot)
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class GridArgs(C.Structure):
+    _fields_ = [("strategy", C.c_int), ("X_train", C.c_void_p), ("y_train", C.c_void_p), ("n", C.c_int64),
+                ("d", C.c_int64), ("X_test", C.c_void_p), ("y_test", C.c_void_p), ("t", C.c_int64),
+                ("X_eval", C.c_void_p), ("y_eval", C.c_void_p), ("t_eval", C.c_int64), ("p", C.c_int64),
+                ("lambdas", C.c_void_p), ("n_lambdas", C.c_int64), ("sigmas", C.c_void_p),
+                ("n_sigmas", C.c_int64), ("seed", C.c_uint64), ("km_threshold", C.c_double),
+                ("km_max_iters", C.c_int), ("rank", C.c_int), ("world", C.c_int)]
+
+
+class GridOut(C.Structure):
+    _fields_ = [("cell_mse", C.c_void_p), ("cell_failed", C.c_void_p), ("cell_residual", C.c_void_p),
+                ("cell_eval_mse", C.c_void_p), ("best_index", C.c_int64), ("part_sse", C.c_void_p),
+                ("part_eval_sse", C.c_void_p), ("part_failed", C.c_void_p), ("part_residual", C.c_void_p),
+                ("part_test_count", C.c_void_p), ("part_eval_count", C.c_void_p), ("part_of", C.c_void_p),
+                ("centers", C.c_void_p), ("part_sizes", C.c_void_p), ("best_pred", C.c_void_p),
+                ("best_eval_pred", C.c_void_p), ("p_effective", C.c_int64), ("flops_chol", C.c_double),
+                ("flops_gram", C.c_double), ("flops_other", C.c_double)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libpkrr_gpu.so (built by build.py).  Raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with `python -m paper_1805_00569_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(path)
+    sig = {
+        "pkrrgpu_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+        "pkrrgpu_destroy": (None, [C.c_void_p]),
+        "pkrrgpu_last_error": (C.c_char_p, []),
+        "pkrrgpu_launch_count": (C.c_int64, [C.c_void_p]),
+        "pkrrgpu_version": (C.c_char_p, []),
+        "pkrrgpu_gram": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64,
+                                   C.c_double, C.c_void_p]),
+        "pkrrgpu_assemble": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_int64, C.c_void_p]),
+        "pkrrgpu_cholesky": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, _i64]),
+        "pkrrgpu_solve_spd": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+        "pkrrgpu_train_krr": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_double,
+                                        C.c_double, C.c_void_p, _d, _i64]),
+        "pkrrgpu_predict": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_double,
+                                      C.c_void_p, C.c_int64, C.c_void_p]),
+        "pkrrgpu_kmeans": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_uint64,
+                                     C.c_double, C.c_int, C.c_void_p, C.c_void_p, _i64, C.POINTER(C.c_int)]),
+        "pkrrgpu_kbalance": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_uint64,
+                                       C.c_double, C.c_int, C.c_int, C.c_void_p, C.c_void_p, _i64]),
+        "pkrrgpu_nearest_center": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64,
+                                             C.c_void_p]),
+        "pkrrgpu_make_partition": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
+                                             C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, _i64]),
+        "pkrrgpu_train_partitions": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                               C.c_int64, C.c_uint64, C.c_double, C.c_double,
+                                               C.POINTER(C.c_void_p), _i64, _i64]),
+        "pkrrgpu_models_count": (C.c_int64, [C.c_void_p]),
+        "pkrrgpu_models_size": (C.c_int64, [C.c_void_p, C.c_int64]),
+        "pkrrgpu_models_alpha": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p]),
+        "pkrrgpu_models_residual": (C.c_int, [C.c_void_p, C.c_int64, _d]),
+        "pkrrgpu_models_free": (None, [C.c_void_p]),
+        "pkrrgpu_predict_nearest": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+        "pkrrgpu_grid_search": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                          C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
+                                          C.c_void_p, C.c_int64, C.c_uint64, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, _i64]),
+        "pkrrgpu_grid_search_ex": (C.c_int, [C.c_void_p, C.POINTER(GridArgs), C.POINTER(GridOut)]),
+        "pkrrgpu_last_timings": (C.c_int, [C.c_void_p, _d, C.c_int]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def exported_symbols():
+    """Every entry point include/pkrr_gpu.h declares."""
+    import re
+    hdr = open(os.path.join(os.path.dirname(HERE), "include", "pkrr_gpu.h")).read()
+    return sorted(set(re.findall(r"\b(pkrrgpu_[a-z_]+)\s*\(", hdr)))
+
+
+def _check(rc, pivot=None):
+    if rc == OK:
+        return
+    msg = _lib.pkrrgpu_last_error().decode()
+    if rc == NPD:
+        raise NotPositiveDefinite(pivot if pivot is not None else -1, msg)
+    if rc == INVALID:
+        raise ValueError(msg)
+    if rc == LOGIC:
+        raise RuntimeError(msg)
+    raise CudaError(msg)
+
+
+def _ptr(a):
+    """(pointer, keepalive) for numpy arrays or torch tensors (host or CUDA)."""
+    if a is None:
+        return None, None
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            a = a.contiguous()
+        return a.data_ptr(), a
+    return a.ctypes.data, a
+
+
+def _f64(a):
+    if a is None or hasattr(a, "data_ptr"):
+        return a
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Engine:
+    """One engine per GPU (pkrrgpu_ctx).  One process per GPU for multi-GPU runs."""
+
+    def __init__(self, device: int = 0):
+        lib = load_library()
+        h = C.c_void_p()
+        _check(lib.pkrrgpu_create(device, C.byref(h)))
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.pkrrgpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launches(self) -> int:
+        return int(_lib.pkrrgpu_launch_count(self._h))
+
+    def timings(self):
+        ms = (C.c_double * 8)()
+        _lib.pkrrgpu_last_timings(self._h, ms, 8)
+        return dict(partition=ms[0], train=ms[1], predict=ms[2], total=ms[3], cholesky=ms[4], gram=ms[5])
+
+    # ---- kernel.hpp ---------------------------------------------------------
+    def gram(self, X, Y, sigma):
+        X = _f64(X)
+        same = Y is None or Y is X
+        Y = X if same else _f64(Y)
+        na, d = X.shape
+        nb = Y.shape[0]
+        K = np.empty((na, nb))
+        px, kx = _ptr(X)
+        py, ky = (px, kx) if same else _ptr(Y)
+        _check(_lib.pkrrgpu_gram(self._h, px, na, py, nb, d, float(sigma), K.ctypes.data))
+        return K
+
+    def assemble_system(self, K, lam, m):
+        K = _f64(K)
+        A = np.empty_like(K)
+        _check(_lib.pkrrgpu_assemble(self._h, K.ctypes.data, K.shape[0], float(lam), int(m), A.ctypes.data))
+        return A
+
+    # ---- solver.hpp ---------------------------------------------------------
+    def cholesky(self, A):
+        A = _f64(A)
+        L = np.empty_like(A)
+        piv = C.c_int64(-1)
+        rc = _lib.pkrrgpu_cholesky(self._h, A.ctypes.data, A.shape[0], L.ctypes.data, C.byref(piv))
+        _check(rc, piv.value)
+        return L
+
+    def solve_spd(self, L, b):
+        L, b = _f64(L), _f64(b)
+        x = np.empty(L.shape[0])
+        _check(_lib.pkrrgpu_solve_spd(self._h, L.ctypes.data, L.shape[0], b.ctypes.data, x.ctypes.data))
+        return x
+
+    def train_krr(self, X, y, sigma, lam):
+        X, y = _f64(X), _f64(y)
+        m, d = X.shape
+        alpha = np.empty(m)
+        res = C.c_double(0)
+        piv = C.c_int64(-1)
+        px, kx = _ptr(X)
+        py, ky = _ptr(y)
+        rc = _lib.pkrrgpu_train_krr(self._h, px, py, m, d, float(sigma), float(lam), alpha.ctypes.data,
+                                    C.byref(res), C.byref(piv))
+        _check(rc, piv.value)
+        return KrrModel(support=np.asarray(X) if not hasattr(X, "data_ptr") else X.cpu().numpy(),
+                        alpha=alpha, sigma=float(sigma), lam=float(lam), residual_ratio=res.value, engine=self)
+
+    def predict(self, S, alpha, sigma, Q):
+        S, alpha, Q = _f64(S), _f64(alpha), _f64(Q)
+        out = np.empty(Q.shape[0])
+        _check(_lib.pkrrgpu_predict(self._h, S.ctypes.data, alpha.ctypes.data, S.shape[0], S.shape[1],
+                                    float(sigma), Q.ctypes.data, Q.shape[0], out.ctypes.data))
+        return out
+
+    # ---- clustering.hpp -----------------------------------------------------
+    def kmeans(self, X, k, seed, threshold=0.01, max_iters=100):
+        X = _f64(X)
+        n, d = X.shape
+        mem = np.empty(n, np.int32)
+        cen = np.empty((k, d))
+        sz = np.empty(k, np.int64)
+        it = C.c_int(0)
+        px, kx = _ptr(X)
+        _check(_lib.pkrrgpu_kmeans(self._h, px, n, d, k, seed, threshold, max_iters, mem.ctypes.data,
+                                   cen.ctypes.data, sz.ctypes.data_as(_i64), C.byref(it)))
+        return Clustering(k=k, centers=cen, membership=mem, sizes=sz, iterations=it.value)
+
+    def kbalance(self, X, k, seed, threshold=0.01, max_iters=100, recompute_centers=True):
+        X = _f64(X)
+        n, d = X.shape
+        mem = np.empty(n, np.int32)
+        cen = np.empty((k, d))
+        sz = np.empty(k, np.int64)
+        px, kx = _ptr(X)
+        _check(_lib.pkrrgpu_kbalance(self._h, px, n, d, k, seed, threshold, max_iters, int(recompute_centers),
+                                     mem.ctypes.data, cen.ctypes.data, sz.ctypes.data_as(_i64)))
+        return Clustering(k=k, centers=cen, membership=mem, sizes=sz)
+
+    def nearest_center(self, centers, Q):
+        centers, Q = _f64(centers), _f64(Q)
+        single = Q.ndim == 1
+        Q2 = Q.reshape(1, -1) if single else Q
+        out = np.empty(Q2.shape[0], np.int32)
+        _check(_lib.pkrrgpu_nearest_center(self._h, centers.ctypes.data, centers.shape[0], centers.shape[1],
+                                           np.ascontiguousarray(Q2).ctypes.data, Q2.shape[0], out.ctypes.data))
+        return int(out[0]) if single else out
+
+    # ---- strategies.hpp -----------------------------------------------------
+    def make_partition(self, strategy, X, p, seed):
+        X = _f64(X)
+        n, d = X.shape
+        part = np.empty(n, np.int32)
+        order = np.empty(n, np.int64)
+        cen = np.zeros((max(p, 1), d))
+        pe = C.c_int64(0)
+        px, kx = _ptr(X)
+        _check(_lib.pkrrgpu_make_partition(self._h, STRATEGIES[strategy], px, n, d, p, seed, part.ctypes.data,
+                                           order.ctypes.data, cen.ctypes.data, C.byref(pe)))
+        pe = pe.value
+        sizes = np.bincount(part, minlength=pe)
+        parts, at = [], 0
+        for t in range(pe):
+            parts.append(order[at:at + sizes[t]].copy())
+            at += sizes[t]
+        has_c = STRATEGIES[strategy] not in (0, 1)
+        return PartitionSet(p=pe, parts=parts, centers=cen[:pe] if has_c else None)
+
+    def train_partitions(self, strategy, X, y, p, seed, sigma, lam):
+        X, y = _f64(X), _f64(y)
+        n, d = X.shape
+        h = C.c_void_p()
+        fp, piv = C.c_int64(-1), C.c_int64(-1)
+        px, kx = _ptr(X)
+        py, ky = _ptr(y)
+        rc = _lib.pkrrgpu_train_partitions(self._h, STRATEGIES[strategy], px, py, n, d, p, seed, float(sigma),
+                                           float(lam), C.byref(h), C.byref(fp), C.byref(piv))
+        _check(rc, piv.value)
+        return TrainedPartitions(self, h)
+
+    def grid_search(self, strategy, train_X, train_y, test_X, test_y, p, lambdas, sigmas, seed, *,
+                    eval_X=None, eval_y=None, km_threshold=0.01, km_max_iters=0, rank=0, world=1,
+                    want_partition=False):
+        """strategies.cpp:343-507.  Returns GridResult (cells lambda-major)."""
+        lam = np.ascontiguousarray(lambdas, np.float64)
+        sig = np.ascontiguousarray(sigmas, np.float64)
+        tX, ty, sX, sy = _f64(train_X), _f64(train_y), _f64(test_X), _f64(test_y)
+        eX, ey = _f64(eval_X), _f64(eval_y)
+        n, d = tX.shape
+        t = sX.shape[0]
+        te = 0 if eX is None else eX.shape[0]
+        keep = []
+
+        def P(a):
+            p_, k_ = _ptr(a)
+            keep.append(k_)
+            return p_
+
+        args = GridArgs(strategy=STRATEGIES[strategy], X_train=P(tX), y_train=P(ty), n=n, d=d, X_test=P(sX),
+                        y_test=P(sy), t=t, X_eval=P(eX), y_eval=P(ey), t_eval=te, p=p,
+                        lambdas=lam.ctypes.data, n_lambdas=lam.size, sigmas=sig.ctypes.data,
+                        n_sigmas=sig.size, seed=seed, km_threshold=km_threshold, km_max_iters=km_max_iters,
+                        rank=rank, world=world)
+        nc = lam.size * sig.size
+        pmax = max(p, 1)
+        res = dict(cell_mse=np.full(nc, np.nan), cell_failed=np.zeros(nc, np.uint8), cell_residual=np.zeros(nc),
+                   cell_eval_mse=np.full(nc, np.nan), part_sse=np.zeros(nc * pmax),
+                   part_eval_sse=np.zeros(nc * pmax), part_failed=np.zeros(nc * pmax, np.uint8),
+                   part_residual=np.zeros(nc * pmax), part_test_count=np.zeros(pmax, np.int64),
+                   part_eval_count=np.zeros(pmax, np.int64), part_sizes=np.zeros(pmax, np.int64),
+                   best_pred=np.zeros(t), best_eval_pred=np.zeros(max(te, 1)))
+        if want_partition:
+            res["part_of"] = np.zeros(n, np.int32)
+            res["centers"] = np.zeros((pmax, d))
+        out = GridOut(**{k: v.ctypes.data for k, v in res.items()})
+        _check(_lib.pkrrgpu_grid_search_ex(self._h, C.byref(args), C.byref(out)))
+        pe = out.p_effective
+        for k in ("part_sse", "part_eval_sse", "part_failed", "part_residual"):
+            res[k] = res[k][: nc * pe].reshape(nc, pe)
+        for k in ("part_test_count", "part_eval_count", "part_sizes"):
+            res[k] = res[k][:pe]
+        return GridResult(strategy=strategy, p=pe, lambdas=lam, sigmas=sig, best_index=int(out.best_index),
+                          mse=res["cell_mse"], failed=res["cell_failed"].astype(bool),
+                          residual=res["cell_residual"], eval_mse=res["cell_eval_mse"] if te else None,
+                          best_pred=res["best_pred"], best_eval_pred=res["best_eval_pred"][:te] if te else None,
+                          parts=res, flops=dict(chol=out.flops_chol, gram=out.flops_gram, other=out.flops_other))
+
+
+@dataclass
+class Clustering:
+    k: int
+    centers: np.ndarray
+    membership: np.ndarray
+    sizes: np.ndarray
+    iterations: int = 0
+
+
+@dataclass
+class PartitionSet:
+    p: int
+    parts: list
+    centers: object = None
+
+    def has_centers(self):
+        return self.centers is not None
+
+
+@dataclass
+class KrrModel:
+    support: np.ndarray
+    alpha: np.ndarray
+    sigma: float
+    lam: float
+    residual_ratio: float
+    engine: Engine = field(repr=False, default=None)
+
+    def predict(self, Q):
+        Q = np.asarray(Q, np.float64)
+        single = Q.ndim == 1
+        out = self.engine.predict(self.support, self.alpha, self.sigma, Q.reshape(1, -1) if single else Q)
+        return float(out[0]) if single else out
+
+
+class TrainedPartitions:
+    """TrainedPartitions (strategies.hpp:44-47) resident on the GPU."""
+
+    def __init__(self, engine: Engine, handle):
+        self.engine = engine
+        self._h = handle
+
+    def __del__(self):
+        try:
+            if self._h:
+                _lib.pkrrgpu_models_free(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def __len__(self):
+        return int(_lib.pkrrgpu_models_count(self._h))
+
+    def alpha(self, t):
+        a = np.empty(int(_lib.pkrrgpu_models_size(self._h, t)))
+        _check(_lib.pkrrgpu_models_alpha(self._h, t, a.ctypes.data))
+        return a
+
+    def residual(self, t):
+        r = C.c_double(0)
+        _check(_lib.pkrrgpu_models_residual(self._h, t, C.byref(r)))
+        return r.value
+
+    def predict_nearest(self, Q):
+        Q = np.ascontiguousarray(Q, np.float64)
+        out = np.empty(Q.shape[0])
+        _check(_lib.pkrrgpu_predict_nearest(self.engine._h, self._h, Q.ctypes.data, Q.shape[0], out.ctypes.data))
+        return out
+
+
+@dataclass
+class GridResult:
+    strategy: str
+    p: int
+    lambdas: np.ndarray
+    sigmas: np.ndarray
+    best_index: int
+    mse: np.ndarray
+    failed: np.ndarray
+    residual: np.ndarray
+    eval_mse: object = None
+    best_pred: object = None
+    best_eval_pred: object = None
+    parts: dict = field(default_factory=dict, repr=False)
+    flops: dict = field(default_factory=dict)
+
+    def has_best(self):
+        return self.best_index >= 0
+
+    def max_residual(self):
+        ok = ~self.failed
+        return float(self.residual[ok].max()) if ok.any() else 0.0
+
+
+def mse(pred, truth):
+    """strategies.cpp:168-177 (host helper; the grid computes MSE on device)."""
+    pred, truth = np.asarray(pred, np.float64), np.asarray(truth, np.float64)
+    if pred.shape != truth.shape or pred.size == 0:
+        raise ValueError("mse: length mismatch")
+    s = 0.0
+    for a, b in zip(pred, truth):
+        s += (a - b) * (a - b)
+    return s / pred.size
+
+
+def combine_parts(part_sse, part_failed, t):
+    """Multi-rank combine (one process per GPU): per-part SSE gathered from all
+    ranks is summed in PART ORDER, exactly like the single-process engine does,
+    so results are bitwise independent of the GPU count.  Returns (mse, failed,
+    best_index) with the reference's best rule (strategies.cpp:499-505)."""
+    part_sse = np.asarray(part_sse, np.float64)
+    part_failed = np.asarray(part_failed).astype(bool)
+    nc = part_sse.shape[0]
+    mse_c = np.full(nc, np.nan)
+    failed = part_failed.any(axis=1)
+    for c in range(nc):
+        if failed[c]:
+            continue
+        s = 0.0
+        for v in part_sse[c]:
+            s += float(v)
+        mse_c[c] = s / float(t)
+    best = -1
+    for c in range(nc):
+        if failed[c]:
+            continue
+        if best < 0 or mse_c[c] < mse_c[best]:
+            best = c
+    return mse_c, failed, best

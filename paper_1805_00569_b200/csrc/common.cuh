@@ -1,0 +1,97 @@
+// common.cuh -- sm_100a device primitives used by every pkrr kernel:
+// mbarrier + TMA (cp.async.bulk.tensor) staging and the FP64 tensor-core MMA.
+//
+// FP64 on Blackwell: tcgen05.mma has no f64 kind (ptxas rejects .kind::f64), so
+// FP64 tensor-core math is the warp-level mma.sync m8n8k4 f64 (SASS DMMA.8x8x4).
+// Measured on this pool's B200: 37.1 TFLOP/s DMMA vs 33.6 TFLOP/s DFMA
+// (profiles/fp64_peak_r01.json).  Operand tiles still move by TMA into 128B-
+// swizzled shared memory, paced by mbarriers, with a dedicated producer warp.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pk {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// 2-D TMA tile load: box {inner = c0 (elements), outer = c1 (rows)} -> smem.
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// D(8x8) += A(8x4, row) * B(4x8, col), FP64 tensor core.
+// Fragments: a = A[lane/4][lane%4], b = B[k = lane%4][n = lane/4],
+// c = C[lane/4][2*(lane%4) + {0,1}].
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// Byte offset of element (row, k) of a [rows x 16] f64 tile staged by TMA with
+// CU_TENSOR_MAP_SWIZZLE_128B (16-byte chunk index XORed with row % 8).
+__device__ __forceinline__ uint32_t swz128(int row, int k) {
+  return static_cast<uint32_t>(row * 128 + ((((k >> 1) ^ (row & 7)) << 4) | ((k & 1) << 3)));
+}
+
+__device__ __forceinline__ double lds_f64(const unsigned char* base, uint32_t off) {
+  return *reinterpret_cast<const double*>(base + off);
+}
+
+// Named barrier over the consumer warps only (producer warp excluded).
+__device__ __forceinline__ void consumer_sync(int nthreads) {
+  asm volatile("bar.sync 1, %0;\n" ::"r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace pk

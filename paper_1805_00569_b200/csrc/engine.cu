@@ -1,0 +1,1398 @@
+// engine.cu -- host side of the B200 pkrr engine: the C ABI of include/pkrr_gpu.h.
+//
+// Mirrors the reference's 4-stage API (strategies.hpp:40-120): partition ->
+// per-part train -> best-cell select -> predict, with the reference's argument
+// meaning and error semantics.  All arithmetic runs in the sm_100a kernels of
+// kernels.cu / gemm_dmma.cuh; the host only sequences launches, draws the
+// k-means init permutation with the reference's RNG (rng.cpp), and runs the
+// O(k) control decisions of the clustering loops (convergence, empty-cluster
+// reseed, k-balance capacity bookkeeping) exactly as clustering.cpp does.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/pkrr_gpu.h"
+#include "kernels.cuh"
+
+using pk::kNB;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+  int code;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) {
+  g_err = msg;
+  throw Fail{code};
+}
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(PKRRGPU_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// ---- reference RNG (rng.hpp:14-42, rng.cpp:8-63): host side, init only ----
+class HostRng {
+ public:
+  explicit HostRng(uint64_t seed) : eng_(seed) {}
+  uint64_t below(uint64_t n) {
+    if (n <= 1) return 0;
+    const uint64_t limit = UINT64_MAX - UINT64_MAX % n;
+    uint64_t x;
+    do {
+      x = eng_();
+    } while (x >= limit);
+    return x % n;
+  }
+  std::vector<int64_t> permutation(int64_t n) {
+    std::vector<int64_t> perm(n);
+    for (int64_t i = 0; i < n; ++i) perm[i] = i;
+    for (int64_t i = n; i > 1; --i) {
+      const int64_t j = static_cast<int64_t>(below(static_cast<uint64_t>(i)));
+      std::swap(perm[i - 1], perm[j]);
+    }
+    return perm;
+  }
+
+ private:
+  std::mt19937_64 eng_;
+};
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int predictor_of(int s) {
+  switch (s) {
+    case PKRRGPU_EXACT: return 0;
+    case PKRRGPU_DCKRR: case PKRRGPU_KKRR: case PKRRGPU_BKRR: return 1;
+    case PKRRGPU_KKRR2: case PKRRGPU_BKRR2: return 2;
+    default: return 3;
+  }
+}
+
+int partitioner_of(int s) {
+  switch (s) {
+    case PKRRGPU_EXACT: return 0;
+    case PKRRGPU_DCKRR: return 1;
+    case PKRRGPU_KKRR: case PKRRGPU_KKRR2: case PKRRGPU_KKRR3: return 2;
+    default: return 3;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// context: streams + caching device allocator
+// ---------------------------------------------------------------------------
+struct pkrrgpu_ctx {
+  int device = 0;
+  cudaStream_t main = nullptr;
+  std::vector<cudaStream_t> work;
+  pk::Counter counter;
+  double timings[8] = {0};
+  std::multimap<size_t, void*> free_blocks;
+  std::map<void*, size_t> live;
+  size_t cached_bytes = 0;
+
+  void* alloc(size_t bytes) {
+    bytes = static_cast<size_t>(round_up(static_cast<int64_t>(bytes ? bytes : 256), 256));
+    auto it = free_blocks.lower_bound(bytes);
+    if (it != free_blocks.end() && it->first <= bytes * 2 + (1 << 20)) {
+      void* p = it->second;
+      live[p] = it->first;
+      cached_bytes -= it->first;
+      free_blocks.erase(it);
+      return p;
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      trim();
+      ck(cudaMalloc(&p, bytes), "cudaMalloc");
+    }
+    live[p] = bytes;
+    return p;
+  }
+  void release(void* p) {
+    auto it = live.find(p);
+    if (it == live.end()) return;
+    free_blocks.emplace(it->second, p);
+    cached_bytes += it->second;
+    live.erase(it);
+  }
+  void trim() {
+    cudaDeviceSynchronize();
+    for (auto& kv : free_blocks) cudaFree(kv.second);
+    free_blocks.clear();
+    cached_bytes = 0;
+  }
+};
+
+namespace {
+
+// Per-call allocation scope: everything is returned to the cache at the end
+// (after the context has synchronised its streams).
+struct Scope {
+  pkrrgpu_ctx* ctx;
+  std::vector<void*> ptrs;
+  explicit Scope(pkrrgpu_ctx* c) : ctx(c) {}
+  ~Scope() {
+    cudaDeviceSynchronize();
+    for (void* p : ptrs) ctx->release(p);
+  }
+  template <typename T>
+  T* alloc(int64_t count) {
+    void* p = ctx->alloc(sizeof(T) * static_cast<size_t>(count > 0 ? count : 1));
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  template <typename T>
+  T* zeros(int64_t count, cudaStream_t s) {
+    T* p = alloc<T>(count);
+    ck(cudaMemsetAsync(p, 0, sizeof(T) * static_cast<size_t>(count > 0 ? count : 1), s), "memset");
+    return p;
+  }
+  // device view of a caller array (host or device pointer)
+  template <typename T>
+  const T* in(const T* src, int64_t count, cudaStream_t s) {
+    if (!src || count <= 0) return src;
+    if (is_device_ptr(src)) return src;
+    T* p = alloc<T>(count);
+    ck(cudaMemcpyAsync(p, src, sizeof(T) * count, cudaMemcpyHostToDevice, s), "H2D");
+    return p;
+  }
+  template <typename T>
+  T* upload(const std::vector<T>& v, cudaStream_t s) {
+    T* p = alloc<T>(static_cast<int64_t>(v.size()));
+    if (!v.empty())
+      ck(cudaMemcpyAsync(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, s), "H2D");
+    return p;
+  }
+};
+
+template <typename T>
+void copy_out(T* dst, const T* dsrc, int64_t count, cudaStream_t s) {
+  if (!dst || count <= 0) return;
+  ck(cudaMemcpyAsync(dst, dsrc, sizeof(T) * count, cudaMemcpyDefault, s), "copy out");
+}
+
+template <typename T>
+std::vector<T> to_host(const T* dsrc, int64_t count, cudaStream_t s) {
+  std::vector<T> v(static_cast<size_t>(count > 0 ? count : 0));
+  if (count > 0) {
+    ck(cudaMemcpyAsync(v.data(), dsrc, sizeof(T) * count, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "sync");
+  }
+  return v;
+}
+
+__global__ void set_diag_kernel(double* A, int64_t from, int64_t mp, double v) {
+  const int64_t i = from + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < mp) A[i * mp + i] = v;
+}
+
+__global__ void iota_kernel(int64_t* p, int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) p[i] = i;
+}
+
+__global__ void fill_i32_kernel(int32_t* p, int64_t n, int32_t v) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+__global__ void part_labels_kernel(const int64_t* order, const int64_t* bounds, int64_t p,
+                                   int32_t* part_of, int64_t n) {
+  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (q >= n) return;
+  int64_t t = 0;
+  while (t + 1 < p && bounds[t + 1] <= q) ++t;
+  part_of[order[q]] = static_cast<int32_t>(t);
+}
+
+unsigned blocks_for(int64_t n, int t = 256) { return static_cast<unsigned>((n + t - 1) / t); }
+
+// ---------------------------------------------------------------------------
+// padded single-part buffers
+// ---------------------------------------------------------------------------
+struct PartBuf {
+  int64_t m = 0, mp = 0, dp = 0;
+  double* Xp = nullptr;     // mp x dp
+  double* yp = nullptr;     // mp
+  double* norms = nullptr;  // mp
+  double* K = nullptr;      // mp x mp (full symmetric)
+  double* A = nullptr;      // mp x mp (factor)
+  double* Linv = nullptr;   // mp x 128
+  double* z = nullptr;
+  double* alpha = nullptr;
+  double* Ka = nullptr;
+  int* scratch = nullptr;   // trsv tickets/flags
+  CUtensorMap tmX, tmA, tmLinv;
+};
+
+void part_alloc(Scope& sc, PartBuf& pb, int64_t m, int64_t d, bool need_K) {
+  pb.m = m;
+  pb.mp = round_up(m, kNB);
+  pb.dp = round_up(d, 16);
+  pb.Xp = sc.alloc<double>(pb.mp * pb.dp);
+  pb.yp = sc.alloc<double>(pb.mp);
+  pb.norms = sc.alloc<double>(pb.mp);
+  if (need_K) pb.K = sc.alloc<double>(pb.mp * pb.mp);
+  pb.A = sc.alloc<double>(pb.mp * pb.mp);
+  pb.Linv = sc.alloc<double>(pb.mp * kNB);
+  pb.z = sc.alloc<double>(pb.mp);
+  pb.alpha = sc.alloc<double>(pb.mp);
+  pb.Ka = sc.alloc<double>(pb.mp);
+  pb.scratch = sc.alloc<int>(2 * (pb.mp / kNB) + 2);
+  if (!pk::make_tmap(&pb.tmX, pb.Xp, pb.mp, pb.dp, pb.dp) ||
+      !pk::make_tmap(&pb.tmA, pb.A, pb.mp, pb.mp, pb.mp) ||
+      !pk::make_tmap(&pb.tmLinv, pb.Linv, pb.mp, kNB, kNB))
+    fail(PKRRGPU_CUDA, "cuTensorMapEncodeTiled failed");
+}
+
+// Q rows (targets) padded to 64 for the cross-kernel tiles
+struct QueryBuf {
+  int64_t q = 0, qp = 0;
+  double* Xq = nullptr;
+  double* norms = nullptr;
+  double* cross = nullptr;  // qp x mp
+  double* pred = nullptr;   // qp
+  CUtensorMap tmQ;
+};
+
+void query_alloc(Scope& sc, QueryBuf& qb, int64_t q, int64_t dp, int64_t mp) {
+  qb.q = q;
+  qb.qp = round_up(q > 0 ? q : 1, 64);
+  qb.Xq = sc.alloc<double>(qb.qp * dp);
+  qb.norms = sc.alloc<double>(qb.qp);
+  qb.cross = sc.alloc<double>(qb.qp * mp);
+  qb.pred = sc.alloc<double>(qb.qp);
+  if (!pk::make_tmap(&qb.tmQ, qb.Xq, qb.qp, dp, dp)) fail(PKRRGPU_CUDA, "tensor map (Q)");
+}
+
+// ---------------------------------------------------------------------------
+// clustering drivers (clustering.cpp:53-180)
+// ---------------------------------------------------------------------------
+struct ClusterOut {
+  int32_t* label = nullptr;    // n
+  double* centers = nullptr;   // k x d
+  int64_t* sizes = nullptr;    // k (device)
+  int64_t* start = nullptr;    // k
+  int64_t* members = nullptr;  // n (row order within cluster)
+  int64_t* tmp = nullptr;      // grouping scratch
+  std::vector<int64_t> h_sizes, h_start;
+  int iterations = 0;
+};
+
+void group_labels(pkrrgpu_ctx* ctx, Scope& sc, const int32_t* label, int64_t n, int k,
+                  ClusterOut& co, cudaStream_t s) {
+  if (!co.sizes) {
+    co.sizes = sc.alloc<int64_t>(k);
+    co.start = sc.alloc<int64_t>(k);
+    co.members = sc.alloc<int64_t>(n);
+    co.tmp = sc.alloc<int64_t>(((n + 255) / 256) * k + 2 * k);
+  }
+  pk::launch_group(label, n, k, co.sizes, co.start, co.members, co.tmp, s, ctx->counter);
+}
+
+void kmeans_device(pkrrgpu_ctx* ctx, Scope& sc, const double* dX, int64_t n, int64_t d, int k,
+                   uint64_t seed, double threshold, int max_iters, const double* xnorm,
+                   ClusterOut& co) {
+  cudaStream_t s = ctx->main;
+  if (k < 1 || static_cast<int64_t>(k) > n) fail(PKRRGPU_INVALID, "kmeans: need 1 <= k <= n");
+  co.label = sc.alloc<int32_t>(n);
+  co.centers = sc.alloc<double>(static_cast<int64_t>(k) * d);
+  // init: k distinct samples, Rng(seed) + random_permutation (clustering.cpp:64-68)
+  HostRng rng(seed);
+  const std::vector<int64_t> perm = rng.permutation(n);
+  std::vector<int64_t> first(perm.begin(), perm.begin() + k);
+  int64_t* didx = sc.upload(first, s);
+  pk::launch_gather_rows(dX, d, didx, k, co.centers, k, d, s, ctx->counter);
+  fill_i32_kernel<<<blocks_for(n), 256, 0, s>>>(co.label, n, -1);
+  ++ctx->counter.launches;
+  double* best = sc.alloc<double>(n);
+  double* cnorm = sc.alloc<double>(k);
+  unsigned long long* changed = sc.alloc<unsigned long long>(2);
+  unsigned long long* far = sc.alloc<unsigned long long>(2);
+  std::vector<int64_t> sz(k);
+  int iter = 0;
+  for (; iter < max_iters; ++iter) {
+    pk::launch_row_norms(co.centers, k, d, d, cnorm, s, ctx->counter);
+    ck(cudaMemsetAsync(changed, 0, sizeof(unsigned long long), s), "memset");
+    pk::launch_assign(dX, n, d, xnorm, co.centers, cnorm, k, 0, nullptr, 0, co.label, best, changed, s,
+                      ctx->counter);
+    group_labels(ctx, sc, co.label, n, k, co, s);
+    sz = to_host(co.sizes, k, s);
+    unsigned long long ch = to_host(changed, 1, s)[0];
+    // empty-cluster reseed (clustering.cpp:98-117)
+    bool reseeded = false;
+    for (int j = 0; j < k; ++j) {
+      if (sz[j] != 0) continue;
+      ck(cudaMemcpyAsync(co.sizes, sz.data(), sizeof(int64_t) * k, cudaMemcpyHostToDevice, s), "H2D");
+      pk::launch_farthest(best, co.label, co.sizes, n, far, s, ctx->counter);
+      const std::vector<unsigned long long> f = to_host(far, 2, s);
+      const int64_t far_i = f[0] == 0 ? 0 : static_cast<int64_t>(f[1]);
+      int32_t old = to_host(co.label + far_i, 1, s)[0];
+      --sz[old];
+      const int32_t jj = j;
+      const double zero = 0.0;
+      ck(cudaMemcpyAsync(co.label + far_i, &jj, sizeof(int32_t), cudaMemcpyHostToDevice, s), "H2D");
+      ck(cudaMemcpyAsync(best + far_i, &zero, sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+      ck(cudaStreamSynchronize(s), "sync");
+      sz[j] = 1;
+      ++ch;
+      reseeded = true;
+    }
+    if (reseeded) group_labels(ctx, sc, co.label, n, k, co, s);
+    pk::launch_means(dX, d, co.members, co.start, co.sizes, k, co.centers, s, ctx->counter);
+    if (static_cast<double>(ch) / static_cast<double>(n) <= threshold) {
+      ++iter;
+      break;
+    }
+  }
+  co.iterations = iter;
+  co.h_sizes = to_host(co.sizes, k, s);
+  co.h_start = to_host(co.start, k, s);
+}
+
+void kbalance_device(pkrrgpu_ctx* ctx, Scope& sc, const double* dX, int64_t n, int64_t d, int k,
+                     uint64_t seed, double threshold, int max_iters, bool recompute,
+                     const double* xnorm, ClusterOut& co) {
+  if (k < 1 || static_cast<int64_t>(k) > n) fail(PKRRGPU_INVALID, "kbalance: need 1 <= k <= n");
+  kmeans_device(ctx, sc, dX, n, d, k, seed, threshold, max_iters, xnorm, co);
+  cudaStream_t s = ctx->main;
+  const int64_t base = n / k, extra = n % k;
+  // exact parallel replay of the sequential capacity scan (clustering.cpp:159-176):
+  // between two closure events every remaining sample's choice is the argmin over
+  // a fixed open set; the next event is the first position where some open
+  // cluster reaches its cap.  <= k+1 rounds.
+  fill_i32_kernel<<<blocks_for(n), 256, 0, s>>>(co.label, n, -1);
+  ++ctx->counter.launches;
+  double* cnorm = sc.alloc<double>(k);
+  pk::launch_row_norms(co.centers, k, d, d, cnorm, s, ctx->counter);
+  std::vector<int64_t> sizes(k, 0), thr(k);
+  std::vector<uint8_t> open(k, 1);
+  uint8_t* dopen = sc.alloc<uint8_t>(k);
+  int64_t* dthr = sc.alloc<int64_t>(k);
+  int64_t* dpos = sc.alloc<int64_t>(k);
+  int64_t* dhist = sc.alloc<int64_t>(k);
+  int64_t grown = 0, pos = 0;
+  while (pos < n) {
+    ck(cudaMemcpyAsync(dopen, open.data(), k, cudaMemcpyHostToDevice, s), "H2D");
+    pk::launch_assign(dX, n, d, xnorm, co.centers, cnorm, k, 1, dopen, pos, co.label, nullptr, nullptr,
+                      s, ctx->counter);
+    for (int j = 0; j < k; ++j)
+      thr[j] = open[j] ? (grown < extra ? base + 1 - sizes[j] : base - sizes[j]) : 0;
+    ck(cudaMemcpyAsync(dthr, thr.data(), sizeof(int64_t) * k, cudaMemcpyHostToDevice, s), "H2D");
+    pk::launch_events(co.label, pos, n, k, dthr, dpos, s, ctx->counter);
+    const std::vector<int64_t> ev = to_host(dpos, k, s);
+    int64_t e = INT64_MAX;
+    int jstar = -1;
+    for (int j = 0; j < k; ++j)
+      if (ev[j] < e) {
+        e = ev[j];
+        jstar = j;
+      }
+    const int64_t last = jstar < 0 ? n - 1 : e;
+    pk::launch_hist(co.label, pos, last, k, dhist, s, ctx->counter);
+    const std::vector<int64_t> h = to_host(dhist, k, s);
+    int64_t added = 0;
+    for (int j = 0; j < k; ++j) {
+      sizes[j] += h[j];
+      added += h[j];
+    }
+    if (added != last - pos + 1) fail(PKRRGPU_LOGIC, "kbalance: no open cluster");
+    if (jstar < 0) break;
+    if (grown < extra) {
+      ++grown;  // jstar grew to base + 1
+      open[jstar] = 0;
+      if (grown == extra)
+        for (int j = 0; j < k; ++j)
+          if (sizes[j] == base) open[j] = 0;
+    } else {
+      open[jstar] = 0;  // reached base with no growth slots left
+    }
+    pos = e + 1;
+  }
+  group_labels(ctx, sc, co.label, n, k, co, s);
+  if (recompute) pk::launch_means(dX, d, co.members, co.start, co.sizes, k, co.centers, s, ctx->counter);
+  co.h_sizes = to_host(co.sizes, k, s);
+  co.h_start = to_host(co.start, k, s);
+}
+
+// make_partition (strategies.cpp:64-102) on device.  Returns p_eff.
+struct PartitionOut {
+  int64_t p = 0;
+  int32_t* part_of = nullptr;   // n
+  int64_t* order = nullptr;     // n (rows part by part)
+  double* centers = nullptr;    // p x d or null
+  std::vector<int64_t> sizes, start;
+  int iterations = 0;
+};
+
+void make_partition_device(pkrrgpu_ctx* ctx, Scope& sc, int strategy, const double* dX, int64_t n,
+                           int64_t d, int64_t p, uint64_t seed, double thr, int max_iters,
+                           PartitionOut& po) {
+  cudaStream_t s = ctx->main;
+  const int pk_kind = partitioner_of(strategy);
+  if (pk_kind == 0) {
+    po.p = 1;
+    po.part_of = sc.zeros<int32_t>(n, s);
+    po.order = sc.alloc<int64_t>(n);
+    iota_kernel<<<blocks_for(n), 256, 0, s>>>(po.order, n);
+    ++ctx->counter.launches;
+    po.sizes = {n};
+    po.start = {0};
+    return;
+  }
+  if (p < 1 || p > n) fail(PKRRGPU_INVALID, "partition: need 1 <= p <= n");
+  po.p = p;
+  if (pk_kind == 1) {
+    HostRng rng(seed);
+    const std::vector<int64_t> perm = rng.permutation(n);
+    po.order = sc.upload(perm, s);
+    const int64_t base = n / p, extra = n % p;
+    std::vector<int64_t> bounds(p + 1, 0);
+    po.sizes.resize(p);
+    po.start.resize(p);
+    for (int64_t t = 0; t < p; ++t) {
+      po.sizes[t] = base + (t < extra ? 1 : 0);
+      po.start[t] = bounds[t];
+      bounds[t + 1] = bounds[t] + po.sizes[t];
+    }
+    int64_t* db = sc.upload(bounds, s);
+    po.part_of = sc.alloc<int32_t>(n);
+    part_labels_kernel<<<blocks_for(n), 256, 0, s>>>(po.order, db, p, po.part_of, n);
+    ++ctx->counter.launches;
+    return;
+  }
+  double* xnorm = sc.alloc<double>(n);
+  pk::launch_row_norms(dX, n, d, d, xnorm, s, ctx->counter);
+  ClusterOut co;
+  if (pk_kind == 2)
+    kmeans_device(ctx, sc, dX, n, d, static_cast<int>(p), seed, thr, max_iters, xnorm, co);
+  else
+    kbalance_device(ctx, sc, dX, n, d, static_cast<int>(p), seed, thr, max_iters, true, xnorm, co);
+  po.part_of = co.label;
+  po.order = co.members;
+  po.centers = co.centers;
+  po.sizes = co.h_sizes;
+  po.start = co.h_start;
+  po.iterations = co.iterations;
+}
+
+// nearest_center routing of q rows (clustering.cpp:182-195) + stable grouping
+struct RouteOut {
+  int32_t* route = nullptr;
+  int64_t* members = nullptr;
+  std::vector<int64_t> sizes, start;
+};
+
+void route_rows(pkrrgpu_ctx* ctx, Scope& sc, const double* dQ, int64_t q, int64_t d,
+                const double* centers, int k, RouteOut& ro) {
+  cudaStream_t s = ctx->main;
+  double* qn = sc.alloc<double>(q);
+  double* cn = sc.alloc<double>(k);
+  pk::launch_row_norms(dQ, q, d, d, qn, s, ctx->counter);
+  pk::launch_row_norms(centers, k, d, d, cn, s, ctx->counter);
+  ro.route = sc.alloc<int32_t>(q);
+  fill_i32_kernel<<<blocks_for(q), 256, 0, s>>>(ro.route, q, -1);
+  ++ctx->counter.launches;
+  pk::launch_assign(dQ, q, d, qn, centers, cn, k, 0, nullptr, 0, ro.route, nullptr, nullptr, s,
+                    ctx->counter);
+  ClusterOut co;
+  group_labels(ctx, sc, ro.route, q, k, co, s);
+  ro.members = co.members;
+  ro.sizes = to_host(co.sizes, k, s);
+  ro.start = to_host(co.start, k, s);
+}
+
+// ---------------------------------------------------------------------------
+// one part: gram -> assemble -> potrf -> solve -> residual (train_krr)
+// ---------------------------------------------------------------------------
+void part_load(pkrrgpu_ctx* ctx, PartBuf& pb, const double* dX, const double* dy, int64_t d,
+               const int64_t* rows, cudaStream_t s) {
+  pk::launch_gather_rows(dX, d, rows, pb.m, pb.Xp, pb.mp, pb.dp, s, ctx->counter);
+  pk::launch_gather_vec(dy, rows, pb.m, pb.yp, pb.mp, s, ctx->counter);
+  pk::launch_row_norms(pb.Xp, pb.mp, pb.dp, pb.dp, pb.norms, s, ctx->counter);
+}
+
+void part_solve(pkrrgpu_ctx* ctx, PartBuf& pb, double lambda, int* status, double* res_out,
+                cudaStream_t s) {
+  const double shift = lambda * static_cast<double>(pb.m);
+  pk::launch_assemble(pb.K, pb.A, pb.mp, shift, status, s, ctx->counter);
+  pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, status, s, ctx->counter);
+  pk::launch_trsv(pb.A, pb.Linv, pb.mp, pb.yp, pb.z, pb.alpha, pb.scratch, status, s, ctx->counter);
+  if (res_out) {
+    pk::launch_gemv_rows(pb.K, pb.mp, pb.m, pb.m, pb.alpha, pb.Ka, status, s, ctx->counter);
+    pk::launch_residual_finish(pb.Ka, pb.alpha, pb.yp, pb.m, shift, res_out, status, s, ctx->counter);
+  }
+}
+
+struct Timer {
+  cudaEvent_t a, b;
+  Timer() {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+  }
+  ~Timer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+double chol_flops(int64_t m) {
+  const double mu = static_cast<double>(m);
+  return mu * (mu + 1) * (2 * mu + 1) / 6.0;
+}
+
+int guard(pkrrgpu_ctx* ctx) {
+  if (!ctx) {
+    g_err = "null context";
+    return PKRRGPU_INVALID;
+  }
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  return 0;
+}
+
+}  // namespace
+
+#define API_BEGIN \
+  try {           \
+    if (int g_ = guard(ctx)) return g_;
+#define API_END                                      \
+  return PKRRGPU_OK;                                 \
+  }                                                  \
+  catch (const Fail& f) {                            \
+    return f.code;                                   \
+  }                                                  \
+  catch (const std::exception& e) {                  \
+    g_err = e.what();                                \
+    return PKRRGPU_CUDA;                             \
+  }
+
+extern "C" {
+
+const char* pkrrgpu_version(void) { return "pkrr-b200 0.1 (sm_100a, DMMA f64 + TMA)"; }
+const char* pkrrgpu_last_error(void) { return g_err.c_str(); }
+
+int pkrrgpu_create(int device, pkrrgpu_ctx** out) {
+  try {
+    if (!out) fail(PKRRGPU_INVALID, "null out");
+    int count = 0;
+    ck(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    if (device < 0 || device >= count) fail(PKRRGPU_INVALID, "no such CUDA device");
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, device), "props");
+    if (prop.major != 10) fail(PKRRGPU_CUDA, "pkrr-b200 needs an sm_100a (Blackwell) device");
+    auto* c = new pkrrgpu_ctx();
+    c->device = device;
+    ck(cudaStreamCreateWithFlags(&c->main, cudaStreamNonBlocking), "stream");
+    c->work.resize(8);
+    for (auto& s : c->work) ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    *out = c;
+    return PKRRGPU_OK;
+  } catch (const Fail& f) {
+    return f.code;
+  }
+}
+
+void pkrrgpu_destroy(pkrrgpu_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  ctx->trim();
+  for (auto& kv : ctx->live) cudaFree(kv.first);
+  for (auto s : ctx->work) cudaStreamDestroy(s);
+  cudaStreamDestroy(ctx->main);
+  delete ctx;
+}
+
+int64_t pkrrgpu_launch_count(const pkrrgpu_ctx* ctx) { return ctx ? ctx->counter.launches : 0; }
+
+int pkrrgpu_last_timings(const pkrrgpu_ctx* ctx, double* ms, int n) {
+  if (!ctx || !ms) return PKRRGPU_INVALID;
+  for (int i = 0; i < n && i < 8; ++i) ms[i] = ctx->timings[i];
+  return PKRRGPU_OK;
+}
+
+// ---- kernel -----------------------------------------------------------------
+int pkrrgpu_gram(pkrrgpu_ctx* ctx, const double* A, int64_t na, const double* B, int64_t nb,
+                 int64_t d, double sigma, double* K) {
+  API_BEGIN
+  if (!(sigma > 0.0)) fail(PKRRGPU_INVALID, "gaussian kernel needs sigma > 0");
+  if (na <= 0 || nb <= 0 || d <= 0) fail(PKRRGPU_INVALID, "gram: empty input");
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  const bool same = A == B && na == nb;
+  const double* dA = sc.in(A, na * d, s);
+  const double* dB = same ? dA : sc.in(B, nb * d, s);
+  PartBuf pb;
+  part_alloc(sc, pb, nb, d, true);
+  int64_t* idx = sc.alloc<int64_t>(nb);
+  iota_kernel<<<blocks_for(nb), 256, 0, s>>>(idx, nb);
+  ++ctx->counter.launches;
+  pk::launch_gather_rows(dB, d, idx, nb, pb.Xp, pb.mp, pb.dp, s, ctx->counter);
+  pk::launch_row_norms(pb.Xp, pb.mp, pb.dp, pb.dp, pb.norms, s, ctx->counter);
+  if (same) {
+    pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, nb, sigma, pb.K, pb.mp, nullptr, s, ctx->counter);
+    ck(cudaMemcpy2DAsync(K, sizeof(double) * nb, pb.K, sizeof(double) * pb.mp, sizeof(double) * nb, na,
+                         cudaMemcpyDefault, s),
+       "copy K");
+  } else {
+    QueryBuf qb;
+    query_alloc(sc, qb, na, pb.dp, pb.mp);
+    int64_t* qidx = sc.alloc<int64_t>(na);
+    iota_kernel<<<blocks_for(na), 256, 0, s>>>(qidx, na);
+    ++ctx->counter.launches;
+    pk::launch_gather_rows(dA, d, qidx, na, qb.Xq, qb.qp, pb.dp, s, ctx->counter);
+    pk::launch_row_norms(qb.Xq, qb.qp, pb.dp, pb.dp, qb.norms, s, ctx->counter);
+    pk::launch_gram_cross(qb.tmQ, pb.tmX, qb.norms, pb.norms, qb.qp, na, pb.mp, nb, pb.dp, sigma,
+                          qb.cross, s, ctx->counter);
+    ck(cudaMemcpy2DAsync(K, sizeof(double) * nb, qb.cross, sizeof(double) * pb.mp, sizeof(double) * nb,
+                         na, cudaMemcpyDefault, s),
+       "copy K");
+  }
+  ck(cudaStreamSynchronize(s), "sync");
+  API_END
+}
+
+int pkrrgpu_assemble(pkrrgpu_ctx* ctx, const double* K, int64_t m, double lambda, int64_t mult,
+                     double* A) {
+  API_BEGIN
+  if (!(lambda > 0.0)) fail(PKRRGPU_INVALID, "assemble_system: lambda must be > 0");
+  if (m <= 0) fail(PKRRGPU_INVALID, "assemble_system: empty matrix");
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  // pad to an even count of doubles for the vectorised kernel
+  const int64_t mp = round_up(m, 2);
+  double* Kp = sc.zeros<double>(mp * mp, s);
+  double* Ap = sc.alloc<double>(mp * mp);
+  ck(cudaMemcpy2DAsync(Kp, sizeof(double) * mp, K, sizeof(double) * m, sizeof(double) * m, m,
+                       cudaMemcpyDefault, s),
+     "copy");
+  pk::launch_assemble(Kp, Ap, mp, lambda * static_cast<double>(mult), nullptr, s, ctx->counter);
+  ck(cudaMemcpy2DAsync(A, sizeof(double) * m, Ap, sizeof(double) * mp, sizeof(double) * m, m,
+                       cudaMemcpyDefault, s),
+     "copy");
+  ck(cudaStreamSynchronize(s), "sync");
+  API_END
+}
+
+// ---- solver -------------------------------------------------------------------
+int pkrrgpu_cholesky(pkrrgpu_ctx* ctx, const double* A, int64_t m, double* L, int64_t* npd_pivot) {
+  API_BEGIN
+  if (m <= 0) fail(PKRRGPU_INVALID, "cholesky: empty matrix");
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  PartBuf pb;
+  part_alloc(sc, pb, m, 1, false);
+  ck(cudaMemsetAsync(pb.A, 0, sizeof(double) * pb.mp * pb.mp, s), "memset");
+  ck(cudaMemcpy2DAsync(pb.A, sizeof(double) * pb.mp, A, sizeof(double) * m, sizeof(double) * m, m,
+                       cudaMemcpyDefault, s),
+     "copy A");
+  if (pb.mp > m) {
+    set_diag_kernel<<<blocks_for(pb.mp - m), 256, 0, s>>>(pb.A, m, pb.mp, 1.0);
+    ++ctx->counter.launches;
+  }
+  int* status = sc.zeros<int>(2, s);
+  pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, m, status, s, ctx->counter);
+  std::vector<int> st = to_host(status, 2, s);
+  if (st[0]) {
+    if (npd_pivot) *npd_pivot = st[1];
+    fail(PKRRGPU_NPD, "matrix not positive definite: pivot " + std::to_string(st[1]));
+  }
+  pk::launch_zero_upper(pb.A, pb.mp, s, ctx->counter);
+  ck(cudaMemcpy2DAsync(L, sizeof(double) * m, pb.A, sizeof(double) * pb.mp, sizeof(double) * m, m,
+                       cudaMemcpyDefault, s),
+     "copy L");
+  ck(cudaStreamSynchronize(s), "sync");
+  API_END
+}
+
+int pkrrgpu_solve_spd(pkrrgpu_ctx* ctx, const double* L, int64_t m, const double* b, double* x) {
+  API_BEGIN
+  if (m <= 0) fail(PKRRGPU_INVALID, "solve_spd: size mismatch");
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  PartBuf pb;
+  part_alloc(sc, pb, m, 1, false);
+  ck(cudaMemsetAsync(pb.A, 0, sizeof(double) * pb.mp * pb.mp, s), "memset");
+  ck(cudaMemcpy2DAsync(pb.A, sizeof(double) * pb.mp, L, sizeof(double) * m, sizeof(double) * m, m,
+                       cudaMemcpyDefault, s),
+     "copy L");
+  if (pb.mp > m) {
+    set_diag_kernel<<<blocks_for(pb.mp - m), 256, 0, s>>>(pb.A, m, pb.mp, 1.0);
+    ++ctx->counter.launches;
+  }
+  ck(cudaMemsetAsync(pb.yp, 0, sizeof(double) * pb.mp, s), "memset");
+  ck(cudaMemcpyAsync(pb.yp, b, sizeof(double) * m, cudaMemcpyDefault, s), "copy b");
+  pk::launch_diag_inverses(pb.A, pb.mp, pb.Linv, s, ctx->counter);
+  pk::launch_trsv(pb.A, pb.Linv, pb.mp, pb.yp, pb.z, pb.alpha, pb.scratch, nullptr, s, ctx->counter);
+  copy_out(x, pb.alpha, m, s);
+  ck(cudaStreamSynchronize(s), "sync");
+  API_END
+}
+
+int pkrrgpu_train_krr(pkrrgpu_ctx* ctx, const double* X, const double* y, int64_t m, int64_t d,
+                      double sigma, double lambda, double* alpha, double* residual,
+                      int64_t* npd_pivot) {
+  API_BEGIN
+  if (m <= 0) fail(PKRRGPU_INVALID, "train_krr: empty dataset");
+  if (!(lambda > 0.0)) fail(PKRRGPU_INVALID, "train_krr: lambda must be > 0");
+  if (!(sigma > 0.0)) fail(PKRRGPU_INVALID, "gaussian kernel needs sigma > 0");
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  const double* dX = sc.in(X, m * d, s);
+  const double* dy = sc.in(y, m, s);
+  PartBuf pb;
+  part_alloc(sc, pb, m, d, true);
+  int64_t* idx = sc.alloc<int64_t>(m);
+  iota_kernel<<<blocks_for(m), 256, 0, s>>>(idx, m);
+  ++ctx->counter.launches;
+  part_load(ctx, pb, dX, dy, d, idx, s);
+  pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, m, sigma, pb.K, pb.mp, nullptr, s, ctx->counter);
+  int* status = sc.zeros<int>(2, s);
+  double* res = sc.zeros<double>(2, s);
+  part_solve(ctx, pb, lambda, status, res, s);
+  std::vector<int> st = to_host(status, 2, s);
+  if (st[0]) {
+    if (npd_pivot) *npd_pivot = st[1];
+    fail(PKRRGPU_NPD, "matrix not positive definite: pivot " + std::to_string(st[1]));
+  }
+  copy_out(alpha, pb.alpha, m, s);
+  if (residual) *residual = to_host(res, 2, s)[1];  // solver.cpp:119 form
+  ck(cudaStreamSynchronize(s), "sync");
+  API_END
+}
+
+int pkrrgpu_predict(pkrrgpu_ctx* ctx, const double* S, const double* alpha, int64_t m, int64_t d,
+                    double sigma, const double* Q, int64_t q, double* out) {
+  API_BEGIN
+  if (m <= 0 || q <= 0) fail(PKRRGPU_INVALID, "predict: empty input");
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  const double* dS = sc.in(S, m * d, s);
+  const double* dQ = sc.in(Q, q * d, s);
+  PartBuf pb;
+  pb.m = m;
+  pb.mp = round_up(m, kNB);
+  pb.dp = round_up(d, 16);
+  pb.Xp = sc.alloc<double>(pb.mp * pb.dp);
+  pb.norms = sc.alloc<double>(pb.mp);
+  pb.alpha = sc.zeros<double>(pb.mp, s);
+  if (!pk::make_tmap(&pb.tmX, pb.Xp, pb.mp, pb.dp, pb.dp)) fail(PKRRGPU_CUDA, "tensor map");
+  ck(cudaMemcpyAsync(pb.alpha, alpha, sizeof(double) * m, cudaMemcpyDefault, s), "copy alpha");
+  int64_t* idx = sc.alloc<int64_t>(std::max(m, q));
+  iota_kernel<<<blocks_for(std::max(m, q)), 256, 0, s>>>(idx, std::max(m, q));
+  ++ctx->counter.launches;
+  pk::launch_gather_rows(dS, d, idx, m, pb.Xp, pb.mp, pb.dp, s, ctx->counter);
+  pk::launch_row_norms(pb.Xp, pb.mp, pb.dp, pb.dp, pb.norms, s, ctx->counter);
+  QueryBuf qb;
+  query_alloc(sc, qb, q, pb.dp, pb.mp);
+  pk::launch_gather_rows(dQ, d, idx, q, qb.Xq, qb.qp, pb.dp, s, ctx->counter);
+  pk::launch_row_norms(qb.Xq, qb.qp, pb.dp, pb.dp, qb.norms, s, ctx->counter);
+  pk::launch_gram_cross(qb.tmQ, pb.tmX, qb.norms, pb.norms, qb.qp, q, pb.mp, m, pb.dp, sigma, qb.cross,
+                        s, ctx->counter);
+  pk::launch_gemv_rows(qb.cross, pb.mp, q, m, pb.alpha, qb.pred, nullptr, s, ctx->counter);
+  copy_out(out, qb.pred, q, s);
+  ck(cudaStreamSynchronize(s), "sync");
+  API_END
+}
+
+// ---- clustering -------------------------------------------------------------
+int pkrrgpu_kmeans(pkrrgpu_ctx* ctx, const double* X, int64_t n, int64_t d, int k, uint64_t seed,
+                   double threshold, int max_iters, int32_t* membership, double* centers,
+                   int64_t* sizes, int* iterations) {
+  API_BEGIN
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  const double* dX = sc.in(X, n * d, s);
+  double* xnorm = sc.alloc<double>(n);
+  pk::launch_row_norms(dX, n, d, d, xnorm, s, ctx->counter);
+  ClusterOut co;
+  kmeans_device(ctx, sc, dX, n, d, k, seed, threshold, max_iters, xnorm, co);
+  copy_out(membership, co.label, n, s);
+  copy_out(centers, co.centers, static_cast<int64_t>(k) * d, s);
+  if (sizes) std::memcpy(sizes, co.h_sizes.data(), sizeof(int64_t) * k);
+  if (iterations) *iterations = co.iterations;
+  ck(cudaStreamSynchronize(s), "sync");
+  API_END
+}
+
+int pkrrgpu_kbalance(pkrrgpu_ctx* ctx, const double* X, int64_t n, int64_t d, int k, uint64_t seed,
+                     double threshold, int max_iters, int recompute, int32_t* membership,
+                     double* centers, int64_t* sizes) {
+  API_BEGIN
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  const double* dX = sc.in(X, n * d, s);
+  double* xnorm = sc.alloc<double>(n);
+  pk::launch_row_norms(dX, n, d, d, xnorm, s, ctx->counter);
+  ClusterOut co;
+  kbalance_device(ctx, sc, dX, n, d, k, seed, threshold, max_iters, recompute != 0, xnorm, co);
+  copy_out(membership, co.label, n, s);
+  copy_out(centers, co.centers, static_cast<int64_t>(k) * d, s);
+  if (sizes) std::memcpy(sizes, co.h_sizes.data(), sizeof(int64_t) * k);
+  ck(cudaStreamSynchronize(s), "sync");
+  API_END
+}
+
+int pkrrgpu_nearest_center(pkrrgpu_ctx* ctx, const double* centers, int k, int64_t d,
+                           const double* Q, int64_t q, int32_t* out) {
+  API_BEGIN
+  if (k < 1) fail(PKRRGPU_INVALID, "nearest_center: no centers");
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  const double* dC = sc.in(centers, static_cast<int64_t>(k) * d, s);
+  const double* dQ = sc.in(Q, q * d, s);
+  RouteOut ro;
+  route_rows(ctx, sc, dQ, q, d, dC, k, ro);
+  copy_out(out, ro.route, q, s);
+  ck(cudaStreamSynchronize(s), "sync");
+  API_END
+}
+
+// ---- strategies ---------------------------------------------------------------
+int pkrrgpu_make_partition(pkrrgpu_ctx* ctx, int strategy, const double* X, int64_t n, int64_t d,
+                           int64_t p, uint64_t seed, int32_t* part_of, int64_t* order,
+                           double* centers, int64_t* p_out) {
+  API_BEGIN
+  if (strategy < 0 || strategy > 7) fail(PKRRGPU_INVALID, "unknown strategy");
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  const double* dX = sc.in(X, n * d, s);
+  PartitionOut po;
+  make_partition_device(ctx, sc, strategy, dX, n, d, p, seed, 0.01, 100, po);
+  copy_out(part_of, po.part_of, n, s);
+  copy_out(order, po.order, n, s);
+  if (centers && po.centers) copy_out(centers, po.centers, po.p * d, s);
+  if (p_out) *p_out = po.p;
+  ck(cudaStreamSynchronize(s), "sync");
+  API_END
+}
+
+}  // extern "C"
+
+// ---- trained models (TrainedPartitions) ---------------------------------------
+struct pkrrgpu_models {
+  pkrrgpu_ctx* ctx = nullptr;
+  int64_t p = 0, d = 0, dp = 0;
+  double sigma = 1.0;
+  std::vector<int64_t> m, mp;
+  std::vector<double*> Xp, norms, alpha;
+  std::vector<CUtensorMap> tmX;
+  std::vector<double> residual;
+  double* centers = nullptr;  // p x d (null for whole/random partitions)
+  int predictor = 2;
+};
+
+extern "C" {
+
+int pkrrgpu_train_partitions(pkrrgpu_ctx* ctx, int strategy, const double* X, const double* y,
+                             int64_t n, int64_t d, int64_t p, uint64_t seed, double sigma,
+                             double lambda, pkrrgpu_models** out, int64_t* failed_part,
+                             int64_t* npd_pivot) {
+  API_BEGIN
+  if (!out) fail(PKRRGPU_INVALID, "null out");
+  if (!(lambda > 0.0)) fail(PKRRGPU_INVALID, "train_krr: lambda must be > 0");
+  if (!(sigma > 0.0)) fail(PKRRGPU_INVALID, "gaussian kernel needs sigma > 0");
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  const double* dX = sc.in(X, n * d, s);
+  const double* dy = sc.in(y, n, s);
+  PartitionOut po;
+  make_partition_device(ctx, sc, strategy, dX, n, d, p, seed, 0.01, 100, po);
+  for (int64_t t = 0; t < po.p; ++t)
+    if (po.sizes[t] == 0) fail(PKRRGPU_INVALID, "train_partitions: empty part");
+  auto* mod = new pkrrgpu_models();
+  mod->ctx = ctx;
+  mod->p = po.p;
+  mod->d = d;
+  mod->dp = round_up(d, 16);
+  mod->sigma = sigma;
+  mod->predictor = predictor_of(strategy);
+  std::vector<PartBuf> parts(po.p);
+  int* status = sc.zeros<int>(2 * po.p, s);
+  double* res = sc.zeros<double>(2 * po.p, s);
+  ck(cudaStreamSynchronize(s), "sync");
+  std::vector<cudaEvent_t> done;
+  for (int64_t t = 0; t < po.p; ++t) {
+    cudaStream_t ws = ctx->work[t % ctx->work.size()];
+    PartBuf& pb = parts[t];
+    part_alloc(sc, pb, po.sizes[t], d, true);
+    part_load(ctx, pb, dX, dy, d, po.order + po.start[t], ws);
+    pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws,
+                        ctx->counter);
+    part_solve(ctx, pb, lambda, status + 2 * t, res + 2 * t, ws);
+  }
+  ck(cudaDeviceSynchronize(), "train");
+  std::vector<int> st = to_host(status, 2 * po.p, s);
+  std::vector<double> rh = to_host(res, 2 * po.p, s);
+  for (int64_t t = 0; t < po.p; ++t)
+    if (st[2 * t]) {
+      if (failed_part) *failed_part = t;
+      if (npd_pivot) *npd_pivot = st[2 * t + 1];
+      delete mod;
+      fail(PKRRGPU_NPD, "partition " + std::to_string(t) + ": matrix not positive definite: pivot " +
+                            std::to_string(st[2 * t + 1]));
+    }
+  // keep support rows, norms, alpha (KrrModel, solver.hpp:37-49)
+  for (int64_t t = 0; t < po.p; ++t) {
+    PartBuf& pb = parts[t];
+    mod->m.push_back(pb.m);
+    mod->mp.push_back(pb.mp);
+    double* x = static_cast<double*>(ctx->alloc(sizeof(double) * pb.mp * pb.dp));
+    double* nm = static_cast<double*>(ctx->alloc(sizeof(double) * pb.mp));
+    double* al = static_cast<double*>(ctx->alloc(sizeof(double) * pb.mp));
+    ck(cudaMemcpyAsync(x, pb.Xp, sizeof(double) * pb.mp * pb.dp, cudaMemcpyDeviceToDevice, s), "copy");
+    ck(cudaMemcpyAsync(nm, pb.norms, sizeof(double) * pb.mp, cudaMemcpyDeviceToDevice, s), "copy");
+    ck(cudaMemcpyAsync(al, pb.alpha, sizeof(double) * pb.mp, cudaMemcpyDeviceToDevice, s), "copy");
+    mod->Xp.push_back(x);
+    mod->norms.push_back(nm);
+    mod->alpha.push_back(al);
+    CUtensorMap tm;
+    if (!pk::make_tmap(&tm, x, pb.mp, pb.dp, pb.dp)) fail(PKRRGPU_CUDA, "tensor map");
+    mod->tmX.push_back(tm);
+    mod->residual.push_back(rh[2 * t + 1]);
+  }
+  if (po.centers) {
+    mod->centers = static_cast<double*>(ctx->alloc(sizeof(double) * po.p * d));
+    ck(cudaMemcpyAsync(mod->centers, po.centers, sizeof(double) * po.p * d, cudaMemcpyDeviceToDevice, s),
+       "copy");
+  }
+  ck(cudaStreamSynchronize(s), "sync");
+  *out = mod;
+  API_END
+}
+
+int64_t pkrrgpu_models_count(const pkrrgpu_models* m) { return m ? m->p : 0; }
+int64_t pkrrgpu_models_size(const pkrrgpu_models* m, int64_t t) {
+  return (m && t >= 0 && t < m->p) ? m->m[t] : -1;
+}
+int pkrrgpu_models_alpha(const pkrrgpu_models* m, int64_t t, double* alpha) {
+  if (!m || t < 0 || t >= m->p || !alpha) return PKRRGPU_INVALID;
+  cudaSetDevice(m->ctx->device);
+  return cudaMemcpy(alpha, m->alpha[t], sizeof(double) * m->m[t], cudaMemcpyDefault) == cudaSuccess
+             ? PKRRGPU_OK
+             : PKRRGPU_CUDA;
+}
+int pkrrgpu_models_residual(const pkrrgpu_models* m, int64_t t, double* r) {
+  if (!m || t < 0 || t >= m->p || !r) return PKRRGPU_INVALID;
+  *r = m->residual[t];
+  return PKRRGPU_OK;
+}
+void pkrrgpu_models_free(pkrrgpu_models* m) {
+  if (!m) return;
+  cudaSetDevice(m->ctx->device);
+  cudaDeviceSynchronize();
+  for (auto* p : m->Xp) m->ctx->release(p);
+  for (auto* p : m->norms) m->ctx->release(p);
+  for (auto* p : m->alpha) m->ctx->release(p);
+  if (m->centers) m->ctx->release(m->centers);
+  delete m;
+}
+
+int pkrrgpu_predict_nearest(pkrrgpu_ctx* ctx, const pkrrgpu_models* models, const double* Q,
+                            int64_t q, double* out) {
+  API_BEGIN
+  if (!models || models->p < 1) fail(PKRRGPU_INVALID, "predict_nearest: no models");
+  if (!models->centers)
+    fail(PKRRGPU_INVALID, "predict_nearest: centers undefined for this partitioning");
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  const int64_t d = models->d, dp = models->dp;
+  const double* dQ = sc.in(Q, q * d, s);
+  RouteOut ro;
+  route_rows(ctx, sc, dQ, q, d, models->centers, static_cast<int>(models->p), ro);
+  double* pred_all = sc.alloc<double>(q);
+  double* ydummy = sc.zeros<double>(q, s);
+  double* sse = sc.alloc<double>(models->p);
+  ck(cudaStreamSynchronize(s), "sync");
+  for (int64_t t = 0; t < models->p; ++t) {
+    const int64_t cnt = ro.sizes[t];
+    if (cnt == 0) continue;
+    cudaStream_t ws = ctx->work[t % ctx->work.size()];
+    QueryBuf qb;
+    query_alloc(sc, qb, cnt, dp, models->mp[t]);
+    const int64_t* rows = ro.members + ro.start[t];
+    pk::launch_gather_rows(dQ, d, rows, cnt, qb.Xq, qb.qp, dp, ws, ctx->counter);
+    pk::launch_row_norms(qb.Xq, qb.qp, dp, dp, qb.norms, ws, ctx->counter);
+    pk::launch_gram_cross(qb.tmQ, models->tmX[t], qb.norms, models->norms[t], qb.qp, cnt,
+                          models->mp[t], models->m[t], dp, models->sigma, qb.cross, ws, ctx->counter);
+    pk::launch_gemv_rows(qb.cross, models->mp[t], cnt, models->m[t], models->alpha[t], qb.pred, nullptr,
+                         ws, ctx->counter);
+    pk::launch_sse_scatter(qb.pred, rows, cnt, ydummy, pred_all, sse + t, nullptr, ws, ctx->counter);
+  }
+  ck(cudaDeviceSynchronize(), "predict");
+  copy_out(out, pred_all, q, s);
+  ck(cudaStreamSynchronize(s), "sync");
+  API_END
+}
+
+// ---- grid search (strategies.cpp:343-507) -----------------------------------
+int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu_grid_out* o) {
+  API_BEGIN
+  if (!a || !o) fail(PKRRGPU_INVALID, "null args");
+  if (a->n_lambdas <= 0 || a->n_sigmas <= 0) fail(PKRRGPU_INVALID, "grid_search: empty grid");
+  if (a->n <= 0 || a->t <= 0) fail(PKRRGPU_INVALID, "grid_search: empty dataset");
+  if (a->strategy < 0 || a->strategy > 7) fail(PKRRGPU_INVALID, "unknown strategy");
+  for (int64_t i = 0; i < a->n_lambdas; ++i)
+    if (!(a->lambdas[i] > 0.0)) fail(PKRRGPU_INVALID, "assemble_system: lambda must be > 0");
+  for (int64_t i = 0; i < a->n_sigmas; ++i)
+    if (!(a->sigmas[i] > 0.0)) fail(PKRRGPU_INVALID, "gaussian kernel needs sigma > 0");
+  const int world = a->world > 0 ? a->world : 1, rank = a->rank;
+  const int64_t n = a->n, d = a->d, t = a->t, te = (a->X_eval && a->t_eval > 0) ? a->t_eval : 0;
+  const int64_t nl = a->n_lambdas, ns = a->n_sigmas, ncell = nl * ns;
+  const int predictor = predictor_of(a->strategy);
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  Timer t_all, t_part;
+  ck(cudaEventRecord(t_all.a, s), "event");
+
+  const double* dX = sc.in(a->X_train, n * d, s);
+  const double* dy = sc.in(a->y_train, n, s);
+  const double* dXt = sc.in(a->X_test, t * d, s);
+  const double* dyt = sc.in(a->y_test, t, s);
+  const double* dXe = te ? sc.in(a->X_eval, te * d, s) : nullptr;
+  const double* dye = te ? sc.in(a->y_eval, te, s) : nullptr;
+
+  // ---- partition (once; sigma independent) ----
+  ck(cudaEventRecord(t_part.a, s), "event");
+  PartitionOut po;
+  const double thr = a->km_max_iters > 0 ? a->km_threshold : 0.01;
+  const int iters = a->km_max_iters > 0 ? a->km_max_iters : 100;
+  make_partition_device(ctx, sc, a->strategy, dX, n, d, a->p, a->seed, thr, iters, po);
+  const int64_t p = po.p;
+  for (int64_t q = 0; q < p; ++q)
+    if (po.sizes[q] == 0) fail(PKRRGPU_INVALID, "train_partitions: empty part");
+  // ---- targets (strategies.cpp:370-381) ----
+  RouteOut rt, re;
+  int64_t* iota_t = nullptr;
+  int64_t* iota_e = nullptr;
+  if (predictor == 2) {
+    if (!po.centers) fail(PKRRGPU_INVALID, "grid_search: nearest predictor needs centers");
+    route_rows(ctx, sc, dXt, t, d, po.centers, static_cast<int>(p), rt);
+    if (te) route_rows(ctx, sc, dXe, te, d, po.centers, static_cast<int>(p), re);
+  } else {
+    iota_t = sc.alloc<int64_t>(t);
+    iota_kernel<<<blocks_for(t), 256, 0, s>>>(iota_t, t);
+    ++ctx->counter.launches;
+    if (te) {
+      iota_e = sc.alloc<int64_t>(te);
+      iota_kernel<<<blocks_for(te), 256, 0, s>>>(iota_e, te);
+      ++ctx->counter.launches;
+    }
+  }
+  ck(cudaEventRecord(t_part.b, s), "event");
+
+  // ---- per-part buffers for the parts this rank owns ----
+  std::vector<int64_t> owned;
+  for (int64_t q = 0; q < p; ++q)
+    if (q % world == rank) owned.push_back(q);
+  const int64_t dp = round_up(d, 16);
+  std::vector<PartBuf> parts(p);
+  std::vector<QueryBuf> qt(p), qe(p);
+  std::vector<int64_t> tcount(p), ecount(p);
+  std::vector<const int64_t*> tpos(p), epos(p);
+  for (int64_t q = 0; q < p; ++q) {
+    tcount[q] = predictor == 2 ? rt.sizes[q] : t;
+    tpos[q] = predictor == 2 ? rt.members + rt.start[q] : iota_t;
+    ecount[q] = te ? (predictor == 2 ? re.sizes[q] : te) : 0;
+    epos[q] = te ? (predictor == 2 ? re.members + re.start[q] : iota_e) : nullptr;
+  }
+  // per (cell, part) result slots: [status0, status1] ints; [res_grid, res_train, sse, esse] doubles
+  int* dstatus = sc.zeros<int>(ncell * p * 2, s);
+  double* dres = sc.zeros<double>(ncell * p * 4, s);
+  // per-cell predictions in test order (nearest/whole) or per-part (average/oracle)
+  const int64_t pp_parts = predictor == 2 || predictor == 0 ? 1 : p;
+  double* pred_t = sc.zeros<double>(ncell * pp_parts * t, s);
+  double* pred_e = te ? sc.zeros<double>(ncell * pp_parts * te, s) : nullptr;
+  ck(cudaStreamSynchronize(s), "sync");
+
+  double f_chol = 0, f_gram = 0, f_other = 0;
+  const size_t S = ctx->work.size();
+  for (int64_t q : owned) {
+    PartBuf& pb = parts[q];
+    part_alloc(sc, pb, po.sizes[q], d, true);
+    cudaStream_t ws = ctx->work[q % S];
+    part_load(ctx, pb, dX, dy, d, po.order + po.start[q], ws);
+    query_alloc(sc, qt[q], tcount[q], pb.dp, pb.mp);
+    if (tcount[q] > 0) {
+      pk::launch_gather_rows(dXt, d, tpos[q], tcount[q], qt[q].Xq, qt[q].qp, pb.dp, ws, ctx->counter);
+      pk::launch_row_norms(qt[q].Xq, qt[q].qp, pb.dp, pb.dp, qt[q].norms, ws, ctx->counter);
+    }
+    if (te) {
+      query_alloc(sc, qe[q], ecount[q], pb.dp, pb.mp);
+      if (ecount[q] > 0) {
+        pk::launch_gather_rows(dXe, d, epos[q], ecount[q], qe[q].Xq, qe[q].qp, pb.dp, ws, ctx->counter);
+        pk::launch_row_norms(qe[q].Xq, qe[q].qp, pb.dp, pb.dp, qe[q].norms, ws, ctx->counter);
+      }
+    }
+  }
+  // phase events (joins on the main stream) for the per-phase device timings
+  std::vector<cudaEvent_t> evs;
+  auto join = [&]() {
+    cudaEvent_t e;
+    for (int64_t q : owned) {
+      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      ck(cudaEventRecord(e, ctx->work[q % S]), "event");
+      ck(cudaStreamWaitEvent(s, e, 0), "wait");
+      evs.push_back(e);
+    }
+    ck(cudaEventCreate(&e), "event");
+    ck(cudaEventRecord(e, s), "event");
+    evs.push_back(e);
+    return e;
+  };
+  auto fork = [&]() {
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    ck(cudaEventRecord(e, s), "event");
+    evs.push_back(e);
+    for (int64_t q : owned) ck(cudaStreamWaitEvent(ctx->work[q % S], e, 0), "wait");
+  };
+  double ms_gram = 0, ms_chol = 0, ms_pred = 0;
+  cudaEvent_t e0 = join();
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gram_w, chol_w, pred_w;
+  for (int64_t si = 0; si < ns; ++si) {
+    const double sigma = a->sigmas[si];
+    fork();
+    for (int64_t q : owned) {
+      PartBuf& pb = parts[q];
+      cudaStream_t ws = ctx->work[q % S];
+      pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws,
+                          ctx->counter);
+      if (tcount[q] > 0)
+        pk::launch_gram_cross(qt[q].tmQ, pb.tmX, qt[q].norms, pb.norms, qt[q].qp, tcount[q], pb.mp, pb.m,
+                              pb.dp, sigma, qt[q].cross, ws, ctx->counter);
+      if (te && ecount[q] > 0)
+        pk::launch_gram_cross(qe[q].tmQ, pb.tmX, qe[q].norms, pb.norms, qe[q].qp, ecount[q], pb.mp, pb.m,
+                              pb.dp, sigma, qe[q].cross, ws, ctx->counter);
+      const double m = static_cast<double>(pb.m);
+      f_gram += static_cast<double>(d) * m * (m + 1) + 2.0 * (tcount[q] + ecount[q]) * m * d;
+    }
+    cudaEvent_t e1 = join();
+    gram_w.push_back({e0, e1});
+    for (int64_t li = 0; li < nl; ++li) {
+      const int64_t cell = li * ns + si;
+      const double lambda = a->lambdas[li];
+      fork();
+      for (int64_t q : owned) {
+        PartBuf& pb = parts[q];
+        cudaStream_t ws = ctx->work[q % S];
+        int* st = dstatus + (cell * p + q) * 2;
+        pk::launch_assemble(pb.K, pb.A, pb.mp, lambda * static_cast<double>(pb.m), st, ws, ctx->counter);
+        pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, st, ws, ctx->counter);
+        f_chol += chol_flops(pb.m);
+      }
+      cudaEvent_t e2 = join();
+      chol_w.push_back({e1, e2});
+      fork();
+      for (int64_t q : owned) {
+        PartBuf& pb = parts[q];
+        cudaStream_t ws = ctx->work[q % S];
+        int* st = dstatus + (cell * p + q) * 2;
+        double* rs = dres + (cell * p + q) * 4;
+        const double shift = lambda * static_cast<double>(pb.m);
+        pk::launch_trsv(pb.A, pb.Linv, pb.mp, pb.yp, pb.z, pb.alpha, pb.scratch, st, ws, ctx->counter);
+        pk::launch_gemv_rows(pb.K, pb.mp, pb.m, pb.m, pb.alpha, pb.Ka, st, ws, ctx->counter);
+        pk::launch_residual_finish(pb.Ka, pb.alpha, pb.yp, pb.m, shift, rs, st, ws, ctx->counter);
+        const double m = static_cast<double>(pb.m);
+        f_other += 4.0 * m * m;
+        if (tcount[q] > 0) {
+          pk::launch_gemv_rows(qt[q].cross, pb.mp, tcount[q], pb.m, pb.alpha, qt[q].pred, st, ws,
+                               ctx->counter);
+          double* dst = pred_t + (cell * pp_parts + (pp_parts > 1 ? q : 0)) * t;
+          pk::launch_sse_scatter(qt[q].pred, tpos[q], tcount[q], dyt, dst, rs + 2, st, ws, ctx->counter);
+          f_other += 2.0 * tcount[q] * m;
+        }
+        if (te && ecount[q] > 0) {
+          pk::launch_gemv_rows(qe[q].cross, pb.mp, ecount[q], pb.m, pb.alpha, qe[q].pred, st, ws,
+                               ctx->counter);
+          double* dst = pred_e + (cell * pp_parts + (pp_parts > 1 ? q : 0)) * te;
+          pk::launch_sse_scatter(qe[q].pred, epos[q], ecount[q], dye, dst, rs + 3, st, ws, ctx->counter);
+          f_other += 2.0 * ecount[q] * m;
+        }
+      }
+      cudaEvent_t e3 = join();
+      pred_w.push_back({e2, e3});
+      e1 = e3;
+    }
+    e0 = e1;
+  }
+  // combine for average/oracle predictors (world == 1)
+  double* dmse = sc.zeros<double>(2 * ncell, s);
+  double* comb_t = sc.alloc<double>(t);
+  double* comb_e = te ? sc.alloc<double>(te) : nullptr;
+  ck(cudaEventRecord(t_all.b, s), "event");
+  ck(cudaDeviceSynchronize(), "grid");
+
+  for (auto& w : gram_w) {
+    float ms;
+    cudaEventElapsedTime(&ms, w.first, w.second);
+    ms_gram += ms;
+  }
+  for (auto& w : chol_w) {
+    float ms;
+    cudaEventElapsedTime(&ms, w.first, w.second);
+    ms_chol += ms;
+  }
+  for (auto& w : pred_w) {
+    float ms;
+    cudaEventElapsedTime(&ms, w.first, w.second);
+    ms_pred += ms;
+  }
+  {
+    float ms_part = 0, ms_all = 0;
+    cudaEventElapsedTime(&ms_part, t_part.a, t_part.b);
+    cudaEventElapsedTime(&ms_all, t_all.a, t_all.b);
+    ctx->timings[0] = ms_part;
+    ctx->timings[1] = ms_gram + ms_chol + ms_pred;
+    ctx->timings[2] = ms_pred;
+    ctx->timings[3] = ms_all;
+    ctx->timings[4] = ms_chol;
+    ctx->timings[5] = ms_gram;
+  }
+  for (auto e : evs) cudaEventDestroy(e);
+
+  const std::vector<int> st = to_host(dstatus, ncell * p * 2, s);
+  const std::vector<double> rs = to_host(dres, ncell * p * 4, s);
+  std::vector<uint8_t> pfail(ncell * p, 0);
+  for (int64_t c = 0; c < ncell; ++c)
+    for (int64_t q : owned) pfail[c * p + q] = st[(c * p + q) * 2] ? 1 : 0;
+  if (o->part_failed) std::memcpy(o->part_failed, pfail.data(), ncell * p);
+  for (int64_t c = 0; c < ncell; ++c)
+    for (int64_t q = 0; q < p; ++q) {
+      const bool mine = (q % world) == rank;
+      if (o->part_sse) o->part_sse[c * p + q] = mine ? rs[(c * p + q) * 4 + 2] : 0.0;
+      if (o->part_eval_sse) o->part_eval_sse[c * p + q] = mine ? rs[(c * p + q) * 4 + 3] : 0.0;
+      if (o->part_residual) o->part_residual[c * p + q] = mine ? rs[(c * p + q) * 4 + 0] : 0.0;
+    }
+  if (o->part_test_count)
+    for (int64_t q = 0; q < p; ++q) o->part_test_count[q] = tcount[q];
+  if (o->part_eval_count)
+    for (int64_t q = 0; q < p; ++q) o->part_eval_count[q] = ecount[q];
+  o->p_effective = p;
+  o->flops_chol = f_chol;
+  o->flops_gram = f_gram;
+  o->flops_other = f_other;
+  if (o->part_of) copy_out(o->part_of, po.part_of, n, s);
+  if (o->centers && po.centers) copy_out(o->centers, po.centers, p * d, s);
+  if (o->part_sizes)
+    for (int64_t q = 0; q < p; ++q) o->part_sizes[q] = po.sizes[q];
+
+  o->best_index = -1;
+  if (world == 1) {
+    std::vector<double> cmse(ncell, std::numeric_limits<double>::quiet_NaN()), cemse(ncell,
+                                                                                       std::numeric_limits<double>::quiet_NaN());
+    std::vector<uint8_t> cfail(ncell, 0);
+    std::vector<double> cres(ncell, 0.0);
+    for (int64_t c = 0; c < ncell; ++c) {
+      for (int64_t q = 0; q < p; ++q) {
+        if (pfail[c * p + q]) cfail[c] = 1;
+        const double r = rs[(c * p + q) * 4 + 0];
+        if (!pfail[c * p + q] && r > cres[c]) cres[c] = r;
+      }
+      if (cfail[c]) continue;
+      if (predictor == 0 || predictor == 2) {
+        // per-part SSE summed in part order (GPU-count independent)
+        double se = 0.0, ee = 0.0;
+        for (int64_t q = 0; q < p; ++q) {
+          se += rs[(c * p + q) * 4 + 2];
+          ee += rs[(c * p + q) * 4 + 3];
+        }
+        cmse[c] = se / static_cast<double>(t);
+        if (te) cemse[c] = ee / static_cast<double>(te);
+      } else {
+        pk::launch_combine(pred_t + c * p * t, p, t, predictor, nullptr, dyt, comb_t, dmse + 2 * c, s,
+                           ctx->counter);
+        if (te)
+          pk::launch_combine(pred_e + c * p * te, p, te, predictor, nullptr, dye, comb_e, dmse + 2 * c + 1,
+                             s, ctx->counter);
+        const std::vector<double> mm = to_host(dmse + 2 * c, 2, s);
+        cmse[c] = mm[0];
+        if (te) cemse[c] = mm[1];
+      }
+    }
+    for (int64_t c = 0; c < ncell; ++c) {
+      if (cfail[c]) continue;
+      if (o->best_index < 0 || cmse[c] < cmse[o->best_index]) o->best_index = c;
+    }
+    if (o->cell_mse) std::memcpy(o->cell_mse, cmse.data(), sizeof(double) * ncell);
+    if (o->cell_failed) std::memcpy(o->cell_failed, cfail.data(), ncell);
+    if (o->cell_residual) std::memcpy(o->cell_residual, cres.data(), sizeof(double) * ncell);
+    if (o->cell_eval_mse && te) std::memcpy(o->cell_eval_mse, cemse.data(), sizeof(double) * ncell);
+    const int64_t b = o->best_index;
+    if (b >= 0 && o->best_pred) {
+      if (pp_parts == 1) {
+        copy_out(o->best_pred, pred_t + b * t, t, s);
+      } else {
+        pk::launch_combine(pred_t + b * p * t, p, t, predictor, nullptr, dyt, comb_t, dmse, s, ctx->counter);
+        copy_out(o->best_pred, comb_t, t, s);
+      }
+    }
+    if (b >= 0 && o->best_eval_pred && te) {
+      if (pp_parts == 1) {
+        copy_out(o->best_eval_pred, pred_e + b * te, te, s);
+      } else {
+        pk::launch_combine(pred_e + b * p * te, p, te, predictor, nullptr, dye, comb_e, dmse + 1, s,
+                           ctx->counter);
+        copy_out(o->best_eval_pred, comb_e, te, s);
+      }
+    }
+  }
+  ck(cudaStreamSynchronize(s), "sync");
+  API_END
+}
+
+int pkrrgpu_grid_search(pkrrgpu_ctx* ctx, int strategy, const double* X_train,
+                        const double* y_train, int64_t n, int64_t d, const double* X_test,
+                        const double* y_test, int64_t t, int64_t p, const double* lambdas,
+                        int64_t n_lambdas, const double* sigmas, int64_t n_sigmas, uint64_t seed,
+                        double* cell_mse, uint8_t* cell_failed, double* cell_residual,
+                        int64_t* best_index) {
+  pkrrgpu_grid_args a{};
+  a.strategy = strategy;
+  a.X_train = X_train;
+  a.y_train = y_train;
+  a.n = n;
+  a.d = d;
+  a.X_test = X_test;
+  a.y_test = y_test;
+  a.t = t;
+  a.p = p;
+  a.lambdas = lambdas;
+  a.n_lambdas = n_lambdas;
+  a.sigmas = sigmas;
+  a.n_sigmas = n_sigmas;
+  a.seed = seed;
+  a.world = 1;
+  pkrrgpu_grid_out o{};
+  o.cell_mse = cell_mse;
+  o.cell_failed = cell_failed;
+  o.cell_residual = cell_residual;
+  const int rc = pkrrgpu_grid_search_ex(ctx, &a, &o);
+  if (best_index) *best_index = o.best_index;
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,927 @@
+// kernels.cu -- sm_100a kernels of the pkrr engine (everything except the DMMA
+// GEMM template, which lives in gemm_dmma.cuh and is instantiated here).
+//
+// Bit-exactness: the clustering kernels (norms, assign, means) use explicit
+// __dmul_rn/__dadd_rn so nvcc cannot contract to FMA; together with the
+// reference's summation order this makes partition labels bit-identical to
+// clustering.cpp.
+#include <cstdio>
+#include <cmath>
+
+#include "gemm_dmma.cuh"
+#include "kernels.cuh"
+
+namespace pk {
+
+// ---------------------------------------------------------------------------
+// TMA descriptors (driver entry point fetched through the runtime)
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+bool make_tmap(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 8)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), 64u};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// ---------------------------------------------------------------------------
+// row norms (dataset.cpp:49-53 squared_norm; clustering.cpp:28-32)
+// ---------------------------------------------------------------------------
+constexpr int kNormRows = 128, kChunk = 32;
+
+__global__ void __launch_bounds__(kNormRows) row_norms_kernel(const double* __restrict__ X,
+                                                               int64_t rows, int64_t d, int64_t ld,
+                                                               double* __restrict__ out) {
+  __shared__ double xs[kNormRows][kChunk + 1];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kNormRows;
+  const int64_t i = r0 + threadIdx.x;
+  double s = 0.0;
+  for (int64_t c0 = 0; c0 < d; c0 += kChunk) {
+    const int cw = static_cast<int>(d - c0 < kChunk ? d - c0 : kChunk);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kNormRows * kChunk; e += kNormRows) {
+      const int rr = e / kChunk, cc = e % kChunk;
+      const int64_t gr = r0 + rr;
+      xs[rr][cc] = (gr < rows && cc < cw) ? X[gr * ld + c0 + cc] : 0.0;
+    }
+    __syncthreads();
+    for (int cc = 0; cc < cw; ++cc) {
+      const double v = xs[threadIdx.x][cc];
+      s = __dadd_rn(s, __dmul_rn(v, v));
+    }
+  }
+  if (i < rows) out[i] = s;
+}
+
+void launch_row_norms(const double* X, int64_t rows, int64_t d, int64_t ld, double* out,
+                      cudaStream_t s, Counter& c) {
+  if (rows <= 0) return;
+  row_norms_kernel<<<static_cast<unsigned>((rows + kNormRows - 1) / kNormRows), kNormRows, 0, s>>>(
+      X, rows, d, ld, out);
+  ++c.launches;
+}
+
+// ---------------------------------------------------------------------------
+// gathers
+// ---------------------------------------------------------------------------
+__global__ void gather_rows_kernel(const double* __restrict__ X, int64_t d,
+                                   const int64_t* __restrict__ idx, int64_t cnt,
+                                   double* __restrict__ dst, int64_t rows_pad, int64_t dp) {
+  const int64_t total = rows_pad * dp;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = e / dp, col = e % dp;
+    dst[e] = (r < cnt && col < d) ? X[idx[r] * d + col] : 0.0;
+  }
+}
+
+void launch_gather_rows(const double* X, int64_t d, const int64_t* idx, int64_t cnt, double* dst,
+                        int64_t rows_pad, int64_t dp, cudaStream_t s, Counter& c) {
+  const int64_t total = rows_pad * dp;
+  if (total <= 0) return;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  gather_rows_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(X, d, idx, cnt, dst, rows_pad, dp);
+  ++c.launches;
+}
+
+__global__ void gather_vec_kernel(const double* __restrict__ y, const int64_t* __restrict__ idx,
+                                  int64_t cnt, double* __restrict__ dst, int64_t pad) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < pad) dst[i] = i < cnt ? y[idx[i]] : 0.0;
+}
+
+void launch_gather_vec(const double* y, const int64_t* idx, int64_t cnt, double* dst, int64_t pad,
+                       cudaStream_t s, Counter& c) {
+  if (pad <= 0) return;
+  gather_vec_kernel<<<static_cast<unsigned>((pad + 255) / 256), 256, 0, s>>>(y, idx, cnt, dst, pad);
+  ++c.launches;
+}
+
+// ---------------------------------------------------------------------------
+// DMMA GEMM launches
+// ---------------------------------------------------------------------------
+template <int BM, int MODE>
+static void gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p,
+                        int blocks, cudaStream_t s, Counter& c) {
+  if (blocks <= 0) return;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(dgemm_tn_kernel<BM, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         GemmCfg<BM>::SMEM);
+    attr_set = true;
+  }
+  dgemm_tn_kernel<BM, MODE><<<blocks, kGemmThreads, GemmCfg<BM>::SMEM, s>>>(a, b, p);
+  ++c.launches;
+}
+
+void launch_gram_sym(const CUtensorMap& tmX, const double* norms, int64_t mp, int64_t dp,
+                     int64_t m, double sigma, double* K, int64_t ldk, const int* abort,
+                     cudaStream_t s, Counter& c) {
+  GemmParams p{};
+  p.a_row0 = p.b_row0 = 0;
+  p.a_k0 = p.b_k0 = 0;
+  p.ktiles = static_cast<int>(dp / kBK);
+  p.C = K;
+  p.ldc = ldk;
+  const int T = static_cast<int>(mp / 128);
+  p.tiles_m = p.tiles_n = T;
+  p.lower = 1;
+  p.norm_a = p.norm_b = norms;
+  p.valid_a = p.valid_b = static_cast<int>(m);
+  p.denom = (2.0 * sigma) * sigma;
+  p.abort_flag = abort;
+  gemm_launch<128, G_GRAM_SYM>(tmX, tmX, p, T * (T + 1) / 2, s, c);
+}
+
+void launch_gram_cross(const CUtensorMap& tmQ, const CUtensorMap& tmX, const double* qnorms,
+                       const double* xnorms, int64_t qp, int64_t q, int64_t mp, int64_t m,
+                       int64_t dp, double sigma, double* Kc, cudaStream_t s, Counter& c) {
+  GemmParams p{};
+  p.ktiles = static_cast<int>(dp / kBK);
+  p.C = Kc;
+  p.ldc = mp;
+  p.tiles_m = static_cast<int>(qp / 64);
+  p.tiles_n = static_cast<int>(mp / 128);
+  p.norm_a = qnorms;
+  p.norm_b = xnorms;
+  p.valid_a = static_cast<int>(q);
+  p.valid_b = static_cast<int>(m);
+  p.denom = (2.0 * sigma) * sigma;
+  gemm_launch<64, G_GRAM_CROSS>(tmQ, tmX, p, p.tiles_m * p.tiles_n, s, c);
+}
+
+// ---------------------------------------------------------------------------
+// Cholesky leaf: factor the 128x128 diagonal block (solver.cpp:18-33 order of
+// operations within the block: pivot test, sqrt, column divide, rank-1 update)
+// and invert it in place (LAPACK trti2-style, lower).
+// ---------------------------------------------------------------------------
+constexpr int kLeafThreads = 512;
+constexpr int kLS = kNB + 1;  // padded smem stride
+constexpr int kLeafSmem = (kNB * kLS + kNB) * 8;
+
+__global__ void __launch_bounds__(kLeafThreads, 1)
+    potrf_leaf_kernel(double* __restrict__ A, int64_t lda, int kb, double* __restrict__ Linv,
+                      int* status, int64_t m_valid, int factor) {
+  if (status && *reinterpret_cast<volatile int*>(status)) return;
+  extern __shared__ double sm[];
+  double* L = sm;              // [128][129]
+  double* tmp = sm + kNB * kLS;  // [128]
+  const int tid = threadIdx.x;
+  const int64_t base = static_cast<int64_t>(kb) * kNB;
+  double* Ab = A + base * lda + base;
+  for (int e = tid; e < kNB * kNB; e += kLeafThreads) {
+    const int r = e / kNB, col = e % kNB;
+    L[r * kLS + col] = col <= r ? Ab[static_cast<int64_t>(r) * lda + col] : 0.0;
+  }
+  __syncthreads();
+  if (factor) {
+    for (int j = 0; j < kNB; ++j) {
+      const double piv = L[j * kLS + j];
+      if (!(piv > 0.0)) {
+        if (tid == 0 && status) {
+          status[1] = static_cast<int>(base + j);
+          __threadfence();
+          atomicExch(&status[0], 1);
+        }
+        return;
+      }
+      const double dj = sqrt(piv);
+      if (tid > j && tid < kNB) L[tid * kLS + j] = L[tid * kLS + j] / dj;
+      __syncthreads();
+      const int T = kNB - 1 - j;
+      for (int e = tid; e < T * T; e += kLeafThreads) {
+        const int ii = e / T, kk = e % T;
+        if (kk <= ii) {
+          const int i = j + 1 + ii, k = j + 1 + kk;
+          L[i * kLS + k] -= L[i * kLS + j] * L[k * kLS + j];
+        }
+      }
+      if (tid == 0) L[j * kLS + j] = dj;
+      __syncthreads();
+    }
+    // L (lower, zero upper inside the block) back to A
+    for (int e = tid; e < kNB * kNB; e += kLeafThreads) {
+      const int r = e / kNB, col = e % kNB;
+      Ab[static_cast<int64_t>(r) * lda + col] = col <= r ? L[r * kLS + col] : 0.0;
+    }
+  }
+  // in-place inverse of the lower triangular block, column j = 127 .. 0
+  const int row = tid >> 2, sub = tid & 3;
+  for (int j = kNB - 1; j >= 0; --j) {
+    if (tid < kNB) tmp[tid] = L[tid * kLS + j];
+    __syncthreads();
+    const double inv_jj = 1.0 / tmp[j];
+    double s = 0.0;
+    if (row > j) {
+      for (int k = j + 1 + sub; k <= row; k += 4) s += L[row * kLS + k] * tmp[k];
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if (sub == 0) {
+      if (row > j) L[row * kLS + j] = -s * inv_jj;
+      else if (row == j) L[row * kLS + j] = inv_jj;
+    }
+    __syncthreads();
+  }
+  double* Lo = Linv + base * kNB;
+  for (int e = tid; e < kNB * kNB; e += kLeafThreads) {
+    const int r = e / kNB, col = e % kNB;
+    Lo[e] = col <= r ? L[r * kLS + col] : 0.0;
+  }
+}
+
+void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, double* Linv,
+                  int64_t mp, int64_t m_valid, int* status, cudaStream_t s, Counter& c) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(potrf_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLeafSmem);
+    attr = true;
+  }
+  const int nb = static_cast<int>(mp / kNB);
+  for (int kb = 0; kb < nb; ++kb) {
+    potrf_leaf_kernel<<<1, kLeafThreads, kLeafSmem, s>>>(A, mp, kb, Linv, status, m_valid, 1);
+    ++c.launches;
+    const int rem = nb - 1 - kb;
+    if (rem <= 0) continue;
+    // panel: A21 := A21 * inv(L11)^T  (in place, 64-row blocks)
+    GemmParams t{};
+    t.a_row0 = (kb + 1) * kNB;
+    t.a_k0 = kb * kNB;
+    t.b_row0 = kb * kNB;
+    t.b_k0 = 0;
+    t.ktiles = kNB / kBK;
+    t.C = A;
+    t.ldc = mp;
+    t.c_row0 = (kb + 1) * kNB;
+    t.c_col0 = kb * kNB;
+    t.tiles_m = rem * 2;
+    t.tiles_n = 1;
+    t.abort_flag = status;
+    gemm_launch<64, G_STORE>(tmA, tmLinv, t, rem * 2, s, c);
+    // trailing: A22 -= L21 L21^T on lower tiles
+    GemmParams u{};
+    u.a_row0 = u.b_row0 = (kb + 1) * kNB;
+    u.a_k0 = u.b_k0 = kb * kNB;
+    u.ktiles = kNB / kBK;
+    u.C = A;
+    u.ldc = mp;
+    u.c_row0 = u.c_col0 = (kb + 1) * kNB;
+    u.tiles_m = u.tiles_n = rem;
+    u.lower = 1;
+    u.abort_flag = status;
+    gemm_launch<128, G_UPDATE>(tmA, tmA, u, rem * (rem + 1) / 2, s, c);
+  }
+}
+
+void launch_diag_inverses(const double* L, int64_t mp, double* Linv, cudaStream_t s, Counter& c) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(potrf_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLeafSmem);
+    attr = true;
+  }
+  const int nb = static_cast<int>(mp / kNB);
+  for (int kb = 0; kb < nb; ++kb) {
+    potrf_leaf_kernel<<<1, kLeafThreads, kLeafSmem, s>>>(const_cast<double*>(L), mp, kb, Linv,
+                                                         nullptr, mp, 0);
+    ++c.launches;
+  }
+}
+
+__global__ void zero_upper_kernel(double* A, int64_t mp) {
+  const int64_t total = mp * mp;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (e % mp > e / mp) A[e] = 0.0;
+  }
+}
+
+void launch_zero_upper(double* A, int64_t mp, cudaStream_t s, Counter& c) {
+  zero_upper_kernel<<<148 * 8, 256, 0, s>>>(A, mp);
+  ++c.launches;
+}
+
+// ---------------------------------------------------------------------------
+// blocked triangular solves with inter-CTA flags (ticket-ordered: CTA I only
+// waits on blocks finished by CTAs that started before it -> no deadlock)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+// rows GEMV on a 128x128 block: out[r] += sum_c M[r][c] v[c]; 8 warps x 16 rows
+__device__ __forceinline__ void block_gemv_rows(const double* __restrict__ M, int64_t ld,
+                                                const double* v, double* out, int warp, int lane) {
+  for (int rr = 0; rr < 16; ++rr) {
+    const int r = warp * 16 + rr;
+    const double* row = M + static_cast<int64_t>(r) * ld;
+    const double4 a = *reinterpret_cast<const double4*>(row + lane * 4);
+    double s = a.x * v[lane * 4] + a.y * v[lane * 4 + 1] + a.z * v[lane * 4 + 2] +
+               a.w * v[lane * 4 + 3];
+    s = warp_sum(s);
+    if (lane == 0) out[r] += s;
+  }
+}
+
+// cols GEMV on a 128x128 block: out[c] += sum_r M[r][c] v[r]; 256 threads
+__device__ __forceinline__ void block_gemv_cols(const double* __restrict__ M, int64_t ld,
+                                                const double* v, double* part, double* out,
+                                                int tid) {
+  const int c = tid & 127, h = tid >> 7;
+  double s = 0.0;
+  for (int r = h * 64; r < h * 64 + 64; ++r) s += M[static_cast<int64_t>(r) * ld + c] * v[r];
+  part[h * 128 + c] = s;
+  __syncthreads();
+  if (tid < 128) out[tid] += part[tid] + part[128 + tid];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) trsv_fwd_kernel(const double* __restrict__ L, int64_t ld,
+                                                       const double* __restrict__ Linv,
+                                                       const double* __restrict__ b, double* z,
+                                                       int nb, int* ticket, int* flags,
+                                                       const int* abort) {
+  if (abort && *reinterpret_cast<const volatile int*>(abort)) return;
+  __shared__ double acc[kNB], vk[kNB];
+  __shared__ int sI;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) sI = atomicAdd(ticket, 1);
+  if (tid < kNB) acc[tid] = 0.0;
+  __syncthreads();
+  const int I = sI;
+  for (int K = 0; K < I; ++K) {
+    if (tid == 0)
+      while (ld_acquire(&flags[K]) == 0) {
+      }
+    __syncthreads();
+    if (tid < kNB) vk[tid] = __ldcg(&z[K * kNB + tid]);
+    __syncthreads();
+    block_gemv_rows(L + static_cast<int64_t>(I) * kNB * ld + K * kNB, ld, vk, acc, warp, lane);
+    __syncthreads();
+  }
+  if (tid < kNB) {
+    vk[tid] = b[I * kNB + tid] - acc[tid];
+    acc[tid] = 0.0;
+  }
+  __syncthreads();
+  block_gemv_rows(Linv + static_cast<int64_t>(I) * kNB * kNB, kNB, vk, acc, warp, lane);
+  __syncthreads();
+  if (tid < kNB) z[I * kNB + tid] = acc[tid];
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) st_release(&flags[I], 1);
+}
+
+__global__ void __launch_bounds__(256) trsv_bwd_kernel(const double* __restrict__ L, int64_t ld,
+                                                       const double* __restrict__ Linv,
+                                                       const double* __restrict__ z, double* x,
+                                                       int nb, int* ticket, int* flags,
+                                                       const int* abort) {
+  if (abort && *reinterpret_cast<const volatile int*>(abort)) return;
+  __shared__ double acc[kNB], vk[kNB], part[2 * kNB];
+  __shared__ int sI;
+  const int tid = threadIdx.x;
+  if (tid == 0) sI = nb - 1 - atomicAdd(ticket, 1);
+  if (tid < kNB) acc[tid] = 0.0;
+  __syncthreads();
+  const int I = sI;
+  for (int K = nb - 1; K > I; --K) {
+    if (tid == 0)
+      while (ld_acquire(&flags[K]) == 0) {
+      }
+    __syncthreads();
+    if (tid < kNB) vk[tid] = __ldcg(&x[K * kNB + tid]);
+    __syncthreads();
+    block_gemv_cols(L + static_cast<int64_t>(K) * kNB * ld + I * kNB, ld, vk, part, acc, tid);
+  }
+  if (tid < kNB) {
+    vk[tid] = z[I * kNB + tid] - acc[tid];
+    acc[tid] = 0.0;
+  }
+  __syncthreads();
+  block_gemv_cols(Linv + static_cast<int64_t>(I) * kNB * kNB, kNB, vk, part, acc, tid);
+  if (tid < kNB) x[I * kNB + tid] = acc[tid];
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) st_release(&flags[I], 1);
+}
+
+void launch_trsv(const double* L, const double* Linv, int64_t mp, const double* b, double* z,
+                 double* x, int* scratch, const int* abort, cudaStream_t s, Counter& c) {
+  const int nb = static_cast<int>(mp / kNB);
+  cudaMemsetAsync(scratch, 0, sizeof(int) * (2 * nb + 2), s);
+  trsv_fwd_kernel<<<nb, 256, 0, s>>>(L, mp, Linv, b, z, nb, scratch, scratch + 2, abort);
+  trsv_bwd_kernel<<<nb, 256, 0, s>>>(L, mp, Linv, z, x, nb, scratch + 1, scratch + 2 + nb, abort);
+  c.launches += 2;
+}
+
+// ---------------------------------------------------------------------------
+// assemble / GEMV / reductions
+// ---------------------------------------------------------------------------
+__global__ void assemble_kernel(const double2* __restrict__ K, double2* __restrict__ A, int64_t mp,
+                                double shift, const int* abort) {
+  if (abort && *reinterpret_cast<const volatile int*>(abort)) return;
+  const int64_t total = mp * mp / 2;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double2 v = K[e];
+    const int64_t r = (2 * e) / mp, col = (2 * e) % mp;
+    if (col == r) v.x += shift;
+    if (col + 1 == r) v.y += shift;
+    A[e] = v;
+  }
+}
+
+void launch_assemble(const double* K, double* A, int64_t mp, double shift, const int* abort,
+                     cudaStream_t s, Counter& c) {
+  assemble_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<const double2*>(K),
+                                         reinterpret_cast<double2*>(A), mp, shift, abort);
+  ++c.launches;
+}
+
+__global__ void __launch_bounds__(256) gemv_rows_kernel(const double* __restrict__ M, int64_t ld,
+                                                        int64_t rows, int64_t cols,
+                                                        const double* __restrict__ v,
+                                                        double* __restrict__ out, const int* abort) {
+  if (abort && *reinterpret_cast<const volatile int*>(abort)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+  if (i >= rows) return;
+  const double* row = M + i * ld;
+  double s = 0.0;
+  for (int64_t j = lane; j < cols; j += 32) s += row[j] * v[j];
+  s = warp_sum(s);
+  if (lane == 0) out[i] = s;
+}
+
+void launch_gemv_rows(const double* M, int64_t ld, int64_t rows, int64_t cols, const double* v,
+                      double* out, const int* abort, cudaStream_t s, Counter& c) {
+  if (rows <= 0) return;
+  gemv_rows_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(M, ld, rows, cols, v, out,
+                                                                        abort);
+  ++c.launches;
+}
+
+// fixed-shape block tree reduction (deterministic)
+__device__ double block_sum_1024(double v, double* red) {
+  v = warp_sum(v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (warp == 0) {
+    t = lane < static_cast<int>(blockDim.x >> 5) ? red[lane] : 0.0;
+    t = warp_sum(t);
+  }
+  __syncthreads();
+  return t;  // valid in warp 0
+}
+
+__global__ void __launch_bounds__(1024) residual_finish_kernel(const double* __restrict__ Ka,
+                                                               const double* __restrict__ alpha,
+                                                               const double* __restrict__ y,
+                                                               int64_t m, double shift,
+                                                               double* out, const int* abort) {
+  if (abort && *reinterpret_cast<const volatile int*>(abort)) return;
+  __shared__ double red[32];
+  double rs = 0.0, ys = 0.0;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const double acc = (shift * alpha[i] - y[i]) + Ka[i];
+    rs += acc * acc;
+    ys += y[i] * y[i];
+  }
+  const double R = block_sum_1024(rs, red);
+  const double Y = block_sum_1024(ys, red);
+  if (threadIdx.x == 0) {
+    out[0] = Y > 0.0 ? sqrt(R / Y) : sqrt(R);
+    out[1] = Y > 0.0 ? sqrt(R) / sqrt(Y) : sqrt(R);
+  }
+}
+
+void launch_residual_finish(const double* Kalpha, const double* alpha, const double* y, int64_t m,
+                            double shift, double* out, const int* abort, cudaStream_t s,
+                            Counter& c) {
+  residual_finish_kernel<<<1, 1024, 0, s>>>(Kalpha, alpha, y, m, shift, out, abort);
+  ++c.launches;
+}
+
+__global__ void __launch_bounds__(1024) sse_scatter_kernel(const double* __restrict__ pred,
+                                                           const int64_t* __restrict__ pos,
+                                                           int64_t cnt,
+                                                           const double* __restrict__ ytest,
+                                                           double* pred_all, double* out,
+                                                           const int* abort) {
+  if (abort && *reinterpret_cast<const volatile int*>(abort)) return;
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t j = threadIdx.x; j < cnt; j += blockDim.x) {
+    const double v = pred[j];
+    const int64_t g = pos[j];
+    if (pred_all) pred_all[g] = v;
+    const double diff = v - ytest[g];
+    s += diff * diff;
+  }
+  const double S = block_sum_1024(s, red);
+  if (threadIdx.x == 0) out[0] = S;
+}
+
+void launch_sse_scatter(const double* pred, const int64_t* pos, int64_t cnt, const double* ytest,
+                        double* pred_all, double* out, const int* abort, cudaStream_t s,
+                        Counter& c) {
+  sse_scatter_kernel<<<1, 1024, 0, s>>>(pred, pos, cnt, ytest, pred_all, out, abort);
+  ++c.launches;
+}
+
+// predictor: 0 whole, 1 average, 2 nearest, 3 oracle (strategies.cpp:458-495)
+__global__ void __launch_bounds__(1024) combine_kernel(const double* __restrict__ pp, int64_t p,
+                                                       int64_t t, int predictor,
+                                                       const int32_t* __restrict__ route,
+                                                       const double* __restrict__ ytest,
+                                                       double* pred, double* mse_out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t j = threadIdx.x; j < t; j += blockDim.x) {
+    double v = 0.0;
+    if (predictor == 0) {
+      v = pp[j];
+    } else if (predictor == 1) {
+      for (int64_t q = 0; q < p; ++q) v += pp[q * t + j];
+      v *= 1.0 / static_cast<double>(p);
+    } else if (predictor == 2) {
+      v = pp[static_cast<int64_t>(route[j]) * t + j];
+    } else {
+      double be = INFINITY;
+      for (int64_t q = 0; q < p; ++q) {
+        const double u = pp[q * t + j];
+        const double err = (u - ytest[j]) * (u - ytest[j]);
+        if (err < be) {
+          be = err;
+          v = u;
+        }
+      }
+    }
+    pred[j] = v;
+    const double diff = v - ytest[j];
+    s += diff * diff;
+  }
+  const double S = block_sum_1024(s, red);
+  if (threadIdx.x == 0) mse_out[0] = S / static_cast<double>(t);
+}
+
+void launch_combine(const double* pp, int64_t p, int64_t t, int predictor, const int32_t* route,
+                    const double* ytest, double* pred, double* mse_out, cudaStream_t s,
+                    Counter& c) {
+  combine_kernel<<<1, 1024, 0, s>>>(pp, p, t, predictor, route, ytest, pred, mse_out);
+  ++c.launches;
+}
+
+// ---------------------------------------------------------------------------
+// clustering
+// ---------------------------------------------------------------------------
+constexpr int kAssignRows = 128;
+
+// clustering.cpp:79-96 (assign) / :159-176 (k-balance scan step) / :182-195 (route)
+template <int KP>
+__global__ void __launch_bounds__(kAssignRows)
+    assign_kernel(const double* __restrict__ X, int64_t n, int64_t d,
+                  const double* __restrict__ xnorm, const double* __restrict__ centers,
+                  const double* __restrict__ cnorm, int k, int mode,
+                  const uint8_t* __restrict__ open, int64_t row0, int32_t* label,
+                  double* best_dist, unsigned long long* changed) {
+  __shared__ double xs[kAssignRows][kChunk + 1];
+  __shared__ double cs[KP][kChunk + 1];
+  const int64_t rbase = row0 + static_cast<int64_t>(blockIdx.x) * kAssignRows;
+  const int64_t i = rbase + threadIdx.x;
+  bool need = i < n;
+  if (need && mode == 1) {
+    const int cur = label[i];
+    need = cur < 0 || !open[cur];
+  }
+  if (!__syncthreads_or(need)) return;
+  double min_d = INFINITY;
+  int min_j = mode == 0 ? 0 : -1;
+  const double xn = need ? xnorm[i] : 0.0;
+  for (int jb = 0; jb < k; jb += KP) {
+    double dot[KP];
+#pragma unroll
+    for (int q = 0; q < KP; ++q) dot[q] = 0.0;
+    for (int64_t c0 = 0; c0 < d; c0 += kChunk) {
+      const int cw = static_cast<int>(d - c0 < kChunk ? d - c0 : kChunk);
+      __syncthreads();
+      for (int e = threadIdx.x; e < kAssignRows * kChunk; e += kAssignRows) {
+        const int rr = e / kChunk, cc = e % kChunk;
+        const int64_t gr = rbase + rr;
+        xs[rr][cc] = (gr < n && cc < cw) ? X[gr * d + c0 + cc] : 0.0;
+      }
+      for (int e = threadIdx.x; e < KP * kChunk; e += kAssignRows) {
+        const int q = e / kChunk, cc = e % kChunk;
+        cs[q][cc] = (jb + q < k && cc < cw) ? centers[static_cast<int64_t>(jb + q) * d + c0 + cc] : 0.0;
+      }
+      __syncthreads();
+      if (need) {
+        for (int cc = 0; cc < cw; ++cc) {
+          const double x = xs[threadIdx.x][cc];
+#pragma unroll
+          for (int q = 0; q < KP; ++q) dot[q] = __dadd_rn(dot[q], __dmul_rn(x, cs[q][cc]));
+        }
+      }
+    }
+    if (need) {
+#pragma unroll
+      for (int q = 0; q < KP; ++q) {
+        const int j = jb + q;
+        if (j >= k) break;
+        if (mode == 1 && !open[j]) continue;
+        double dist = __dsub_rn(__dadd_rn(xn, cnorm[j]), __dmul_rn(2.0, dot[q]));
+        if (dist < 0.0) dist = 0.0;
+        if (dist < min_d) {
+          min_d = dist;
+          min_j = j;
+        }
+      }
+    }
+  }
+  unsigned ch = 0;
+  if (need) {
+    if (mode == 0) {
+      if (label[i] != min_j) {
+        label[i] = min_j;
+        ch = 1;
+      }
+      if (best_dist) best_dist[i] = min_d;
+    } else {
+      label[i] = min_j;
+    }
+  }
+  if (changed) {
+    const int cnt = __syncthreads_count(ch);
+    if (threadIdx.x == 0 && cnt) atomicAdd(changed, static_cast<unsigned long long>(cnt));
+  }
+}
+
+void launch_assign(const double* X, int64_t n, int64_t d, const double* xnorm,
+                   const double* centers, const double* cnorm, int k, int mode,
+                   const uint8_t* open, int64_t row0, int32_t* label, double* best_dist,
+                   unsigned long long* changed, cudaStream_t s, Counter& c) {
+  const int64_t rows = n - row0;
+  if (rows <= 0) return;
+  const unsigned blocks = static_cast<unsigned>((rows + kAssignRows - 1) / kAssignRows);
+  if (k <= 8)
+    assign_kernel<8><<<blocks, kAssignRows, 0, s>>>(X, n, d, xnorm, centers, cnorm, k, mode, open,
+                                                   row0, label, best_dist, changed);
+  else if (k <= 16)
+    assign_kernel<16><<<blocks, kAssignRows, 0, s>>>(X, n, d, xnorm, centers, cnorm, k, mode, open,
+                                                    row0, label, best_dist, changed);
+  else
+    assign_kernel<32><<<blocks, kAssignRows, 0, s>>>(X, n, d, xnorm, centers, cnorm, k, mode, open,
+                                                    row0, label, best_dist, changed);
+  ++c.launches;
+}
+
+// ---- stable grouping: block counts -> scan -> scatter ----------------------
+constexpr int kGroupRows = 256;
+
+__global__ void group_count_kernel(const int32_t* __restrict__ label, int64_t n, int k,
+                                   int64_t* counts) {
+  extern __shared__ int cnt_s[];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) cnt_s[j] = 0;
+  __syncthreads();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kGroupRows + threadIdx.x;
+  if (i < n) atomicAdd(&cnt_s[label[i]], 1);
+  __syncthreads();
+  for (int j = threadIdx.x; j < k; j += blockDim.x) counts[static_cast<int64_t>(blockIdx.x) * k + j] = cnt_s[j];
+}
+
+__global__ void group_scan_kernel(int64_t* counts, int64_t nblk, int k, int64_t* sizes,
+                                  int64_t* start) {
+  // thread j: exclusive scan of counts[:, j] over blocks (in place)
+  __shared__ int64_t tot[1024];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    int64_t run = 0;
+    for (int64_t b = 0; b < nblk; ++b) {
+      const int64_t v = counts[b * k + j];
+      counts[b * k + j] = run;
+      run += v;
+    }
+    tot[j] = run;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t run = 0;
+    for (int j = 0; j < k; ++j) {
+      sizes[j] = tot[j];
+      start[j] = run;
+      run += tot[j];
+    }
+  }
+}
+
+__global__ void group_scatter_kernel(const int32_t* __restrict__ label, int64_t n, int k,
+                                     const int64_t* __restrict__ offs,
+                                     const int64_t* __restrict__ start, int64_t* members) {
+  extern __shared__ int wc[];  // [8][k]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int e = threadIdx.x; e < 8 * k; e += blockDim.x) wc[e] = 0;
+  __syncthreads();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kGroupRows + threadIdx.x;
+  const bool valid = i < n;
+  const int lab = valid ? label[i] : -1 - lane;  // unique dummies never match real labels
+  const unsigned mask = __match_any_sync(0xffffffffu, lab);
+  const int rank = __popc(mask & ((1u << lane) - 1u));
+  if (valid && rank == 0) wc[warp * k + lab] = __popc(mask);
+  __syncthreads();
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    int run = 0;
+    for (int w = 0; w < 8; ++w) {
+      const int v = wc[w * k + j];
+      wc[w * k + j] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  if (valid)
+    members[start[lab] + offs[static_cast<int64_t>(blockIdx.x) * k + lab] + wc[warp * k + lab] + rank] = i;
+}
+
+void launch_group(const int32_t* label, int64_t n, int k, int64_t* sizes, int64_t* start,
+                  int64_t* members, int64_t* tmp, cudaStream_t s, Counter& c) {
+  if (n <= 0) return;
+  const int64_t nblk = (n + kGroupRows - 1) / kGroupRows;
+  group_count_kernel<<<static_cast<unsigned>(nblk), kGroupRows, sizeof(int) * k, s>>>(label, n, k, tmp);
+  group_scan_kernel<<<1, 1024, 0, s>>>(tmp, nblk, k, sizes, start);
+  group_scatter_kernel<<<static_cast<unsigned>(nblk), kGroupRows, sizeof(int) * 8 * k, s>>>(
+      label, n, k, tmp, start, members);
+  c.launches += 3;
+}
+
+// clustering.cpp:34-49: zero, row-order sums, then * (1.0 / size)
+__global__ void means_kernel(const double* __restrict__ X, int64_t d,
+                             const int64_t* __restrict__ members, const int64_t* __restrict__ start,
+                             const int64_t* __restrict__ sizes, int k, double* centers) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e >= static_cast<int64_t>(k) * d) return;
+  const int j = static_cast<int>(e / d);
+  const int64_t f = e % d;
+  const int64_t sz = sizes[j], st = start[j];
+  double s = 0.0;
+  int64_t q = 0;
+  for (; q + 8 <= sz; q += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = X[members[st + q + u] * d + f];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
+  }
+  for (; q < sz; ++q) s = __dadd_rn(s, X[members[st + q] * d + f]);
+  centers[e] = sz > 0 ? __dmul_rn(s, __ddiv_rn(1.0, static_cast<double>(sz))) : 0.0;
+}
+
+void launch_means(const double* X, int64_t d, const int64_t* members, const int64_t* start,
+                  const int64_t* sizes, int k, double* centers, cudaStream_t s, Counter& c) {
+  const int64_t total = static_cast<int64_t>(k) * d;
+  means_kernel<<<static_cast<unsigned>((total + 63) / 64), 64, 0, s>>>(X, d, members, start, sizes, k,
+                                                                      centers);
+  ++c.launches;
+}
+
+// clustering.cpp:101-110: farthest sample among clusters of size > 1, first index
+__global__ void farthest_max_kernel(const double* __restrict__ best, const int32_t* __restrict__ label,
+                                    const int64_t* __restrict__ sizes, int64_t n,
+                                    unsigned long long* out) {
+  unsigned long long m = 0;
+  bool any = false;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double v = best[i];
+    if (sizes[label[i]] <= 1 || !(v >= 0.0)) continue;
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    if (!any || b > m) m = b;
+    any = true;
+  }
+  if (any) atomicMax(&out[0], m + 1);  // +1 so 0 means "no eligible sample"
+}
+
+__global__ void farthest_idx_kernel(const double* __restrict__ best, const int32_t* __restrict__ label,
+                                    const int64_t* __restrict__ sizes, int64_t n,
+                                    unsigned long long* out) {
+  const unsigned long long target = out[0];
+  if (target == 0) return;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double v = best[i];
+    if (sizes[label[i]] <= 1 || !(v >= 0.0)) continue;
+    if (static_cast<unsigned long long>(__double_as_longlong(v)) + 1 == target)
+      atomicMin(&out[1], static_cast<unsigned long long>(i));
+  }
+}
+
+void launch_farthest(const double* best, const int32_t* label, const int64_t* sizes, int64_t n,
+                     unsigned long long* out, cudaStream_t s, Counter& c) {
+  cudaMemsetAsync(out, 0, sizeof(unsigned long long), s);
+  cudaMemsetAsync(out + 1, 0xff, sizeof(unsigned long long), s);
+  farthest_max_kernel<<<148 * 4, 256, 0, s>>>(best, label, sizes, n, out);
+  farthest_idx_kernel<<<148 * 4, 256, 0, s>>>(best, label, sizes, n, out);
+  c.launches += 2;
+}
+
+__global__ void hist_kernel(const int32_t* __restrict__ label, int64_t row0, int64_t row1, int k,
+                            unsigned long long* hist) {
+  extern __shared__ int hs[];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) hs[j] = 0;
+  __syncthreads();
+  for (int64_t i = row0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i <= row1;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int l = label[i];
+    if (l >= 0 && l < k) atomicAdd(&hs[l], 1);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < k; j += blockDim.x)
+    if (hs[j]) atomicAdd(&hist[j], static_cast<unsigned long long>(hs[j]));
+}
+
+void launch_hist(const int32_t* label, int64_t row0, int64_t row1, int k, int64_t* hist,
+                 cudaStream_t s, Counter& c) {
+  cudaMemsetAsync(hist, 0, sizeof(int64_t) * k, s);
+  if (row1 < row0) return;
+  int64_t blocks = (row1 - row0 + 256) / 256;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  hist_kernel<<<static_cast<unsigned>(blocks), 256, sizeof(int) * k, s>>>(
+      label, row0, row1, k, reinterpret_cast<unsigned long long*>(hist));
+  ++c.launches;
+}
+
+// one CTA per cluster: position of the thr[j]-th occurrence of j in label[row0, n)
+__global__ void __launch_bounds__(1024) events_kernel(const int32_t* __restrict__ label, int64_t row0,
+                                                      int64_t n, const int64_t* __restrict__ thr,
+                                                      int64_t* pos) {
+  __shared__ int wsum[32];
+  __shared__ int64_t found;
+  const int j = blockIdx.x;
+  const int64_t need = thr[j];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) found = INT64_MAX;
+  __syncthreads();
+  if (need <= 0) {
+    if (threadIdx.x == 0) pos[j] = INT64_MAX;
+    return;
+  }
+  int64_t run = 0;
+  for (int64_t base = row0; base < n; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const bool hit = i < n && label[i] == j;
+    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      if (w < warp) before += wsum[w];
+      total += wsum[w];
+    }
+    const int rank = before + __popc(bal & ((1u << lane) - 1u));
+    if (run + total >= need) {
+      if (hit && run + rank + 1 == need) found = i;
+      __syncthreads();
+      break;
+    }
+    run += total;
+    __syncthreads();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) pos[j] = found;
+}
+
+void launch_events(const int32_t* label, int64_t row0, int64_t n, int k, const int64_t* thr,
+                   int64_t* pos, cudaStream_t s, Counter& c) {
+  events_kernel<<<k, 1024, 0, s>>>(label, row0, n, thr, pos);
+  ++c.launches;
+}
+
+}  // namespace pk

@@ -1,0 +1,103 @@
+// kernels.cuh -- launch wrappers for the sm_100a kernels of the pkrr engine.
+// All launchers are asynchronous on the given stream and count launches in
+// *launches (evidence for bench.py's gpu_launches).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pk {
+
+constexpr int kNB = 128;  // Cholesky block (leaf / panel) size; parts are padded to it
+
+struct Counter {
+  int64_t launches = 0;
+};
+
+// ---- TMA descriptors -------------------------------------------------------
+bool make_tmap(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld);
+
+// ---- row norms: out[i] = sum_k x_ik^2, sequential, no FMA (dataset.cpp:49-53)
+void launch_row_norms(const double* X, int64_t rows, int64_t d, int64_t ld, double* out,
+                      cudaStream_t s, Counter& c);
+
+// ---- gather rows idx[0..cnt) of X (n x d) into dst (rows_pad x dp), zero padded
+void launch_gather_rows(const double* X, int64_t d, const int64_t* idx, int64_t cnt,
+                        double* dst, int64_t rows_pad, int64_t dp, cudaStream_t s, Counter& c);
+void launch_gather_vec(const double* y, const int64_t* idx, int64_t cnt, double* dst,
+                       int64_t pad, cudaStream_t s, Counter& c);
+
+// ---- DMMA GEMM family (gemm_dmma.cuh) -------------------------------------
+// K (ldk x ldk, padded mp) = gaussian gram of Xp (mp x dp) ; valid = m
+void launch_gram_sym(const CUtensorMap& tmX, const double* norms, int64_t mp, int64_t dp,
+                     int64_t m, double sigma, double* K, int64_t ldk, const int* abort,
+                     cudaStream_t s, Counter& c);
+// Kc (qp x mp) = k(Q_q, X_i); valid rows q, valid cols m
+void launch_gram_cross(const CUtensorMap& tmQ, const CUtensorMap& tmX, const double* qnorms,
+                       const double* xnorms, int64_t qp, int64_t q, int64_t mp, int64_t m,
+                       int64_t dp, double sigma, double* Kc, cudaStream_t s, Counter& c);
+// Blocked right-looking Cholesky of A (mp x mp, lower, mp % 128 == 0) in place.
+// Linv: mp x 128 scratch receiving inv(L_kk) per diagonal block.
+// status[0] = abort flag, status[1] = first failing global column (int).
+void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, double* Linv,
+                  int64_t mp, int64_t m_valid, int* status, cudaStream_t s, Counter& c);
+// Recompute inv(L_kk) for every diagonal block of an existing factor.
+void launch_diag_inverses(const double* L, int64_t mp, double* Linv, cudaStream_t s, Counter& c);
+// Zero the strict upper triangle (API parity with solver.cpp:34).
+void launch_zero_upper(double* A, int64_t mp, cudaStream_t s, Counter& c);
+
+// ---- triangular solves (L L^T x = b) on the blocked factor ----------------
+// scratch: 2*nb + 2 ints (tickets + flags), zeroed by the launcher
+void launch_trsv(const double* L, const double* Linv, int64_t mp, const double* b, double* z,
+                 double* x, int* scratch, const int* abort, cudaStream_t s, Counter& c);
+
+// ---- assemble: A = K + shift * I (full copy) ------------------------------
+void launch_assemble(const double* K, double* A, int64_t mp, double shift, const int* abort,
+                     cudaStream_t s, Counter& c);
+
+// ---- GEMV rows: out[i] = sum_{j<cols} M[i][j] v[j], i < rows (deterministic)
+void launch_gemv_rows(const double* M, int64_t ld, int64_t rows, int64_t cols, const double* v,
+                      double* out, const int* abort, cudaStream_t s, Counter& c);
+// residual ratio of (K + shift I) alpha = y from Kalpha (strategies.cpp:310-320 and
+// solver.cpp:103-119): out[0] = sqrt(res/yy), out[1] = sqrt(res)/sqrt(yy)
+void launch_residual_finish(const double* Kalpha, const double* alpha, const double* y,
+                            int64_t m, double shift, double* out, const int* abort,
+                            cudaStream_t s, Counter& c);
+// pred rows -> scatter to test order (pred_all[pos[j]] = pred[j]) and
+// sse = sum (pred_j - ytest[pos[j]])^2 (fixed-order tree), out[0] = sse
+void launch_sse_scatter(const double* pred, const int64_t* pos, int64_t cnt, const double* ytest,
+                        double* pred_all, double* out, const int* abort, cudaStream_t s,
+                        Counter& c);
+// combine per-part predictions (average / oracle / nearest / whole) in part order
+// into pred[t] and mse over all rows (strategies.cpp:458-495)
+void launch_combine(const double* pp, int64_t p, int64_t t, int predictor, const int32_t* route,
+                    const double* ytest, double* pred, double* mse_out, cudaStream_t s,
+                    Counter& c);
+
+// ---- clustering (bit-exact with clustering.cpp) ---------------------------
+// mode 0: kmeans assign (all clusters, min_j init 0, counts changes)
+// mode 1: kbalance re-argmin over open clusters for rows in [row0, n) whose
+//         current choice is closed (or < 0), min_j init -1
+void launch_assign(const double* X, int64_t n, int64_t d, const double* xnorm,
+                   const double* centers, const double* cnorm, int k, int mode,
+                   const uint8_t* open, int64_t row0, int32_t* label, double* best_dist,
+                   unsigned long long* changed, cudaStream_t s, Counter& c);
+// stable grouping of rows by label: sizes[k], start[k], members[n] (row order)
+// tmp: >= (ceil(n/256) * k + 2k) int64
+void launch_group(const int32_t* label, int64_t n, int k, int64_t* sizes, int64_t* start,
+                  int64_t* members, int64_t* tmp, cudaStream_t s, Counter& c);
+// centers[j][f] = (sum over members in row order) * (1.0 / size)  (clustering.cpp:34-49)
+void launch_means(const double* X, int64_t d, const int64_t* members, const int64_t* start,
+                  const int64_t* sizes, int k, double* centers, cudaStream_t s, Counter& c);
+// argmax_i best[i] over rows whose cluster has size > 1 (first index on ties)
+void launch_farthest(const double* best, const int32_t* label, const int64_t* sizes, int64_t n,
+                     unsigned long long* out, cudaStream_t s, Counter& c);
+// histogram of label[row0..row1] (inclusive) into hist[k] (zeroed by launcher)
+void launch_hist(const int32_t* label, int64_t row0, int64_t row1, int k, int64_t* hist,
+                 cudaStream_t s, Counter& c);
+// per-cluster position of the thr[j]-th occurrence of j in label[row0..n)
+void launch_events(const int32_t* label, int64_t row0, int64_t n, int k, const int64_t* thr,
+                   int64_t* pos, cudaStream_t s, Counter& c);
+
+}  // namespace pk
