@@ -220,6 +220,14 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* args,
  * [2] predict + reduce, [3] total.  Cholesky-only time in [4]. */
 int pkrrgpu_last_timings(const pkrrgpu_ctx* ctx, double* ms, int n);
 
+/* The context's launch stream (cudaStream_t), so callers can time calls with
+ * CUDA events on the stream the engine launches on. */
+void* pkrrgpu_stream(pkrrgpu_ctx* ctx);
+
+/* FP64 tensor-core peak probe: a DMMA (mma.sync m8n8k4 f64) loop over every
+ * SM; *tflops = measured dense FP64 TFLOP/s (roofline denominator). */
+int pkrrgpu_fp64_peak(pkrrgpu_ctx* ctx, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

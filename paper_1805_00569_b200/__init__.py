@@ -120,6 +120,8 @@ def load_library(path: str = LIB_PATH):
                                           C.c_void_p, _i64]),
         "pkrrgpu_grid_search_ex": (C.c_int, [C.c_void_p, C.POINTER(GridArgs), C.POINTER(GridOut)]),
         "pkrrgpu_last_timings": (C.c_int, [C.c_void_p, _d, C.c_int]),
+        "pkrrgpu_stream": (C.c_void_p, [C.c_void_p]),
+        "pkrrgpu_fp64_peak": (C.c_int, [C.c_void_p, _d]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -190,6 +192,16 @@ class Engine:
     @property
     def launches(self) -> int:
         return int(_lib.pkrrgpu_launch_count(self._h))
+
+    @property
+    def stream_handle(self) -> int:
+        """cudaStream_t the engine launches on (wrap with torch.cuda.ExternalStream)."""
+        return int(_lib.pkrrgpu_stream(self._h))
+
+    def fp64_peak(self) -> float:
+        v = C.c_double(0)
+        _check(_lib.pkrrgpu_fp64_peak(self._h, C.byref(v)))
+        return v.value
 
     def timings(self):
         ms = (C.c_double * 8)()

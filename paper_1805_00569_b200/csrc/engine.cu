@@ -628,6 +628,29 @@ void pkrrgpu_destroy(pkrrgpu_ctx* ctx) {
 
 int64_t pkrrgpu_launch_count(const pkrrgpu_ctx* ctx) { return ctx ? ctx->counter.launches : 0; }
 
+void* pkrrgpu_stream(pkrrgpu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->main) : nullptr; }
+
+int pkrrgpu_fp64_peak(pkrrgpu_ctx* ctx, double* tflops) {
+  API_BEGIN
+  if (!tflops) fail(PKRRGPU_INVALID, "null out");
+  int sms = 0;
+  ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device), "attr");
+  double* sink = nullptr;
+  ck(cudaMalloc(&sink, 4096), "malloc");
+  Timer tm;
+  const int blocks = sms * 2, threads = 512, iters = 20000;
+  pk::launch_dmma_probe(blocks, threads, 200, sink, ctx->main, ctx->counter);
+  ck(cudaEventRecord(tm.a, ctx->main), "event");
+  pk::launch_dmma_probe(blocks, threads, iters, sink, ctx->main, ctx->counter);
+  ck(cudaEventRecord(tm.b, ctx->main), "event");
+  ck(cudaEventSynchronize(tm.b), "sync");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, tm.a, tm.b);
+  cudaFree(sink);
+  *tflops = 2.0 * 256.0 * 8.0 * iters * blocks * (threads / 32) / (ms * 1e-3) / 1e12;
+  API_END
+}
+
 int pkrrgpu_last_timings(const pkrrgpu_ctx* ctx, double* ms, int n) {
   if (!ctx || !ms) return PKRRGPU_INVALID;
   for (int i = 0; i < n && i < 8; ++i) ms[i] = ctx->timings[i];

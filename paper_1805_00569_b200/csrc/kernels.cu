@@ -924,4 +924,27 @@ void launch_events(const int32_t* label, int64_t row0, int64_t n, int k, const i
   ++c.launches;
 }
 
+// ---------------------------------------------------------------------------
+// FP64 tensor-core peak probe
+// ---------------------------------------------------------------------------
+__global__ void dmma_probe_kernel(double* sink, int iters) {
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma(c[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.678) sink[threadIdx.x] = s;
+}
+
+void launch_dmma_probe(int blocks, int threads, int iters, double* sink, cudaStream_t s, Counter& c) {
+  dmma_probe_kernel<<<blocks, threads, 0, s>>>(sink, iters);
+  ++c.launches;
+}
+
 }  // namespace pk

@@ -100,4 +100,7 @@ void launch_hist(const int32_t* label, int64_t row0, int64_t row1, int k, int64_
 void launch_events(const int32_t* label, int64_t row0, int64_t n, int k, const int64_t* thr,
                    int64_t* pos, cudaStream_t s, Counter& c);
 
+// FP64 DMMA throughput probe (8 independent accumulator chains per warp)
+void launch_dmma_probe(int blocks, int threads, int iters, double* sink, cudaStream_t s, Counter& c);
+
 }  // namespace pk
