@@ -9,6 +9,7 @@
 #include <cmath>
 
 #include "gemm_dmma.cuh"
+#include "syrk_persistent.cuh"
 #include "kernels.cuh"
 
 namespace pk {
@@ -175,90 +176,227 @@ void launch_gram_cross(const CUtensorMap& tmQ, const CUtensorMap& tmX, const dou
 }
 
 // ---------------------------------------------------------------------------
-// Cholesky leaf: factor the 128x128 diagonal block (solver.cpp:18-33 order of
-// operations within the block: pivot test, sqrt, column divide, rank-1 update)
-// and invert it in place (LAPACK trti2-style, lower).
+// Cholesky leaf (128 x 128 diagonal block), one CTA of 8 warps:
+//   for each 32-column panel: warp-level register Cholesky of the 32x32
+//   diagonal block (+ its inverse), DMMA panel TRSM and DMMA SYRK inside smem;
+//   then the blocked inverse of the whole 128 block (DMMA) for the panel TRSM
+//   of the outer algorithm and for the triangular solves.
+// Pivot test / sqrt / column divide / rank-1 update per column follow
+// solver.cpp:18-33; only the blocking (summation order) differs.
 // ---------------------------------------------------------------------------
-constexpr int kLeafThreads = 512;
-constexpr int kLS = kNB + 1;  // padded smem stride
-constexpr int kLeafSmem = (kNB * kLS + kNB) * 8;
+constexpr int kLeafThreads = 256;
+constexpr int kLS = 132;  // S stride (doubles): == 4 (mod 16) -> conflict-free DMMA fragments
+constexpr int kBS = 36;   // 32x32 block stride
+constexpr int kLeafSmem = (kNB * kLS + 4 * 32 * kBS + 3 * 32 * kBS) * 8 + 16;
+
+// acc(8x8) += A(rows a0.., k) * Bt(rows b0.., k)^T over k in [0, K), both row-major
+__device__ __forceinline__ void mma_tile_rt(double (&acc)[2], const double* A, int lda,
+                                            const double* Bt, int ldb, int K, int lr, int lk) {
+#pragma unroll 8
+  for (int k = 0; k < K; k += 4)
+    dmma(acc, A[lr * lda + k + lk], Bt[lr * ldb + k + lk]);
+}
+// acc(8x8) += A(rows, k) * B(k, cols) with B row-major [k][n]
+__device__ __forceinline__ void mma_tile_rn(double (&acc)[2], const double* A, int lda,
+                                            const double* B, int ldb, int K, int lr, int lk) {
+#pragma unroll 8
+  for (int k = 0; k < K; k += 4)
+    dmma(acc, A[lr * lda + k + lk], B[(k + lk) * ldb + lr]);
+}
+
+// lane i owns row i of the 32x32 block at Sd (stride kLS); returns the first
+// failing column or -1 (solver.cpp:18-33 per column: test, sqrt, divide, update)
+__device__ __noinline__ int warp_potrf32(double* Sd, int lane) {
+  double a[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) a[c] = Sd[lane * kLS + c];
+  int bad = -1;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    double piv = __shfl_sync(0xffffffffu, a[j], j);
+    if (!(piv > 0.0) && bad < 0) bad = j;
+    piv = bad >= 0 ? 1.0 : piv;  // keep the warp going; the result is discarded
+    const double dj = sqrt(piv);
+    const double l = a[j] / dj;
+    a[j] = lane == j ? dj : (lane > j ? l : 0.0);
+#pragma unroll
+    for (int k = j + 1; k < 32; ++k) {
+      const double lkj = __shfl_sync(0xffffffffu, l, k);
+      a[k] = lane >= k ? a[k] - l * lkj : a[k];
+    }
+  }
+  if (bad < 0) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) Sd[lane * kLS + c] = c <= lane ? a[c] : 0.0;
+  }
+  return bad;
+}
+
+// inverse of the lower 32x32 block at Sd into Db (row-major, stride kBS);
+// lane c computes column c by forward substitution
+__device__ __noinline__ void warp_trtri32(const double* Sd, double* Db, int lane) {
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    double s = lane == i ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) s -= Sd[i * kLS + k] * x[k];
+    x[i] = i >= lane ? s / Sd[i * kLS + i] : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) Db[i * kBS + lane] = x[i];
+}
 
 __global__ void __launch_bounds__(kLeafThreads, 1)
     potrf_leaf_kernel(double* __restrict__ A, int64_t lda, int kb, double* __restrict__ Linv,
                       int* status, int64_t m_valid, int factor) {
   if (status && *reinterpret_cast<volatile int*>(status)) return;
   extern __shared__ double sm[];
-  double* L = sm;              // [128][129]
-  double* tmp = sm + kNB * kLS;  // [128]
-  const int tid = threadIdx.x;
+  double* S = sm;                        // [128][132]: L (lower), X_ij^T in the upper blocks
+  double* D = S + kNB * kLS;             // 4 x [32][36]: inv(L_bb)
+  double* Tt = D + 4 * 32 * kBS;         // 3 x [32][36]: temporaries (transposed)
+  int* flag = reinterpret_cast<int*>(Tt + 3 * 32 * kBS);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int lr = lane >> 2, lk = lane & 3;
   const int64_t base = static_cast<int64_t>(kb) * kNB;
   double* Ab = A + base * lda + base;
-  for (int e = tid; e < kNB * kNB; e += kLeafThreads) {
-    const int r = e / kNB, col = e % kNB;
-    L[r * kLS + col] = col <= r ? Ab[static_cast<int64_t>(r) * lda + col] : 0.0;
+  if (tid == 0) *flag = 0;
+  for (int e = tid; e < kNB * kNB / 2; e += kLeafThreads) {
+    const int r = e / 64, c = (e % 64) * 2;
+    const double2 v = *reinterpret_cast<const double2*>(Ab + static_cast<int64_t>(r) * lda + c);
+    S[r * kLS + c] = c <= r ? v.x : 0.0;
+    S[r * kLS + c + 1] = c + 1 <= r ? v.y : 0.0;
   }
   __syncthreads();
-  if (factor) {
-    for (int j = 0; j < kNB; ++j) {
-      const double piv = L[j * kLS + j];
-      if (!(piv > 0.0)) {
-        if (tid == 0 && status) {
-          status[1] = static_cast<int>(base + j);
+
+  for (int pb = 0; pb < 4; ++pb) {
+    double* Sd = S + (32 * pb) * kLS + 32 * pb;
+    if (factor && warp == 0) {
+      // ---- warp Cholesky of the 32x32 diagonal block: lane i owns row i ----
+      const int bad = warp_potrf32(Sd, lane);
+      const bool ok = bad < 0;
+      if (!ok && lane == 0) {
+        *flag = 1;
+        if (status) {
+          status[1] = static_cast<int>(base + 32 * pb + bad);
           __threadfence();
           atomicExch(&status[0], 1);
         }
-        return;
       }
-      const double dj = sqrt(piv);
-      if (tid > j && tid < kNB) L[tid * kLS + j] = L[tid * kLS + j] / dj;
-      __syncthreads();
-      const int T = kNB - 1 - j;
-      for (int e = tid; e < T * T; e += kLeafThreads) {
-        const int ii = e / T, kk = e % T;
-        if (kk <= ii) {
-          const int i = j + 1 + ii, k = j + 1 + kk;
-          L[i * kLS + k] -= L[i * kLS + j] * L[k * kLS + j];
-        }
+    }
+    __syncthreads();
+    if (*flag) return;
+    if (warp == 0 || !factor) {
+      if (warp == (factor ? 0 : pb % 8)) {
+        // ---- warp inverse of the 32x32 lower block: lane c computes column c ----
+        warp_trtri32(Sd, D + pb * 32 * kBS, lane);
       }
-      if (tid == 0) L[j * kLS + j] = dj;
-      __syncthreads();
     }
-    // L (lower, zero upper inside the block) back to A
-    for (int e = tid; e < kNB * kNB; e += kLeafThreads) {
-      const int r = e / kNB, col = e % kNB;
-      Ab[static_cast<int64_t>(r) * lda + col] = col <= r ? L[r * kLS + col] : 0.0;
+    __syncthreads();
+    if (!factor || pb == 3) continue;
+    // ---- panel TRSM: P = A[R0:128, 32pb:+32] * D_pb^T (in place after a barrier) ----
+    const int R0 = 32 * (pb + 1), nrt = (kNB - R0) / 8;
+    const double* Db = D + pb * 32 * kBS;
+    double res[6][2];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const int t = warp + 8 * q;
+      res[q][0] = res[q][1] = 0.0;
+      if (t < nrt * 4) {
+        const int rt = t >> 2, ct = t & 3;
+        mma_tile_rt(res[q], S + (R0 + 8 * rt) * kLS + 32 * pb, kLS, Db + (8 * ct) * kBS, kBS, 32, lr, lk);
+      }
     }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const int t = warp + 8 * q;
+      if (t < nrt * 4) {
+        const int rt = t >> 2, ct = t & 3;
+        double* dst = S + (R0 + 8 * rt + lr) * kLS + 32 * pb + 8 * ct + 2 * lk;
+        dst[0] = res[q][0];
+        dst[1] = res[q][1];
+      }
+    }
+    __syncthreads();
+    // ---- trailing SYRK inside the block: S[R0:, R0:] -= P P^T (lower 8x8 tiles) ----
+    const int ntl = nrt * (nrt + 1) / 2;
+    for (int t = warp; t < ntl; t += 8) {
+      int rt = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+      while ((rt + 1) * (rt + 2) / 2 <= t) ++rt;
+      while (rt * (rt + 1) / 2 > t) --rt;
+      const int ct = t - rt * (rt + 1) / 2;
+      double acc[2] = {0.0, 0.0};
+      mma_tile_rt(acc, S + (R0 + 8 * rt) * kLS + 32 * pb, kLS, S + (R0 + 8 * ct) * kLS + 32 * pb, kLS, 32,
+                  lr, lk);
+      double* dst = S + (R0 + 8 * rt + lr) * kLS + R0 + 8 * ct + 2 * lk;
+      dst[0] -= acc[0];
+      dst[1] -= acc[1];
+    }
+    __syncthreads();
   }
-  // in-place inverse of the lower triangular block, column j = 127 .. 0
-  const int row = tid >> 2, sub = tid & 3;
-  for (int j = kNB - 1; j >= 0; --j) {
-    if (tid < kNB) tmp[tid] = L[tid * kLS + j];
-    __syncthreads();
-    const double inv_jj = 1.0 / tmp[j];
-    double s = 0.0;
-    if (row > j) {
-      for (int k = j + 1 + sub; k <= row; k += 4) s += L[row * kLS + k] * tmp[k];
+
+  // ---- blocked inverse: X_ij = -D_i * sum_{k=j}^{i-1} L_ik X_kj, stored as X_ij^T in S's upper block (j, i)
+  for (int bi = 1; bi < 4; ++bi) {
+    for (int t = warp; t < bi * 16; t += 8) {
+      const int bj = t >> 4, rt = (t >> 2) & 3, ct = t & 3;
+      double acc[2] = {0.0, 0.0};
+      const double* Arow = S + (32 * bi + 8 * rt) * kLS;
+      // k == j block: X_jj = D_j (row-major [k][n])
+      mma_tile_rn(acc, Arow + 32 * bj, kLS, D + bj * 32 * kBS + 8 * ct, kBS, 32, lr, lk);
+      for (int bk = bj + 1; bk < bi; ++bk)  // X_kj^T rows c live at S[(32 bj + c)][32 bk + kk]
+        mma_tile_rt(acc, Arow + 32 * bk, kLS, S + (32 * bj + 8 * ct) * kLS + 32 * bk, kLS, 32, lr, lk);
+      double* T = Tt + bj * 32 * kBS;  // store T^T
+      const int r = 8 * rt + lr, c = 8 * ct + 2 * lk;
+      T[c * kBS + r] = acc[0];
+      T[(c + 1) * kBS + r] = acc[1];
     }
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    if (sub == 0) {
-      if (row > j) L[row * kLS + j] = -s * inv_jj;
-      else if (row == j) L[row * kLS + j] = inv_jj;
+    __syncthreads();
+    for (int t = warp; t < bi * 16; t += 8) {
+      const int bj = t >> 4, rt = (t >> 2) & 3, ct = t & 3;
+      double acc[2] = {0.0, 0.0};
+      mma_tile_rt(acc, D + bi * 32 * kBS + (8 * rt) * kBS, kBS, Tt + bj * 32 * kBS + (8 * ct) * kBS, kBS, 32,
+                  lr, lk);
+      const int r = 8 * rt + lr, c = 8 * ct + 2 * lk;
+      S[(32 * bj + c) * kLS + 32 * bi + r] = -acc[0];
+      S[(32 * bj + c + 1) * kLS + 32 * bi + r] = -acc[1];
     }
     __syncthreads();
+  }
+
+  if (factor) {
+    for (int e = tid; e < kNB * kNB / 2; e += kLeafThreads) {
+      const int r = e / 64, c = (e % 64) * 2;
+      double2 v;
+      v.x = c <= r ? S[r * kLS + c] : 0.0;
+      v.y = c + 1 <= r ? S[r * kLS + c + 1] : 0.0;
+      *reinterpret_cast<double2*>(Ab + static_cast<int64_t>(r) * lda + c) = v;
+    }
   }
   double* Lo = Linv + base * kNB;
   for (int e = tid; e < kNB * kNB; e += kLeafThreads) {
-    const int r = e / kNB, col = e % kNB;
-    Lo[e] = col <= r ? L[r * kLS + col] : 0.0;
+    const int r = e / kNB, c = e % kNB, bi = r >> 5, bj = c >> 5;
+    double v = 0.0;
+    if (bi == bj) {
+      v = (c <= r) ? D[bi * 32 * kBS + (r & 31) * kBS + (c & 31)] : 0.0;
+    } else if (bi > bj) {
+      v = S[(32 * bj + (c & 31)) * kLS + 32 * bi + (r & 31)];
+    }
+    Lo[e] = v;
   }
 }
+
+static int g_sms = 148;
 
 void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, double* Linv,
                   int64_t mp, int64_t m_valid, int* status, cudaStream_t s, Counter& c) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(potrf_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLeafSmem);
+    cudaFuncSetAttribute(dsyrk_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSyrkSmem);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
     attr = true;
   }
   const int nb = static_cast<int>(mp / kNB);
@@ -282,18 +420,16 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
     t.tiles_n = 1;
     t.abort_flag = status;
     gemm_launch<64, G_STORE>(tmA, tmLinv, t, rem * 2, s, c);
-    // trailing: A22 -= L21 L21^T on lower tiles
-    GemmParams u{};
-    u.a_row0 = u.b_row0 = (kb + 1) * kNB;
-    u.a_k0 = u.b_k0 = kb * kNB;
+    // trailing: A22 -= L21 L21^T on lower tiles (persistent, C staged by TMA)
+    SyrkParams u{};
+    u.row0 = (kb + 1) * kNB;
+    u.k0 = kb * kNB;
     u.ktiles = kNB / kBK;
-    u.C = A;
-    u.ldc = mp;
-    u.c_row0 = u.c_col0 = (kb + 1) * kNB;
-    u.tiles_m = u.tiles_n = rem;
-    u.lower = 1;
+    u.T = rem;
     u.abort_flag = status;
-    gemm_launch<128, G_UPDATE>(tmA, tmA, u, rem * (rem + 1) / 2, s, c);
+    const int ntl = rem * (rem + 1) / 2;
+    dsyrk_persistent_kernel<<<ntl < g_sms ? ntl : g_sms, kSyrkThreads, kSyrkSmem, s>>>(tmA, u);
+    ++c.launches;
   }
 }
 
@@ -782,33 +918,68 @@ void launch_group(const int32_t* label, int64_t n, int k, int64_t* sizes, int64_
   c.launches += 3;
 }
 
-// clustering.cpp:34-49: zero, row-order sums, then * (1.0 / size)
-__global__ void means_kernel(const double* __restrict__ X, int64_t d,
-                             const int64_t* __restrict__ members, const int64_t* __restrict__ start,
-                             const int64_t* __restrict__ sizes, int k, double* centers) {
-  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (e >= static_cast<int64_t>(k) * d) return;
-  const int j = static_cast<int>(e / d);
-  const int64_t f = e % d;
+// clustering.cpp:34-49: zero, row-order sums, then * (1.0 / size).
+// One CTA per (cluster, 32-feature block).  The cluster's member rows (row
+// order) stream through a double-buffered shared-memory ring via cp.async; warp
+// 0 keeps one strictly sequential accumulator per feature, so every centre
+// coordinate is the same chain of roundings as the reference's loop.
+constexpr int kMeansRows = 64, kMeansF = 32, kMeansThreads = 256;
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __restrict__ X, int64_t d,
+                                                              const int64_t* __restrict__ members,
+                                                              const int64_t* __restrict__ start,
+                                                              const int64_t* __restrict__ sizes, int k,
+                                                              double* centers) {
+  __shared__ double buf[2][kMeansRows][kMeansF];
+  const int j = blockIdx.x;
+  const int64_t f0 = static_cast<int64_t>(blockIdx.y) * kMeansF;
+  const int fw = static_cast<int>(d - f0 < kMeansF ? d - f0 : kMeansF);
   const int64_t sz = sizes[j], st = start[j];
+  const int64_t nchunks = (sz + kMeansRows - 1) / kMeansRows;
+  auto issue = [&](int64_t c) {
+    const int64_t r0 = c * kMeansRows;
+    const int rows = static_cast<int>(sz - r0 < kMeansRows ? sz - r0 : kMeansRows);
+    double(*b)[kMeansF] = buf[c & 1];
+    for (int e = threadIdx.x; e < rows * kMeansF; e += kMeansThreads) {
+      const int r = e / kMeansF, f = e % kMeansF;
+      if (f < fw) cp_async8(&b[r][f], X + members[st + r0 + r] * d + f0 + f);
+    }
+    cp_async_commit();
+  };
   double s = 0.0;
-  int64_t q = 0;
-  for (; q + 8 <= sz; q += 8) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = X[members[st + q + u] * d + f];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
+  if (nchunks > 0) issue(0);
+  for (int64_t c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) {
+      issue(c + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (threadIdx.x < kMeansF) {
+      const int64_t r0 = c * kMeansRows;
+      const int rows = static_cast<int>(sz - r0 < kMeansRows ? sz - r0 : kMeansRows);
+      const double(*b)[kMeansF] = buf[c & 1];
+      for (int r = 0; r < rows; ++r) s = __dadd_rn(s, b[r][threadIdx.x]);
+    }
+    __syncthreads();
   }
-  for (; q < sz; ++q) s = __dadd_rn(s, X[members[st + q] * d + f]);
-  centers[e] = sz > 0 ? __dmul_rn(s, __ddiv_rn(1.0, static_cast<double>(sz))) : 0.0;
+  if (threadIdx.x < fw)
+    centers[static_cast<int64_t>(j) * d + f0 + threadIdx.x] =
+        sz > 0 ? __dmul_rn(s, __ddiv_rn(1.0, static_cast<double>(sz))) : 0.0;
 }
 
 void launch_means(const double* X, int64_t d, const int64_t* members, const int64_t* start,
                   const int64_t* sizes, int k, double* centers, cudaStream_t s, Counter& c) {
-  const int64_t total = static_cast<int64_t>(k) * d;
-  means_kernel<<<static_cast<unsigned>((total + 63) / 64), 64, 0, s>>>(X, d, members, start, sizes, k,
-                                                                      centers);
+  dim3 grid(k, static_cast<unsigned>((d + kMeansF - 1) / kMeansF));
+  means_kernel<<<grid, kMeansThreads, 0, s>>>(X, d, members, start, sizes, k, centers);
   ++c.launches;
 }
 
