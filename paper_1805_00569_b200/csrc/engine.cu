@@ -247,7 +247,7 @@ struct PartBuf {
   CUtensorMap tmX, tmA, tmLinv;
 };
 
-void part_alloc(Scope& sc, PartBuf& pb, int64_t m, int64_t d, bool need_K) {
+void part_alloc(Scope& sc, PartBuf& pb, int64_t m, int64_t d, bool need_K, cudaStream_t s) {
   pb.m = m;
   pb.mp = round_up(m, kNB);
   pb.dp = round_up(d, 16);
@@ -256,7 +256,7 @@ void part_alloc(Scope& sc, PartBuf& pb, int64_t m, int64_t d, bool need_K) {
   pb.norms = sc.alloc<double>(pb.mp);
   if (need_K) pb.K = sc.alloc<double>(pb.mp * pb.mp);
   pb.A = sc.alloc<double>(pb.mp * pb.mp);
-  pb.Linv = sc.alloc<double>(pb.mp * kNB);
+  pb.Linv = sc.zeros<double>(pb.mp * kNB, s);  // upper 32x32 blocks stay zero (the leaf writes lower)
   pb.z = sc.alloc<double>(pb.mp);
   pb.alpha = sc.alloc<double>(pb.mp);
   pb.Ka = sc.alloc<double>(pb.mp);
@@ -669,7 +669,7 @@ int pkrrgpu_gram(pkrrgpu_ctx* ctx, const double* A, int64_t na, const double* B,
   const double* dA = sc.in(A, na * d, s);
   const double* dB = same ? dA : sc.in(B, nb * d, s);
   PartBuf pb;
-  part_alloc(sc, pb, nb, d, true);
+  part_alloc(sc, pb, nb, d, true, s);
   int64_t* idx = sc.alloc<int64_t>(nb);
   iota_kernel<<<blocks_for(nb), 256, 0, s>>>(idx, nb);
   ++ctx->counter.launches;
@@ -727,7 +727,7 @@ int pkrrgpu_cholesky(pkrrgpu_ctx* ctx, const double* A, int64_t m, double* L, in
   Scope sc(ctx);
   cudaStream_t s = ctx->main;
   PartBuf pb;
-  part_alloc(sc, pb, m, 1, false);
+  part_alloc(sc, pb, m, 1, false, s);
   ck(cudaMemsetAsync(pb.A, 0, sizeof(double) * pb.mp * pb.mp, s), "memset");
   ck(cudaMemcpy2DAsync(pb.A, sizeof(double) * pb.mp, A, sizeof(double) * m, sizeof(double) * m, m,
                        cudaMemcpyDefault, s),
@@ -757,7 +757,7 @@ int pkrrgpu_solve_spd(pkrrgpu_ctx* ctx, const double* L, int64_t m, const double
   Scope sc(ctx);
   cudaStream_t s = ctx->main;
   PartBuf pb;
-  part_alloc(sc, pb, m, 1, false);
+  part_alloc(sc, pb, m, 1, false, s);
   ck(cudaMemsetAsync(pb.A, 0, sizeof(double) * pb.mp * pb.mp, s), "memset");
   ck(cudaMemcpy2DAsync(pb.A, sizeof(double) * pb.mp, L, sizeof(double) * m, sizeof(double) * m, m,
                        cudaMemcpyDefault, s),
@@ -787,7 +787,7 @@ int pkrrgpu_train_krr(pkrrgpu_ctx* ctx, const double* X, const double* y, int64_
   const double* dX = sc.in(X, m * d, s);
   const double* dy = sc.in(y, m, s);
   PartBuf pb;
-  part_alloc(sc, pb, m, d, true);
+  part_alloc(sc, pb, m, d, true, s);
   int64_t* idx = sc.alloc<int64_t>(m);
   iota_kernel<<<blocks_for(m), 256, 0, s>>>(idx, m);
   ++ctx->counter.launches;
@@ -961,7 +961,7 @@ int pkrrgpu_train_partitions(pkrrgpu_ctx* ctx, int strategy, const double* X, co
   for (int64_t t = 0; t < po.p; ++t) {
     cudaStream_t ws = ctx->work[t % ctx->work.size()];
     PartBuf& pb = parts[t];
-    part_alloc(sc, pb, po.sizes[t], d, true);
+    part_alloc(sc, pb, po.sizes[t], d, true, ws);
     part_load(ctx, pb, dX, dy, d, po.order + po.start[t], ws);
     pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws,
                         ctx->counter);
@@ -1155,8 +1155,8 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   const size_t S = ctx->work.size();
   for (int64_t q : owned) {
     PartBuf& pb = parts[q];
-    part_alloc(sc, pb, po.sizes[q], d, true);
     cudaStream_t ws = ctx->work[q % S];
+    part_alloc(sc, pb, po.sizes[q], d, true, ws);
     part_load(ctx, pb, dX, dy, d, po.order + po.start[q], ws);
     query_alloc(sc, qt[q], tcount[q], pb.dp, pb.mp);
     if (tcount[q] > 0) {

@@ -187,7 +187,7 @@ void launch_gram_cross(const CUtensorMap& tmQ, const CUtensorMap& tmX, const dou
 constexpr int kLeafThreads = 256;
 constexpr int kLS = 132;  // S stride (doubles): == 4 (mod 16) -> conflict-free DMMA fragments
 constexpr int kBS = 36;   // 32x32 block stride
-constexpr int kLeafSmem = (kNB * kLS + 4 * 32 * kBS + 3 * 32 * kBS) * 8 + 16;
+constexpr int kLeafSmem = (kNB * kLS + 4 * 32 * kBS + 3 * 32 * kBS) * 8 + 32;
 
 // acc(8x8) += A(rows a0.., k) * Bt(rows b0.., k)^T over k in [0, K), both row-major
 __device__ __forceinline__ void mma_tile_rt(double (&acc)[2], const double* A, int lda,
@@ -216,8 +216,10 @@ __device__ __noinline__ int warp_potrf32(double* Sd, int lane) {
     double piv = __shfl_sync(0xffffffffu, a[j], j);
     if (!(piv > 0.0) && bad < 0) bad = j;
     piv = bad >= 0 ? 1.0 : piv;  // keep the warp going; the result is discarded
-    const double dj = sqrt(piv);
-    const double l = a[j] / dj;
+    // one reciprocal square root on the pivot chain instead of sqrt + divide
+    const double rj = rsqrt(piv);
+    const double dj = piv * rj;
+    const double l = a[j] * rj;
     a[j] = lane == j ? dj : (lane > j ? l : 0.0);
 #pragma unroll
     for (int k = j + 1; k < 32; ++k) {
@@ -235,17 +237,33 @@ __device__ __noinline__ int warp_potrf32(double* Sd, int lane) {
 // inverse of the lower 32x32 block at Sd into Db (row-major, stride kBS);
 // lane c computes column c by forward substitution
 __device__ __noinline__ void warp_trtri32(const double* Sd, double* Db, int lane) {
+  const double rinv = 1.0 / Sd[lane * kLS + lane];  // lane i: 1 / L_ii, off the chain
   double x[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
-    double s = lane == i ? 1.0 : 0.0;
+    double s0 = lane == i ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // 4 chains
 #pragma unroll
-    for (int k = 0; k < i; ++k) s -= Sd[i * kLS + k] * x[k];
-    x[i] = i >= lane ? s / Sd[i * kLS + i] : 0.0;
+    for (int k = 0; k < i; ++k) {
+      const double t = Sd[i * kLS + k] * x[k];
+      if ((k & 3) == 0) s0 -= t;
+      else if ((k & 3) == 1) s1 -= t;
+      else if ((k & 3) == 2) s2 -= t;
+      else s3 -= t;
+    }
+    const double ri = __shfl_sync(0xffffffffu, rinv, i);
+    x[i] = i >= lane ? ((s0 + s1) + (s2 + s3)) * ri : 0.0;
   }
 #pragma unroll
   for (int i = 0; i < 32; ++i) Db[i * kBS + lane] = x[i];
 }
+
+#ifdef PKRR_LEAF_TRACE
+__device__ long long g_leaf_trace[64];
+#define LEAF_MARK(i) \
+  if (threadIdx.x == 0) g_leaf_trace[i] = clock64();
+#else
+#define LEAF_MARK(i)
+#endif
 
 __global__ void __launch_bounds__(kLeafThreads, 1)
     potrf_leaf_kernel(double* __restrict__ A, int64_t lda, int kb, double* __restrict__ Linv,
@@ -255,22 +273,29 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
   double* S = sm;                        // [128][132]: L (lower), X_ij^T in the upper blocks
   double* D = S + kNB * kLS;             // 4 x [32][36]: inv(L_bb)
   double* Tt = D + 4 * 32 * kBS;         // 3 x [32][36]: temporaries (transposed)
-  int* flag = reinterpret_cast<int*>(Tt + 3 * 32 * kBS);
+  uint64_t* lbar = reinterpret_cast<uint64_t*>(Tt + 3 * 32 * kBS);
+  int* flag = reinterpret_cast<int*>(lbar + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int lr = lane >> 2, lk = lane & 3;
   const int64_t base = static_cast<int64_t>(kb) * kNB;
   double* Ab = A + base * lda + base;
-  if (tid == 0) *flag = 0;
-  for (int e = tid; e < kNB * kNB / 2; e += kLeafThreads) {
-    const int r = e / 64, c = (e % 64) * 2;
-    const double2 v = *reinterpret_cast<const double2*>(Ab + static_cast<int64_t>(r) * lda + c);
-    S[r * kLS + c] = c <= r ? v.x : 0.0;
-    S[r * kLS + c + 1] = c + 1 <= r ? v.y : 0.0;
+  // stage the 128 x 128 block: 128 row copies of 1 KB in flight at once (the
+  // strict upper triangle is stale but never read as data)
+  if (tid == 0) {
+    *flag = 0;
+    mbar_init(lbar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(lbar, kNB * kNB * 8);
+    for (int r = 0; r < kNB; ++r) bulk_load(S + r * kLS, Ab + static_cast<int64_t>(r) * lda, kNB * 8, lbar);
   }
+  LEAF_MARK(0);
   __syncthreads();
+  mbar_wait(lbar, 0);
+  LEAF_MARK(1);
 
   for (int pb = 0; pb < 4; ++pb) {
     double* Sd = S + (32 * pb) * kLS + 32 * pb;
+    LEAF_MARK(2 + 5 * pb);
     if (factor && warp == 0) {
       // ---- warp Cholesky of the 32x32 diagonal block: lane i owns row i ----
       const int bad = warp_potrf32(Sd, lane);
@@ -285,6 +310,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
       }
     }
     __syncthreads();
+    LEAF_MARK(3 + 5 * pb);
     if (*flag) return;
     if (warp == 0 || !factor) {
       if (warp == (factor ? 0 : pb % 8)) {
@@ -293,6 +319,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
       }
     }
     __syncthreads();
+    LEAF_MARK(4 + 5 * pb);
     if (!factor || pb == 3) continue;
     // ---- panel TRSM: P = A[R0:128, 32pb:+32] * D_pb^T (in place after a barrier) ----
     const int R0 = 32 * (pb + 1), nrt = (kNB - R0) / 8;
@@ -319,6 +346,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
       }
     }
     __syncthreads();
+    LEAF_MARK(5 + 5 * pb);
     // ---- trailing SYRK inside the block: S[R0:, R0:] -= P P^T (lower 8x8 tiles) ----
     const int ntl = nrt * (nrt + 1) / 2;
     for (int t = warp; t < ntl; t += 8) {
@@ -336,54 +364,56 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
     __syncthreads();
   }
 
-  // ---- blocked inverse: X_ij = -D_i * sum_{k=j}^{i-1} L_ik X_kj, stored as X_ij^T in S's upper block (j, i)
+  LEAF_MARK(22);
+  // ---- blocked inverse: X_ij = -D_i * sum_{k=j}^{i-1} L_ik X_kj, X_ij stored (not
+  // transposed) in S's free upper block (j, i); T_j row-major in Tt[j]
   for (int bi = 1; bi < 4; ++bi) {
     for (int t = warp; t < bi * 16; t += 8) {
       const int bj = t >> 4, rt = (t >> 2) & 3, ct = t & 3;
       double acc[2] = {0.0, 0.0};
       const double* Arow = S + (32 * bi + 8 * rt) * kLS;
-      // k == j block: X_jj = D_j (row-major [k][n])
-      mma_tile_rn(acc, Arow + 32 * bj, kLS, D + bj * 32 * kBS + 8 * ct, kBS, 32, lr, lk);
-      for (int bk = bj + 1; bk < bi; ++bk)  // X_kj^T rows c live at S[(32 bj + c)][32 bk + kk]
-        mma_tile_rt(acc, Arow + 32 * bk, kLS, S + (32 * bj + 8 * ct) * kLS + 32 * bk, kLS, 32, lr, lk);
-      double* T = Tt + bj * 32 * kBS;  // store T^T
-      const int r = 8 * rt + lr, c = 8 * ct + 2 * lk;
-      T[c * kBS + r] = acc[0];
-      T[(c + 1) * kBS + r] = acc[1];
+      mma_tile_rn(acc, Arow + 32 * bj, kLS, D + bj * 32 * kBS + 8 * ct, kBS, 32, lr, lk);  // X_jj = D_j
+      for (int bk = bj + 1; bk < bi; ++bk)
+        mma_tile_rn(acc, Arow + 32 * bk, kLS, S + (32 * bj) * kLS + 32 * bk + 8 * ct, kLS,
+                    32, lr, lk);
+      double* T = Tt + bj * 32 * kBS;
+      *reinterpret_cast<double2*>(T + (8 * rt + lr) * kBS + 8 * ct + 2 * lk) = make_double2(acc[0], acc[1]);
     }
     __syncthreads();
     for (int t = warp; t < bi * 16; t += 8) {
       const int bj = t >> 4, rt = (t >> 2) & 3, ct = t & 3;
       double acc[2] = {0.0, 0.0};
-      mma_tile_rt(acc, D + bi * 32 * kBS + (8 * rt) * kBS, kBS, Tt + bj * 32 * kBS + (8 * ct) * kBS, kBS, 32,
-                  lr, lk);
-      const int r = 8 * rt + lr, c = 8 * ct + 2 * lk;
-      S[(32 * bj + c) * kLS + 32 * bi + r] = -acc[0];
-      S[(32 * bj + c + 1) * kLS + 32 * bi + r] = -acc[1];
+      mma_tile_rn(acc, D + bi * 32 * kBS + (8 * rt) * kBS, kBS, Tt + bj * 32 * kBS + 8 * ct, kBS, 32, lr, lk);
+      *reinterpret_cast<double2*>(S + (32 * bj + 8 * rt + lr) * kLS + 32 * bi + 8 * ct + 2 * lk) =
+          make_double2(-acc[0], -acc[1]);
     }
     __syncthreads();
   }
 
-  if (factor) {
-    for (int e = tid; e < kNB * kNB / 2; e += kLeafThreads) {
-      const int r = e / 64, c = (e % 64) * 2;
-      double2 v;
-      v.x = c <= r ? S[r * kLS + c] : 0.0;
-      v.y = c + 1 <= r ? S[r * kLS + c + 1] : 0.0;
-      *reinterpret_cast<double2*>(Ab + static_cast<int64_t>(r) * lda + c) = v;
+  LEAF_MARK(23);
+  // write-out by the bulk-copy engine: L rows (the strict upper part of the
+  // diagonal block is never read as data) and the 10 lower 32x32 blocks of
+  // inv(L) (the upper blocks of the Linv scratch are zeroed once at allocation)
+  fence_proxy_async();
+  __syncthreads();
+  if (warp == 0) {
+    if (factor)
+      for (int r = lane; r < kNB; r += 32) bulk_store(Ab + static_cast<int64_t>(r) * lda, S + r * kLS, kNB * 8);
+    bulk_commit();
+  } else {
+    // 10 lower 32x32 blocks of inv(L): warps 1..7, one 32-double row segment per warp step
+    double* Lo = Linv + base * kNB;
+    for (int q = warp - 1; q < 10 * 32; q += 7) {
+      const int blk = q >> 5, r = q & 31;
+      int bi = 0;
+      while ((bi + 1) * (bi + 2) / 2 <= blk) ++bi;
+      const int bj = blk - bi * (bi + 1) / 2;
+      const double* src = bi == bj ? D + bi * 32 * kBS + r * kBS : S + (32 * bj + r) * kLS + 32 * bi;
+      Lo[(32 * bi + r) * kNB + 32 * bj + lane] = src[lane];
     }
   }
-  double* Lo = Linv + base * kNB;
-  for (int e = tid; e < kNB * kNB; e += kLeafThreads) {
-    const int r = e / kNB, c = e % kNB, bi = r >> 5, bj = c >> 5;
-    double v = 0.0;
-    if (bi == bj) {
-      v = (c <= r) ? D[bi * 32 * kBS + (r & 31) * kBS + (c & 31)] : 0.0;
-    } else if (bi > bj) {
-      v = S[(32 * bj + (c & 31)) * kLS + 32 * bi + (r & 31)];
-    }
-    Lo[e] = v;
-  }
+  if (warp == 0) bulk_wait_read0();  // smem drained; global completion is ordered by the kernel boundary
+  LEAF_MARK(24);
 }
 
 static int g_sms = 148;
@@ -943,13 +973,25 @@ __global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __re
   const int fw = static_cast<int>(d - f0 < kMeansF ? d - f0 : kMeansF);
   const int64_t sz = sizes[j], st = start[j];
   const int64_t nchunks = (sz + kMeansRows - 1) / kMeansRows;
+  // thread -> feature f, rows r0 + tid/32 + 8q (q < 8): indices loaded first (batched),
+  // then the 8-byte async copies
+  const int f = threadIdx.x & (kMeansF - 1), rsub = threadIdx.x >> 5;
   auto issue = [&](int64_t c) {
     const int64_t r0 = c * kMeansRows;
     const int rows = static_cast<int>(sz - r0 < kMeansRows ? sz - r0 : kMeansRows);
+    int64_t idx[kMeansRows / 8];
+#pragma unroll
+    for (int q = 0; q < kMeansRows / 8; ++q) {
+      const int r = rsub + 8 * q;
+      idx[q] = r < rows ? __ldg(members + st + r0 + r) : 0;
+    }
     double(*b)[kMeansF] = buf[c & 1];
-    for (int e = threadIdx.x; e < rows * kMeansF; e += kMeansThreads) {
-      const int r = e / kMeansF, f = e % kMeansF;
-      if (f < fw) cp_async8(&b[r][f], X + members[st + r0 + r] * d + f0 + f);
+    if (f < fw) {
+#pragma unroll
+      for (int q = 0; q < kMeansRows / 8; ++q) {
+        const int r = rsub + 8 * q;
+        if (r < rows) cp_async8(&b[r][f], X + idx[q] * d + f0 + f);
+      }
     }
     cp_async_commit();
   };
@@ -967,7 +1009,15 @@ __global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __re
       const int64_t r0 = c * kMeansRows;
       const int rows = static_cast<int>(sz - r0 < kMeansRows ? sz - r0 : kMeansRows);
       const double(*b)[kMeansF] = buf[c & 1];
-      for (int r = 0; r < rows; ++r) s = __dadd_rn(s, b[r][threadIdx.x]);
+      int r = 0;
+      for (; r + 8 <= rows; r += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = b[r + u][threadIdx.x];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
+      }
+      for (; r < rows; ++r) s = __dadd_rn(s, b[r][threadIdx.x]);
     }
     __syncthreads();
   }

@@ -137,11 +137,11 @@ __global__ void __launch_bounds__(kSyrkThreads, 1)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int r = wm * 64 + i * 8 + lr, c = wn * 32 + j * 8 + 2 * lk;
-        double2* q = reinterpret_cast<double2*>(cbuf + c_off(r, c));
-        double2 v = *q;
+        const uint32_t q = smem_u32(cbuf) + c_off(r, c);
+        double2 v = lds_f64x2(q);
         v.x -= acc[i][j][0];
         v.y -= acc[i][j][1];
-        *q = v;
+        sts_f64x2(q, v);
       }
     fence_proxy_async();
     consumer_sync(kConsumerWarps * 32);
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1)
       mbar_arrive(cempty);
     }
   }
-  if (threadIdx.x == 128) bulk_wait0();
+  if (threadIdx.x == 128) bulk_wait_read0();
 }
 
 }  // namespace pk
