@@ -217,7 +217,8 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* args,
 
 /* Device time (ms, CUDA events on the engine's streams) spent in the last
  * grid call by phase: [0] partition, [1] train (gram + Cholesky + solves),
- * [2] predict + reduce, [3] total.  Cholesky-only time in [4]. */
+ * [2] solves + predict, [3] total, [4] Cholesky, [5] gram; [8 + t] = when part
+ * t's first Cholesky finished, ms after that phase started (n >= 8 + p). */
 int pkrrgpu_last_timings(const pkrrgpu_ctx* ctx, double* ms, int n);
 
 /* The context's launch stream (cudaStream_t), so callers can time calls with

@@ -203,10 +203,13 @@ class Engine:
         _check(_lib.pkrrgpu_fp64_peak(self._h, C.byref(v)))
         return v.value
 
-    def timings(self):
-        ms = (C.c_double * 8)()
-        _lib.pkrrgpu_last_timings(self._h, ms, 8)
-        return dict(partition=ms[0], train=ms[1], predict=ms[2], total=ms[3], cholesky=ms[4], gram=ms[5])
+    def timings(self, parts: int = 0):
+        ms = (C.c_double * (8 + parts))()
+        _lib.pkrrgpu_last_timings(self._h, ms, 8 + parts)
+        out = dict(partition=ms[0], train=ms[1], predict=ms[2], total=ms[3], cholesky=ms[4], gram=ms[5])
+        if parts:
+            out["part_chol_end_ms"] = [ms[8 + i] for i in range(parts)]
+        return out
 
     # ---- kernel.hpp ---------------------------------------------------------
     def gram(self, X, Y, sigma):

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -107,6 +108,7 @@ struct pkrrgpu_ctx {
   std::vector<cudaStream_t> work;
   pk::Counter counter;
   double timings[8] = {0};
+  std::vector<double> part_ms;  // last grid call: per-part Cholesky end, ms after the phase start
   std::multimap<size_t, void*> free_blocks;
   std::map<void*, size_t> live;
   size_t cached_bytes = 0;
@@ -605,9 +607,19 @@ int pkrrgpu_create(int device, pkrrgpu_ctx** out) {
     if (prop.major != 10) fail(PKRRGPU_CUDA, "pkrr-b200 needs an sm_100a (Blackwell) device");
     auto* c = new pkrrgpu_ctx();
     c->device = device;
+    if (const char* g = std::getenv("PKRR_PANEL_GROUP")) pk::set_panel_group(std::atoi(g));
+    if (const char* g = std::getenv("PKRR_SYRK_PERSISTENT")) pk::set_syrk_persistent(std::atoi(g));
     ck(cudaStreamCreateWithFlags(&c->main, cudaStreamNonBlocking), "stream");
+    // work streams in decreasing priority: the grid maps parts to them largest
+    // first (LPT on one GPU), so the critical part wins the block scheduler
+    int least = 0, greatest = 0;
+    ck(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
     c->work.resize(8);
-    for (auto& s : c->work) ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    for (size_t i = 0; i < c->work.size(); ++i) {
+      int prio = greatest + static_cast<int>(i);
+      if (prio > least) prio = least;
+      ck(cudaStreamCreateWithPriority(&c->work[i], cudaStreamNonBlocking, prio), "stream");
+    }
     *out = c;
     return PKRRGPU_OK;
   } catch (const Fail& f) {
@@ -654,6 +666,8 @@ int pkrrgpu_fp64_peak(pkrrgpu_ctx* ctx, double* tflops) {
 int pkrrgpu_last_timings(const pkrrgpu_ctx* ctx, double* ms, int n) {
   if (!ctx || !ms) return PKRRGPU_INVALID;
   for (int i = 0; i < n && i < 8; ++i) ms[i] = ctx->timings[i];
+  // [8 ...]: per-part Cholesky completion (ms after the first Cholesky phase start)
+  for (int i = 8; i < n && i - 8 < static_cast<int>(ctx->part_ms.size()); ++i) ms[i] = ctx->part_ms[i - 8];
   return PKRRGPU_OK;
 }
 
@@ -1153,9 +1167,15 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
 
   double f_chol = 0, f_gram = 0, f_other = 0;
   const size_t S = ctx->work.size();
+  // owned parts sorted by size (largest first) -> stream rank = priority rank
+  std::vector<int64_t> by_size(owned);
+  std::stable_sort(by_size.begin(), by_size.end(),
+                   [&](int64_t x, int64_t y) { return po.sizes[x] > po.sizes[y]; });
+  std::vector<size_t> sidx(p, 0);
+  for (size_t r = 0; r < by_size.size(); ++r) sidx[by_size[r]] = r % S;
   for (int64_t q : owned) {
     PartBuf& pb = parts[q];
-    cudaStream_t ws = ctx->work[q % S];
+    cudaStream_t ws = ctx->work[sidx[q]];
     part_alloc(sc, pb, po.sizes[q], d, true, ws);
     part_load(ctx, pb, dX, dy, d, po.order + po.start[q], ws);
     query_alloc(sc, qt[q], tcount[q], pb.dp, pb.mp);
@@ -1177,7 +1197,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
     cudaEvent_t e;
     for (int64_t q : owned) {
       ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-      ck(cudaEventRecord(e, ctx->work[q % S]), "event");
+      ck(cudaEventRecord(e, ctx->work[sidx[q]]), "event");
       ck(cudaStreamWaitEvent(s, e, 0), "wait");
       evs.push_back(e);
     }
@@ -1191,9 +1211,11 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
     ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     ck(cudaEventRecord(e, s), "event");
     evs.push_back(e);
-    for (int64_t q : owned) ck(cudaStreamWaitEvent(ctx->work[q % S], e, 0), "wait");
+    for (int64_t q : owned) ck(cudaStreamWaitEvent(ctx->work[sidx[q]], e, 0), "wait");
   };
   double ms_gram = 0, ms_chol = 0, ms_pred = 0;
+  std::vector<cudaEvent_t> part_end(p, nullptr);
+  cudaEvent_t chol0_start = nullptr;
   cudaEvent_t e0 = join();
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gram_w, chol_w, pred_w;
   for (int64_t si = 0; si < ns; ++si) {
@@ -1201,7 +1223,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
     fork();
     for (int64_t q : owned) {
       PartBuf& pb = parts[q];
-      cudaStream_t ws = ctx->work[q % S];
+      cudaStream_t ws = ctx->work[sidx[q]];
       pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws,
                           ctx->counter);
       if (tcount[q] > 0)
@@ -1221,18 +1243,26 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
       fork();
       for (int64_t q : owned) {
         PartBuf& pb = parts[q];
-        cudaStream_t ws = ctx->work[q % S];
+        cudaStream_t ws = ctx->work[sidx[q]];
         int* st = dstatus + (cell * p + q) * 2;
         pk::launch_assemble(pb.K, pb.A, pb.mp, lambda * static_cast<double>(pb.m), st, ws, ctx->counter);
         pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, st, ws, ctx->counter);
         f_chol += chol_flops(pb.m);
+        if (li == 0 && si == 0) {
+          cudaEvent_t pe;
+          ck(cudaEventCreate(&pe), "event");
+          ck(cudaEventRecord(pe, ws), "event");
+          part_end[q] = pe;
+          evs.push_back(pe);
+        }
       }
+      if (li == 0 && si == 0) chol0_start = e1;
       cudaEvent_t e2 = join();
       chol_w.push_back({e1, e2});
       fork();
       for (int64_t q : owned) {
         PartBuf& pb = parts[q];
-        cudaStream_t ws = ctx->work[q % S];
+        cudaStream_t ws = ctx->work[sidx[q]];
         int* st = dstatus + (cell * p + q) * 2;
         double* rs = dres + (cell * p + q) * 4;
         const double shift = lambda * static_cast<double>(pb.m);
@@ -1295,6 +1325,13 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
     ctx->timings[4] = ms_chol;
     ctx->timings[5] = ms_gram;
   }
+  ctx->part_ms.assign(p, 0.0);
+  for (int64_t q = 0; q < p; ++q)
+    if (part_end[q] && chol0_start) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, chol0_start, part_end[q]);
+      ctx->part_ms[q] = ms;
+    }
   for (auto e : evs) cudaEventDestroy(e);
 
   const std::vector<int> st = to_host(dstatus, ncell * p * 2, s);

@@ -418,6 +418,16 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
 
 static int g_sms = 148;
 
+// Panel-grouped blocked right-looking Cholesky.  G consecutive 128-column panels
+// are factored with narrow column updates restricted to the group (leaf + DMMA
+// TRSM each), then ONE trailing SYRK with K = 128*G updates the rest: the
+// trailing matrix is streamed through HBM nb/G times instead of nb times.
+static int g_panel_group = 4;
+static int g_syrk_persistent = 0;  // 0: one tile per CTA (priority-responsive); 1: one CTA per SM
+
+void set_panel_group(int g) { g_panel_group = g < 1 ? 1 : (g > 8 ? 8 : g); }
+void set_syrk_persistent(int on) { g_syrk_persistent = on; }
+
 void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, double* Linv,
                   int64_t mp, int64_t m_valid, int* status, cudaStream_t s, Counter& c) {
   static bool attr = false;
@@ -430,35 +440,57 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
     attr = true;
   }
   const int nb = static_cast<int>(mp / kNB);
-  for (int kb = 0; kb < nb; ++kb) {
-    potrf_leaf_kernel<<<1, kLeafThreads, kLeafSmem, s>>>(A, mp, kb, Linv, status, m_valid, 1);
-    ++c.launches;
-    const int rem = nb - 1 - kb;
+  const int G = g_panel_group;
+  for (int kb0 = 0; kb0 < nb; kb0 += G) {
+    const int kend = kb0 + G < nb ? kb0 + G : nb;
+    for (int kb = kb0; kb < kend; ++kb) {
+      if (kb > kb0) {
+        // column block kb (rows >= kb) -= A[:, kb0:kb] A[kb, kb0:kb]^T
+        GemmParams u{};
+        u.a_row0 = kb * kNB;
+        u.b_row0 = kb * kNB;
+        u.a_k0 = u.b_k0 = kb0 * kNB;
+        u.ktiles = (kb - kb0) * (kNB / kBK);
+        u.C = A;
+        u.ldc = mp;
+        u.c_row0 = u.c_col0 = kb * kNB;
+        u.tiles_m = nb - kb;
+        u.tiles_n = 1;
+        u.abort_flag = status;
+        gemm_launch<128, G_UPDATE>(tmA, tmA, u, nb - kb, s, c);
+      }
+      potrf_leaf_kernel<<<1, kLeafThreads, kLeafSmem, s>>>(A, mp, kb, Linv, status, m_valid, 1);
+      ++c.launches;
+      const int rem = nb - 1 - kb;
+      if (rem <= 0) continue;
+      // panel: A21 := A21 * inv(L11)^T  (in place, 64-row blocks)
+      GemmParams t{};
+      t.a_row0 = (kb + 1) * kNB;
+      t.a_k0 = kb * kNB;
+      t.b_row0 = kb * kNB;
+      t.b_k0 = 0;
+      t.ktiles = kNB / kBK;
+      t.C = A;
+      t.ldc = mp;
+      t.c_row0 = (kb + 1) * kNB;
+      t.c_col0 = kb * kNB;
+      t.tiles_m = rem * 2;
+      t.tiles_n = 1;
+      t.abort_flag = status;
+      gemm_launch<64, G_STORE>(tmA, tmLinv, t, rem * 2, s, c);
+    }
+    const int rem = nb - kend;
     if (rem <= 0) continue;
-    // panel: A21 := A21 * inv(L11)^T  (in place, 64-row blocks)
-    GemmParams t{};
-    t.a_row0 = (kb + 1) * kNB;
-    t.a_k0 = kb * kNB;
-    t.b_row0 = kb * kNB;
-    t.b_k0 = 0;
-    t.ktiles = kNB / kBK;
-    t.C = A;
-    t.ldc = mp;
-    t.c_row0 = (kb + 1) * kNB;
-    t.c_col0 = kb * kNB;
-    t.tiles_m = rem * 2;
-    t.tiles_n = 1;
-    t.abort_flag = status;
-    gemm_launch<64, G_STORE>(tmA, tmLinv, t, rem * 2, s, c);
-    // trailing: A22 -= L21 L21^T on lower tiles (persistent, C staged by TMA)
+    // trailing: A22 -= L21 L21^T over the whole group (K = 128 * group), persistent, C staged by TMA
     SyrkParams u{};
-    u.row0 = (kb + 1) * kNB;
-    u.k0 = kb * kNB;
-    u.ktiles = kNB / kBK;
+    u.row0 = kend * kNB;
+    u.k0 = kb0 * kNB;
+    u.ktiles = (kend - kb0) * (kNB / kBK);
     u.T = rem;
     u.abort_flag = status;
     const int ntl = rem * (rem + 1) / 2;
-    dsyrk_persistent_kernel<<<ntl < g_sms ? ntl : g_sms, kSyrkThreads, kSyrkSmem, s>>>(tmA, u);
+    const int grid = g_syrk_persistent ? (ntl < g_sms ? ntl : g_sms) : ntl;
+    dsyrk_persistent_kernel<<<grid, kSyrkThreads, kSyrkSmem, s>>>(tmA, u);
     ++c.launches;
   }
 }

@@ -42,6 +42,10 @@ void launch_gram_cross(const CUtensorMap& tmQ, const CUtensorMap& tmX, const dou
 // status[0] = abort flag, status[1] = first failing global column (int).
 void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, double* Linv,
                   int64_t mp, int64_t m_valid, int* status, cudaStream_t s, Counter& c);
+// Number of 128-column panels per trailing update (K = 128 * G); default 4.
+void set_panel_group(int g);
+// SYRK grid: 0 = one 128x128 tile per CTA (default), 1 = persistent (one CTA per SM).
+void set_syrk_persistent(int on);
 // Recompute inv(L_kk) for every diagonal block of an existing factor.
 void launch_diag_inverses(const double* L, int64_t mp, double* Linv, cudaStream_t s, Counter& c);
 // Zero the strict upper triangle (API parity with solver.cpp:34).
