@@ -221,15 +221,12 @@ def run_ours(args):
         tms = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tms, op=dist.ReduceOp.MAX)
         ms = float(tms.item())
+        from paper_1805_00569_b200 import sharding
         parts = res.parts
-        sse = torch.from_numpy(parts["part_sse"].copy()).to(dev)
-        esse = torch.from_numpy(parts["part_eval_sse"].copy()).to(dev)
-        fl = torch.from_numpy(parts["part_failed"].astype(np.float64)).to(dev)
-        for tsr in (sse, esse):
-            dist.all_reduce(tsr, op=dist.ReduceOp.SUM)  # disjoint parts: x + 0 is exact
-        dist.all_reduce(fl, op=dist.ReduceOp.MAX)
-        val_mse, failed, best = pk.combine_parts(sse.cpu().numpy(), fl.cpu().numpy() > 0, N_VAL)
-        test_mse, _, _ = pk.combine_parts(esse.cpu().numpy(), fl.cpu().numpy() > 0, N_TEST)
+        sse, fl = sharding.allreduce_tables(parts["part_sse"], parts["part_failed"], dist, device=dev)
+        esse, _ = sharding.allreduce_tables(parts["part_eval_sse"], parts["part_failed"], dist, device=dev)
+        val_mse, failed, best = sharding.combine(sse, fl, N_VAL)
+        test_mse, _, _ = sharding.combine(esse, fl, N_TEST)
     else:
         val_mse, test_mse, best = res.mse, res.eval_mse, res.best_index
     samples = n_train + N_VAL + N_TEST
