@@ -78,6 +78,9 @@ __device__ __forceinline__ double2 lds_f64x2(uint32_t addr) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ void sts_f64(uint32_t addr, double v) {
+  asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(addr), "d"(v) : "memory");
+}
 __device__ __forceinline__ void sts_f64x2(uint32_t addr, double2 v) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
 }

@@ -109,6 +109,7 @@ struct pkrrgpu_ctx {
   pk::Counter counter;
   double timings[8] = {0};
   std::vector<double> part_ms;  // last grid call: per-part Cholesky end, ms after the phase start
+  void* pinned = nullptr;  // 64 KB pinned staging for small device->host reads
   std::multimap<size_t, void*> free_blocks;
   std::map<void*, size_t> live;
   size_t cached_bytes = 0;
@@ -341,8 +342,18 @@ void kmeans_device(pkrrgpu_ctx* ctx, Scope& sc, const double* dX, int64_t n, int
     pk::launch_assign(dX, n, d, xnorm, co.centers, cnorm, k, 0, nullptr, 0, co.label, best, changed, s,
                       ctx->counter);
     group_labels(ctx, sc, co.label, n, k, co, s);
-    sz = to_host(co.sizes, k, s);
-    unsigned long long ch = to_host(changed, 1, s)[0];
+    // one round trip per iteration: sizes and the changed count together
+    {
+      auto* pin = static_cast<unsigned char*>(ctx->pinned);
+      ck(cudaMemcpyAsync(pin, co.sizes, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s), "D2H");
+      ck(cudaMemcpyAsync(pin + sizeof(int64_t) * k, changed, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                         s),
+         "D2H");
+      ck(cudaStreamSynchronize(s), "sync");
+      std::memcpy(sz.data(), pin, sizeof(int64_t) * k);
+    }
+    unsigned long long ch = 0;
+    std::memcpy(&ch, static_cast<unsigned char*>(ctx->pinned) + sizeof(int64_t) * k, sizeof(ch));
     // empty-cluster reseed (clustering.cpp:98-117)
     bool reseeded = false;
     for (int j = 0; j < k; ++j) {
@@ -610,6 +621,7 @@ int pkrrgpu_create(int device, pkrrgpu_ctx** out) {
     if (const char* g = std::getenv("PKRR_PANEL_GROUP")) pk::set_panel_group(std::atoi(g));
     if (const char* g = std::getenv("PKRR_SYRK_PERSISTENT")) pk::set_syrk_persistent(std::atoi(g));
     ck(cudaStreamCreateWithFlags(&c->main, cudaStreamNonBlocking), "stream");
+    ck(cudaMallocHost(&c->pinned, 64 * 1024), "pinned");
     // work streams in decreasing priority: the grid maps parts to them largest
     // first (LPT on one GPU), so the critical part wins the block scheduler
     int least = 0, greatest = 0;
@@ -635,6 +647,7 @@ void pkrrgpu_destroy(pkrrgpu_ctx* ctx) {
   for (auto& kv : ctx->live) cudaFree(kv.first);
   for (auto s : ctx->work) cudaStreamDestroy(s);
   cudaStreamDestroy(ctx->main);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;
 }
 
@@ -1191,106 +1204,79 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
       }
     }
   }
-  // phase events (joins on the main stream) for the per-phase device timings
+  // Each part flows gram -> (assemble -> Cholesky -> solves -> predict) per cell on
+  // its own prioritised stream, with no cross-part joins: a small part's gram or
+  // solves overlap the large part's Cholesky.  Phase times are the UNION of the
+  // per-(part, cell) intervals, from events on the launching streams.
   std::vector<cudaEvent_t> evs;
-  auto join = [&]() {
+  auto ev_on = [&](cudaStream_t st) {
     cudaEvent_t e;
-    for (int64_t q : owned) {
-      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-      ck(cudaEventRecord(e, ctx->work[sidx[q]]), "event");
-      ck(cudaStreamWaitEvent(s, e, 0), "wait");
-      evs.push_back(e);
-    }
     ck(cudaEventCreate(&e), "event");
-    ck(cudaEventRecord(e, s), "event");
+    ck(cudaEventRecord(e, st), "event");
     evs.push_back(e);
     return e;
   };
-  auto fork = [&]() {
-    cudaEvent_t e;
-    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-    ck(cudaEventRecord(e, s), "event");
-    evs.push_back(e);
-    for (int64_t q : owned) ck(cudaStreamWaitEvent(ctx->work[sidx[q]], e, 0), "wait");
+  {
+    cudaEvent_t f = ev_on(s);
+    for (int64_t q : owned) ck(cudaStreamWaitEvent(ctx->work[sidx[q]], f, 0), "wait");
+  }
+  struct Iv {
+    cudaEvent_t a, b;
   };
-  double ms_gram = 0, ms_chol = 0, ms_pred = 0;
+  std::vector<Iv> gram_iv, chol_iv, pred_iv;
   std::vector<cudaEvent_t> part_end(p, nullptr);
-  cudaEvent_t chol0_start = nullptr;
-  cudaEvent_t e0 = join();
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gram_w, chol_w, pred_w;
-  for (int64_t si = 0; si < ns; ++si) {
-    const double sigma = a->sigmas[si];
-    fork();
-    for (int64_t q : owned) {
-      PartBuf& pb = parts[q];
-      cudaStream_t ws = ctx->work[sidx[q]];
-      pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws,
-                          ctx->counter);
+  for (int64_t q : by_size) {  // largest part enqueued first
+    PartBuf& pb = parts[q];
+    cudaStream_t ws = ctx->work[sidx[q]];
+    const double m = static_cast<double>(pb.m);
+    for (int64_t si = 0; si < ns; ++si) {
+      const double sigma = a->sigmas[si];
+      cudaEvent_t g0 = ev_on(ws);
+      pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws, ctx->counter);
       if (tcount[q] > 0)
-        pk::launch_gram_cross(qt[q].tmQ, pb.tmX, qt[q].norms, pb.norms, qt[q].qp, tcount[q], pb.mp, pb.m,
-                              pb.dp, sigma, qt[q].cross, ws, ctx->counter);
+        pk::launch_gram_cross(qt[q].tmQ, pb.tmX, qt[q].norms, pb.norms, qt[q].qp, tcount[q], pb.mp, pb.m, pb.dp,
+                              sigma, qt[q].cross, ws, ctx->counter);
       if (te && ecount[q] > 0)
-        pk::launch_gram_cross(qe[q].tmQ, pb.tmX, qe[q].norms, pb.norms, qe[q].qp, ecount[q], pb.mp, pb.m,
-                              pb.dp, sigma, qe[q].cross, ws, ctx->counter);
-      const double m = static_cast<double>(pb.m);
+        pk::launch_gram_cross(qe[q].tmQ, pb.tmX, qe[q].norms, pb.norms, qe[q].qp, ecount[q], pb.mp, pb.m, pb.dp,
+                              sigma, qe[q].cross, ws, ctx->counter);
       f_gram += static_cast<double>(d) * m * (m + 1) + 2.0 * (tcount[q] + ecount[q]) * m * d;
-    }
-    cudaEvent_t e1 = join();
-    gram_w.push_back({e0, e1});
-    for (int64_t li = 0; li < nl; ++li) {
-      const int64_t cell = li * ns + si;
-      const double lambda = a->lambdas[li];
-      fork();
-      for (int64_t q : owned) {
-        PartBuf& pb = parts[q];
-        cudaStream_t ws = ctx->work[sidx[q]];
-        int* st = dstatus + (cell * p + q) * 2;
-        pk::launch_assemble(pb.K, pb.A, pb.mp, lambda * static_cast<double>(pb.m), st, ws, ctx->counter);
-        pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, st, ws, ctx->counter);
-        f_chol += chol_flops(pb.m);
-        if (li == 0 && si == 0) {
-          cudaEvent_t pe;
-          ck(cudaEventCreate(&pe), "event");
-          ck(cudaEventRecord(pe, ws), "event");
-          part_end[q] = pe;
-          evs.push_back(pe);
-        }
-      }
-      if (li == 0 && si == 0) chol0_start = e1;
-      cudaEvent_t e2 = join();
-      chol_w.push_back({e1, e2});
-      fork();
-      for (int64_t q : owned) {
-        PartBuf& pb = parts[q];
-        cudaStream_t ws = ctx->work[sidx[q]];
+      gram_iv.push_back({g0, ev_on(ws)});
+      for (int64_t li = 0; li < nl; ++li) {
+        const int64_t cell = li * ns + si;
+        const double lambda = a->lambdas[li];
+        const double shift = lambda * m;
         int* st = dstatus + (cell * p + q) * 2;
         double* rs = dres + (cell * p + q) * 4;
-        const double shift = lambda * static_cast<double>(pb.m);
+        cudaEvent_t c0 = ev_on(ws);
+        pk::launch_assemble(pb.K, pb.A, pb.mp, shift, st, ws, ctx->counter);
+        pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, st, ws, ctx->counter);
+        cudaEvent_t c1 = ev_on(ws);
+        chol_iv.push_back({c0, c1});
+        if (li == 0 && si == 0) part_end[q] = c1;
+        f_chol += chol_flops(pb.m);
         pk::launch_trsv(pb.A, pb.Linv, pb.mp, pb.yp, pb.z, pb.alpha, pb.scratch, st, ws, ctx->counter);
         pk::launch_gemv_rows(pb.K, pb.mp, pb.m, pb.m, pb.alpha, pb.Ka, st, ws, ctx->counter);
         pk::launch_residual_finish(pb.Ka, pb.alpha, pb.yp, pb.m, shift, rs, st, ws, ctx->counter);
-        const double m = static_cast<double>(pb.m);
         f_other += 4.0 * m * m;
         if (tcount[q] > 0) {
-          pk::launch_gemv_rows(qt[q].cross, pb.mp, tcount[q], pb.m, pb.alpha, qt[q].pred, st, ws,
-                               ctx->counter);
+          pk::launch_gemv_rows(qt[q].cross, pb.mp, tcount[q], pb.m, pb.alpha, qt[q].pred, st, ws, ctx->counter);
           double* dst = pred_t + (cell * pp_parts + (pp_parts > 1 ? q : 0)) * t;
           pk::launch_sse_scatter(qt[q].pred, tpos[q], tcount[q], dyt, dst, rs + 2, st, ws, ctx->counter);
           f_other += 2.0 * tcount[q] * m;
         }
         if (te && ecount[q] > 0) {
-          pk::launch_gemv_rows(qe[q].cross, pb.mp, ecount[q], pb.m, pb.alpha, qe[q].pred, st, ws,
-                               ctx->counter);
+          pk::launch_gemv_rows(qe[q].cross, pb.mp, ecount[q], pb.m, pb.alpha, qe[q].pred, st, ws, ctx->counter);
           double* dst = pred_e + (cell * pp_parts + (pp_parts > 1 ? q : 0)) * te;
           pk::launch_sse_scatter(qe[q].pred, epos[q], ecount[q], dye, dst, rs + 3, st, ws, ctx->counter);
           f_other += 2.0 * ecount[q] * m;
         }
+        pred_iv.push_back({c1, ev_on(ws)});
       }
-      cudaEvent_t e3 = join();
-      pred_w.push_back({e2, e3});
-      e1 = e3;
     }
-    e0 = e1;
+  }
+  for (int64_t q : owned) {
+    cudaEvent_t e = ev_on(ctx->work[sidx[q]]);
+    ck(cudaStreamWaitEvent(s, e, 0), "wait");
   }
   // combine for average/oracle predictors (world == 1)
   double* dmse = sc.zeros<double>(2 * ncell, s);
@@ -1299,27 +1285,42 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   ck(cudaEventRecord(t_all.b, s), "event");
   ck(cudaDeviceSynchronize(), "grid");
 
-  for (auto& w : gram_w) {
-    float ms;
-    cudaEventElapsedTime(&ms, w.first, w.second);
-    ms_gram += ms;
-  }
-  for (auto& w : chol_w) {
-    float ms;
-    cudaEventElapsedTime(&ms, w.first, w.second);
-    ms_chol += ms;
-  }
-  for (auto& w : pred_w) {
-    float ms;
-    cudaEventElapsedTime(&ms, w.first, w.second);
-    ms_pred += ms;
+  // union of [start, end] intervals (ms after the call start)
+  auto union_ms = [&](const std::vector<Iv>& iv) {
+    std::vector<std::pair<float, float>> x;
+    for (const Iv& v : iv) {
+      float a0 = 0, a1 = 0;
+      cudaEventElapsedTime(&a0, t_all.a, v.a);
+      cudaEventElapsedTime(&a1, t_all.a, v.b);
+      x.push_back({a0, a1});
+    }
+    std::sort(x.begin(), x.end());
+    double tot = 0, cs = -1, ce = -1;
+    for (auto& v : x) {
+      if (v.first > ce) {
+        if (ce > cs) tot += ce - cs;
+        cs = v.first;
+        ce = v.second;
+      } else if (v.second > ce) {
+        ce = v.second;
+      }
+    }
+    if (ce > cs) tot += ce - cs;
+    return tot;
+  };
+  const double ms_gram = union_ms(gram_iv), ms_chol = union_ms(chol_iv), ms_pred = union_ms(pred_iv);
+  float chol0 = 1e30f;
+  for (const Iv& v : chol_iv) {
+    float a0 = 0;
+    cudaEventElapsedTime(&a0, t_all.a, v.a);
+    chol0 = std::min(chol0, a0);
   }
   {
     float ms_part = 0, ms_all = 0;
     cudaEventElapsedTime(&ms_part, t_part.a, t_part.b);
     cudaEventElapsedTime(&ms_all, t_all.a, t_all.b);
     ctx->timings[0] = ms_part;
-    ctx->timings[1] = ms_gram + ms_chol + ms_pred;
+    ctx->timings[1] = ms_all - ms_part;
     ctx->timings[2] = ms_pred;
     ctx->timings[3] = ms_all;
     ctx->timings[4] = ms_chol;
@@ -1327,10 +1328,10 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   }
   ctx->part_ms.assign(p, 0.0);
   for (int64_t q = 0; q < p; ++q)
-    if (part_end[q] && chol0_start) {
+    if (part_end[q]) {
       float ms = 0;
-      cudaEventElapsedTime(&ms, chol0_start, part_end[q]);
-      ctx->part_ms[q] = ms;
+      cudaEventElapsedTime(&ms, t_all.a, part_end[q]);
+      ctx->part_ms[q] = ms - chol0;
     }
   for (auto e : evs) cudaEventDestroy(e);
 

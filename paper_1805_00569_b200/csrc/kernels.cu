@@ -63,10 +63,16 @@ __global__ void __launch_bounds__(kNormRows) row_norms_kernel(const double* __re
   for (int64_t c0 = 0; c0 < d; c0 += kChunk) {
     const int cw = static_cast<int>(d - c0 < kChunk ? d - c0 : kChunk);
     __syncthreads();
-    for (int e = threadIdx.x; e < kNormRows * kChunk; e += kNormRows) {
-      const int rr = e / kChunk, cc = e % kChunk;
-      const int64_t gr = r0 + rr;
-      xs[rr][cc] = (gr < rows && cc < cw) ? X[gr * ld + c0 + cc] : 0.0;
+    {
+      double v[kChunk];
+      const int cc = threadIdx.x & (kChunk - 1), rb = threadIdx.x / kChunk;
+#pragma unroll
+      for (int u = 0; u < kChunk; ++u) {
+        const int64_t gr = r0 + rb + u * (kNormRows / kChunk);
+        v[u] = (gr < rows && cc < cw) ? __ldg(X + gr * ld + c0 + cc) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kChunk; ++u) xs[rb + u * (kNormRows / kChunk)][cc] = v[u];
     }
     __syncthreads();
     for (int cc = 0; cc < cw; ++cc) {
@@ -834,10 +840,17 @@ __global__ void __launch_bounds__(kAssignRows)
     for (int64_t c0 = 0; c0 < d; c0 += kChunk) {
       const int cw = static_cast<int>(d - c0 < kChunk ? d - c0 : kChunk);
       __syncthreads();
-      for (int e = threadIdx.x; e < kAssignRows * kChunk; e += kAssignRows) {
-        const int rr = e / kChunk, cc = e % kChunk;
-        const int64_t gr = rbase + rr;
-        xs[rr][cc] = (gr < n && cc < cw) ? X[gr * d + c0 + cc] : 0.0;
+      {
+        // all 32 staging loads of this thread in flight before the first store
+        double v[kChunk];
+        const int cc = threadIdx.x & (kChunk - 1), r0 = threadIdx.x / kChunk;
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) {
+          const int64_t gr = rbase + r0 + u * (kAssignRows / kChunk);
+          v[u] = (gr < n && cc < cw) ? __ldg(X + gr * d + c0 + cc) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) xs[r0 + u * (kAssignRows / kChunk)][cc] = v[u];
       }
       for (int e = threadIdx.x; e < KP * kChunk; e += kAssignRows) {
         const int q = e / kChunk, cc = e % kChunk;
@@ -920,16 +933,24 @@ __global__ void group_count_kernel(const int32_t* __restrict__ label, int64_t n,
 
 __global__ void group_scan_kernel(int64_t* counts, int64_t nblk, int k, int64_t* sizes,
                                   int64_t* start) {
-  // thread j: exclusive scan of counts[:, j] over blocks (in place)
+  // warp w: exclusive scan of counts[:, j] over blocks (in place), 32 blocks per step
   __shared__ int64_t tot[1024];
-  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int j = warp; j < k; j += nw) {
     int64_t run = 0;
-    for (int64_t b = 0; b < nblk; ++b) {
-      const int64_t v = counts[b * k + j];
-      counts[b * k + j] = run;
-      run += v;
+    for (int64_t b0 = 0; b0 < nblk; b0 += 32) {
+      const int64_t b = b0 + lane;
+      const int64_t v = b < nblk ? counts[b * k + j] : 0;
+      int64_t incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (b < nblk) counts[b * k + j] = run + incl - v;
+      run += __shfl_sync(0xffffffffu, incl, 31);
     }
-    tot[j] = run;
+    if (lane == 0) tot[j] = run;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -985,7 +1006,8 @@ void launch_group(const int32_t* label, int64_t n, int k, int64_t* sizes, int64_
 // order) stream through a double-buffered shared-memory ring via cp.async; warp
 // 0 keeps one strictly sequential accumulator per feature, so every centre
 // coordinate is the same chain of roundings as the reference's loop.
-constexpr int kMeansRows = 64, kMeansF = 32, kMeansThreads = 256;
+constexpr int kMeansRows = 64, kMeansF = 32, kMeansThreads = 256, kMeansRing = 10;
+constexpr int kMeansSmem = kMeansRing * kMeansRows * kMeansF * 8;
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
@@ -994,64 +1016,95 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// Producer/consumer: warps 1-7 stream the member-row chunks into a kMeansRing-deep
+// shared ring with cp.async (each loader thread signals the slot's "full"
+// mbarrier when its copies land, cp.async.mbarrier.arrive.noinc); warp 0 only runs
+// the sequential per-coordinate chains and frees slots through "empty" mbarriers.
+// The loaders run up to kMeansRing chunks ahead, so the DADD chain sets the pace.
+constexpr int kMeansLoaders = kMeansThreads - 32;
+
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __restrict__ X, int64_t d,
                                                               const int64_t* __restrict__ members,
                                                               const int64_t* __restrict__ start,
                                                               const int64_t* __restrict__ sizes, int k,
                                                               double* centers) {
-  __shared__ double buf[2][kMeansRows][kMeansF];
+  extern __shared__ double mbuf[];  // [ring][rows][F]
+  __shared__ uint64_t full[kMeansRing], empty[kMeansRing];
   const int j = blockIdx.x;
   const int64_t f0 = static_cast<int64_t>(blockIdx.y) * kMeansF;
   const int fw = static_cast<int>(d - f0 < kMeansF ? d - f0 : kMeansF);
   const int64_t sz = sizes[j], st = start[j];
   const int64_t nchunks = (sz + kMeansRows - 1) / kMeansRows;
-  // thread -> feature f, rows r0 + tid/32 + 8q (q < 8): indices loaded first (batched),
-  // then the 8-byte async copies
-  const int f = threadIdx.x & (kMeansF - 1), rsub = threadIdx.x >> 5;
-  auto issue = [&](int64_t c) {
-    const int64_t r0 = c * kMeansRows;
-    const int rows = static_cast<int>(sz - r0 < kMeansRows ? sz - r0 : kMeansRows);
-    int64_t idx[kMeansRows / 8];
-#pragma unroll
-    for (int q = 0; q < kMeansRows / 8; ++q) {
-      const int r = rsub + 8 * q;
-      idx[q] = r < rows ? __ldg(members + st + r0 + r) : 0;
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < kMeansRing; ++r) {
+      mbar_init(&full[r], kMeansLoaders);
+      mbar_init(&empty[r], 1);
     }
-    double(*b)[kMeansF] = buf[c & 1];
-    if (f < fw) {
-#pragma unroll
-      for (int q = 0; q < kMeansRows / 8; ++q) {
-        const int r = rsub + 8 * q;
-        if (r < rows) cp_async8(&b[r][f], X + idx[q] * d + f0 + f);
-      }
-    }
-    cp_async_commit();
-  };
-  double s = 0.0;
-  if (nchunks > 0) issue(0);
-  for (int64_t c = 0; c < nchunks; ++c) {
-    if (c + 1 < nchunks) {
-      issue(c + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    if (threadIdx.x < kMeansF) {
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x >= 32) {
+    const int l = threadIdx.x - 32;
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const int slot = static_cast<int>(c % kMeansRing);
+      mbar_wait(&empty[slot], static_cast<uint32_t>(((c / kMeansRing) & 1) ^ 1));
       const int64_t r0 = c * kMeansRows;
       const int rows = static_cast<int>(sz - r0 < kMeansRows ? sz - r0 : kMeansRows);
-      const double(*b)[kMeansF] = buf[c & 1];
-      int r = 0;
-      for (; r + 8 <= rows; r += 8) {
-        double v[8];
+      double* b = mbuf + slot * kMeansRows * kMeansF;
+      constexpr int kPer = (kMeansRows * kMeansF + kMeansLoaders - 1) / kMeansLoaders;
+      int64_t idx[kPer];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = b[r + u][threadIdx.x];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
+      for (int q = 0; q < kPer; ++q) {
+        const int e = l + kMeansLoaders * q, r = e / kMeansF;
+        idx[q] = (e < kMeansRows * kMeansF && r < rows) ? __ldg(members + st + r0 + r) : -1;
       }
-      for (; r < rows; ++r) s = __dadd_rn(s, b[r][threadIdx.x]);
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int e = l + kMeansLoaders * q, r = e / kMeansF, f = e % kMeansF;
+        if (idx[q] >= 0 && f < fw) cp_async8(b + r * kMeansF + f, X + idx[q] * d + f0 + f);
+      }
+      cp_async_mbar_arrive_noinc(&full[slot]);
     }
-    __syncthreads();
+    return;
+  }
+  double s = 0.0;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int slot = static_cast<int>(c % kMeansRing);
+    mbar_wait(&full[slot], static_cast<uint32_t>((c / kMeansRing) & 1));
+    const int64_t r0 = c * kMeansRows;
+    const int rows = static_cast<int>(sz - r0 < kMeansRows ? sz - r0 : kMeansRows);
+    // volatile shared loads issued 16 rows ahead of the (strictly ordered) DADD chain
+    const uint32_t b = smem_u32(mbuf + slot * kMeansRows * kMeansF + threadIdx.x);
+    int r = 0;
+    double v[16], w[16];
+    if (rows >= 16) {
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = lds_f64_at(b + (u * kMeansF) * 8);
+    }
+    for (; r + 32 <= rows; r += 32) {
+#pragma unroll
+      for (int u = 0; u < 16; ++u) w[u] = lds_f64_at(b + ((r + 16 + u) * kMeansF) * 8);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) s = __dadd_rn(s, v[u]);
+      if (r + 48 <= rows) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = lds_f64_at(b + ((r + 32 + u) * kMeansF) * 8);
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) s = __dadd_rn(s, w[u]);
+    }
+    if (r + 16 <= rows) {
+#pragma unroll
+      for (int u = 0; u < 16; ++u) s = __dadd_rn(s, v[u]);
+      r += 16;
+    }
+    for (; r < rows; ++r) s = __dadd_rn(s, lds_f64_at(b + (r * kMeansF) * 8));
+    __syncwarp();
+    if (threadIdx.x == 0) mbar_arrive(&empty[slot]);
   }
   if (threadIdx.x < fw)
     centers[static_cast<int64_t>(j) * d + f0 + threadIdx.x] =
@@ -1060,8 +1113,13 @@ __global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __re
 
 void launch_means(const double* X, int64_t d, const int64_t* members, const int64_t* start,
                   const int64_t* sizes, int k, double* centers, cudaStream_t s, Counter& c) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(means_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMeansSmem);
+    attr = true;
+  }
   dim3 grid(k, static_cast<unsigned>((d + kMeansF - 1) / kMeansF));
-  means_kernel<<<grid, kMeansThreads, 0, s>>>(X, d, members, start, sizes, k, centers);
+  means_kernel<<<grid, kMeansThreads, kMeansSmem, s>>>(X, d, members, start, sizes, k, centers);
   ++c.launches;
 }
 

@@ -98,6 +98,17 @@ __global__ void __launch_bounds__(kSyrkThreads, 1)
   const int cw = warp - 4;
   const int wm = cw >> 2, wn = cw & 3;
   const int lr = lane >> 2, lk = lane & 3;
+  // fragment row -> tile row permutation: lanes 0-15 read tile rows {0,2,4,6},
+  // lanes 16-31 rows {1,3,5,7}, so each half-warp of an LDS.64 touches 8 distinct
+  // 16-byte chunks of the 128B-swizzled rows (conflict-free); the same
+  // permutation on the B rows permutes the output columns (undone in the epilogue)
+  const int pr = ((lr & 3) << 1) | (lr >> 2);
+  int pc[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int n = 2 * lk + e;
+    pc[e] = ((n & 3) << 1) | (n >> 2);
+  }
   uint32_t g = 0;
   int it = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -119,9 +130,9 @@ __global__ void __launch_bounds__(kSyrkThreads, 1)
         const int k = ks * 4 + lk;
         double af[8], bf[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) af[i] = lds_f64(sa, swz128(wm * 64 + i * 8 + lr, k));
+        for (int i = 0; i < 8; ++i) af[i] = lds_f64(sa, swz128(wm * 64 + i * 8 + pr, k));
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bf[j] = lds_f64(sb, swz128(wn * 32 + j * 8 + lr, k));
+        for (int j = 0; j < 4; ++j) bf[j] = lds_f64(sb, swz128(wn * 32 + j * 8 + pr, k));
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -135,14 +146,13 @@ __global__ void __launch_bounds__(kSyrkThreads, 1)
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int r = wm * 64 + i * 8 + lr, c = wn * 32 + j * 8 + 2 * lk;
-        const uint32_t q = smem_u32(cbuf) + c_off(r, c);
-        double2 v = lds_f64x2(q);
-        v.x -= acc[i][j][0];
-        v.y -= acc[i][j][1];
-        sts_f64x2(q, v);
-      }
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = wm * 64 + i * 8 + pr, c = wn * 32 + j * 8 + pc[e];
+          const uint32_t q = smem_u32(cbuf) + c_off(r, c);
+          sts_f64(q, lds_f64_at(q) - acc[i][j][e]);
+        }
     fence_proxy_async();
     consumer_sync(kConsumerWarps * 32);
     if (threadIdx.x == 128) {
