@@ -1,16 +1,17 @@
 #!/usr/bin/env python
 """Benchmark of the partitioned Gaussian KRR hot path (BASELINE.json configs[1]).
 
-Workload ("step") -- KKRR2 at BASELINE config 1, synthetic (datagen.py, seed 1):
-  n_train = 65536*N, n_val = 2048, n_test = 2048, d = 90, 16*N-component mixture;
-  Lloyd k-means into p = 8*N parts (exactly 20 iterations), one Gaussian KRR
-  model per part (sigma 3, lambda 1e-4: gram + lambda*m_t*I + Cholesky + solves
-  + residual), val and test rows routed to the nearest centroid's model, MSE,
-  best cell selected on validation MSE.  Weak scaling: per-GPU work (8 parts of
-  ~8192 rows) is fixed as N grows; parts are sharded t % N == rank with no
-  data-path collective (per-part SSE combined in part order afterwards).
+Default workload ("step", --config c1) -- KKRR2 at BASELINE configs[1], synthetic
+(datagen.py, seed 1): n_train = 65536*N, n_val = 2048, n_test = 2048, d = 90,
+16*N-component mixture; Lloyd k-means into p = 8*N parts (exactly 20 iterations),
+one Gaussian KRR model per part (sigma 3, lambda 1e-4: gram + lambda*m_t*I +
+Cholesky + solves + residual), val and test rows routed to the nearest centroid's
+model, MSE, best cell selected on validation MSE.  Weak scaling: per-GPU work (8
+parts of ~8192 rows) is fixed as N grows; parts are sharded t % N == rank with no
+data-path collective (per-part SSE combined in part order afterwards).
+--config c0|c2|c3|c4 runs the other BASELINE configs (see CONFIGS).
 
-Metric: train+predict samples/s = (n_train + n_val + n_test) / step time.
+Metric: train+predict samples/s = (n_train + n_val + n_test) * cells / step time.
 `value` times the engine with inputs resident in HBM (CUDA events on the engine's
 launch stream, L2 flushed between steps); `e2e` times the public API with pinned
 HOST buffers (H2D of inputs and D2H of results inside the timed region).
@@ -33,10 +34,27 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_TRAIN, N_VAL, N_TEST, D, COMPS, P = 65536, 2048, 2048, 90, 16, 8
-SIGMA, LAMBDA, KM_ITERS = 3.0, 1e-4, 20
-METRIC = "train+predict samples/sec (KKRR2, FP64)"
+METRIC = "train+predict samples/sec (FP64)"
 UNIT = "samples/s"
+
+# BASELINE.json configs (per GPU for the weak-scaled ones).  km_iters 20 = exactly
+# 20 Lloyd iterations (threshold -1); 0 = the reference defaults (0.01 / 100).
+CONFIGS = {
+    "c0": dict(name="configs[0]: exact KRR, one part", strategy="exact", n=4096, val=0, test=1024, d=90, comps=8,
+               p=1, sigmas=[3.0], lambdas=[1e-4], bump=3.0, clipped=False, km_iters=0, scale_n=False),
+    "c1": dict(name="configs[1]: KKRR2, k-means(20 it) p=8, val-selected", strategy="kkrr2", n=65536, val=2048,
+               test=2048, d=90, comps=16, p=8, sigmas=[3.0], lambdas=[1e-4], bump=3.0, clipped=False, km_iters=20,
+               scale_n=True),
+    "c2": dict(name="configs[2]: BKRR2, k-balance p=16, 3 sigma x 3 lambda", strategy="bkrr2", n=131072, val=2048,
+               test=2048, d=90, comps=32, p=16, sigmas=[1.0, 3.0, 10.0], lambdas=[1e-6, 1e-4, 1e-2], bump=3.0,
+               clipped=False, km_iters=0, scale_n=True),
+    "c3": dict(name="configs[3]: weak-scaling BKRR2, 16384 rows/part, p=8 per GPU", strategy="bkrr2", n=131072,
+               val=2048, test=2048, d=90, comps=64, p=8, sigmas=[3.0], lambdas=[1e-5], bump=3.0, clipped=False,
+               km_iters=0, scale_n=True),
+    "c4": dict(name="configs[4]: wide-feature KKRR2, d=784, p=8", strategy="kkrr2", n=262144, val=0, test=4096,
+               d=784, comps=10, p=8, sigmas=[8.0], lambdas=[1e-4], bump=8.0, clipped=True, km_iters=0,
+               scale_n=False),
+}
 
 
 def parse():
@@ -47,6 +65,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sample-n", type=int, default=0, help="reference sample train rows (0 = auto)")
+    ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
     return ap.parse_args()
 
 
@@ -55,10 +74,19 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def workload(world):
+def workload(cfg, world):
     from paper_1805_00569_b200 import datagen
-    dd = datagen.make(N_TRAIN * world, N_VAL, N_TEST, D, COMPS * world, bumps=16, bump_sigma=3.0, seed=1)
-    return dd
+    mult = world if cfg["scale_n"] else 1
+    return datagen.make(cfg["n"] * mult, cfg["val"], cfg["test"], cfg["d"], cfg["comps"] * mult,
+                        bumps=32 if cfg["clipped"] else 16, bump_sigma=cfg["bump"], clipped=cfg["clipped"], seed=1)
+
+
+def selection(dd):
+    """(selection X, y, eval X, y): val selects and test is scored when there is a
+    validation split; otherwise test selects (the reference's grid_search semantics)."""
+    if dd["X_val"].shape[0]:
+        return dd["X_val"], dd["y_val"], dd["X_test"], dd["y_test"]
+    return dd["X_test"], dd["y_test"], None, None
 
 
 # ---------------------------------------------------------------- clocks ----
@@ -107,53 +135,63 @@ class Clocks:
 
 
 # ------------------------------------------------------------ reference ----
-def reference_sample(dd, n_s, workers):
+def reference_sample(cfg, dd, n_s, workers):
     """Time the UNMODIFIED reference (oracle/_ref, compiled from /root/reference
-    sources) on a bounded sample of the workload: the first n_s train rows (same
-    generator), p = 8 k-means parts, selection set = val + test rows."""
+    sources) through its own grid_search on a bounded sample of the workload: the
+    first n_s train rows (same generator), the config's strategy, p and grid, all
+    val+test rows as its (selection) test set."""
     from oracle import Reference
     ref = Reference()
     Xs, ys = dd["X_train"][:n_s], dd["y_train"][:n_s]
     Xq = np.concatenate([dd["X_val"], dd["X_test"]])
     yq = np.concatenate([dd["y_val"], dd["y_test"]])
     t0 = time.perf_counter()
-    r = ref.grid_search("kkrr2", Xs, ys, Xq, yq, P, [LAMBDA], [SIGMA], 1, workers=workers)
+    r = ref.grid_search(cfg["strategy"], Xs, ys, Xq, yq, cfg["p"], cfg["lambdas"], cfg["sigmas"], 1,
+                        workers=workers)
     dt = time.perf_counter() - t0
     return r, dt, (Xs, ys, Xq, yq)
 
 
-def sample_rows(steps, warmup, override):
+def sample_rows(cfg, steps, warmup, override):
+    """Bounded CPU sample: parts of ~2048 rows (1024 for multi-cell grids), so one
+    reference step is a few seconds on the host's cores."""
     if override:
         return override
-    return 16384 if steps + warmup <= 30 else 8192
+    per_part = 2048 if len(cfg["sigmas"]) * len(cfg["lambdas"]) == 1 else 1024
+    if steps + warmup > 30 or cfg["d"] > 200:
+        per_part //= 2
+    return min(cfg["n"], per_part * cfg["p"])
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    dd = workload(1)
+    cfg = CONFIGS[args.config]
+    dd = workload(cfg, 1)
     cores = os.cpu_count() or 1
-    n_s = sample_rows(args.steps, args.warmup, args.sample_n)
+    n_s = sample_rows(cfg, args.steps, args.warmup, args.sample_n)
     for _ in range(args.warmup):
-        reference_sample(dd, n_s, cores)
+        reference_sample(cfg, dd, n_s, cores)
     times = []
     for _ in range(args.steps):
-        _, dt, _ = reference_sample(dd, n_s, cores)
+        _, dt, _ = reference_sample(cfg, dd, n_s, cores)
         times.append(dt)
     ms = 1e3 * statistics.mean(times)
-    samples = n_s + N_VAL + N_TEST
+    ncell = len(cfg["sigmas"]) * len(cfg["lambdas"])
+    samples = (n_s + cfg["val"] + cfg["test"]) * ncell
     value = samples / (ms / 1e3)
-    sample = (f"first {n_s} of {N_TRAIN} train rows of the bench workload, KKRR2 p={P} (parts ~{n_s // P} rows vs "
-              f"~{N_TRAIN // P} at full size), sigma={SIGMA}, lambda={LAMBDA}, {N_VAL + N_TEST} routed val+test rows; "
-              f"reference grid_search with GridOptions.workers={cores}")
+    sample = (f"first {n_s} of {cfg['n']} train rows, {cfg['strategy']} p={cfg['p']} (parts ~{n_s // cfg['p']} rows "
+              f"vs ~{cfg['n'] // cfg['p']} at full size), {ncell} cell(s), {cfg['val'] + cfg['test']} val+test "
+              f"rows; reference grid_search with GridOptions.workers={cores}")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "BASELINE configs[1] KKRR2 (bounded CPU sample)", "n_train_sample": n_s,
-                       "n_train": N_TRAIN, "n_val": N_VAL, "n_test": N_TEST, "d": D, "p": P},
+            "config": {"workload": f"BASELINE {cfg['name']} (bounded CPU sample)", "n_train_sample": n_s,
+                       "n_train": cfg["n"], "n_val": cfg["val"], "n_test": cfg["test"], "d": cfg["d"],
+                       "p": cfg["p"]},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample,
-                             "extrapolated_full_value": value * (n_s / N_TRAIN) ** 2},
+                             "extrapolated_full_value": value * (n_s / cfg["n"]) ** 2},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -164,30 +202,34 @@ def run_ours(args):
     import torch
     import paper_1805_00569_b200 as pk
 
+    cfg = CONFIGS[args.config]
     rank, world, local = dist_env()
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    dd = workload(world)
-    n_train = N_TRAIN * world
-    p = P * world
+    dd = workload(cfg, world)
+    mult = world if cfg["scale_n"] else 1
+    n_train = cfg["n"] * mult
+    p = cfg["p"] * mult if cfg["p"] > 1 else 1
+    ncell = len(cfg["sigmas"]) * len(cfg["lambdas"])
     eng = pk.Engine(local)
     stream = torch.cuda.ExternalStream(eng.stream_handle, device=dev)
     peak = eng.fp64_peak()
 
     g = {k: torch.from_numpy(v).to(dev) for k, v in dd.items()}
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    thr, iters = (-1.0, cfg["km_iters"]) if cfg["km_iters"] else (0.01, 0)
 
-    def step(host=False):
-        src = h if host else g
-        return eng.grid_search("kkrr2", src["X_train"], src["y_train"], src["X_val"], src["y_val"], p,
-                               [LAMBDA], [SIGMA], 1, eval_X=src["X_test"], eval_y=src["y_test"],
-                               km_threshold=-1.0, km_max_iters=KM_ITERS, rank=rank, world=world)
+    def step(src):
+        sX, sy, eX, ey = selection(src)
+        return eng.grid_search(cfg["strategy"], src["X_train"], src["y_train"], sX, sy, p, cfg["lambdas"],
+                               cfg["sigmas"], 1, eval_X=eX, eval_y=ey, km_threshold=thr, km_max_iters=iters,
+                               rank=rank, world=world)
 
     for _ in range(args.warmup):
-        step()
+        step(g)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -198,13 +240,14 @@ def run_ours(args):
     phase = {"chol": 0.0, "gram": 0.0, "partition": 0.0, "total": 0.0}
     flops = {"chol": 0.0, "gram": 0.0, "other": 0.0}
     res = None
+    t = {}
     with torch.cuda.stream(stream):
         for i in range(args.steps):
             flush.zero_()
             ev[i][0].record(stream)
-            res = step()
+            res = step(g)
             ev[i][1].record(stream)
-            t = eng.timings(parts=p)
+            t = eng.timings(parts=res.p)
             phase["chol"] += t["cholesky"]
             phase["gram"] += t["gram"]
             phase["partition"] += t["partition"]
@@ -216,22 +259,27 @@ def run_ours(args):
     clocks = clk.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = statistics.mean(step_ms)
+    n_sel = cfg["val"] if cfg["val"] else cfg["test"]
+    n_eval = cfg["test"] if cfg["val"] else 0
     # --- multi-rank: max time over ranks, part-order combine of per-part SSE ---
     if world > 1:
+        from paper_1805_00569_b200 import sharding
         tms = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tms, op=dist.ReduceOp.MAX)
         ms = float(tms.item())
-        from paper_1805_00569_b200 import sharding
         parts = res.parts
         sse, fl = sharding.allreduce_tables(parts["part_sse"], parts["part_failed"], dist, device=dev)
-        esse, _ = sharding.allreduce_tables(parts["part_eval_sse"], parts["part_failed"], dist, device=dev)
-        val_mse, failed, best = sharding.combine(sse, fl, N_VAL)
-        test_mse, _, _ = sharding.combine(esse, fl, N_TEST)
+        sel_mse, failed, best = sharding.combine(sse, fl, n_sel)
+        if n_eval:
+            esse, _ = sharding.allreduce_tables(parts["part_eval_sse"], parts["part_failed"], dist, device=dev)
+            eval_mse, _, _ = sharding.combine(esse, fl, n_eval)
+        else:
+            eval_mse = sel_mse
     else:
-        val_mse, test_mse, best = res.mse, res.eval_mse, res.best_index
-    samples = n_train + N_VAL + N_TEST
+        sel_mse, best = res.mse, res.best_index
+        eval_mse = res.eval_mse if n_eval else res.mse
+    samples = (n_train + cfg["val"] + cfg["test"]) * ncell
     value = samples / (ms / 1e3)
-    part_end = t.get("part_chol_end_ms")
     chol_tflops = flops["chol"] / (phase["chol"] / 1e3) / 1e12 if phase["chol"] > 0 else 0.0
     step_tflops = (flops["chol"] + flops["gram"] + flops["other"]) / (sum(step_ms) / 1e3) / 1e12
 
@@ -242,61 +290,64 @@ def run_ours(args):
         for i in range(max(1, min(args.steps, 3))):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            r2 = step(host=True)
+            step(h)
             b.record(stream)
             b.synchronize()
             e2e_ms.append(a.elapsed_time(b))
     e2e = statistics.mean(e2e_ms)
     if world > 1:
-        t = torch.tensor([e2e], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e = float(t.item())
+        tt = torch.tensor([e2e], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = float(tt.item())
     h2d = sum(v.nbytes for v in dd.values())
-    nc = 1
-    d2h = nc * (8 * 4 + 1) + 8 * (N_VAL + N_TEST) + nc * p * (8 * 3 + 1) + 8 * 3 * p
+    d2h = ncell * (8 * 4 + 1) + 8 * (cfg["val"] + cfg["test"]) + ncell * p * (8 * 3 + 1) + 8 * 3 * p
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (datagen.py seed 1, BASELINE configs[1] shapes)",
-        "config": {"workload": "BASELINE configs[1]: KKRR2 k-means(20 it) p=8*N, per-part Gaussian KRR, "
-                               "nearest-centroid predict, val-selected best cell",
-                   "n_train": n_train, "n_val": N_VAL, "n_test": N_TEST, "d": D, "p": p, "sigma": SIGMA,
-                   "lambda": LAMBDA, "parallelism": f"parts sharded t % {world}",
-                   "l2": "256 MB buffer written between timed steps (per-step K/A working set 8.6 GB >> L2)",
+        "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (datagen.py seed 1, BASELINE {cfg['name'].split(':')[0]} shapes)",
+        "config": {"workload": f"BASELINE {cfg['name']}", "strategy": cfg["strategy"],
+                   "n_train": n_train, "n_val": cfg["val"], "n_test": cfg["test"], "d": cfg["d"], "p": p,
+                   "sigmas": cfg["sigmas"], "lambdas": cfg["lambdas"], "cells": ncell,
+                   "samples_per_step": samples, "parallelism": f"parts sharded t % {world}",
+                   "l2": "256 MB buffer written between timed steps (per-step K/A working set >> L2)",
                    "part_sizes": [int(x) for x in res.parts["part_sizes"]]},
         "gpu_launches": int(launches),
         "fp64_tflops_step": step_tflops,
         "phase_ms_per_step": {k: v / args.steps for k, v in phase.items()},
-        "part_chol_end_ms": part_end,
+        "part_chol_end_ms": t.get("part_chol_end_ms"),
         "roofline": {"bound": "tensor", "kernel": "Cholesky (leaf potrf + DMMA TRSM + DMMA SYRK) over all parts",
                      "achieved": chol_tflops, "peak": peak, "unit": "TFLOP/s",
                      "frac": chol_tflops / peak if peak else None, "traffic": None,
                      "peak_source": "measured live: FP64 DMMA (mma.sync m8n8k4) probe over 148 SMs; "
                                     "MEASURED_PEAKS.json has no FP64 entry",
-                     "algorithmic": "sum over parts of m(m+1)(2m+1)/6 (solver.cpp:39-42) / Cholesky phase time"},
-        "mse": {"val_best": float(val_mse[best]) if best >= 0 else None,
-                "test_of_best": float(test_mse[best]) if best >= 0 else None, "best_index": int(best)},
+                     "algorithmic": "sum over parts and cells of m(m+1)(2m+1)/6 (solver.cpp:39-42) / "
+                                    "union of the per-part Cholesky intervals"},
+        "mse": {"selection_best": float(sel_mse[best]) if best >= 0 else None,
+                "eval_of_best": float(eval_mse[best]) if best >= 0 else None, "best_index": int(best)},
         "e2e": {"value": samples / (e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e},
         "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
-        n_s = sample_rows(args.steps, args.warmup, args.sample_n)
+        n_s = sample_rows(cfg, args.steps, args.warmup, args.sample_n)
         try:
-            r, dt, (Xs, ys, Xq, yq) = reference_sample(dd, n_s, cores)
-            cpu_v = (n_s + N_VAL + N_TEST) / dt
+            r, dt, (Xs, ys, Xq, yq) = reference_sample(cfg, dd, n_s, cores)
+            cpu_v = (n_s + cfg["val"] + cfg["test"]) * ncell / dt
             # the same sample through the GPU engine: MSE match against the reference
-            gs = eng.grid_search("kkrr2", Xs, ys, Xq, yq, P, [LAMBDA], [SIGMA], 1)
-            rel = abs(gs.mse[0] - r["mse"][0]) / abs(r["mse"][0])
+            gs = eng.grid_search(cfg["strategy"], Xs, ys, Xq, yq, cfg["p"], cfg["lambdas"], cfg["sigmas"], 1)
+            ok = ~r["failed"]
+            rel = float(np.max(np.abs(gs.mse[ok] - r["mse"][ok]) / np.abs(r["mse"][ok]))) if ok.any() else None
             line["cpu_baseline"] = {
                 "value": cpu_v, "unit": UNIT, "cores": cores, "kind": "reference",
-                "sample": f"first {n_s} train rows, KKRR2 p={P}, {N_VAL + N_TEST} val+test rows, reference "
-                          f"grid_search workers={cores}, {dt:.2f} s",
-                "extrapolated_full_value": cpu_v * (n_s / N_TRAIN) ** 2,
-                "mse_reference": float(r["mse"][0]), "mse_gpu_same_sample": float(gs.mse[0]),
-                "mse_rel_diff": rel}
+                "sample": f"first {n_s} train rows, {cfg['strategy']} p={cfg['p']}, {ncell} cell(s), "
+                          f"{cfg['val'] + cfg['test']} val+test rows, reference grid_search workers={cores}, "
+                          f"{dt:.2f} s",
+                "extrapolated_full_value": cpu_v * (n_s / cfg["n"]) ** 2,
+                "mse_reference": [float(x) for x in r["mse"]], "mse_gpu_same_sample": [float(x) for x in gs.mse],
+                "mse_max_rel_diff": rel, "best_cell_equal": bool(gs.best_index == r["best"])}
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": cores, "kind": "reference",
                                     "sample": f"unavailable: {e}"}

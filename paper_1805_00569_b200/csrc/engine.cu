@@ -105,7 +105,8 @@ int partitioner_of(int s) {
 struct pkrrgpu_ctx {
   int device = 0;
   cudaStream_t main = nullptr;
-  std::vector<cudaStream_t> work;
+  std::vector<cudaStream_t> work;      // graded priorities (highest first)
+  std::vector<cudaStream_t> work_eq;   // equal (default) priority
   pk::Counter counter;
   double timings[8] = {0};
   std::vector<double> part_ms;  // last grid call: per-part Cholesky end, ms after the phase start
@@ -627,10 +628,12 @@ int pkrrgpu_create(int device, pkrrgpu_ctx** out) {
     int least = 0, greatest = 0;
     ck(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
     c->work.resize(8);
+    c->work_eq.resize(8);
     for (size_t i = 0; i < c->work.size(); ++i) {
       int prio = greatest + static_cast<int>(i);
       if (prio > least) prio = least;
       ck(cudaStreamCreateWithPriority(&c->work[i], cudaStreamNonBlocking, prio), "stream");
+      ck(cudaStreamCreateWithFlags(&c->work_eq[i], cudaStreamNonBlocking), "stream");
     }
     *out = c;
     return PKRRGPU_OK;
@@ -646,6 +649,7 @@ void pkrrgpu_destroy(pkrrgpu_ctx* ctx) {
   ctx->trim();
   for (auto& kv : ctx->live) cudaFree(kv.first);
   for (auto s : ctx->work) cudaStreamDestroy(s);
+  for (auto s : ctx->work_eq) cudaStreamDestroy(s);
   cudaStreamDestroy(ctx->main);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;
@@ -1180,103 +1184,162 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
 
   double f_chol = 0, f_gram = 0, f_other = 0;
   const size_t S = ctx->work.size();
-  // owned parts sorted by size (largest first) -> stream rank = priority rank
+  // LPT: parts (largest first) go to the least-loaded stream (load = m^3 per cell).
+  // Uneven loads (KKRR2) -> graded stream priorities, the most-loaded stream first,
+  // so the critical part wins the block scheduler; balanced loads -> equal priority.
   std::vector<int64_t> by_size(owned);
   std::stable_sort(by_size.begin(), by_size.end(),
                    [&](int64_t x, int64_t y) { return po.sizes[x] > po.sizes[y]; });
+  std::vector<size_t> slot(p, 0);
+  std::vector<double> load(S, 0.0);
+  for (int64_t q : by_size) {
+    size_t best = 0;
+    for (size_t i = 1; i < S; ++i)
+      if (load[i] < load[best]) best = i;
+    slot[q] = best;
+    load[best] += static_cast<double>(po.sizes[q]) * po.sizes[q] * po.sizes[q];
+  }
+  std::vector<size_t> order_by_load(S);
+  for (size_t i = 0; i < S; ++i) order_by_load[i] = i;
+  std::stable_sort(order_by_load.begin(), order_by_load.end(),
+                   [&](size_t x, size_t y) { return load[x] > load[y]; });
+  std::vector<size_t> rank_of(S);
+  for (size_t r = 0; r < S; ++r) rank_of[order_by_load[r]] = r;
+  std::vector<double> nz;
+  for (double l : load)
+    if (l > 0) nz.push_back(l);
+  std::sort(nz.begin(), nz.end());
+  const bool graded = !nz.empty() && nz.back() > 1.5 * nz[nz.size() / 2];
+  std::vector<cudaStream_t>& streams = graded ? ctx->work : ctx->work_eq;
   std::vector<size_t> sidx(p, 0);
-  for (size_t r = 0; r < by_size.size(); ++r) sidx[by_size[r]] = r % S;
-  for (int64_t q : owned) {
-    PartBuf& pb = parts[q];
-    cudaStream_t ws = ctx->work[sidx[q]];
-    part_alloc(sc, pb, po.sizes[q], d, true, ws);
-    part_load(ctx, pb, dX, dy, d, po.order + po.start[q], ws);
-    query_alloc(sc, qt[q], tcount[q], pb.dp, pb.mp);
-    if (tcount[q] > 0) {
-      pk::launch_gather_rows(dXt, d, tpos[q], tcount[q], qt[q].Xq, qt[q].qp, pb.dp, ws, ctx->counter);
-      pk::launch_row_norms(qt[q].Xq, qt[q].qp, pb.dp, pb.dp, qt[q].norms, ws, ctx->counter);
-    }
-    if (te) {
-      query_alloc(sc, qe[q], ecount[q], pb.dp, pb.mp);
-      if (ecount[q] > 0) {
-        pk::launch_gather_rows(dXe, d, epos[q], ecount[q], qe[q].Xq, qe[q].qp, pb.dp, ws, ctx->counter);
-        pk::launch_row_norms(qe[q].Xq, qe[q].qp, pb.dp, pb.dp, qe[q].norms, ws, ctx->counter);
-      }
-    }
-  }
-  // Each part flows gram -> (assemble -> Cholesky -> solves -> predict) per cell on
-  // its own prioritised stream, with no cross-part joins: a small part's gram or
-  // solves overlap the large part's Cholesky.  Phase times are the UNION of the
-  // per-(part, cell) intervals, from events on the launching streams.
-  std::vector<cudaEvent_t> evs;
-  auto ev_on = [&](cudaStream_t st) {
-    cudaEvent_t e;
-    ck(cudaEventCreate(&e), "event");
-    ck(cudaEventRecord(e, st), "event");
-    evs.push_back(e);
-    return e;
+  for (int64_t q : owned) sidx[q] = rank_of[slot[q]];
+  // ---- memory-aware batches of parts (largest first) ----
+  auto part_bytes = [&](int64_t q) {
+    const int64_t mp = round_up(po.sizes[q], kNB);
+    auto qbytes = [&](int64_t cnt) {
+      const int64_t qp = round_up(cnt > 0 ? cnt : 1, 64);
+      return qp * dp + 2 * qp + qp * mp;
+    };
+    return 8.0 * static_cast<double>(mp * dp + 8 * mp + 2 * mp * mp + mp * kNB + qbytes(tcount[q]) +
+                                     (te ? qbytes(ecount[q]) : 0));
   };
+  std::vector<std::vector<int64_t>> batches;
   {
-    cudaEvent_t f = ev_on(s);
-    for (int64_t q : owned) ck(cudaStreamWaitEvent(ctx->work[sidx[q]], f, 0), "wait");
+    size_t free_b = 0, total_b = 0;
+    ck(cudaMemGetInfo(&free_b, &total_b), "meminfo");
+    const double budget = 0.92 * static_cast<double>(free_b + ctx->cached_bytes) - 2.0e9;
+    double used = 0.0;
+    for (int64_t q : by_size) {
+      const double b = part_bytes(q);
+      if (batches.empty() || (used + b > budget && !batches.back().empty())) {
+        batches.emplace_back();
+        used = 0.0;
+      }
+      batches.back().push_back(q);
+      used += b;
+    }
   }
+  std::vector<cudaEvent_t> evs;
   struct Iv {
     cudaEvent_t a, b;
   };
   std::vector<Iv> gram_iv, chol_iv, pred_iv;
   std::vector<cudaEvent_t> part_end(p, nullptr);
-  for (int64_t q : by_size) {  // largest part enqueued first
-    PartBuf& pb = parts[q];
-    cudaStream_t ws = ctx->work[sidx[q]];
-    const double m = static_cast<double>(pb.m);
+  for (const std::vector<int64_t>& batch : batches) {
+    Scope bsc(ctx);  // released (after a device sync) before the next batch
+      for (int64_t q : batch) {
+      PartBuf& pb = parts[q];
+      cudaStream_t ws = streams[sidx[q]];
+      part_alloc(bsc, pb, po.sizes[q], d, true, ws);
+      part_load(ctx, pb, dX, dy, d, po.order + po.start[q], ws);
+      query_alloc(bsc, qt[q], tcount[q], pb.dp, pb.mp);
+      if (tcount[q] > 0) {
+        pk::launch_gather_rows(dXt, d, tpos[q], tcount[q], qt[q].Xq, qt[q].qp, pb.dp, ws, ctx->counter);
+        pk::launch_row_norms(qt[q].Xq, qt[q].qp, pb.dp, pb.dp, qt[q].norms, ws, ctx->counter);
+      }
+      if (te) {
+        query_alloc(bsc, qe[q], ecount[q], pb.dp, pb.mp);
+        if (ecount[q] > 0) {
+          pk::launch_gather_rows(dXe, d, epos[q], ecount[q], qe[q].Xq, qe[q].qp, pb.dp, ws, ctx->counter);
+          pk::launch_row_norms(qe[q].Xq, qe[q].qp, pb.dp, pb.dp, qe[q].norms, ws, ctx->counter);
+        }
+      }
+    }
+    // Each part flows gram -> (assemble -> Cholesky -> solves -> predict) per cell on
+    // its own prioritised stream, with no cross-part joins: a small part's gram or
+    // solves overlap the large part's Cholesky.  Phase times are the UNION of the
+    // per-(part, cell) intervals, from events on the launching streams.
+    auto ev_on = [&](cudaStream_t st) {
+      cudaEvent_t e;
+      ck(cudaEventCreate(&e), "event");
+      ck(cudaEventRecord(e, st), "event");
+      evs.push_back(e);
+      return e;
+    };
+    {
+      cudaEvent_t f = ev_on(s);
+      for (int64_t q : batch) ck(cudaStreamWaitEvent(streams[sidx[q]], f, 0), "wait");
+    }
+    // enqueue round-robin over (cell, part) so every stream's launch queue fills
+    // evenly (a deep queue on one stream would block the host and starve others)
     for (int64_t si = 0; si < ns; ++si) {
       const double sigma = a->sigmas[si];
-      cudaEvent_t g0 = ev_on(ws);
-      pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws, ctx->counter);
-      if (tcount[q] > 0)
-        pk::launch_gram_cross(qt[q].tmQ, pb.tmX, qt[q].norms, pb.norms, qt[q].qp, tcount[q], pb.mp, pb.m, pb.dp,
-                              sigma, qt[q].cross, ws, ctx->counter);
-      if (te && ecount[q] > 0)
-        pk::launch_gram_cross(qe[q].tmQ, pb.tmX, qe[q].norms, pb.norms, qe[q].qp, ecount[q], pb.mp, pb.m, pb.dp,
-                              sigma, qe[q].cross, ws, ctx->counter);
-      f_gram += static_cast<double>(d) * m * (m + 1) + 2.0 * (tcount[q] + ecount[q]) * m * d;
-      gram_iv.push_back({g0, ev_on(ws)});
+      for (int64_t q : batch) {  // largest part first
+        PartBuf& pb = parts[q];
+        cudaStream_t ws = streams[sidx[q]];
+        const double m = static_cast<double>(pb.m);
+        cudaEvent_t g0 = ev_on(ws);
+        pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws, ctx->counter);
+        if (tcount[q] > 0)
+          pk::launch_gram_cross(qt[q].tmQ, pb.tmX, qt[q].norms, pb.norms, qt[q].qp, tcount[q], pb.mp, pb.m, pb.dp,
+                                sigma, qt[q].cross, ws, ctx->counter);
+        if (te && ecount[q] > 0)
+          pk::launch_gram_cross(qe[q].tmQ, pb.tmX, qe[q].norms, pb.norms, qe[q].qp, ecount[q], pb.mp, pb.m, pb.dp,
+                                sigma, qe[q].cross, ws, ctx->counter);
+        f_gram += static_cast<double>(d) * m * (m + 1) + 2.0 * (tcount[q] + ecount[q]) * m * d;
+        gram_iv.push_back({g0, ev_on(ws)});
+      }
       for (int64_t li = 0; li < nl; ++li) {
         const int64_t cell = li * ns + si;
         const double lambda = a->lambdas[li];
-        const double shift = lambda * m;
-        int* st = dstatus + (cell * p + q) * 2;
-        double* rs = dres + (cell * p + q) * 4;
-        cudaEvent_t c0 = ev_on(ws);
-        pk::launch_assemble(pb.K, pb.A, pb.mp, shift, st, ws, ctx->counter);
-        pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, st, ws, ctx->counter);
-        cudaEvent_t c1 = ev_on(ws);
-        chol_iv.push_back({c0, c1});
-        if (li == 0 && si == 0) part_end[q] = c1;
-        f_chol += chol_flops(pb.m);
-        pk::launch_trsv(pb.A, pb.Linv, pb.mp, pb.yp, pb.z, pb.alpha, pb.scratch, st, ws, ctx->counter);
-        pk::launch_gemv_rows(pb.K, pb.mp, pb.m, pb.m, pb.alpha, pb.Ka, st, ws, ctx->counter);
-        pk::launch_residual_finish(pb.Ka, pb.alpha, pb.yp, pb.m, shift, rs, st, ws, ctx->counter);
-        f_other += 4.0 * m * m;
-        if (tcount[q] > 0) {
-          pk::launch_gemv_rows(qt[q].cross, pb.mp, tcount[q], pb.m, pb.alpha, qt[q].pred, st, ws, ctx->counter);
-          double* dst = pred_t + (cell * pp_parts + (pp_parts > 1 ? q : 0)) * t;
-          pk::launch_sse_scatter(qt[q].pred, tpos[q], tcount[q], dyt, dst, rs + 2, st, ws, ctx->counter);
-          f_other += 2.0 * tcount[q] * m;
+        for (int64_t q : batch) {
+          PartBuf& pb = parts[q];
+          cudaStream_t ws = streams[sidx[q]];
+          const double m = static_cast<double>(pb.m);
+          const double shift = lambda * m;
+          int* st = dstatus + (cell * p + q) * 2;
+          double* rs = dres + (cell * p + q) * 4;
+          cudaEvent_t c0 = ev_on(ws);
+          pk::launch_assemble(pb.K, pb.A, pb.mp, shift, st, ws, ctx->counter);
+          pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, st, ws, ctx->counter);
+          cudaEvent_t c1 = ev_on(ws);
+          chol_iv.push_back({c0, c1});
+          if (li == 0 && si == 0) part_end[q] = c1;
+          f_chol += chol_flops(pb.m);
+          pk::launch_trsv(pb.A, pb.Linv, pb.mp, pb.yp, pb.z, pb.alpha, pb.scratch, st, ws, ctx->counter);
+          pk::launch_gemv_rows(pb.K, pb.mp, pb.m, pb.m, pb.alpha, pb.Ka, st, ws, ctx->counter);
+          pk::launch_residual_finish(pb.Ka, pb.alpha, pb.yp, pb.m, shift, rs, st, ws, ctx->counter);
+          f_other += 4.0 * m * m;
+          if (tcount[q] > 0) {
+            pk::launch_gemv_rows(qt[q].cross, pb.mp, tcount[q], pb.m, pb.alpha, qt[q].pred, st, ws, ctx->counter);
+            double* dst = pred_t + (cell * pp_parts + (pp_parts > 1 ? q : 0)) * t;
+            pk::launch_sse_scatter(qt[q].pred, tpos[q], tcount[q], dyt, dst, rs + 2, st, ws, ctx->counter);
+            f_other += 2.0 * tcount[q] * m;
+          }
+          if (te && ecount[q] > 0) {
+            pk::launch_gemv_rows(qe[q].cross, pb.mp, ecount[q], pb.m, pb.alpha, qe[q].pred, st, ws, ctx->counter);
+            double* dst = pred_e + (cell * pp_parts + (pp_parts > 1 ? q : 0)) * te;
+            pk::launch_sse_scatter(qe[q].pred, epos[q], ecount[q], dye, dst, rs + 3, st, ws, ctx->counter);
+            f_other += 2.0 * ecount[q] * m;
+          }
+          pred_iv.push_back({c1, ev_on(ws)});
         }
-        if (te && ecount[q] > 0) {
-          pk::launch_gemv_rows(qe[q].cross, pb.mp, ecount[q], pb.m, pb.alpha, qe[q].pred, st, ws, ctx->counter);
-          double* dst = pred_e + (cell * pp_parts + (pp_parts > 1 ? q : 0)) * te;
-          pk::launch_sse_scatter(qe[q].pred, epos[q], ecount[q], dye, dst, rs + 3, st, ws, ctx->counter);
-          f_other += 2.0 * ecount[q] * m;
-        }
-        pred_iv.push_back({c1, ev_on(ws)});
       }
     }
-  }
-  for (int64_t q : owned) {
-    cudaEvent_t e = ev_on(ctx->work[sidx[q]]);
-    ck(cudaStreamWaitEvent(s, e, 0), "wait");
+    for (int64_t q : batch) {
+      cudaEvent_t e = ev_on(streams[sidx[q]]);
+      ck(cudaStreamWaitEvent(s, e, 0), "wait");
+    }
   }
   // combine for average/oracle predictors (world == 1)
   double* dmse = sc.zeros<double>(2 * ncell, s);
