@@ -111,6 +111,7 @@ struct pkrrgpu_ctx {
   double timings[8] = {0};
   std::vector<double> part_ms;  // last grid call: per-part Cholesky end, ms after the phase start
   void* pinned = nullptr;  // 64 KB pinned staging for small device->host reads
+  double total_mem = 0.0;  // device HBM bytes
   std::multimap<size_t, void*> free_blocks;
   std::map<void*, size_t> live;
   size_t cached_bytes = 0;
@@ -617,8 +618,10 @@ int pkrrgpu_create(int device, pkrrgpu_ctx** out) {
     cudaDeviceProp prop;
     ck(cudaGetDeviceProperties(&prop, device), "props");
     if (prop.major != 10) fail(PKRRGPU_CUDA, "pkrr-b200 needs an sm_100a (Blackwell) device");
+    const double total_mem = static_cast<double>(prop.totalGlobalMem);
     auto* c = new pkrrgpu_ctx();
     c->device = device;
+    c->total_mem = total_mem;
     if (const char* g = std::getenv("PKRR_PANEL_GROUP")) pk::set_panel_group(std::atoi(g));
     if (const char* g = std::getenv("PKRR_SYRK_PERSISTENT")) pk::set_syrk_persistent(std::atoi(g));
     ck(cudaStreamCreateWithFlags(&c->main, cudaStreamNonBlocking), "stream");
@@ -1225,9 +1228,14 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   };
   std::vector<std::vector<int64_t>> batches;
   {
-    size_t free_b = 0, total_b = 0;
-    ck(cudaMemGetInfo(&free_b, &total_b), "meminfo");
-    const double budget = 0.92 * static_cast<double>(free_b + ctx->cached_bytes) - 2.0e9;
+    double need = 0.0;
+    for (int64_t q : by_size) need += part_bytes(q);
+    double budget = 1e300;
+    if (need > 0.4 * ctx->total_mem) {  // only then ask the driver (the query is not free)
+      size_t free_b = 0, total_b = 0;
+      ck(cudaMemGetInfo(&free_b, &total_b), "meminfo");
+      budget = 0.92 * static_cast<double>(free_b + ctx->cached_bytes) - 2.0e9;
+    }
     double used = 0.0;
     for (int64_t q : by_size) {
       const double b = part_bytes(q);
