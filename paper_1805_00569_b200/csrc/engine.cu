@@ -662,6 +662,58 @@ int64_t pkrrgpu_launch_count(const pkrrgpu_ctx* ctx) { return ctx ? ctx->counter
 
 void* pkrrgpu_stream(pkrrgpu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->main) : nullptr; }
 
+int pkrrgpu_probe_potrf(pkrrgpu_ctx* ctx, int64_t m, double* out) {
+  API_BEGIN
+  if (m <= 0 || !out) fail(PKRRGPU_INVALID, "probe_potrf: bad arguments");
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  // SPD test system: gaussian gram of m seeded points (d = 90) + 1e-4 * m * I
+  const int64_t d = 90;
+  std::vector<double> X(m * d);
+  std::mt19937_64 eng(12345);
+  std::normal_distribution<double> nd(0.0, 1.0);
+  for (auto& v : X) v = nd(eng);
+  PartBuf pb;
+  part_alloc(sc, pb, m, d, true, s);
+  const double* dX = sc.in(X.data(), m * d, s);
+  int64_t* idx = sc.alloc<int64_t>(m);
+  iota_kernel<<<blocks_for(m), 256, 0, s>>>(idx, m);
+  ++ctx->counter.launches;
+  pk::launch_gather_rows(dX, d, idx, m, pb.Xp, pb.mp, pb.dp, s, ctx->counter);
+  pk::launch_row_norms(pb.Xp, pb.mp, pb.dp, pb.dp, pb.norms, s, ctx->counter);
+  pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, m, 3.0, pb.K, pb.mp, nullptr, s, ctx->counter);
+  int* status = sc.zeros<int>(2, s);
+  pk::launch_assemble(pb.K, pb.A, pb.mp, 1e-4 * static_cast<double>(m), status, s, ctx->counter);
+  ck(cudaStreamSynchronize(s), "sync");
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  std::vector<double> fl;
+  Timer tm;
+  pk::set_syrk_probe(&ev, &fl);
+  ck(cudaEventRecord(tm.a, s), "event");
+  pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, m, status, s, ctx->counter);
+  ck(cudaEventRecord(tm.b, s), "event");
+  pk::set_syrk_probe(nullptr, nullptr);
+  ck(cudaStreamSynchronize(s), "sync");
+  float total = 0;
+  cudaEventElapsedTime(&total, tm.a, tm.b);
+  double syrk_ms = 0, syrk_fl = 0;
+  for (size_t i = 0; i < ev.size(); ++i) {
+    float msi = 0;
+    cudaEventElapsedTime(&msi, ev[i].first, ev[i].second);
+    syrk_ms += msi;
+    syrk_fl += fl[i];
+    cudaEventDestroy(ev[i].first);
+    cudaEventDestroy(ev[i].second);
+  }
+  out[0] = total;                      // whole factorization, ms
+  out[1] = chol_flops(m);              // its algorithmic flops
+  out[2] = syrk_ms;                    // trailing-SYRK launches, ms (sum)
+  out[3] = syrk_fl;                    // their algorithmic flops
+  out[4] = static_cast<double>(ev.size());
+  out[5] = to_host(status, 1, s)[0];   // NPD flag (must be 0)
+  API_END
+}
+
 int pkrrgpu_fp64_peak(pkrrgpu_ctx* ctx, double* tflops) {
   API_BEGIN
   if (!tflops) fail(PKRRGPU_INVALID, "null out");

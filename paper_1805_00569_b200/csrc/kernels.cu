@@ -7,6 +7,7 @@
 // clustering.cpp.
 #include <cstdio>
 #include <cmath>
+#include <vector>
 
 #include "gemm_dmma.cuh"
 #include "syrk_persistent.cuh"
@@ -429,6 +430,13 @@ static int g_sms = 148;
 // TRSM each), then ONE trailing SYRK with K = 128*G updates the rest: the
 // trailing matrix is streamed through HBM nb/G times instead of nb times.
 static int g_panel_group = 4;
+// optional per-launch timing of the trailing SYRK (bench probe only)
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* g_syrk_events = nullptr;
+static std::vector<double>* g_syrk_flops = nullptr;
+void set_syrk_probe(std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* ev, std::vector<double>* fl) {
+  g_syrk_events = ev;
+  g_syrk_flops = fl;
+}
 static int g_syrk_persistent = 0;  // 0: one tile per CTA (priority-responsive); 1: one CTA per SM
 
 void set_panel_group(int g) { g_panel_group = g < 1 ? 1 : (g > 8 ? 8 : g); }
@@ -496,8 +504,21 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
     u.abort_flag = status;
     const int ntl = rem * (rem + 1) / 2;
     const int grid = g_syrk_persistent ? (ntl < g_sms ? ntl : g_sms) : ntl;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (g_syrk_events) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, s);
+    }
     dsyrk_persistent_kernel<<<grid, kSyrkThreads, kSyrkSmem, s>>>(tmA, u);
     ++c.launches;
+    if (g_syrk_events) {
+      cudaEventRecord(e1, s);
+      g_syrk_events->push_back({e0, e1});
+      // algorithmic: A22 -= L21 L21^T on the lower triangle incl. diagonal, K = 128*group
+      const double rows = static_cast<double>(rem) * kNB, kk = static_cast<double>(kend - kb0) * kNB;
+      g_syrk_flops->push_back(rows * (rows + 1.0) * kk);
+    }
   }
 }
 

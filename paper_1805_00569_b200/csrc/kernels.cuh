@@ -7,6 +7,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+#include <vector>
+
 namespace pk {
 
 constexpr int kNB = 128;  // Cholesky block (leaf / panel) size; parts are padded to it
@@ -46,6 +49,9 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
 void set_panel_group(int g);
 // SYRK grid: 0 = one 128x128 tile per CTA (default), 1 = persistent (one CTA per SM).
 void set_syrk_persistent(int on);
+// Probe hook: when set, every trailing-SYRK launch is bracketed by events and its
+// algorithmic flop count recorded (used by pkrrgpu_probe_potrf only).
+void set_syrk_probe(std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* ev, std::vector<double>* flops);
 // Recompute inv(L_kk) for every diagonal block of an existing factor.
 void launch_diag_inverses(const double* L, int64_t mp, double* Linv, cudaStream_t s, Counter& c);
 // Zero the strict upper triangle (API parity with solver.cpp:34).
