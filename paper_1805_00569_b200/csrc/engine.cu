@@ -249,6 +249,8 @@ struct PartBuf {
   double* alpha = nullptr;
   double* Ka = nullptr;
   int* scratch = nullptr;   // trsv tickets/flags
+  int8_t* slices = nullptr; // Ozaki SYRK scratch: int8 [8 x mp x 512]
+  int* exps = nullptr;      // [mp]
   CUtensorMap tmX, tmA, tmLinv;
 };
 
@@ -266,6 +268,10 @@ void part_alloc(Scope& sc, PartBuf& pb, int64_t m, int64_t d, bool need_K, cudaS
   pb.alpha = sc.alloc<double>(pb.mp);
   pb.Ka = sc.alloc<double>(pb.mp);
   pb.scratch = sc.alloc<int>(2 * (pb.mp / kNB) + 2);
+  if (pk::syrk_ozaki()) {
+    pb.slices = sc.alloc<int8_t>(8 * pb.mp * 512);
+    pb.exps = sc.alloc<int>(pb.mp);
+  }
   if (!pk::make_tmap(&pb.tmX, pb.Xp, pb.mp, pb.dp, pb.dp) ||
       !pk::make_tmap(&pb.tmA, pb.A, pb.mp, pb.mp, pb.mp) ||
       !pk::make_tmap(&pb.tmLinv, pb.Linv, pb.mp, kNB, kNB))
@@ -553,7 +559,7 @@ void part_solve(pkrrgpu_ctx* ctx, PartBuf& pb, double lambda, int* status, doubl
                 cudaStream_t s) {
   const double shift = lambda * static_cast<double>(pb.m);
   pk::launch_assemble(pb.K, pb.A, pb.mp, shift, status, s, ctx->counter);
-  pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, status, s, ctx->counter);
+  pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, status, s, ctx->counter, pb.slices, pb.exps);
   pk::launch_trsv(pb.A, pb.Linv, pb.mp, pb.yp, pb.z, pb.alpha, pb.scratch, status, s, ctx->counter);
   if (res_out) {
     pk::launch_gemv_rows(pb.K, pb.mp, pb.m, pb.m, pb.alpha, pb.Ka, status, s, ctx->counter);
@@ -624,6 +630,7 @@ int pkrrgpu_create(int device, pkrrgpu_ctx** out) {
     c->total_mem = total_mem;
     if (const char* g = std::getenv("PKRR_PANEL_GROUP")) pk::set_panel_group(std::atoi(g));
     if (const char* g = std::getenv("PKRR_SYRK_PERSISTENT")) pk::set_syrk_persistent(std::atoi(g));
+    if (const char* g = std::getenv("PKRR_SYRK")) pk::set_syrk_ozaki(std::strcmp(g, "ozaki") == 0 ? 1 : 0);
     ck(cudaStreamCreateWithFlags(&c->main, cudaStreamNonBlocking), "stream");
     ck(cudaMallocHost(&c->pinned, 64 * 1024), "pinned");
     // work streams in decreasing priority: the grid maps parts to them largest
@@ -690,7 +697,7 @@ int pkrrgpu_probe_potrf(pkrrgpu_ctx* ctx, int64_t m, double* out) {
   Timer tm;
   pk::set_syrk_probe(&ev, &fl);
   ck(cudaEventRecord(tm.a, s), "event");
-  pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, m, status, s, ctx->counter);
+  pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, m, status, s, ctx->counter, pb.slices, pb.exps);
   ck(cudaEventRecord(tm.b, s), "event");
   pk::set_syrk_probe(nullptr, nullptr);
   ck(cudaStreamSynchronize(s), "sync");
@@ -823,7 +830,7 @@ int pkrrgpu_cholesky(pkrrgpu_ctx* ctx, const double* A, int64_t m, double* L, in
     ++ctx->counter.launches;
   }
   int* status = sc.zeros<int>(2, s);
-  pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, m, status, s, ctx->counter);
+  pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, m, status, s, ctx->counter, pb.slices, pb.exps);
   std::vector<int> st = to_host(status, 2, s);
   if (st[0]) {
     if (npd_pivot) *npd_pivot = st[1];
@@ -1238,7 +1245,8 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   ck(cudaStreamSynchronize(s), "sync");
 
   double f_chol = 0, f_gram = 0, f_other = 0;
-  const size_t S = ctx->work.size();
+  size_t S = ctx->work.size();
+  if (const char* e = std::getenv("PKRR_STREAMS")) S = std::max<size_t>(1, std::min<size_t>(S, std::atoi(e)));
   // LPT: parts (largest first) go to the least-loaded stream (load = m^3 per cell).
   // Uneven loads (KKRR2) -> graded stream priorities, the most-loaded stream first,
   // so the critical part wins the block scheduler; balanced loads -> equal priority.
@@ -1264,7 +1272,8 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   for (double l : load)
     if (l > 0) nz.push_back(l);
   std::sort(nz.begin(), nz.end());
-  const bool graded = !nz.empty() && nz.back() > 1.5 * nz[nz.size() / 2];
+  bool graded = !nz.empty() && nz.back() > 1.5 * nz[nz.size() / 2];
+  if (const char* e = std::getenv("PKRR_PRIO")) graded = std::atoi(e) != 0;
   std::vector<cudaStream_t>& streams = graded ? ctx->work : ctx->work_eq;
   std::vector<size_t> sidx(p, 0);
   for (int64_t q : owned) sidx[q] = rank_of[slot[q]];
@@ -1276,7 +1285,8 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
       return qp * dp + 2 * qp + qp * mp;
     };
     return 8.0 * static_cast<double>(mp * dp + 8 * mp + 2 * mp * mp + mp * kNB + qbytes(tcount[q]) +
-                                     (te ? qbytes(ecount[q]) : 0));
+                                     (te ? qbytes(ecount[q]) : 0)) +
+           (pk::syrk_ozaki() ? 8.0 * 512.0 * static_cast<double>(mp) : 0.0);
   };
   std::vector<std::vector<int64_t>> batches;
   {
@@ -1371,7 +1381,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
           double* rs = dres + (cell * p + q) * 4;
           cudaEvent_t c0 = ev_on(ws);
           pk::launch_assemble(pb.K, pb.A, pb.mp, shift, st, ws, ctx->counter);
-          pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, st, ws, ctx->counter);
+          pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, st, ws, ctx->counter, pb.slices, pb.exps);
           cudaEvent_t c1 = ev_on(ws);
           chol_iv.push_back({c0, c1});
           if (li == 0 && si == 0) part_end[q] = c1;
@@ -1401,6 +1411,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
       ck(cudaStreamWaitEvent(s, e, 0), "wait");
     }
   }
+  pk::shadow_report();
   // combine for average/oracle predictors (world == 1)
   double* dmse = sc.zeros<double>(2 * ncell, s);
   double* comb_t = sc.alloc<double>(t);

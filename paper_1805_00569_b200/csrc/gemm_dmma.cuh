@@ -42,6 +42,7 @@ constexpr int kConsumerWarps = 8;
 constexpr int kGemmThreads = (kConsumerWarps + 1) * 32;
 constexpr int kStages = 4;
 
+
 template <int BM>
 struct GemmCfg {
   static constexpr int A_BYTES = BM * kBK * 8;
@@ -130,6 +131,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int s = kt % kStages;
     const uint32_t ph = (kt / kStages) & 1;
     mbar_wait(&full[s], ph);
+    // Deferred release of the previous stage: its LDS results have been consumed by
+    // the DMMAs issued before this wait, so the reads are complete.  Releasing right
+    // after the last LDS let the TMA refill race a still-queued LDS (seen as rare
+    // wrong fragments when a co-resident CTA congested the LSU).
+    if (kt > 0) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[(kt - 1) % kStages]);
+    }
     const unsigned char* sa = smem + s * Cfg::STAGE_BYTES;
     const unsigned char* sb = sa + Cfg::A_BYTES;
 #pragma unroll
@@ -145,8 +154,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
         for (int j = 0; j < Cfg::NT; ++j) dmma(acc[i][j], af[i], bf[j]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
   }
 
   // ---------------- epilogues ----------------

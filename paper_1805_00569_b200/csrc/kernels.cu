@@ -8,9 +8,12 @@
 #include <cstdio>
 #include <cmath>
 #include <vector>
+#include <cstdlib>
 
 #include "gemm_dmma.cuh"
 #include "syrk_persistent.cuh"
+#include "ozaki_syrk.cuh"
+#include <string>
 #include "kernels.cuh"
 
 namespace pk {
@@ -438,21 +441,144 @@ void set_syrk_probe(std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* ev, std::v
   g_syrk_flops = fl;
 }
 static int g_syrk_persistent = 0;  // 0: one tile per CTA (priority-responsive); 1: one CTA per SM
+static int g_syrk_ozaki = 0;       // 1: trailing SYRK on the int8 tensor cores (Ozaki splitting)
 
 void set_panel_group(int g) { g_panel_group = g < 1 ? 1 : (g > 8 ? 8 : g); }
 void set_syrk_persistent(int on) { g_syrk_persistent = on; }
+void set_syrk_ozaki(int on) { g_syrk_ozaki = on; }
+int syrk_ozaki() { return g_syrk_ozaki; }
+
+// int8 slice tensor {K, R, 8} (K-contiguous), boxes {32, box_rows, 8}, 32B swizzle
+static bool make_tmap_slices(CUtensorMap* m, const int8_t* base, int64_t R, int64_t K, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(R), 8};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(K * R)};
+  cuuint32_t box[3] = {32u, static_cast<cuuint32_t>(box_rows), 8u};
+  cuuint32_t es[3] = {1u, 1u, 1u};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// ---- PKRR_SHADOW (debug): determinism checker for the factorisation steps ----
+// Every step is run twice, on the live buffers and on copies taken just before it;
+// a step whose output differs between the two runs depends on timing/concurrency.
+// Each comparison records (max |diff|, count of differing elements) in a managed
+// table; shadow_report() prints the differing steps and "N of M checks differ".
+namespace {
+constexpr int kShadowSlots = 1 << 16;
+struct ShadowSlot {
+  unsigned long long maxbits, count;
+};
+ShadowSlot* g_shadow = nullptr;
+int g_shadow_n = 0;
+std::vector<std::string> g_shadow_name;
+}  // namespace
+
+__global__ void shadow_diff_kernel(const double* A, const double* B, int64_t n, ShadowSlot* out) {
+  double w = 0.0;
+  unsigned long long cnt = 0;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double a = A[e], b = B[e];
+    if (a == b || (a != a && b != b)) continue;  // equal, or both NaN
+    const double d = fabs(a - b);
+    w = d > w ? d : w;
+    ++cnt;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    w = fmax(w, __shfl_xor_sync(0xffffffffu, w, o));
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&out->maxbits, static_cast<unsigned long long>(__double_as_longlong(w)));
+    atomicAdd(&out->count, cnt);
+  }
+}
+
+static void shadow_diff(const double* A, const double* B, int64_t n, cudaStream_t s, const std::string& name) {
+  if (!g_shadow) {
+    cudaMallocManaged(&g_shadow, sizeof(ShadowSlot) * kShadowSlots);
+    memset(g_shadow, 0, sizeof(ShadowSlot) * kShadowSlots);
+  }
+  if (g_shadow_n >= kShadowSlots) return;
+  g_shadow_name.push_back(name);
+  shadow_diff_kernel<<<296, 256, 0, s>>>(A, B, n, g_shadow + g_shadow_n++);
+}
+
+void shadow_report() {
+  if (!g_shadow) return;
+  cudaDeviceSynchronize();
+  int bad = 0;
+  for (int i = 0; i < g_shadow_n; ++i) {
+    if (g_shadow[i].count == 0) continue;
+    ++bad;
+    double w;
+    memcpy(&w, &g_shadow[i].maxbits, 8);
+    fprintf(stderr, "pkrr shadow: %s differs in %llu elements, max |diff| %.3e\n", g_shadow_name[i].c_str(),
+            g_shadow[i].count, w);
+  }
+  fprintf(stderr, "pkrr shadow: %d of %d checks differ\n", bad, g_shadow_n);
+  memset(g_shadow, 0, sizeof(ShadowSlot) * kShadowSlots);
+  g_shadow_n = 0;
+  g_shadow_name.clear();
+}
+
+namespace {
+// the buffers one factorisation works on (the real ones, or the PKRR_SHADOW copies)
+struct FactorBufs {
+  double* A;
+  CUtensorMap tmA;
+  double* Linv;
+  CUtensorMap tmLinv;
+  int* status;
+};
+}  // namespace
 
 void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, double* Linv,
-                  int64_t mp, int64_t m_valid, int* status, cudaStream_t s, Counter& c) {
+                  int64_t mp, int64_t m_valid, int* status, cudaStream_t s, Counter& c, int8_t* slices,
+                  int* exps) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(potrf_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLeafSmem);
     cudaFuncSetAttribute(dsyrk_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSyrkSmem);
+    cudaFuncSetAttribute(ozaki_syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzSmem);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
     attr = true;
   }
+  // Debug (PKRR_SHADOW): every step is run twice -- on A and on a copy taken just
+  // before it -- and the two outputs compared (reported by shadow_report): a step
+  // whose result depends on timing/concurrency shows up by name.
+  static const bool shadow = std::getenv("PKRR_SHADOW") != nullptr;
+  FactorBufs main{A, tmA, Linv, tmLinv, status}, sh{};
+  if (shadow) {
+    cudaMallocAsync(&sh.A, sizeof(double) * mp * mp, s);
+    cudaMallocAsync(&sh.Linv, sizeof(double) * mp * kNB, s);
+    if (status) {
+      cudaMallocAsync(&sh.status, sizeof(int) * 8, s);
+      cudaMemcpyAsync(sh.status, status, sizeof(int) * 2, cudaMemcpyDeviceToDevice, s);
+    }
+    make_tmap(&sh.tmA, sh.A, mp, mp, mp);
+    make_tmap(&sh.tmLinv, sh.Linv, mp, kNB, kNB);
+  }
+  int cur = 0;  // block index of the current step (shadow report tag)
+  auto step = [&](const char* name, auto&& fn) {
+    if (!shadow) {
+      fn(main);
+      return;
+    }
+    cudaMemcpyAsync(sh.A, A, sizeof(double) * mp * mp, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(sh.Linv, Linv, sizeof(double) * mp * kNB, cudaMemcpyDeviceToDevice, s);
+    fn(main);
+    fn(sh);
+    const std::string tag = std::string(name) + " (mp " + std::to_string(mp) + ", block " + std::to_string(cur) + ")";
+    shadow_diff(A, sh.A, mp * mp, s, tag);
+    shadow_diff(Linv, sh.Linv, mp * kNB, s, tag + " Linv");
+  };
   const int nb = static_cast<int>(mp / kNB);
   const int G = g_panel_group;
   for (int kb0 = 0; kb0 < nb; kb0 += G) {
@@ -460,65 +586,106 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
     for (int kb = kb0; kb < kend; ++kb) {
       if (kb > kb0) {
         // column block kb (rows >= kb) -= A[:, kb0:kb] A[kb, kb0:kb]^T
-        GemmParams u{};
-        u.a_row0 = kb * kNB;
-        u.b_row0 = kb * kNB;
-        u.a_k0 = u.b_k0 = kb0 * kNB;
-        u.ktiles = (kb - kb0) * (kNB / kBK);
-        u.C = A;
-        u.ldc = mp;
-        u.c_row0 = u.c_col0 = kb * kNB;
-        u.tiles_m = nb - kb;
-        u.tiles_n = 1;
-        u.abort_flag = status;
-        gemm_launch<128, G_UPDATE>(tmA, tmA, u, nb - kb, s, c);
+        cur = kb;
+        step("col-update", [&](FactorBufs& f) {
+          GemmParams u{};
+          u.a_row0 = kb * kNB;
+          u.b_row0 = kb * kNB;
+          u.a_k0 = u.b_k0 = kb0 * kNB;
+          u.ktiles = (kb - kb0) * (kNB / kBK);
+          u.C = f.A;
+          u.ldc = mp;
+          u.c_row0 = u.c_col0 = kb * kNB;
+          u.tiles_m = nb - kb;
+          u.tiles_n = 1;
+          u.abort_flag = f.status;
+          gemm_launch<128, G_UPDATE>(f.tmA, f.tmA, u, nb - kb, s, c);
+        });
       }
-      potrf_leaf_kernel<<<1, kLeafThreads, kLeafSmem, s>>>(A, mp, kb, Linv, status, m_valid, 1);
-      ++c.launches;
+      cur = kb;
+      step("leaf", [&](FactorBufs& f) {
+        potrf_leaf_kernel<<<1, kLeafThreads, kLeafSmem, s>>>(f.A, mp, kb, f.Linv, f.status, m_valid, 1);
+        ++c.launches;
+      });
       const int rem = nb - 1 - kb;
       if (rem <= 0) continue;
       // panel: A21 := A21 * inv(L11)^T  (in place, 64-row blocks)
-      GemmParams t{};
-      t.a_row0 = (kb + 1) * kNB;
-      t.a_k0 = kb * kNB;
-      t.b_row0 = kb * kNB;
-      t.b_k0 = 0;
-      t.ktiles = kNB / kBK;
-      t.C = A;
-      t.ldc = mp;
-      t.c_row0 = (kb + 1) * kNB;
-      t.c_col0 = kb * kNB;
-      t.tiles_m = rem * 2;
-      t.tiles_n = 1;
-      t.abort_flag = status;
-      gemm_launch<64, G_STORE>(tmA, tmLinv, t, rem * 2, s, c);
+      cur = kb;
+      step("trsm", [&](FactorBufs& f) {
+        GemmParams t{};
+        t.a_row0 = (kb + 1) * kNB;
+        t.a_k0 = kb * kNB;
+        t.b_row0 = kb * kNB;
+        t.b_k0 = 0;
+        t.ktiles = kNB / kBK;
+        t.C = f.A;
+        t.ldc = mp;
+        t.c_row0 = (kb + 1) * kNB;
+        t.c_col0 = kb * kNB;
+        t.tiles_m = rem * 2;
+        t.tiles_n = 1;
+        t.abort_flag = f.status;
+        gemm_launch<64, G_STORE>(f.tmA, f.tmLinv, t, rem * 2, s, c);
+      });
     }
     const int rem = nb - kend;
     if (rem <= 0) continue;
-    // trailing: A22 -= L21 L21^T over the whole group (K = 128 * group), persistent, C staged by TMA
-    SyrkParams u{};
-    u.row0 = kend * kNB;
-    u.k0 = kb0 * kNB;
-    u.ktiles = (kend - kb0) * (kNB / kBK);
-    u.T = rem;
-    u.abort_flag = status;
-    const int ntl = rem * (rem + 1) / 2;
-    const int grid = g_syrk_persistent ? (ntl < g_sms ? ntl : g_sms) : ntl;
+    const int Kg = (kend - kb0) * kNB;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (g_syrk_events) {
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
       cudaEventRecord(e0, s);
     }
-    dsyrk_persistent_kernel<<<grid, kSyrkThreads, kSyrkSmem, s>>>(tmA, u);
-    ++c.launches;
+    cur = kend;
+    if (g_syrk_ozaki && slices && exps && Kg == 512) {
+      // int8 tensor-core trailing update (Ozaki splitting), FP64-accurate; fixed
+      // geometry per part (slice stride mp rows) -> the same descriptors every group
+      const int R = rem * kNB;
+      step("int8-syrk", [&](FactorBufs& f) {
+        ozaki_slice_kernel<<<(R * 32 + 255) / 256, 256, 0, s>>>(f.A, mp, kend * kNB, kb0 * kNB, R, Kg, slices,
+                                                                exps, f.status, static_cast<int>(mp));
+        CUtensorMap ta, tb;
+        if (!make_tmap_slices(&ta, slices, mp, Kg, kOzM) || !make_tmap_slices(&tb, slices, mp, Kg, kOzN)) {
+          fprintf(stderr, "pkrr: slice tensor map failed\n");
+          abort();
+        }
+        OzParams op{};
+        op.row0 = kend * kNB;
+        op.R = R;
+        op.ksteps = Kg / kOzK;
+        op.exps = exps;
+        op.abort_flag = f.status;
+        ozaki_syrk_kernel<<<rem * (rem + 1), kOzThreads, kOzSmem, s>>>(ta, tb, f.tmA, op);
+        c.launches += 2;
+      });
+    } else {
+      // trailing: A22 -= L21 L21^T over the whole group (K = 128 * group), C staged by TMA
+      step("syrk", [&](FactorBufs& f) {
+        SyrkParams u{};
+        u.row0 = kend * kNB;
+        u.k0 = kb0 * kNB;
+        u.ktiles = (kend - kb0) * (kNB / kBK);
+        u.T = rem;
+        u.abort_flag = f.status;
+        const int ntl = rem * (rem + 1) / 2;
+        const int grid = g_syrk_persistent ? (ntl < g_sms ? ntl : g_sms) : ntl;
+        dsyrk_persistent_kernel<<<grid, kSyrkThreads, kSyrkSmem, s>>>(f.tmA, u);
+        ++c.launches;
+      });
+    }
     if (g_syrk_events) {
       cudaEventRecord(e1, s);
       g_syrk_events->push_back({e0, e1});
       // algorithmic: A22 -= L21 L21^T on the lower triangle incl. diagonal, K = 128*group
-      const double rows = static_cast<double>(rem) * kNB, kk = static_cast<double>(kend - kb0) * kNB;
-      g_syrk_flops->push_back(rows * (rows + 1.0) * kk);
+      const double rows = static_cast<double>(rem) * kNB;
+      g_syrk_flops->push_back(rows * (rows + 1.0) * Kg);
     }
+  }
+  if (shadow) {
+    cudaFreeAsync(sh.A, s);
+    cudaFreeAsync(sh.Linv, s);
+    if (sh.status) cudaFreeAsync(sh.status, s);
   }
 }
 
@@ -1096,6 +1263,12 @@ __global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __re
   for (int64_t c = 0; c < nchunks; ++c) {
     const int slot = static_cast<int>(c % kMeansRing);
     mbar_wait(&full[slot], static_cast<uint32_t>((c / kMeansRing) & 1));
+    // deferred release of the previous slot: its loads were consumed by the DADD
+    // chain before this wait (see dgemm_tn_kernel for the WAR race this avoids)
+    if (c > 0) {
+      __syncwarp();
+      if (threadIdx.x == 0) mbar_arrive(&empty[(c - 1) % kMeansRing]);
+    }
     const int64_t r0 = c * kMeansRows;
     const int rows = static_cast<int>(sz - r0 < kMeansRows ? sz - r0 : kMeansRows);
     // volatile shared loads issued 16 rows ahead of the (strictly ordered) DADD chain
@@ -1124,8 +1297,6 @@ __global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __re
       r += 16;
     }
     for (; r < rows; ++r) s = __dadd_rn(s, lds_f64_at(b + (r * kMeansF) * 8));
-    __syncwarp();
-    if (threadIdx.x == 0) mbar_arrive(&empty[slot]);
   }
   if (threadIdx.x < fw)
     centers[static_cast<int64_t>(j) * d + f0 + threadIdx.x] =

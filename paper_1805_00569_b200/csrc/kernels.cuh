@@ -43,12 +43,19 @@ void launch_gram_cross(const CUtensorMap& tmQ, const CUtensorMap& tmX, const dou
 // Blocked right-looking Cholesky of A (mp x mp, lower, mp % 128 == 0) in place.
 // Linv: mp x 128 scratch receiving inv(L_kk) per diagonal block.
 // status[0] = abort flag, status[1] = first failing global column (int).
+// slices/exps: int8 [8 x mp x 512] and int [mp] scratch for the Ozaki SYRK mode (may be null).
+void shadow_report();  // PKRR_SHADOW debug mode (see launch_potrf)
 void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, double* Linv,
-                  int64_t mp, int64_t m_valid, int* status, cudaStream_t s, Counter& c);
+                  int64_t mp, int64_t m_valid, int* status, cudaStream_t s, Counter& c,
+                  int8_t* slices = nullptr, int* exps = nullptr);
 // Number of 128-column panels per trailing update (K = 128 * G); default 4.
 void set_panel_group(int g);
 // SYRK grid: 0 = one 128x128 tile per CTA (default), 1 = persistent (one CTA per SM).
 void set_syrk_persistent(int on);
+// Trailing SYRK on the int8 tensor cores (tcgen05 kind::i8, Ozaki splitting into 8
+// 7-bit slices, FP64-accurate) when 1; DMMA f64 when 0 (default).
+void set_syrk_ozaki(int on);
+int syrk_ozaki();
 // Probe hook: when set, every trailing-SYRK launch is bracketed by events and its
 // algorithmic flop count recorded (used by pkrrgpu_probe_potrf only).
 void set_syrk_probe(std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* ev, std::vector<double>* flops);

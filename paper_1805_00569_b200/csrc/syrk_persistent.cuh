@@ -123,6 +123,10 @@ __global__ void __launch_bounds__(kSyrkThreads, 1)
       const int s = g % kSyrkStages;
       const uint32_t ph = (g / kSyrkStages) & 1;
       mbar_wait(&full[s], ph);
+      if (g > 0) {  // deferred release of the previous stage (see dgemm_tn_kernel)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[(g - 1) % kSyrkStages]);
+      }
       const unsigned char* sa = ring + s * kSyrkStageBytes;
       const unsigned char* sb = sa + 128 * kBK * 8;
 #pragma unroll
@@ -138,8 +142,6 @@ __global__ void __launch_bounds__(kSyrkThreads, 1)
 #pragma unroll
           for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
     }
     // epilogue: C (smem) -= acc, then TMA store
     mbar_wait(cfull, it & 1);
