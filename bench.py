@@ -29,6 +29,8 @@ import sys
 import tempfile
 import time
 
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # before any CUDA context (see pkrrgpu_create)
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))

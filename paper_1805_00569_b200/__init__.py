@@ -23,6 +23,10 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+
+# up to 17 concurrent streams per context (see pkrrgpu_create); must precede the
+# process's CUDA context creation to take effect
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -213,11 +217,14 @@ class Engine:
                     syrk_launches=int(out[4]), npd=int(out[5]))
 
     def timings(self, parts: int = 0):
-        ms = (C.c_double * (8 + parts))()
-        _lib.pkrrgpu_last_timings(self._h, ms, 8 + parts)
+        n = 8 + 6 * parts
+        ms = (C.c_double * n)()
+        _lib.pkrrgpu_last_timings(self._h, ms, n)
         out = dict(partition=ms[0], train=ms[1], predict=ms[2], total=ms[3], cholesky=ms[4], gram=ms[5])
         if parts:
             out["part_chol_end_ms"] = [ms[8 + i] for i in range(parts)]
+            # first cell, per part: gram start/end, Cholesky start/end, predict end (ms from the call start)
+            out["part_timeline_ms"] = [[ms[8 + parts + 5 * i + j] for j in range(5)] for i in range(parts)]
         return out
 
     # ---- kernel.hpp ---------------------------------------------------------

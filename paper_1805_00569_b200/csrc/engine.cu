@@ -8,6 +8,7 @@
 // O(k) control decisions of the clustering loops (convergence, empty-cluster
 // reseed, k-balance capacity bookkeeping) exactly as clustering.cpp does.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -17,6 +18,7 @@
 #include <random>
 #include <string>
 #include <vector>
+#include <array>
 
 #include "../../include/pkrr_gpu.h"
 #include "kernels.cuh"
@@ -107,9 +109,12 @@ struct pkrrgpu_ctx {
   cudaStream_t main = nullptr;
   std::vector<cudaStream_t> work;      // graded priorities (highest first)
   std::vector<cudaStream_t> work_eq;   // equal (default) priority
+  std::vector<cudaStream_t> aux, aux_eq;  // lookahead companions of work / work_eq (same priorities)
+  cudaStream_t aux_main = nullptr;        // lookahead companion of main
   pk::Counter counter;
   double timings[8] = {0};
   std::vector<double> part_ms;  // last grid call: per-part Cholesky end, ms after the phase start
+  std::vector<double> part_tl;  // last grid call, first cell: per part {gram0, gram1, chol0, chol1, pred1} ms after start
   void* pinned = nullptr;  // 64 KB pinned staging for small device->host reads
   double total_mem = 0.0;  // device HBM bytes
   std::multimap<size_t, void*> free_blocks;
@@ -556,10 +561,11 @@ void part_load(pkrrgpu_ctx* ctx, PartBuf& pb, const double* dX, const double* dy
 }
 
 void part_solve(pkrrgpu_ctx* ctx, PartBuf& pb, double lambda, int* status, double* res_out,
-                cudaStream_t s) {
+                cudaStream_t s, cudaStream_t s2) {
   const double shift = lambda * static_cast<double>(pb.m);
   pk::launch_assemble(pb.K, pb.A, pb.mp, shift, status, s, ctx->counter);
-  pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, status, s, ctx->counter, pb.slices, pb.exps);
+  pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, status, s, ctx->counter, pb.slices, pb.exps,
+                   s2);
   pk::launch_trsv(pb.A, pb.Linv, pb.mp, pb.yp, pb.z, pb.alpha, pb.scratch, status, s, ctx->counter);
   if (res_out) {
     pk::launch_gemv_rows(pb.K, pb.mp, pb.m, pb.m, pb.alpha, pb.Ka, status, s, ctx->counter);
@@ -617,6 +623,11 @@ const char* pkrrgpu_last_error(void) { return g_err.c_str(); }
 int pkrrgpu_create(int device, pkrrgpu_ctx** out) {
   try {
     if (!out) fail(PKRRGPU_INVALID, "null out");
+    // The grid runs up to 17 streams (8 part streams, their 8 lookahead companions,
+    // main); with the default 8 hardware work queues streams share queues and pick up
+    // false dependencies.  Read at context creation: effective when this library
+    // creates the context (the Python package sets it at import as well).
+    setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
     int count = 0;
     ck(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
     if (device < 0 || device >= count) fail(PKRRGPU_INVALID, "no such CUDA device");
@@ -631,20 +642,28 @@ int pkrrgpu_create(int device, pkrrgpu_ctx** out) {
     if (const char* g = std::getenv("PKRR_PANEL_GROUP")) pk::set_panel_group(std::atoi(g));
     if (const char* g = std::getenv("PKRR_SYRK_PERSISTENT")) pk::set_syrk_persistent(std::atoi(g));
     if (const char* g = std::getenv("PKRR_SYRK")) pk::set_syrk_ozaki(std::strcmp(g, "ozaki") == 0 ? 1 : 0);
-    ck(cudaStreamCreateWithFlags(&c->main, cudaStreamNonBlocking), "stream");
+    int least = 0, greatest = 0;
+    ck(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
+    // the panel chain of a factorisation outranks its lookahead trailing update
+    ck(cudaStreamCreateWithPriority(&c->main, cudaStreamNonBlocking, greatest), "stream");
     ck(cudaMallocHost(&c->pinned, 64 * 1024), "pinned");
     // work streams in decreasing priority: the grid maps parts to them largest
     // first (LPT on one GPU), so the critical part wins the block scheduler
-    int least = 0, greatest = 0;
-    ck(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
     c->work.resize(8);
     c->work_eq.resize(8);
+    c->aux.resize(8);
+    c->aux_eq.resize(8);
     for (size_t i = 0; i < c->work.size(); ++i) {
       int prio = greatest + static_cast<int>(i);
       if (prio > least) prio = least;
+      const int below = prio + 1 > least ? least : prio + 1;
+      const int eq = least - 1 < greatest ? greatest : least - 1;
       ck(cudaStreamCreateWithPriority(&c->work[i], cudaStreamNonBlocking, prio), "stream");
-      ck(cudaStreamCreateWithFlags(&c->work_eq[i], cudaStreamNonBlocking), "stream");
+      ck(cudaStreamCreateWithPriority(&c->work_eq[i], cudaStreamNonBlocking, eq), "stream");
+      ck(cudaStreamCreateWithPriority(&c->aux[i], cudaStreamNonBlocking, below), "stream");
+      ck(cudaStreamCreateWithPriority(&c->aux_eq[i], cudaStreamNonBlocking, least), "stream");
     }
+    ck(cudaStreamCreateWithPriority(&c->aux_main, cudaStreamNonBlocking, least), "stream");
     *out = c;
     return PKRRGPU_OK;
   } catch (const Fail& f) {
@@ -660,6 +679,9 @@ void pkrrgpu_destroy(pkrrgpu_ctx* ctx) {
   for (auto& kv : ctx->live) cudaFree(kv.first);
   for (auto s : ctx->work) cudaStreamDestroy(s);
   for (auto s : ctx->work_eq) cudaStreamDestroy(s);
+  for (auto s : ctx->aux) cudaStreamDestroy(s);
+  for (auto s : ctx->aux_eq) cudaStreamDestroy(s);
+  if (ctx->aux_main) cudaStreamDestroy(ctx->aux_main);
   cudaStreamDestroy(ctx->main);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;
@@ -746,7 +768,12 @@ int pkrrgpu_last_timings(const pkrrgpu_ctx* ctx, double* ms, int n) {
   if (!ctx || !ms) return PKRRGPU_INVALID;
   for (int i = 0; i < n && i < 8; ++i) ms[i] = ctx->timings[i];
   // [8 ...]: per-part Cholesky completion (ms after the first Cholesky phase start)
-  for (int i = 8; i < n && i - 8 < static_cast<int>(ctx->part_ms.size()); ++i) ms[i] = ctx->part_ms[i - 8];
+  const int np = static_cast<int>(ctx->part_ms.size());
+  for (int i = 8; i < n && i - 8 < np; ++i) ms[i] = ctx->part_ms[i - 8];
+  // [8 + p ...]: per part {gram start, gram end, Cholesky start, Cholesky end, predict end}
+  // of the first cell, ms after the grid call's start event
+  for (int i = 8 + np; i < n && i - 8 - np < static_cast<int>(ctx->part_tl.size()); ++i)
+    ms[i] = ctx->part_tl[i - 8 - np];
   return PKRRGPU_OK;
 }
 
@@ -830,7 +857,8 @@ int pkrrgpu_cholesky(pkrrgpu_ctx* ctx, const double* A, int64_t m, double* L, in
     ++ctx->counter.launches;
   }
   int* status = sc.zeros<int>(2, s);
-  pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, m, status, s, ctx->counter, pb.slices, pb.exps);
+  pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, m, status, s, ctx->counter, pb.slices, pb.exps,
+                   ctx->aux_main);
   std::vector<int> st = to_host(status, 2, s);
   if (st[0]) {
     if (npd_pivot) *npd_pivot = st[1];
@@ -888,7 +916,7 @@ int pkrrgpu_train_krr(pkrrgpu_ctx* ctx, const double* X, const double* y, int64_
   pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, m, sigma, pb.K, pb.mp, nullptr, s, ctx->counter);
   int* status = sc.zeros<int>(2, s);
   double* res = sc.zeros<double>(2, s);
-  part_solve(ctx, pb, lambda, status, res, s);
+  part_solve(ctx, pb, lambda, status, res, s, ctx->aux_main);
   std::vector<int> st = to_host(status, 2, s);
   if (st[0]) {
     if (npd_pivot) *npd_pivot = st[1];
@@ -1058,7 +1086,7 @@ int pkrrgpu_train_partitions(pkrrgpu_ctx* ctx, int strategy, const double* X, co
     part_load(ctx, pb, dX, dy, d, po.order + po.start[t], ws);
     pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws,
                         ctx->counter);
-    part_solve(ctx, pb, lambda, status + 2 * t, res + 2 * t, ws);
+    part_solve(ctx, pb, lambda, status + 2 * t, res + 2 * t, ws, ctx->aux[t % ctx->aux.size()]);
   }
   ck(cudaDeviceSynchronize(), "train");
   std::vector<int> st = to_host(status, 2 * po.p, s);
@@ -1183,6 +1211,14 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   cudaStream_t s = ctx->main;
   Timer t_all, t_part;
   ck(cudaEventRecord(t_all.a, s), "event");
+  // PKRR_TRACE_HOST=1: host-side timestamps of the grid call's phases (stderr)
+  static const bool htrace = std::getenv("PKRR_TRACE_HOST") != nullptr;
+  const auto h0 = std::chrono::steady_clock::now();
+  auto hmark = [&](const char* what) {
+    if (htrace)
+      fprintf(stderr, "pkrr host %8.3f ms  %s\n",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count(), what);
+  };
 
   const double* dX = sc.in(a->X_train, n * d, s);
   const double* dy = sc.in(a->y_train, n, s);
@@ -1196,7 +1232,9 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   PartitionOut po;
   const double thr = a->km_max_iters > 0 ? a->km_threshold : 0.01;
   const int iters = a->km_max_iters > 0 ? a->km_max_iters : 100;
+  hmark("inputs enqueued");
   make_partition_device(ctx, sc, a->strategy, dX, n, d, a->p, a->seed, thr, iters, po);
+  hmark("partition returned");
   const int64_t p = po.p;
   for (int64_t q = 0; q < p; ++q)
     if (po.sizes[q] == 0) fail(PKRRGPU_INVALID, "train_partitions: empty part");
@@ -1219,6 +1257,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
     }
   }
   ck(cudaEventRecord(t_part.b, s), "event");
+  hmark("routing returned");
 
   // ---- per-part buffers for the parts this rank owns ----
   std::vector<int64_t> owned;
@@ -1243,6 +1282,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   double* pred_t = sc.zeros<double>(ncell * pp_parts * t, s);
   double* pred_e = te ? sc.zeros<double>(ncell * pp_parts * te, s) : nullptr;
   ck(cudaStreamSynchronize(s), "sync");
+  hmark("result slots ready");
 
   double f_chol = 0, f_gram = 0, f_other = 0;
   size_t S = ctx->work.size();
@@ -1266,6 +1306,10 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   for (size_t i = 0; i < S; ++i) order_by_load[i] = i;
   std::stable_sort(order_by_load.begin(), order_by_load.end(),
                    [&](size_t x, size_t y) { return load[x] > load[y]; });
+  static const int prio_mode = std::getenv("PKRR_PRIO") ? std::atoi(std::getenv("PKRR_PRIO")) : -1;
+  if (prio_mode == 2 && S > 2)  // the critical stream first, then the others shortest-first
+    std::stable_sort(order_by_load.begin() + 1, order_by_load.end(),
+                     [&](size_t x, size_t y) { return load[x] < load[y]; });
   std::vector<size_t> rank_of(S);
   for (size_t r = 0; r < S; ++r) rank_of[order_by_load[r]] = r;
   std::vector<double> nz;
@@ -1275,6 +1319,9 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   bool graded = !nz.empty() && nz.back() > 1.5 * nz[nz.size() / 2];
   if (const char* e = std::getenv("PKRR_PRIO")) graded = std::atoi(e) != 0;
   std::vector<cudaStream_t>& streams = graded ? ctx->work : ctx->work_eq;
+  static const bool no_look = std::getenv("PKRR_LOOKAHEAD") && std::atoi(std::getenv("PKRR_LOOKAHEAD")) == 0;
+  std::vector<cudaStream_t> look_streams(graded ? ctx->aux : ctx->aux_eq);
+  if (no_look) std::fill(look_streams.begin(), look_streams.end(), nullptr);
   std::vector<size_t> sidx(p, 0);
   for (int64_t q : owned) sidx[q] = rank_of[slot[q]];
   // ---- memory-aware batches of parts (largest first) ----
@@ -1315,6 +1362,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   };
   std::vector<Iv> gram_iv, chol_iv, pred_iv;
   std::vector<cudaEvent_t> part_end(p, nullptr);
+  std::vector<std::array<cudaEvent_t, 5>> part_ev(p, std::array<cudaEvent_t, 5>{});
   for (const std::vector<int64_t>& batch : batches) {
     Scope bsc(ctx);  // released (after a device sync) before the next batch
       for (int64_t q : batch) {
@@ -1335,6 +1383,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
         }
       }
     }
+    hmark("part buffers allocated + loads enqueued");
     // Each part flows gram -> (assemble -> Cholesky -> solves -> predict) per cell on
     // its own prioritised stream, with no cross-part joins: a small part's gram or
     // solves overlap the large part's Cholesky.  Phase times are the UNION of the
@@ -1368,6 +1417,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
                                 sigma, qe[q].cross, ws, ctx->counter);
         f_gram += static_cast<double>(d) * m * (m + 1) + 2.0 * (tcount[q] + ecount[q]) * m * d;
         gram_iv.push_back({g0, ev_on(ws)});
+        if (si == 0) part_ev[q][0] = g0, part_ev[q][1] = gram_iv.back().b;
       }
       for (int64_t li = 0; li < nl; ++li) {
         const int64_t cell = li * ns + si;
@@ -1381,10 +1431,11 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
           double* rs = dres + (cell * p + q) * 4;
           cudaEvent_t c0 = ev_on(ws);
           pk::launch_assemble(pb.K, pb.A, pb.mp, shift, st, ws, ctx->counter);
-          pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, st, ws, ctx->counter, pb.slices, pb.exps);
+          pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, st, ws, ctx->counter, pb.slices, pb.exps,
+                           look_streams[sidx[q]]);
           cudaEvent_t c1 = ev_on(ws);
           chol_iv.push_back({c0, c1});
-          if (li == 0 && si == 0) part_end[q] = c1;
+          if (li == 0 && si == 0) part_end[q] = c1, part_ev[q][2] = c0, part_ev[q][3] = c1;
           f_chol += chol_flops(pb.m);
           pk::launch_trsv(pb.A, pb.Linv, pb.mp, pb.yp, pb.z, pb.alpha, pb.scratch, st, ws, ctx->counter);
           pk::launch_gemv_rows(pb.K, pb.mp, pb.m, pb.m, pb.alpha, pb.Ka, st, ws, ctx->counter);
@@ -1403,6 +1454,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
             f_other += 2.0 * ecount[q] * m;
           }
           pred_iv.push_back({c1, ev_on(ws)});
+          if (li == 0 && si == 0) part_ev[q][4] = pred_iv.back().b;
         }
       }
     }
@@ -1410,6 +1462,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
       cudaEvent_t e = ev_on(streams[sidx[q]]);
       ck(cudaStreamWaitEvent(s, e, 0), "wait");
     }
+    hmark("batch enqueued");
   }
   pk::shadow_report();
   // combine for average/oracle predictors (world == 1)
@@ -1467,6 +1520,14 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
       cudaEventElapsedTime(&ms, t_all.a, part_end[q]);
       ctx->part_ms[q] = ms - chol0;
     }
+  ctx->part_tl.assign(5 * p, 0.0);
+  for (int64_t q = 0; q < p; ++q)
+    for (int j = 0; j < 5; ++j)
+      if (part_ev[q][j]) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, t_all.a, part_ev[q][j]);
+        ctx->part_tl[5 * q + j] = ms;
+      }
   for (auto e : evs) cudaEventDestroy(e);
 
   const std::vector<int> st = to_host(dstatus, ncell * p * 2, s);

@@ -539,7 +539,7 @@ struct FactorBufs {
 
 void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, double* Linv,
                   int64_t mp, int64_t m_valid, int* status, cudaStream_t s, Counter& c, int8_t* slices,
-                  int* exps) {
+                  int* exps, cudaStream_t s2) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(potrf_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLeafSmem);
@@ -581,6 +581,14 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
   };
   const int nb = static_cast<int>(mp / kNB);
   const int G = g_panel_group;
+  // lookahead needs a second stream; not with the shadow checker or the int8 update
+  const bool look = s2 != nullptr && !shadow && !(g_syrk_ozaki && slices && exps) && nb > 2 * G;
+  cudaEvent_t ev_panel = nullptr, ev_b = nullptr;
+  bool b_pending = false;
+  if (look) {
+    cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming);
+  }
   for (int kb0 = 0; kb0 < nb; kb0 += G) {
     const int kend = kb0 + G < nb ? kb0 + G : nb;
     for (int kb = kb0; kb < kend; ++kb) {
@@ -659,6 +667,40 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
         ozaki_syrk_kernel<<<rem * (rem + 1), kOzThreads, kOzSmem, s>>>(ta, tb, f.tmA, op);
         c.launches += 2;
       });
+    } else if (look) {
+      // lookahead: (a) the next panel's G tile columns now, on s, so the next panel
+      // chain starts at once; (b) the rest of the trailing triangle on s2, overlapping
+      // that chain.  Per tile the arithmetic is the full-update kernel's (same K order),
+      // and (b) of this group runs after (b) of the previous one on s2, (a) after it too,
+      // so every element sees the panels in the same order: bitwise the same factor.
+      const int G2 = rem < G ? rem : G;
+      cudaEventRecord(ev_panel, s);
+      cudaStreamWaitEvent(s2, ev_panel, 0);
+      if (b_pending) cudaStreamWaitEvent(s, ev_b, 0);
+      SyrkParams u{};
+      u.row0 = kend * kNB;
+      u.k0 = kb0 * kNB;
+      u.ktiles = (kend - kb0) * (kNB / kBK);
+      u.T = rem;
+      u.abort_flag = status;
+      u.narrow = G2;
+      dsyrk_persistent_kernel<<<syrk_tile_count(rem, G2), kSyrkThreads, kSyrkSmem, s>>>(tmA, u);
+      ++c.launches;
+      if (rem > G2) {
+        SyrkParams v = u;
+        v.row0 = (kend + G2) * kNB;
+        v.T = rem - G2;
+        v.narrow = 0;
+        // persistent grid on all but `reserve` SMs, so the (higher-priority) panel chain
+        // always finds free SMs instead of waiting for a SYRK wave to drain
+        static const int reserve = std::getenv("PKRR_LOOK_RESERVE") ? std::atoi(std::getenv("PKRR_LOOK_RESERVE")) : 8;
+        const int nt = syrk_tile_count(v.T, 0);
+        const int cap = g_sms - reserve;
+        dsyrk_persistent_kernel<<<reserve > 0 && nt > cap ? cap : nt, kSyrkThreads, kSyrkSmem, s2>>>(tmA, v);
+        ++c.launches;
+        cudaEventRecord(ev_b, s2);
+        b_pending = true;
+      }
     } else {
       // trailing: A22 -= L21 L21^T over the whole group (K = 128 * group), C staged by TMA
       step("syrk", [&](FactorBufs& f) {
@@ -681,6 +723,11 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
       const double rows = static_cast<double>(rem) * kNB;
       g_syrk_flops->push_back(rows * (rows + 1.0) * Kg);
     }
+  }
+  if (look) {
+    if (b_pending) cudaStreamWaitEvent(s, ev_b, 0);
+    cudaEventDestroy(ev_panel);  // destruction is deferred until the recorded work completes
+    cudaEventDestroy(ev_b);
   }
   if (shadow) {
     cudaFreeAsync(sh.A, s);
@@ -729,98 +776,145 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 
-// rows GEMV on a 128x128 block: out[r] += sum_c M[r][c] v[c]; 8 warps x 16 rows
-__device__ __forceinline__ void block_gemv_rows(const double* __restrict__ M, int64_t ld,
-                                                const double* v, double* out, int warp, int lane) {
-  for (int rr = 0; rr < 16; ++rr) {
-    const int r = warp * 16 + rr;
-    const double* row = M + static_cast<int64_t>(r) * ld;
-    const double4 a = *reinterpret_cast<const double4*>(row + lane * 4);
-    double s = a.x * v[lane * 4] + a.y * v[lane * 4 + 1] + a.z * v[lane * 4 + 2] +
-               a.w * v[lane * 4 + 3];
-    s = warp_sum(s);
-    if (lane == 0) out[r] += s;
+// Both solves: CTA (ticket order) owns one 128-row block; thread (warp w, lane l)
+// covers rows 16w..16w+15 x columns 4l..4l+3 of every 128x128 block it streams.
+// A block's 16 row segments are loaded into registers BEFORE waiting for the flag
+// of the vector block it multiplies, and partial sums stay per thread across all
+// blocks (one cross-lane / cross-warp reduction per CTA), so the dependency chain
+// costs one flag hand-off + one small diagonal-block product per step.
+__device__ __forceinline__ double4 ldg_d4(const double* p) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ double4 ldcg_d4(const double* p) {
+  const double2 a = __ldcg(reinterpret_cast<const double2*>(p)), b = __ldcg(reinterpret_cast<const double2*>(p) + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ void load_block16(const double* __restrict__ base, int64_t ld, double4 (&m)[16]) {
+#pragma unroll
+  for (int rr = 0; rr < 16; ++rr) m[rr] = ldg_d4(base + rr * ld);
+}
+__device__ __forceinline__ void wait_flag(const int* f, int lane) {
+  if (lane == 0)
+    while (ld_acquire(f) == 0) {
+    }
+  __syncwarp();
+}
+__device__ __forceinline__ void prefetch_l2_block(const double* blk, int64_t ld, int tid) {
+  // 128 rows x 1 KB: 1024 lines of 128 B, 4 per thread
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int line = tid + 256 * q, r = line >> 3, c = (line & 7) * 16;
+    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(blk + r * ld + c));
   }
 }
 
-// cols GEMV on a 128x128 block: out[c] += sum_r M[r][c] v[r]; 256 threads
-__device__ __forceinline__ void block_gemv_cols(const double* __restrict__ M, int64_t ld,
-                                                const double* v, double* part, double* out,
-                                                int tid) {
-  const int c = tid & 127, h = tid >> 7;
-  double s = 0.0;
-  for (int r = h * 64; r < h * 64 + 64; ++r) s += M[static_cast<int64_t>(r) * ld + c] * v[r];
-  part[h * 128 + c] = s;
-  __syncthreads();
-  if (tid < 128) out[tid] += part[tid] + part[128 + tid];
-  __syncthreads();
-}
-
+// forward: z_I = inv(L_II) (b_I - sum_{K<I} L_IK z_K)
 __global__ void __launch_bounds__(256) trsv_fwd_kernel(const double* __restrict__ L, int64_t ld,
                                                        const double* __restrict__ Linv,
                                                        const double* __restrict__ b, double* z,
                                                        int nb, int* ticket, int* flags,
                                                        const int* abort) {
   if (abort && *reinterpret_cast<const volatile int*>(abort)) return;
-  __shared__ double acc[kNB], vk[kNB];
+  __shared__ double sacc[kNB];
   __shared__ int sI;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   if (tid == 0) sI = atomicAdd(ticket, 1);
-  if (tid < kNB) acc[tid] = 0.0;
   __syncthreads();
   const int I = sI;
+  prefetch_l2_block(Linv + static_cast<int64_t>(I) * kNB * kNB, kNB, tid);
+  const double* rows = L + (static_cast<int64_t>(I) * kNB + w * 16) * ld + lane * 4;
+  double acc[16];
+#pragma unroll
+  for (int rr = 0; rr < 16; ++rr) acc[rr] = 0.0;
   for (int K = 0; K < I; ++K) {
-    if (tid == 0)
-      while (ld_acquire(&flags[K]) == 0) {
-      }
-    __syncthreads();
-    if (tid < kNB) vk[tid] = __ldcg(&z[K * kNB + tid]);
-    __syncthreads();
-    block_gemv_rows(L + static_cast<int64_t>(I) * kNB * ld + K * kNB, ld, vk, acc, warp, lane);
-    __syncthreads();
+    double4 m[16];
+    load_block16(rows + K * kNB, ld, m);
+    wait_flag(&flags[K], lane);
+    const double4 v = ldcg_d4(z + K * kNB + lane * 4);
+#pragma unroll
+    for (int rr = 0; rr < 16; ++rr)
+      acc[rr] = fma(m[rr].w, v.w, fma(m[rr].z, v.z, fma(m[rr].y, v.y, fma(m[rr].x, v.x, acc[rr]))));
   }
-  if (tid < kNB) {
-    vk[tid] = b[I * kNB + tid] - acc[tid];
-    acc[tid] = 0.0;
+#pragma unroll
+  for (int rr = 0; rr < 16; ++rr) {
+    const double sum = warp_sum(acc[rr]);
+    if (lane == 0) sacc[w * 16 + rr] = b[I * kNB + w * 16 + rr] - sum;
   }
   __syncthreads();
-  block_gemv_rows(Linv + static_cast<int64_t>(I) * kNB * kNB, kNB, vk, acc, warp, lane);
-  __syncthreads();
-  if (tid < kNB) z[I * kNB + tid] = acc[tid];
+  const double4 v = *reinterpret_cast<const double4*>(sacc + lane * 4);
+  double4 m[16];
+  load_block16(Linv + (static_cast<int64_t>(I) * kNB + w * 16) * kNB + lane * 4, kNB, m);
+#pragma unroll
+  for (int rr = 0; rr < 16; ++rr) {
+    const double sum = warp_sum(fma(m[rr].w, v.w, fma(m[rr].z, v.z, fma(m[rr].y, v.y, m[rr].x * v.x))));
+    if (lane == 0) z[I * kNB + w * 16 + rr] = sum;
+  }
   __threadfence();
   __syncthreads();
   if (tid == 0) st_release(&flags[I], 1);
 }
 
+// backward: x_I = inv(L_II)^T (z_I - sum_{K>I} L_KI^T x_K)
 __global__ void __launch_bounds__(256) trsv_bwd_kernel(const double* __restrict__ L, int64_t ld,
                                                        const double* __restrict__ Linv,
                                                        const double* __restrict__ z, double* x,
                                                        int nb, int* ticket, int* flags,
                                                        const int* abort) {
   if (abort && *reinterpret_cast<const volatile int*>(abort)) return;
-  __shared__ double acc[kNB], vk[kNB], part[2 * kNB];
+  __shared__ double red[8][kNB];
+  __shared__ double sv[kNB];
   __shared__ int sI;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   if (tid == 0) sI = nb - 1 - atomicAdd(ticket, 1);
-  if (tid < kNB) acc[tid] = 0.0;
   __syncthreads();
   const int I = sI;
+  prefetch_l2_block(Linv + static_cast<int64_t>(I) * kNB * kNB, kNB, tid);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // columns 4l..4l+3, partial over this warp's rows
   for (int K = nb - 1; K > I; --K) {
-    if (tid == 0)
-      while (ld_acquire(&flags[K]) == 0) {
-      }
-    __syncthreads();
-    if (tid < kNB) vk[tid] = __ldcg(&x[K * kNB + tid]);
-    __syncthreads();
-    block_gemv_cols(L + static_cast<int64_t>(K) * kNB * ld + I * kNB, ld, vk, part, acc, tid);
+    double4 m[16];
+    load_block16(L + (static_cast<int64_t>(K) * kNB + w * 16) * ld + I * kNB + lane * 4, ld, m);
+    wait_flag(&flags[K], lane);
+    const double xv = lane < 16 ? __ldcg(x + K * kNB + w * 16 + lane) : 0.0;
+#pragma unroll
+    for (int rr = 0; rr < 16; ++rr) {
+      const double v = __shfl_sync(0xffffffffu, xv, rr);
+      a0 = fma(m[rr].x, v, a0);
+      a1 = fma(m[rr].y, v, a1);
+      a2 = fma(m[rr].z, v, a2);
+      a3 = fma(m[rr].w, v, a3);
+    }
   }
+  *reinterpret_cast<double4*>(&red[w][lane * 4]) = make_double4(a0, a1, a2, a3);
+  __syncthreads();
   if (tid < kNB) {
-    vk[tid] = z[I * kNB + tid] - acc[tid];
-    acc[tid] = 0.0;
+    double sum = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sum += red[q][tid];
+    sv[tid] = z[I * kNB + tid] - sum;
   }
   __syncthreads();
-  block_gemv_cols(Linv + static_cast<int64_t>(I) * kNB * kNB, kNB, vk, part, acc, tid);
-  if (tid < kNB) x[I * kNB + tid] = acc[tid];
+  // x_I = Linv_I^T sv: column sums over this warp's 16 rows, then across warps
+  double4 m[16];
+  load_block16(Linv + (static_cast<int64_t>(I) * kNB + w * 16) * kNB + lane * 4, kNB, m);
+  a0 = a1 = a2 = a3 = 0.0;
+#pragma unroll
+  for (int rr = 0; rr < 16; ++rr) {
+    const double v = sv[w * 16 + rr];
+    a0 = fma(m[rr].x, v, a0);
+    a1 = fma(m[rr].y, v, a1);
+    a2 = fma(m[rr].z, v, a2);
+    a3 = fma(m[rr].w, v, a3);
+  }
+  __syncthreads();
+  *reinterpret_cast<double4*>(&red[w][lane * 4]) = make_double4(a0, a1, a2, a3);
+  __syncthreads();
+  if (tid < kNB) {
+    double sum = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sum += red[q][tid];
+    x[I * kNB + tid] = sum;
+  }
   __threadfence();
   __syncthreads();
   if (tid == 0) st_release(&flags[I], 1);

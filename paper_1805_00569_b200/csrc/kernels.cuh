@@ -47,7 +47,10 @@ void launch_gram_cross(const CUtensorMap& tmQ, const CUtensorMap& tmX, const dou
 void shadow_report();  // PKRR_SHADOW debug mode (see launch_potrf)
 void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, double* Linv,
                   int64_t mp, int64_t m_valid, int* status, cudaStream_t s, Counter& c,
-                  int8_t* slices = nullptr, int* exps = nullptr);
+                  int8_t* slices = nullptr, int* exps = nullptr, cudaStream_t s2 = nullptr);
+// s2 (optional): a second stream for lookahead -- the next panel's columns are
+// updated first on s and the rest of the trailing update runs on s2, overlapping the
+// next panel factorisation; the result is bitwise the same as without.
 // Number of 128-column panels per trailing update (K = 128 * G); default 4.
 void set_panel_group(int g);
 // SYRK grid: 0 = one 128x128 tile per CTA (default), 1 = persistent (one CTA per SM).

@@ -16,7 +16,13 @@ struct SyrkParams {
   int ktiles;  // panel width / 16
   int T;       // trailing tiles per side (lower tiles: T(T+1)/2)
   const int* abort_flag;
+  int narrow;  // 0: all lower tiles; > 0: only tile columns tn < narrow (lookahead panel update)
 };
+
+__host__ __device__ __forceinline__ int syrk_tile_count(int T, int narrow) {
+  if (narrow <= 0 || narrow >= T) return T * (T + 1) / 2;
+  return narrow * (narrow + 1) / 2 + (T - narrow) * narrow;
+}
 
 constexpr int kSyrkStages = 3;
 constexpr int kSyrkThreads = 384;  // warpgroup 0: TMA producer; warpgroups 1-2: DMMA consumers
@@ -54,8 +60,18 @@ __global__ void __launch_bounds__(kSyrkThreads, 1)
     fence_mbar_init();
   }
   __syncthreads();
-  const int ntiles = p.T * (p.T + 1) / 2;
+  const int ntiles = syrk_tile_count(p.T, p.narrow);
   const int KT = p.ktiles;
+  // tile b -> (tm, tn): the lower triangle, or its first `narrow` tile columns
+  auto coords = [&](int b, int& tm, int& tn) {
+    const int tri = p.narrow * (p.narrow + 1) / 2;
+    if (p.narrow <= 0 || b < tri) {
+      lower_tile_coords(b, tm, tn);
+    } else {
+      tm = p.narrow + (b - tri) / p.narrow;
+      tn = (b - tri) % p.narrow;
+    }
+  };
 
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
@@ -65,7 +81,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1)
       int it = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         int tm, tn;
-        lower_tile_coords(tile, tm, tn);
+        coords(tile, tm, tn);
         const int arow = p.row0 + tm * 128, brow = p.row0 + tn * 128;
         for (int kt = 0; kt < KT; ++kt, ++g) {
           const int s = g % kSyrkStages;
@@ -113,7 +129,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 1)
   int it = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     int tm, tn;
-    lower_tile_coords(tile, tm, tn);
+    coords(tile, tm, tn);
     double acc[8][4][2];
 #pragma unroll
     for (int i = 0; i < 8; ++i)

@@ -79,3 +79,14 @@ def test_int8_mode_reproducible_and_matches_dmma():
     a = np.frombuffer(bytes.fromhex(oz[0]["pred"]), dtype=np.float64)
     b = np.frombuffer(bytes.fromhex(dm[0]["pred"]), dtype=np.float64)
     assert np.linalg.norm(a - b) <= 1e-9 * np.linalg.norm(b)
+
+
+def test_lookahead_is_bitwise_neutral():
+    """The lookahead split of the trailing update (next panel's columns first, the
+    rest on a second stream) keeps every element's update order: the grid result is
+    bitwise the one without lookahead, and repeated runs agree bitwise."""
+    la, _ = _run({}, 65536, 8, reps=2)
+    no, _ = _run({"PKRR_LOOKAHEAD": "0"}, 65536, 8, reps=1)
+    assert la[0]["pred"] == la[1]["pred"] == no[0]["pred"]
+    assert la[0]["mse"] == no[0]["mse"]
+    assert la[0]["res"] == no[0]["res"]
