@@ -213,12 +213,32 @@ typedef struct {
 int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* args,
                            pkrrgpu_grid_out* out);
 
+/* ---- data preparation (dataset.hpp standardize, strategies.hpp auto_sigma_grid) */
+
+/* standardize -- dataset.cpp:199-232 (+ apply_feature_stats :178-197), dense rows:
+ * per-column mean / stddev from the train rows (row-order sums, divisor n, variance
+ * clamped at 0), then (x - mean) / stddev for train and test (0 where stddev == 0).
+ * Bitwise the reference's.  X_test may be NULL with t = 0; the outputs may alias
+ * nothing else; mean_out / stddev_out (d entries) may be NULL. */
+int pkrrgpu_standardize(pkrrgpu_ctx* ctx, const double* X_train, int64_t n, int64_t d,
+                        const double* X_test, int64_t t, double* train_out, double* test_out,
+                        double* mean_out, double* stddev_out);
+
+/* auto_sigma_grid -- strategies.cpp:204-234: min(n, 512) rows drawn by
+ * random_permutation(Rng(sub_seed(seed, "sigma-grid"))), the lower median g of their
+ * pairwise distances (1 if none or 0), grid_out[e + 4] = g * 2^e for e = -4..4.
+ * Bitwise the reference's. */
+int pkrrgpu_auto_sigma_grid(pkrrgpu_ctx* ctx, const double* X, int64_t n, int64_t d, uint64_t seed,
+                            double* grid_out);
+
 /* ---- timing hooks (bench / profiling only) ------------------------------- */
 
 /* Device time (ms, CUDA events on the engine's streams) spent in the last
  * grid call by phase: [0] partition, [1] train (gram + Cholesky + solves),
  * [2] solves + predict, [3] total, [4] Cholesky, [5] gram; [8 + t] = when part
- * t's first Cholesky finished, ms after that phase started (n >= 8 + p). */
+ * t's first Cholesky finished, ms after that phase started; [8 + p + 5t .. +4] =
+ * part t's first-cell {gram start, gram end, Cholesky start, Cholesky end,
+ * predict end}, ms after the call started (n >= 8 + 6p). */
 int pkrrgpu_last_timings(const pkrrgpu_ctx* ctx, double* ms, int n);
 
 /* The context's launch stream (cudaStream_t), so callers can time calls with

@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "pkrr/clustering.hpp"
+#include "pkrr/dataset.hpp"
 #include "pkrr/kernel.hpp"
 #include "pkrr/runtime.hpp"
 #include "pkrr/solver.hpp"
@@ -238,7 +239,50 @@ inline int nearest_center(const std::vector<std::vector<double>>& centers, Spars
 
 inline int nearest_center(const Clustering& c, SparseRow x) { return gpu::nearest_center(c.centers, x); }
 
+// ---- dataset.hpp: standardize (dataset.cpp:199-232) ---------------------------
+inline StandardizeResult standardize(const Dataset& train, const Dataset& test) {
+  if (train.n == 0) throw std::invalid_argument("standardize: empty training set");
+  if (test.n > 0 && test.d > train.d)
+    throw std::invalid_argument("standardize: test dimension exceeds train dimension");
+  const std::size_t d = train.d;
+  const std::vector<double> X = detail::dense(train);
+  std::vector<double> T(test.n * d, 0.0);  // test rows widened to train.d (extra columns dropped below)
+  for (std::size_t i = 0; i < test.n; ++i) {
+    const SparseRow r = test.row(i);
+    for (std::size_t k = 0; k < r.nnz(); ++k) T[i * d + r.idx[k]] = r.val[k];
+  }
+  std::vector<double> Xo(X.size()), To(T.size());
+  StandardizeResult out;
+  out.stats.mean.resize(d);
+  out.stats.stddev.resize(d);
+  detail::check(pkrrgpu_standardize(default_engine().get(), X.data(), train.n, d, test.n ? T.data() : nullptr,
+                                    test.n, Xo.data(), test.n ? To.data() : nullptr, out.stats.mean.data(),
+                                    out.stats.stddev.data()));
+  auto emit = [](Dataset& ds, const std::vector<double>& V, std::size_t rows, std::size_t ld, std::size_t w,
+                 const std::vector<double>& y) {  // apply_feature_stats' dense rows (dataset.cpp:183-193)
+    ds.d = w;
+    std::vector<int> idx(w);
+    for (std::size_t j = 0; j < w; ++j) idx[j] = static_cast<int>(j);
+    for (std::size_t i = 0; i < rows; ++i) ds.add_row(idx, std::span<const double>(V.data() + i * ld, w), y[i]);
+    ds.d = w;
+  };
+  emit(out.train, Xo, train.n, d, d, train.y);
+  if (test.n > 0) {
+    emit(out.test, To, test.n, d, test.d, test.y);
+    if (test.d < train.d) out.test.d = train.d;  // dataset.cpp:229
+  }
+  return out;
+}
+
 // ---- strategies.hpp ----------------------------------------------------------
+inline std::vector<double> auto_sigma_grid(const Dataset& train, std::uint64_t seed) {
+  const std::vector<double> X = detail::dense(train);
+  std::vector<double> g(9);
+  detail::check(pkrrgpu_auto_sigma_grid(default_engine().get(), train.n ? X.data() : nullptr, train.n, train.d,
+                                        seed, g.data()));
+  return g;
+}
+
 inline PartitionSet make_partition(StrategyKind kind, const Dataset& train, std::size_t p, std::uint64_t seed) {
   const std::vector<double> D = detail::dense(train);
   std::vector<int32_t> part_of(train.n);

@@ -107,6 +107,25 @@ class _Base:
         centers, x = _f64(centers), _f64(x)
         return int(self._nearest(_p(centers, _d), centers.shape[0], centers.shape[1], _p(x, _d)))
 
+    # ---- data preparation (dataset.cpp:199-232, strategies.cpp:204-234) -----
+    def standardize(self, Xtr, Xte=None):
+        Xtr = _f64(Xtr)
+        n, d = Xtr.shape
+        Xte = np.zeros((0, d)) if Xte is None else _f64(Xte)
+        tr, te = np.zeros_like(Xtr), np.zeros_like(Xte)
+        mean, sd = np.empty(d), np.empty(d)
+        st = self._standardize(_p(Xtr, _d), n, d, _p(Xte, _d), Xte.shape[0], _p(tr, _d), _p(te, _d),
+                               _p(mean, _d), _p(sd, _d))
+        if st:
+            raise ValueError("standardize failed")
+        return tr, te, mean, sd
+
+    def auto_sigma_grid(self, X, seed):
+        X = _f64(X)
+        g = np.empty(9)
+        self._sigma_grid(_p(X, _d), X.shape[0], X.shape[1], seed, _p(g, _d))
+        return g
+
     def make_partition(self, kind, X, p, seed):
         X = _f64(X)
         n, d = X.shape
@@ -151,6 +170,9 @@ class Oracle(_Base):
         self._sub_seed = self._fn("sub_seed", C.c_uint64, C.c_uint64, C.c_char_p)
         self._sqnorm = self._fn("squared_norm", C.c_double, _d, C.c_int64)
         self._resid = self._fn("residual_slice", C.c_double, _d, C.c_int64, C.c_double, _d, _d)
+        _std = self._fn("standardize", None, _d, C.c_int64, C.c_int64, _d, C.c_int64, _d, _d, _d, _d)
+        self._standardize = lambda *a: (_std(*a), 0)[1]
+        self._sigma_grid = self._fn("auto_sigma_grid", None, _d, C.c_int64, C.c_int64, C.c_uint64, _d)
 
     def cholesky(self, A):
         L = _f64(A).copy()
@@ -216,6 +238,25 @@ class Oracle(_Base):
                           _p(res, _d), _p(part, _i32), _p(cen, _d), _p(best_pred, _d))
         return dict(best=int(best), mse=mse, failed=failed.astype(bool), residual=res, part_of=part,
                     centers=cen, best_pred=best_pred)
+
+    # ---- data preparation (dataset.cpp:199-232, strategies.cpp:204-234) -----
+    def standardize(self, Xtr, Xte=None):
+        Xtr = _f64(Xtr)
+        n, d = Xtr.shape
+        Xte = np.zeros((0, d)) if Xte is None else _f64(Xte)
+        tr, te = np.zeros_like(Xtr), np.zeros_like(Xte)
+        mean, sd = np.empty(d), np.empty(d)
+        st = self._standardize(_p(Xtr, _d), n, d, _p(Xte, _d), Xte.shape[0], _p(tr, _d), _p(te, _d),
+                               _p(mean, _d), _p(sd, _d))
+        if st:
+            raise ValueError("standardize failed")
+        return tr, te, mean, sd
+
+    def auto_sigma_grid(self, X, seed):
+        X = _f64(X)
+        g = np.empty(9)
+        self._sigma_grid(_p(X, _d), X.shape[0], X.shape[1], seed, _p(g, _d))
+        return g
 
     def make_partition(self, kind, X, p, seed):
         """Returns (part_of, order, centers); order = rows part by part."""
@@ -288,6 +329,9 @@ class Reference(_Base):
         self._stream = self._fn("rng_stream", None, C.c_uint64, C.c_int64, _d, _u64, C.c_uint64)
         self._perm = self._fn("random_permutation", None, C.c_uint64, C.c_int64, _u64)
         self._err = self._fn("last_error", C.c_char_p)
+        self._standardize = self._fn("standardize", C.c_int, _d, C.c_int64, C.c_int64, _d, C.c_int64, _d, _d,
+                                     _d, _d)
+        self._sigma_grid = self._fn("auto_sigma_grid", C.c_int, _d, C.c_int64, C.c_int64, C.c_uint64, _d)
 
     def cholesky(self, A):
         A = _f64(A)

@@ -719,3 +719,71 @@ int64_t pko_grid_search(int kind, const double* Xtr, const double* ytr, int64_t 
   free(order);
   return best;
 }
+
+/* ------------------------------------------------------------------------ */
+/* data preparation                                                         */
+/* ------------------------------------------------------------------------ */
+
+/* dataset.cpp:199-232 standardize + apply_feature_stats :178-197, dense rows:
+   row-order sums over the stored entries, divisor n, variance clamped at 0 */
+void pko_standardize(const double* Xtr, int64_t n, int64_t d, const double* Xte, int64_t t,
+                     double* Xtr_out, double* Xte_out, double* mean, double* stddev) {
+  double* sum = (double*)calloc((size_t)d, sizeof(double));
+  double* sq = (double*)calloc((size_t)d, sizeof(double));
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < d; ++j) {
+      const double v = Xtr[i * d + j];
+      sum[j] += v;
+      sq[j] += v * v;
+    }
+  const double inv_n = 1.0 / (double)n;
+  for (int64_t j = 0; j < d; ++j) {
+    mean[j] = sum[j] * inv_n;
+    double var = sq[j] * inv_n - mean[j] * mean[j];
+    if (var < 0.0) var = 0.0;
+    stddev[j] = sqrt(var);
+  }
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < d; ++j)
+      Xtr_out[i * d + j] = stddev[j] == 0.0 ? 0.0 : (Xtr[i * d + j] - mean[j]) / stddev[j];
+  for (int64_t i = 0; i < t; ++i)
+    for (int64_t j = 0; j < d; ++j)
+      Xte_out[i * d + j] = stddev[j] == 0.0 ? 0.0 : (Xte[i * d + j] - mean[j]) / stddev[j];
+  free(sum);
+  free(sq);
+}
+
+static int cmp_double(const void* a, const void* b) {
+  const double x = *(const double*)a, y = *(const double*)b;
+  return (x > y) - (x < y);
+}
+
+/* strategies.cpp:204-234 auto_sigma_grid */
+void pko_auto_sigma_grid(const double* X, int64_t n, int64_t d, uint64_t seed, double* grid9) {
+  const int64_t count = n < 512 ? n : 512;
+  pko_rng rng;
+  pko_rng_init(&rng, pko_sub_seed(seed, "sigma-grid"));
+  uint64_t* perm = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(n > 0 ? n : 1));
+  pko_random_permutation((uint64_t)n, &rng, perm);
+  double* norms = (double*)malloc(sizeof(double) * (size_t)(count > 0 ? count : 1));
+  for (int64_t i = 0; i < count; ++i) norms[i] = pko_squared_norm(X + perm[i] * d, d);
+  const int64_t np = count * (count - 1) / 2;
+  double* dists = (double*)malloc(sizeof(double) * (size_t)(np > 0 ? np : 1));
+  int64_t e = 0;
+  for (int64_t i = 0; i < count; ++i)
+    for (int64_t j = i + 1; j < count; ++j) {
+      double d2 = norms[i] + norms[j] - 2.0 * pko_dot(X + perm[i] * d, X + perm[j] * d, d);
+      if (d2 < 0.0) d2 = 0.0;
+      dists[e++] = sqrt(d2);
+    }
+  double g = 1.0;
+  if (np > 0) {
+    qsort(dists, (size_t)np, sizeof(double), cmp_double);
+    const double median = dists[(np - 1) / 2];
+    if (median > 0.0) g = median;
+  }
+  for (int k = -4; k <= 4; ++k) grid9[k + 4] = g * ldexp(1.0, k);
+  free(perm);
+  free(norms);
+  free(dists);
+}

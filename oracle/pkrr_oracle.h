@@ -68,6 +68,11 @@ int64_t pko_grid_search(int kind, const double* Xtr, const double* ytr, int64_t 
                         double* cell_residual, int32_t* part_of, double* centers,
                         double* best_pred);
 
+/* data preparation: dataset.cpp:199-232, strategies.cpp:204-234 */
+void pko_standardize(const double* Xtr, int64_t n, int64_t d, const double* Xte, int64_t t,
+                     double* Xtr_out, double* Xte_out, double* mean, double* stddev);
+void pko_auto_sigma_grid(const double* X, int64_t n, int64_t d, uint64_t seed, double* grid9);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "pkrr/clustering.hpp"
+#include "pkrr/dataset.hpp"
 #include "pkrr/kernel.hpp"
 #include "pkrr/rng.hpp"
 #include "pkrr/solver.hpp"
@@ -272,6 +273,45 @@ int ref_train_predict_nearest(int kind, const double* Xtr, const double* ytr, in
   } catch (const std::exception& e) {
     g_err = e.what();
     return 1;
+  }
+}
+
+// dataset.cpp:199-232 through the reference's own standardize (dense rows in)
+int ref_standardize(const double* Xtr, int64_t n, int64_t d, const double* Xte, int64_t t, double* Xtr_out,
+                    double* Xte_out, double* mean, double* stddev) {
+  try {
+    const Dataset tr = dense(Xtr, nullptr, n, d);
+    const Dataset te = t > 0 ? dense(Xte, nullptr, t, d) : Dataset{};
+    const StandardizeResult r = standardize(tr, te);
+    for (int64_t i = 0; i < n; ++i) {
+      const SparseRow row = r.train.row(i);
+      for (std::size_t k = 0; k < row.nnz(); ++k) Xtr_out[i * d + row.idx[k]] = row.val[k];
+    }
+    for (int64_t i = 0; i < t; ++i) {
+      const SparseRow row = r.test.row(i);
+      for (std::size_t k = 0; k < row.nnz(); ++k) Xte_out[i * d + row.idx[k]] = row.val[k];
+    }
+    for (int64_t j = 0; j < d; ++j) {
+      mean[j] = r.stats.mean[j];
+      stddev[j] = r.stats.stddev[j];
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// strategies.cpp:204-234
+int ref_auto_sigma_grid(const double* X, int64_t n, int64_t d, uint64_t seed, double* grid9) {
+  try {
+    const Dataset tr = dense(X, nullptr, n, d);
+    const std::vector<double> g = auto_sigma_grid(tr, seed);
+    for (std::size_t i = 0; i < g.size() && i < 9; ++i) grid9[i] = g[i];
+    return static_cast<int>(g.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
   }
 }
 

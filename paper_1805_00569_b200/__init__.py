@@ -105,6 +105,10 @@ def load_library(path: str = LIB_PATH):
                                      C.c_double, C.c_int, C.c_void_p, C.c_void_p, _i64, C.POINTER(C.c_int)]),
         "pkrrgpu_kbalance": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_uint64,
                                        C.c_double, C.c_int, C.c_int, C.c_void_p, C.c_void_p, _i64]),
+        "pkrrgpu_standardize": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
+                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+        "pkrrgpu_auto_sigma_grid": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_uint64,
+                                              C.c_void_p]),
         "pkrrgpu_nearest_center": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64,
                                              C.c_void_p]),
         "pkrrgpu_make_partition": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
@@ -314,6 +318,27 @@ class Engine:
         _check(_lib.pkrrgpu_nearest_center(self._h, centers.ctypes.data, centers.shape[0], centers.shape[1],
                                            np.ascontiguousarray(Q2).ctypes.data, Q2.shape[0], out.ctypes.data))
         return int(out[0]) if single else out
+
+    # ---- dataset.hpp / strategies.hpp data preparation ------------------------
+    def standardize(self, X_train, X_test=None):
+        """dataset.cpp:199-232: (train_std, test_std, mean, stddev), bitwise the reference's."""
+        X = _f64(X_train)
+        n, d = X.shape
+        T = np.zeros((0, d)) if X_test is None else _f64(X_test)
+        tr, te = np.empty_like(X), np.empty_like(T)
+        mean, sd = np.empty(d), np.empty(d)
+        _check(_lib.pkrrgpu_standardize(self._h, X.ctypes.data, n, d, T.ctypes.data if T.size else None,
+                                        T.shape[0], tr.ctypes.data, te.ctypes.data if T.size else None,
+                                        mean.ctypes.data, sd.ctypes.data))
+        return tr, te, mean, sd
+
+    def auto_sigma_grid(self, X, seed):
+        """strategies.cpp:204-234: the 9-point sigma grid around the median distance."""
+        X = _f64(X)
+        g = np.empty(9)
+        _check(_lib.pkrrgpu_auto_sigma_grid(self._h, X.ctypes.data if X.size else None, X.shape[0],
+                                            X.shape[1] if X.ndim == 2 else 0, int(seed), g.ctypes.data))
+        return g
 
     # ---- strategies.hpp -----------------------------------------------------
     def make_partition(self, strategy, X, p, seed):

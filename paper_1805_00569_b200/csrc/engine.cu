@@ -777,6 +777,94 @@ int pkrrgpu_last_timings(const pkrrgpu_ctx* ctx, double* ms, int n) {
   return PKRRGPU_OK;
 }
 
+// ---- data preparation ---------------------------------------------------------
+namespace {
+// rng.cpp:36-56: sub_seed = splitmix64(splitmix64(seed ^ fnv1a64(tag)))
+uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+uint64_t fnv1a64(const char* s) {
+  uint64_t h = 0xCBF29CE484222325ull;
+  for (; *s; ++s) {
+    h ^= static_cast<unsigned char>(*s);
+    h *= 0x100000001B3ull;
+  }
+  return h;
+}
+uint64_t sub_seed(uint64_t seed, const char* tag) { return splitmix64(splitmix64(seed ^ fnv1a64(tag))); }
+}  // namespace
+
+int pkrrgpu_standardize(pkrrgpu_ctx* ctx, const double* X_train, int64_t n, int64_t d, const double* X_test,
+                        int64_t t, double* train_out, double* test_out, double* mean_out, double* stddev_out) {
+  API_BEGIN
+  if (n <= 0) fail(PKRRGPU_INVALID, "standardize: empty training set");
+  if (d <= 0 || !X_train || !train_out) fail(PKRRGPU_INVALID, "standardize: null input");
+  if (t > 0 && (!X_test || !test_out)) fail(PKRRGPU_INVALID, "standardize: null test input");
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  const double* dX = sc.in(X_train, n * d, s);
+  double* mean = sc.alloc<double>(d);
+  double* sd = sc.alloc<double>(d);
+  if (!pk::launch_standardize_stats(dX, n, d, d, mean, sd, s, ctx->counter)) {
+    // odd d or unaligned caller pointer: stream a copy with an even (16-byte) row pitch
+    const int64_t ld = round_up(d, 2);
+    double* P = sc.alloc<double>(n * ld);
+    ck(cudaMemcpy2DAsync(P, sizeof(double) * ld, dX, sizeof(double) * d, sizeof(double) * d, n,
+                         cudaMemcpyDeviceToDevice, s),
+       "pitch copy");
+    if (!pk::launch_standardize_stats(P, n, d, ld, mean, sd, s, ctx->counter))
+      fail(PKRRGPU_CUDA, "standardize: tensor map");
+  }
+  double* out = is_device_ptr(train_out) ? train_out : sc.alloc<double>(n * d);
+  pk::launch_standardize_apply(dX, n, d, mean, sd, out, s, ctx->counter);
+  copy_out(train_out, static_cast<const double*>(out), out == train_out ? 0 : n * d, s);
+  if (t > 0) {
+    const double* dT = sc.in(X_test, t * d, s);
+    double* tout = is_device_ptr(test_out) ? test_out : sc.alloc<double>(t * d);
+    pk::launch_standardize_apply(dT, t, d, mean, sd, tout, s, ctx->counter);
+    copy_out(test_out, static_cast<const double*>(tout), tout == test_out ? 0 : t * d, s);
+  }
+  copy_out(mean_out, static_cast<const double*>(mean), d, s);
+  copy_out(stddev_out, static_cast<const double*>(sd), d, s);
+  ck(cudaStreamSynchronize(s), "sync");
+  API_END
+}
+
+int pkrrgpu_auto_sigma_grid(pkrrgpu_ctx* ctx, const double* X, int64_t n, int64_t d, uint64_t seed,
+                            double* grid_out) {
+  API_BEGIN
+  if (!grid_out || (n > 0 && (!X || d <= 0))) fail(PKRRGPU_INVALID, "auto_sigma_grid: null argument");
+  const int64_t cnt = n < 512 ? n : 512;
+  double g = 1.0;
+  if (cnt > 1) {
+    Scope sc(ctx);
+    cudaStream_t s = ctx->main;
+    HostRng rng(sub_seed(seed, "sigma-grid"));
+    std::vector<int64_t> perm = rng.permutation(n);
+    perm.resize(cnt);
+    const double* dX = sc.in(X, n * d, s);
+    int64_t* didx = sc.upload(perm, s);
+    double* G = sc.alloc<double>(cnt * d);
+    double* nrm = sc.alloc<double>(cnt);
+    pk::launch_gather_rows(dX, d, didx, cnt, G, cnt, d, s, ctx->counter);
+    pk::launch_row_norms(G, cnt, d, d, nrm, s, ctx->counter);
+    const int64_t np = cnt * (cnt - 1) / 2;
+    double* dist = sc.alloc<double>(np);
+    pk::launch_pair_dist(G, nrm, cnt, d, dist, s, ctx->counter);
+    std::vector<double> h = to_host(dist, np, s);
+    // lower median of the sorted distances (strategies.cpp:224-229): any selection
+    // of the ((np - 1) / 2)-th smallest value gives the same number
+    std::nth_element(h.begin(), h.begin() + (np - 1) / 2, h.end());
+    const double median = h[(np - 1) / 2];
+    if (median > 0.0) g = median;
+  }
+  for (int e = -4; e <= 4; ++e) grid_out[e + 4] = g * std::ldexp(1.0, e);
+  API_END
+}
+
 // ---- kernel -----------------------------------------------------------------
 int pkrrgpu_gram(pkrrgpu_ctx* ctx, const double* A, int64_t na, const double* B, int64_t nb,
                  int64_t d, double sigma, double* K) {

@@ -1545,3 +1545,174 @@ void launch_dmma_probe(int blocks, int threads, int iters, double* sink, cudaStr
 }
 
 }  // namespace pk
+
+namespace pk {
+
+// ---------------------------------------------------------------------------
+// data preparation: standardize (dataset.cpp:178-232) and
+// the pairwise distances of auto_sigma_grid (strategies.cpp:204-234), bit-exact
+// ---------------------------------------------------------------------------
+static bool make_tmap_rows(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
+                           int box_cols, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 8)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1u, 1u};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Column sums and sums of squares in row order (dataset.cpp:211-217): one CTA per 32
+// columns; lane j of warp 0 keeps the two strictly sequential chains of column
+// f0 + j; a single producer thread streams 64-row x 32-column boxes through a TMA
+// ring.  The chains are the rounding sequence of the reference loop, so mean and
+// stddev are bitwise the reference's.
+constexpr int kStatRows = 64, kStatCols = 32, kStatStages = 8;
+constexpr int kStatStageBytes = kStatRows * kStatCols * 8;
+constexpr int kStatSmem = kStatStages * kStatStageBytes + 1024 + 256;
+
+__global__ void __launch_bounds__(64) colstats_kernel(const __grid_constant__ CUtensorMap tmX, int64_t n,
+                                                      int64_t d, double* __restrict__ mean,
+                                                      double* __restrict__ stddev) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStatStages * kStatStageBytes);
+  uint64_t* empty = full + kStatStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int f0 = blockIdx.x * kStatCols;
+  const int64_t nchunks = (n + kStatRows - 1) / kStatRows;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStatStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    if (lane == 0) {
+      prefetch_tmap(&tmX);
+      for (int64_t c = 0; c < nchunks; ++c) {
+        const int s = static_cast<int>(c % kStatStages);
+        mbar_wait(&empty[s], static_cast<uint32_t>(((c / kStatStages) & 1) ^ 1));
+        mbar_arrive_expect_tx(&full[s], kStatStageBytes);
+        tma_load_2d(smem + s * kStatStageBytes, &tmX, f0, static_cast<int>(c * kStatRows), &full[s]);
+      }
+      // do not exit before the last loads have landed (their mbarrier lives in this CTA)
+      for (int64_t c = nchunks > kStatStages ? nchunks - kStatStages : 0; c < nchunks; ++c)
+        mbar_wait(&full[c % kStatStages], static_cast<uint32_t>((c / kStatStages) & 1));
+    }
+    return;
+  }
+  double sum = 0.0, sq = 0.0;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int s = static_cast<int>(c % kStatStages);
+    mbar_wait(&full[s], static_cast<uint32_t>((c / kStatStages) & 1));
+    if (c > 0) {  // deferred release of the previous stage (see dgemm_tn_kernel)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[(c - 1) % kStatStages]);
+    }
+    const uint32_t b = smem_u32(smem + s * kStatStageBytes) + lane * 8;
+    const int rows = static_cast<int>(n - c * kStatRows < kStatRows ? n - c * kStatRows : kStatRows);
+    int r = 0;
+    for (; r + 8 <= rows; r += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = lds_f64_at(b + (r + u) * kStatCols * 8);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        sum = __dadd_rn(sum, v[u]);
+        sq = __dadd_rn(sq, __dmul_rn(v[u], v[u]));
+      }
+    }
+    for (; r < rows; ++r) {
+      const double v = lds_f64_at(b + r * kStatCols * 8);
+      sum = __dadd_rn(sum, v);
+      sq = __dadd_rn(sq, __dmul_rn(v, v));
+    }
+  }
+  if (f0 + lane < d) {
+    // dataset.cpp:218-224
+    const double inv_n = __ddiv_rn(1.0, static_cast<double>(n));
+    const double mu = __dmul_rn(sum, inv_n);
+    double var = __dsub_rn(__dmul_rn(sq, inv_n), __dmul_rn(mu, mu));
+    if (var < 0.0) var = 0.0;
+    mean[f0 + lane] = mu;
+    stddev[f0 + lane] = __dsqrt_rn(var);
+  }
+}
+
+// apply_feature_stats (dataset.cpp:187-194): (x - mean) / stddev, 0 where stddev == 0
+__global__ void standardize_apply_kernel(const double* __restrict__ X, int64_t n, int64_t d,
+                                         const double* __restrict__ mean, const double* __restrict__ stddev,
+                                         double* __restrict__ out) {
+  const int64_t total = n * d;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = e % d;
+    const double sd = stddev[j];
+    out[e] = sd == 0.0 ? 0.0 : __ddiv_rn(__dsub_rn(X[e], mean[j]), sd);
+  }
+}
+
+bool launch_standardize_stats(const double* X, int64_t n, int64_t d, int64_t ld, double* mean, double* stddev,
+                              cudaStream_t s, Counter& c) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(colstats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kStatSmem);
+    attr = true;
+  }
+  CUtensorMap tm;  // needs a 16-byte aligned base and row pitch (ld even)
+  if (!make_tmap_rows(&tm, X, n, d, ld, kStatCols, kStatRows)) return false;
+  colstats_kernel<<<static_cast<unsigned>((d + kStatCols - 1) / kStatCols), 64, kStatSmem, s>>>(tm, n, d, mean,
+                                                                                              stddev);
+  ++c.launches;
+  return true;
+}
+
+void launch_standardize_apply(const double* X, int64_t n, int64_t d, const double* mean, const double* stddev,
+                              double* out, cudaStream_t s, Counter& c) {
+  if (n <= 0) return;
+  const int64_t total = n * d;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
+  standardize_apply_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(X, n, d, mean, stddev, out);
+  ++c.launches;
+}
+
+// auto_sigma_grid distances (strategies.cpp:214-222): pair (i, j), i < j, at the
+// reference's push index; sequential dot, (n_i + n_j) - 2 dot, clamp, sqrt
+__global__ void pair_dist_kernel(const double* __restrict__ G, const double* __restrict__ norms, int64_t cnt,
+                                 int64_t d, double* __restrict__ out) {
+  const int64_t total = cnt * (cnt - 1) / 2;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    // invert e = i*cnt - i(i+1)/2 + (j - i - 1)
+    int64_t i = static_cast<int64_t>((2.0 * cnt - 1.0 - sqrt((2.0 * cnt - 1.0) * (2.0 * cnt - 1.0) - 8.0 * e)) * 0.5);
+    auto start = [&](int64_t r) { return r * cnt - r * (r + 1) / 2; };
+    while (i > 0 && start(i) > e) --i;
+    while (start(i + 1) <= e) ++i;
+    const int64_t j = e - start(i) + i + 1;
+    const double* a = G + i * d;
+    const double* b = G + j * d;
+    double dot = 0.0;
+    for (int64_t k = 0; k < d; ++k) dot = __dadd_rn(dot, __dmul_rn(a[k], b[k]));
+    double d2 = __dsub_rn(__dadd_rn(norms[i], norms[j]), __dmul_rn(2.0, dot));
+    if (d2 < 0.0) d2 = 0.0;
+    out[e] = __dsqrt_rn(d2);
+  }
+}
+
+void launch_pair_dist(const double* G, const double* norms, int64_t cnt, int64_t d, double* out, cudaStream_t s,
+                      Counter& c) {
+  const int64_t total = cnt * (cnt - 1) / 2;
+  if (total <= 0) return;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 8);
+  pair_dist_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(G, norms, cnt, d, out);
+  ++c.launches;
+}
+
+}  // namespace pk

@@ -123,4 +123,16 @@ void launch_events(const int32_t* label, int64_t row0, int64_t n, int k, const i
 // FP64 DMMA throughput probe (8 independent accumulator chains per warp)
 void launch_dmma_probe(int blocks, int threads, int iters, double* sink, cudaStream_t s, Counter& c);
 
+// ---- data preparation ----
+// column mean / stddev of X (n x d, row pitch ld), bit-exact with dataset.cpp:199-224;
+// false if X / ld do not meet TMA alignment (16-byte base, even ld)
+bool launch_standardize_stats(const double* X, int64_t n, int64_t d, int64_t ld, double* mean, double* stddev,
+                              cudaStream_t s, Counter& c);
+// out = (X - mean) / stddev per column, 0 where stddev == 0 (dataset.cpp:187-194)
+void launch_standardize_apply(const double* X, int64_t n, int64_t d, const double* mean, const double* stddev,
+                              double* out, cudaStream_t s, Counter& c);
+// auto_sigma_grid's pairwise distances in the reference's push order (strategies.cpp:214-222)
+void launch_pair_dist(const double* G, const double* norms, int64_t cnt, int64_t d, double* out, cudaStream_t s,
+                      Counter& c);
+
 }  // namespace pk

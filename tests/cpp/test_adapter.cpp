@@ -157,6 +157,26 @@ int main() {
       CHECK(counters, what.c_str());
     }
   }
+  // standardize / auto_sigma_grid (dataset.cpp:199-232, strategies.cpp:204-234): bitwise
+  {
+    const Dataset tr = mixture(900, 7, 4, 21), te = mixture(120, 7, 4, 22);
+    const StandardizeResult g = gpu::standardize(tr, te);
+    const StandardizeResult r = pkrr::standardize(tr, te);
+    CHECK(g.stats.mean == r.stats.mean && g.stats.stddev == r.stats.stddev, "standardize: mean/stddev bitwise");
+    CHECK(g.train.val == r.train.val && g.train.col == r.train.col && g.train.row_ptr == r.train.row_ptr &&
+              g.train.y == r.train.y && g.test.val == r.test.val && g.test.d == r.test.d,
+          "standardize: train/test rows bitwise");
+    CHECK(gpu::auto_sigma_grid(tr, 5) == pkrr::auto_sigma_grid(tr, 5), "auto_sigma_grid bitwise (n <= 512)");
+    const Dataset big = mixture(3000, 9, 6, 23);
+    CHECK(gpu::auto_sigma_grid(big, 77) == pkrr::auto_sigma_grid(big, 77), "auto_sigma_grid bitwise (n > 512)");
+    bool threw = false;
+    try {
+      gpu::standardize(Dataset{}, te);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw, "standardize: empty training set -> invalid_argument");
+  }
   std::printf("%d failure(s)\n", g_fail);
   return g_fail ? 1 : 0;
 }

@@ -81,6 +81,16 @@ def main():
         g[f"grid_{kind}_best"] = np.array([res["best"]])
         part, cen = r.make_partition(kind, Xt, 4, 7)
         g[f"part_{kind}"] = part
+    # data preparation (dataset.cpp:199-232, strategies.cpp:204-234)
+    rng = np.random.default_rng(8)
+    Xr = 2.5 * rng.standard_normal((300, 6)) + np.arange(6)
+    Xr[:, 3] = 7.0  # constant feature -> stddev 0 -> standardised to 0
+    Tr = rng.standard_normal((40, 6))
+    g["std_X"], g["std_T"] = Xr, Tr
+    g["std_train"], g["std_test"], g["std_mean"], g["std_stddev"] = r.standardize(Xr, Tr)
+    g["sigma_grid_300"] = r.auto_sigma_grid(Xr, 11)
+    g["sigma_grid_700"] = r.auto_sigma_grid(mixture(700, 5, 3, 9), 11)
+    g["sigma_grid_1"] = r.auto_sigma_grid(Xr[:1], 11)
     np.savez_compressed(os.path.join(OUT, "reference_vectors.npz"), **g)
     print("wrote", os.path.join(OUT, "reference_vectors.npz"), os.path.getsize(os.path.join(OUT, "reference_vectors.npz")), "bytes")
 

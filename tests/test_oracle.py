@@ -110,3 +110,15 @@ def test_restatement_bitwise_equals_reference(oracle):
         b = r.grid_search(kind, X, y, Q, np.sin(Q[:, 0]), 4, [1e-4, 1e-2], [1.0, 3.0], 7)
         assert a["best"] == b["best"] and np.array_equal(a["mse"], b["mse"]), kind
         assert np.array_equal(a["residual"], b["residual"]), kind
+
+
+def test_data_prep_vectors(oracle, g):
+    """standardize (dataset.cpp:199-232) and auto_sigma_grid (strategies.cpp:204-234)
+    bit for bit against the reference's own outputs."""
+    tr, te, mean, sd = oracle.standardize(g["std_X"], g["std_T"])
+    assert np.array_equal(tr, g["std_train"]) and np.array_equal(te, g["std_test"])
+    assert np.array_equal(mean, g["std_mean"]) and np.array_equal(sd, g["std_stddev"])
+    assert sd[3] == 0.0 and np.all(tr[:, 3] == 0.0)
+    assert np.array_equal(oracle.auto_sigma_grid(g["std_X"], 11), g["sigma_grid_300"])
+    assert np.array_equal(oracle.auto_sigma_grid(g["std_X"][:1], 11), g["sigma_grid_1"])
+    assert np.all(g["sigma_grid_1"] == np.ldexp(1.0, np.arange(-4, 5)))
