@@ -1304,6 +1304,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // the sequential per-coordinate chains and frees slots through "empty" mbarriers.
 // The loaders run up to kMeansRing chunks ahead, so the DADD chain sets the pace.
 constexpr int kMeansLoaders = kMeansThreads - 32;
+#ifndef MEANS_EXP
+#define MEANS_EXP 0  // tools/means_probe only: 1 = consumer idle, 2 = producer without copies
+#endif
 
 __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
@@ -1313,7 +1316,7 @@ __global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __re
                                                               const int64_t* __restrict__ members,
                                                               const int64_t* __restrict__ start,
                                                               const int64_t* __restrict__ sizes, int k,
-                                                              double* centers) {
+                                                              double* centers, int bulk) {
   extern __shared__ double mbuf[];  // [ring][rows][F]
   __shared__ uint64_t full[kMeansRing], empty[kMeansRing];
   const int j = blockIdx.x;
@@ -1329,6 +1332,46 @@ __global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __re
     fence_mbar_init();
   }
   __syncthreads();
+  if (bulk && threadIdx.x >= 32) {
+    // Even d, 16-byte aligned X: each member row's feature block is a run of 16-byte
+    // pieces.  Loader warp w handles rows 2(w-1) + {0,1} + 14 i of a chunk (lanes 0-15
+    // and 16-31 one row each, one piece per lane); the row indices of chunk c + 1 are
+    // loaded while chunk c is issued, so their latency is off the critical path.
+    const int w = (threadIdx.x >> 5) - 1, lane = threadIdx.x & 31;
+    const int half = lane >> 4, piece = lane & 15;
+    const int npieces = fw >> 1;
+    constexpr int kSteps = (kMeansRows + 13) / 14;  // 5 rows per half-warp per chunk
+    auto load_idx = [&](int64_t c, int64_t (&ix)[kSteps]) {
+#pragma unroll
+      for (int u = 0; u < kSteps; ++u) {
+        const int rr = 2 * w + half + 14 * u;
+        const int64_t r = c * kMeansRows + rr;
+        ix[u] = (c < nchunks && rr < kMeansRows && r < sz) ? __ldg(members + st + r) : -1;
+      }
+    };
+    int64_t cur[kSteps], nxt[kSteps];
+    load_idx(0, cur);
+    for (int64_t c = 0; c < nchunks; ++c) {
+      load_idx(c + 1, nxt);
+      const int slot = static_cast<int>(c % kMeansRing);
+      mbar_wait(&empty[slot], static_cast<uint32_t>(((c / kMeansRing) & 1) ^ 1));
+      double* b = mbuf + slot * kMeansRows * kMeansF;
+      if (piece < npieces) {
+#pragma unroll
+        for (int u = 0; u < kSteps; ++u) {
+          const int rr = 2 * w + half + 14 * u;
+          if (cur[u] >= 0 && MEANS_EXP != 2)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(b + rr * kMeansF + 2 * piece)),
+                         "l"(X + cur[u] * d + f0 + 2 * piece)
+                         : "memory");
+        }
+      }
+      cp_async_mbar_arrive_noinc(&full[slot]);
+#pragma unroll
+      for (int u = 0; u < kSteps; ++u) cur[u] = nxt[u];
+    }
+    return;
+  }
   if (threadIdx.x >= 32) {
     const int l = threadIdx.x - 32;
     for (int64_t c = 0; c < nchunks; ++c) {
@@ -1353,45 +1396,61 @@ __global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __re
     }
     return;
   }
+  // Consumer: one strictly sequential DADD chain per coordinate (lane).  Full chunks
+  // run through a two-buffer register pipeline of 32-row blocks: the next block's 32
+  // LDS are in flight while the current block's 32 DADDs run, so the chain advances at
+  // the DADD latency.  A slot is released after the DADDs that consumed its last block
+  // (their operands -- the LDS results -- have arrived, so the reads are complete).
   double s = 0.0;
-  for (int64_t c = 0; c < nchunks; ++c) {
-    const int slot = static_cast<int>(c % kMeansRing);
-    mbar_wait(&full[slot], static_cast<uint32_t>((c / kMeansRing) & 1));
-    // deferred release of the previous slot: its loads were consumed by the DADD
-    // chain before this wait (see dgemm_tn_kernel for the WAR race this avoids)
-    if (c > 0) {
-      __syncwarp();
-      if (threadIdx.x == 0) mbar_arrive(&empty[(c - 1) % kMeansRing]);
+  const int64_t nfull = MEANS_EXP == 1 ? 0 : sz / kMeansRows;
+  auto slot_of = [&](int64_t c) { return smem_u32(mbuf + (c % kMeansRing) * kMeansRows * kMeansF + threadIdx.x); };
+  auto wait_full = [&](int64_t c) {
+    mbar_wait(&full[c % kMeansRing], static_cast<uint32_t>((c / kMeansRing) & 1));
+  };
+  if (nfull > 0) {
+    double A[32], B[32];
+    wait_full(0);
+    {
+      const uint32_t b0 = slot_of(0);
+#pragma unroll
+      for (int u = 0; u < 32; ++u) A[u] = lds_f64_at(b0 + (u * kMeansF) * 8);
     }
-    const int64_t r0 = c * kMeansRows;
-    const int rows = static_cast<int>(sz - r0 < kMeansRows ? sz - r0 : kMeansRows);
-    // volatile shared loads issued 16 rows ahead of the (strictly ordered) DADD chain
-    const uint32_t b = smem_u32(mbuf + slot * kMeansRows * kMeansF + threadIdx.x);
-    int r = 0;
-    double v[16], w[16];
-    if (rows >= 16) {
+    for (int64_t c = 0; c < nfull; ++c) {
+      const uint32_t b = slot_of(c);
 #pragma unroll
-      for (int u = 0; u < 16; ++u) v[u] = lds_f64_at(b + (u * kMeansF) * 8);
-    }
-    for (; r + 32 <= rows; r += 32) {
+      for (int u = 0; u < 32; ++u) B[u] = lds_f64_at(b + ((32 + u) * kMeansF) * 8);
+      // probe the next chunk's barrier now and branch on it only after this block's
+      // DADDs, so the probe latency overlaps the chain
+      const uint32_t ready = c + 1 < nfull ? mbar_test(&full[(c + 1) % kMeansRing],
+                                                       static_cast<uint32_t>(((c + 1) / kMeansRing) & 1))
+                                           : 1u;
 #pragma unroll
-      for (int u = 0; u < 16; ++u) w[u] = lds_f64_at(b + ((r + 16 + u) * kMeansF) * 8);
+      for (int u = 0; u < 32; ++u) s = __dadd_rn(s, A[u]);
+      if (c + 1 < nfull) {
+        if (!ready) wait_full(c + 1);
+        const uint32_t bn = slot_of(c + 1);
 #pragma unroll
-      for (int u = 0; u < 16; ++u) s = __dadd_rn(s, v[u]);
-      if (r + 48 <= rows) {
-#pragma unroll
-        for (int u = 0; u < 16; ++u) v[u] = lds_f64_at(b + ((r + 32 + u) * kMeansF) * 8);
+        for (int u = 0; u < 32; ++u) A[u] = lds_f64_at(bn + (u * kMeansF) * 8);
       }
 #pragma unroll
-      for (int u = 0; u < 16; ++u) s = __dadd_rn(s, w[u]);
+      for (int u = 0; u < 32; ++u) s = __dadd_rn(s, B[u]);
+      __syncwarp();
+      if (threadIdx.x == 0) mbar_arrive(&empty[c % kMeansRing]);
     }
-    if (r + 16 <= rows) {
-#pragma unroll
-      for (int u = 0; u < 16; ++u) s = __dadd_rn(s, v[u]);
-      r += 16;
-    }
-    for (; r < rows; ++r) s = __dadd_rn(s, lds_f64_at(b + (r * kMeansF) * 8));
   }
+  if (MEANS_EXP != 1 && nfull < nchunks) {  // the partial last chunk
+    const int64_t c = nfull;
+    wait_full(c);
+    const uint32_t b = slot_of(c);
+    const int rows = static_cast<int>(sz - c * kMeansRows);
+    for (int r = 0; r < rows; ++r) s = __dadd_rn(s, lds_f64_at(b + (r * kMeansF) * 8));
+  }
+  if (MEANS_EXP == 1)
+    for (int64_t c = 0; c < nchunks; ++c) {
+      wait_full(c);
+      __syncwarp();
+      if (threadIdx.x == 0) mbar_arrive(&empty[c % kMeansRing]);
+    }
   if (threadIdx.x < fw)
     centers[static_cast<int64_t>(j) * d + f0 + threadIdx.x] =
         sz > 0 ? __dmul_rn(s, __ddiv_rn(1.0, static_cast<double>(sz))) : 0.0;
@@ -1405,7 +1464,9 @@ void launch_means(const double* X, int64_t d, const int64_t* members, const int6
     attr = true;
   }
   dim3 grid(k, static_cast<unsigned>((d + kMeansF - 1) / kMeansF));
-  means_kernel<<<grid, kMeansThreads, kMeansSmem, s>>>(X, d, members, start, sizes, k, centers);
+  // 16-byte cp.async pieces need 16-byte aligned rows and an even feature count: even d
+  const int bulk = (d % 2 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
+  means_kernel<<<grid, kMeansThreads, kMeansSmem, s>>>(X, d, members, start, sizes, k, centers, bulk);
   ++c.launches;
 }
 
