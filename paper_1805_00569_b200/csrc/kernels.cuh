@@ -51,7 +51,8 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
 // s2 (optional): a second stream for lookahead -- the next panel's columns are
 // updated first on s and the rest of the trailing update runs on s2, overlapping the
 // next panel factorisation; the result is bitwise the same as without.
-// Number of 128-column panels per trailing update (K = 128 * G); default 4.
+// Number of 128-column panels per trailing update (K = 128 * G); 0 (default) = automatic:
+// 4 for m < 8192 or the int8 update, 8 otherwise.
 void set_panel_group(int g);
 // SYRK grid: 0 = one 128x128 tile per CTA (default), 1 = persistent (one CTA per SM).
 void set_syrk_persistent(int on);
