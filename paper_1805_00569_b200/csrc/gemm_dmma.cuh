@@ -33,6 +33,7 @@ struct GemmParams {
   const double* norm_b;
   int valid_a, valid_b;  // rows beyond these are padding (identity / zero)
   double denom;          // (2*sigma)*sigma, kernel.cpp:55
+  double neg_inv_denom;  // -1 / denom (the epilogue multiplies; see below)
   const int* abort_flag; // per-part NPD flag: skip work once a pivot failed
 };
 
@@ -63,11 +64,23 @@ __device__ __forceinline__ void lower_tile_coords(int b, int& tm, int& tn) {
   tn = b - t * (t + 1) / 2;
 }
 
+// The symmetric gram epilogue (exp + mirrored write) needs more registers than the
+// 168 a 9-warp CTA gets (registers are allocated per 4-warp group): that mode runs
+// 3 warpgroups -- producer warpgroup shrunk to 40 registers with setmaxnreg.dec, the
+// two DMMA warpgroups grown to 232 -- like dsyrk_persistent_kernel.
+template <int MODE>
+constexpr int gemm_threads() {
+  return MODE == G_GRAM_SYM ? 384 : kGemmThreads;
+}
+
 template <int BM, int MODE>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(gemm_threads<MODE>(), 1)
     dgemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     GemmParams p) {
   using Cfg = GemmCfg<BM>;
+  constexpr bool kWG = MODE == G_GRAM_SYM;             // warpgroup-specialised layout
+  constexpr int kProducerWarp = kWG ? 0 : kConsumerWarps;
+  constexpr int kFirstConsumer = kWG ? 4 : 0;
   if (p.abort_flag && *reinterpret_cast<const volatile int*>(p.abort_flag)) return;
 
   extern __shared__ unsigned char smem_raw[];
@@ -95,9 +108,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
 
   const int KT = p.ktiles;
-  if (warp == kConsumerWarps) {
+  if (kWG && warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+  if (kWG ? warp < 4 : warp == kConsumerWarps) {
     // ---------------- TMA producer ----------------
-    if (lane == 0) {
+    if (warp == kProducerWarp && lane == 0) {
       prefetch_tmap(&tmA);
       prefetch_tmap(&tmB);
       const int arow = p.a_row0 + tm * BM, brow = p.b_row0 + tn * kBN;
@@ -119,7 +133,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 
   // ---------------- DMMA consumers ----------------
-  const int wm = warp >> 2, wn = warp & 3;
+  if (kWG) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+  const int cwarp = warp - kFirstConsumer;
+  const int wm = cwarp >> 2, wn = cwarp & 3;
   const int lr = lane >> 2, lk = lane & 3;
   double acc[Cfg::MT][Cfg::NT][2];
 #pragma unroll
@@ -202,7 +218,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           } else {
             double dist2 = (na[i] + nb[j][e]) - 2.0 * acc[i][j][e];
             if (dist2 < 0.0) dist2 = 0.0;
-            v = exp(__ddiv_rn(-dist2, p.denom));
+            // kernel.cpp:55 divides; a multiply by -1/denom moves the exponent by <= 1.5 ulp,
+            // i.e. K by <= e^-1 |x| 2^-53 absolute -- far inside the 1e-13 K tolerance
+            v = exp(dist2 * p.neg_inv_denom);
           }
           acc[i][j][e] = v;
         }
@@ -239,7 +257,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               if ((c >> 6) == half) T[(c & 63) * TS + r0 + i * 8] = acc[i][j][e];
             }
         consumer_sync(kConsumerWarps * 32);
-        for (int cc = warp; cc < 64; cc += kConsumerWarps) {
+        for (int cc = cwarp; cc < 64; cc += kConsumerWarps) {
           const int c = half * 64 + cc;
           double* dst = p.C + static_cast<int64_t>(gj0 + c) * p.ldc + gi0;
           for (int r = lane; r < BM; r += 32)

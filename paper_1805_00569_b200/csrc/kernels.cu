@@ -145,7 +145,7 @@ static void gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const GemmPa
                          GemmCfg<BM>::SMEM);
     attr_set = true;
   }
-  dgemm_tn_kernel<BM, MODE><<<blocks, kGemmThreads, GemmCfg<BM>::SMEM, s>>>(a, b, p);
+  dgemm_tn_kernel<BM, MODE><<<blocks, gemm_threads<MODE>(), GemmCfg<BM>::SMEM, s>>>(a, b, p);
   ++c.launches;
 }
 
@@ -164,6 +164,7 @@ void launch_gram_sym(const CUtensorMap& tmX, const double* norms, int64_t mp, in
   p.norm_a = p.norm_b = norms;
   p.valid_a = p.valid_b = static_cast<int>(m);
   p.denom = (2.0 * sigma) * sigma;
+  p.neg_inv_denom = -1.0 / p.denom;
   p.abort_flag = abort;
   gemm_launch<128, G_GRAM_SYM>(tmX, tmX, p, T * (T + 1) / 2, s, c);
 }
@@ -182,6 +183,7 @@ void launch_gram_cross(const CUtensorMap& tmQ, const CUtensorMap& tmX, const dou
   p.valid_a = static_cast<int>(q);
   p.valid_b = static_cast<int>(m);
   p.denom = (2.0 * sigma) * sigma;
+  p.neg_inv_denom = -1.0 / p.denom;
   gemm_launch<64, G_GRAM_CROSS>(tmQ, tmX, p, p.tiles_m * p.tiles_n, s, c);
 }
 
