@@ -38,8 +38,10 @@ sys.path.insert(0, ROOT)
 
 METRIC = "train+predict samples/sec (FP64)"
 # DRAM read+write bytes per 128x128 trailing-SYRK output tile, from the committed
-# ncu --set full capture (profiles/ncu_syrk_r01.txt, m=20544 probe, K=512 launch of 8911 tiles).
-SYRK_TRAFFIC_PER_TILE = 462800  # 4.124e9 B (2.98e9 read + 1.14e9 write) / 8911 tiles
+# DRAM bytes per 128x128 SYRK output tile from the committed ncu --set full captures of the
+# m=20544 factorization probe: K=512 (profiles/ncu_syrk_r01.txt, 8911 tiles, 2.98e9 read +
+# 1.14e9 write) and K=1024 (profiles/ncu_syrk_k1024_r01.txt, 11781 tiles, 9.87e9 + 1.53e9).
+SYRK_TRAFFIC_PER_TILE = {512: 462800, 1024: 967700}
 UNIT = "samples/s"
 
 # BASELINE.json configs (per GPU for the weak-scaled ones).  km_iters 20 = exactly
@@ -291,6 +293,7 @@ def run_ours(args):
     # --- dominant kernel, live: the largest part's factorization alone on one stream,
     # CUDA events around every trailing-SYRK launch (algorithmic flops / launch time)
     big = int(max(res.parts["part_sizes"]))
+    syrk_k = 1024 if big >= 8192 else 512  # the library's automatic panel group (kernels.cu launch_potrf)
     probe = eng.probe_potrf(big)
     syrk_tflops = probe["syrk_flops"] / (probe["syrk_ms"] / 1e3) / 1e12 if probe["syrk_ms"] > 0 else 0.0
 
@@ -329,12 +332,13 @@ def run_ours(args):
         "phase_ms_per_step": {k: v / args.steps for k, v in phase.items()},
         "part_chol_end_ms": t.get("part_chol_end_ms"),
         "roofline": {"bound": "tensor",
-                     "kernel": "dsyrk_persistent_kernel (Cholesky trailing update, DMMA f64, K=512)",
+                     "kernel": f"dsyrk_persistent_kernel (Cholesky trailing update, DMMA f64, K={syrk_k})",
                      "achieved": syrk_tflops, "peak": peak, "unit": "TFLOP/s",
                      "frac": syrk_tflops / peak if peak else None,
-                     "traffic": SYRK_TRAFFIC_PER_TILE,
-                     "traffic_note": "DRAM bytes per 128x128 output tile (K=512) from the committed ncu --set full "
-                                     "capture (profiles/); algorithmic operand+C bytes per tile = 1310720",
+                     "traffic": SYRK_TRAFFIC_PER_TILE[syrk_k],
+                     "traffic_note": f"DRAM bytes per 128x128 output tile (K={syrk_k}) from the committed ncu "
+                                     "--set full capture (profiles/); algorithmic operand+C bytes per tile = "
+                                     f"{2 * 128 * syrk_k * 8 + 2 * 128 * 128 * 8} (panels are L2 hits)",
                      "peak_source": "measured live: FP64 DMMA (mma.sync m8n8k4) probe over 148 SMs; "
                                     "MEASURED_PEAKS.json has no FP64 entry",
                      "algorithmic": "per launch rows(rows+1)*K flops (lower triangle incl. diagonal) / launch time; "
