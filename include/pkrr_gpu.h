@@ -36,7 +36,8 @@ enum pkrrgpu_status {
   PKRRGPU_INVALID = 1,
   PKRRGPU_NPD = 2,
   PKRRGPU_CUDA = 3,
-  PKRRGPU_LOGIC = 4
+  PKRRGPU_LOGIC = 4,
+  PKRRGPU_IO = 5     /* std::runtime_error of the reference's file IO (open / parse / empty) */
 };
 
 /* StrategyKind, same order as strategies.hpp:21. */
@@ -230,6 +231,22 @@ int pkrrgpu_standardize(pkrrgpu_ctx* ctx, const double* X_train, int64_t n, int6
  * Bitwise the reference's. */
 int pkrrgpu_auto_sigma_grid(pkrrgpu_ctx* ctx, const double* X, int64_t n, int64_t d, uint64_t seed,
                             double* grid_out);
+
+/* load_libsvm -- dataset.cpp:83-125: parse a LIBSVM text file (label, then
+ * 1-based strictly increasing index:value pairs; blank lines skipped) with the same
+ * strtod/strtol arithmetic and the same errors ("<path>: parse error at line N: ...",
+ * "cannot open <path>", "<path>: empty dataset" -> PKRRGPU_IO).  The file is parsed
+ * by `threads` host threads (0 = all) into a handle holding the CSR rows exactly as
+ * the reference's Dataset stores them; d = 1 + the largest index. */
+typedef struct pkrrgpu_dataset pkrrgpu_dataset;
+int pkrrgpu_load_libsvm(const char* path, int threads, pkrrgpu_dataset** out);
+int pkrrgpu_dataset_shape(const pkrrgpu_dataset* ds, int64_t* n, int64_t* d, int64_t* nnz);
+/* the CSR arrays (row_ptr: n + 1 entries, col / val: nnz, y: n), host memory */
+int pkrrgpu_dataset_csr(const pkrrgpu_dataset* ds, int64_t* row_ptr, int32_t* col, double* val, double* y);
+/* dense row-major n x d rows (absent features 0) and labels, materialised in pinned
+ * host staging and copied to X / y (host or device pointers; device: one H2D) */
+int pkrrgpu_dataset_dense(pkrrgpu_ctx* ctx, pkrrgpu_dataset* ds, double* X, double* y);
+void pkrrgpu_dataset_free(pkrrgpu_dataset* ds);
 
 /* ---- timing hooks (bench / profiling only) ------------------------------- */
 

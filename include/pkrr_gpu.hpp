@@ -239,6 +239,27 @@ inline int nearest_center(const std::vector<std::vector<double>>& centers, Spars
 
 inline int nearest_center(const Clustering& c, SparseRow x) { return gpu::nearest_center(c.centers, x); }
 
+// ---- dataset.hpp: load_libsvm (dataset.cpp:83-125), host threads -------------------
+inline Dataset load_libsvm(const std::string& path) {
+  pkrrgpu_dataset* h = nullptr;
+  const int rc = pkrrgpu_load_libsvm(path.c_str(), 0, &h);
+  if (rc == PKRRGPU_IO) throw std::runtime_error(pkrrgpu_last_error());
+  detail::check(rc);
+  int64_t n = 0, d = 0, nnz = 0;
+  pkrrgpu_dataset_shape(h, &n, &d, &nnz);
+  std::vector<int64_t> rp(n + 1);
+  Dataset ds;
+  ds.col.resize(nnz);
+  ds.val.resize(nnz);
+  ds.y.resize(n);
+  pkrrgpu_dataset_csr(h, rp.data(), ds.col.data(), ds.val.data(), ds.y.data());
+  pkrrgpu_dataset_free(h);
+  ds.row_ptr.assign(rp.begin(), rp.end());
+  ds.n = static_cast<std::size_t>(n);
+  ds.d = static_cast<std::size_t>(d);
+  return ds;
+}
+
 // ---- dataset.hpp: standardize (dataset.cpp:199-232) ---------------------------
 inline StandardizeResult standardize(const Dataset& train, const Dataset& test) {
   if (train.n == 0) throw std::invalid_argument("standardize: empty training set");

@@ -332,6 +332,18 @@ class Reference(_Base):
         self._standardize = self._fn("standardize", C.c_int, _d, C.c_int64, C.c_int64, _d, C.c_int64, _d, _d,
                                      _d, _d)
         self._sigma_grid = self._fn("auto_sigma_grid", C.c_int, _d, C.c_int64, C.c_int64, C.c_uint64, _d)
+        self._libsvm = self._fn("load_libsvm", C.c_int, C.c_char_p, _i64, _i64, _i64, _i64, _i32, _d, _d)
+
+    def load_libsvm(self, path):
+        """dataset.cpp:83-125: (row_ptr, col, val, y, d) exactly as the reference's Dataset."""
+        n, d, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+        if self._libsvm(path.encode(), C.byref(n), C.byref(d), C.byref(nnz), None, None, None, None):
+            raise RuntimeError(self._err().decode())
+        rp, col = np.empty(n.value + 1, np.int64), np.empty(nnz.value, np.int32)
+        val, y = np.empty(nnz.value), np.empty(n.value)
+        self._libsvm(path.encode(), C.byref(n), C.byref(d), C.byref(nnz), _p(rp, _i64), _p(col, _i32), _p(val, _d),
+                     _p(y, _d))
+        return rp, col, val, y, d.value
 
     def cholesky(self, A):
         A = _f64(A)

@@ -315,4 +315,25 @@ int ref_auto_sigma_grid(const double* X, int64_t n, int64_t d, uint64_t seed, do
   }
 }
 
+// dataset.cpp:83-125 through the reference's own loader; two calls: sizes, then arrays
+int ref_load_libsvm(const char* path, int64_t* n, int64_t* d, int64_t* nnz, int64_t* row_ptr, int32_t* col,
+                    double* val, double* y) {
+  try {
+    const Dataset ds = load_libsvm(path);
+    *n = static_cast<int64_t>(ds.n);
+    *d = static_cast<int64_t>(ds.d);
+    *nnz = static_cast<int64_t>(ds.col.size());
+    if (row_ptr)
+      for (std::size_t i = 0; i < ds.row_ptr.size(); ++i) row_ptr[i] = static_cast<int64_t>(ds.row_ptr[i]);
+    if (col)
+      for (std::size_t i = 0; i < ds.col.size(); ++i) col[i] = ds.col[i];
+    if (val) std::memcpy(val, ds.val.data(), sizeof(double) * ds.val.size());
+    if (y) std::memcpy(y, ds.y.data(), sizeof(double) * ds.y.size());
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
 }  // extern "C"

@@ -35,7 +35,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libpkrr_gpu.so")
 
 STRATEGIES = {"exact": 0, "dckrr": 1, "kkrr": 2, "kkrr2": 3, "kkrr3": 4, "bkrr": 5, "bkrr2": 6, "bkrr3": 7}
-OK, INVALID, NPD, CUDA, LOGIC = 0, 1, 2, 3, 4
+OK, INVALID, NPD, CUDA, LOGIC, IO = 0, 1, 2, 3, 4, 5
 
 _d = C.POINTER(C.c_double)
 _i32 = C.POINTER(C.c_int32)
@@ -109,6 +109,11 @@ def load_library(path: str = LIB_PATH):
                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
         "pkrrgpu_auto_sigma_grid": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_uint64,
                                               C.c_void_p]),
+        "pkrrgpu_load_libsvm": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]),
+        "pkrrgpu_dataset_shape": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+        "pkrrgpu_dataset_csr": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+        "pkrrgpu_dataset_dense": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+        "pkrrgpu_dataset_free": (None, [C.c_void_p]),
         "pkrrgpu_nearest_center": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int64,
                                              C.c_void_p]),
         "pkrrgpu_make_partition": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
@@ -151,6 +156,8 @@ def _check(rc, pivot=None):
     if rc == OK:
         return
     msg = _lib.pkrrgpu_last_error().decode()
+    if rc == IO:
+        raise RuntimeError(msg)
     if rc == NPD:
         raise NotPositiveDefinite(pivot if pivot is not None else -1, msg)
     if rc == INVALID:
@@ -175,6 +182,32 @@ def _f64(a):
     if a is None or hasattr(a, "data_ptr"):
         return a
     return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _open_libsvm(path, threads=0):
+    h = C.c_void_p()
+    _check(load_library().pkrrgpu_load_libsvm(os.fsencode(path), int(threads), C.byref(h)))
+    return h
+
+
+def _shape(h):
+    n, d, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+    _check(_lib.pkrrgpu_dataset_shape(h, C.byref(n), C.byref(d), C.byref(nnz)))
+    return n.value, d.value, nnz.value
+
+
+def libsvm_csr(path, threads=0):
+    """load_libsvm (dataset.cpp:83-125) on the host, no GPU needed: (row_ptr, col, val, y, d),
+    the reference Dataset's CSR arrays."""
+    h = _open_libsvm(path, threads)
+    try:
+        n, d, nnz = _shape(h)
+        rp, col = np.empty(n + 1, np.int64), np.empty(nnz, np.int32)
+        val, y = np.empty(nnz), np.empty(n)
+        _check(_lib.pkrrgpu_dataset_csr(h, rp.ctypes.data, col.ctypes.data, val.ctypes.data, y.ctypes.data))
+        return rp, col, val, y, d
+    finally:
+        _lib.pkrrgpu_dataset_free(h)
 
 
 class Engine:
@@ -318,6 +351,25 @@ class Engine:
         _check(_lib.pkrrgpu_nearest_center(self._h, centers.ctypes.data, centers.shape[0], centers.shape[1],
                                            np.ascontiguousarray(Q2).ctypes.data, Q2.shape[0], out.ctypes.data))
         return int(out[0]) if single else out
+
+    # ---- dataset.hpp: LIBSVM loader (dataset.cpp:83-125) ------------------------
+    def load_libsvm(self, path, threads=0, device=False):
+        """Dense (X, y) of a LIBSVM file: parsed by host threads into CSR, materialised
+        in pinned staging, copied to numpy (or to CUDA tensors with device=True)."""
+        h = _open_libsvm(path, threads)
+        try:
+            n, d, _ = _shape(h)
+            if device:
+                import torch
+                X = torch.empty((n, d), dtype=torch.float64, device=f"cuda:{self.device}")
+                y = torch.empty(n, dtype=torch.float64, device=f"cuda:{self.device}")
+                _check(_lib.pkrrgpu_dataset_dense(self._h, h, X.data_ptr(), y.data_ptr()))
+            else:
+                X, y = np.empty((n, d)), np.empty(n)
+                _check(_lib.pkrrgpu_dataset_dense(self._h, h, X.ctypes.data, y.ctypes.data))
+            return X, y
+        finally:
+            _lib.pkrrgpu_dataset_free(h)
 
     # ---- dataset.hpp / strategies.hpp data preparation ------------------------
     def standardize(self, X_train, X_test=None):

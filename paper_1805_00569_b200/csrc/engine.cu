@@ -8,6 +8,9 @@
 // O(k) control decisions of the clustering loops (convergence, empty-cluster
 // reseed, k-balance capacity bookkeeping) exactly as clustering.cpp does.
 #include <algorithm>
+#include <cctype>
+#include <memory>
+#include <thread>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -864,6 +867,198 @@ int pkrrgpu_auto_sigma_grid(pkrrgpu_ctx* ctx, const double* X, int64_t n, int64_
   for (int e = -4; e <= 4; ++e) grid_out[e + 4] = g * std::ldexp(1.0, e);
   API_END
 }
+
+// ---- LIBSVM loader (dataset.cpp:83-125) ------------------------------------------
+struct pkrrgpu_dataset {
+  int64_t n = 0, d = 0;
+  std::vector<int64_t> row_ptr{0};
+  std::vector<int32_t> col;
+  std::vector<double> val;
+  std::vector<double> y;
+  double* pinned = nullptr;  // dense staging (n x d), cudaMallocHost
+  ~pkrrgpu_dataset() {
+    if (pinned) cudaFreeHost(pinned);
+  }
+};
+
+namespace {
+struct LibsvmChunk {
+  std::vector<int64_t> row_nnz;
+  std::vector<int32_t> col;
+  std::vector<double> val, y;
+  int64_t max_col = -1;
+  int64_t err_line = -1;  // first failing line (1-based) in this chunk
+  std::string err;
+};
+
+// parse lines [b, e) of the buffer; line numbers start at first_line
+void parse_libsvm_lines(const char* buf, const std::vector<int64_t>& starts, int64_t b, int64_t e,
+                        int64_t total_len, LibsvmChunk& out) {
+  std::string line;
+  for (int64_t li = b; li < e; ++li) {
+    const int64_t s0 = starts[li];
+    int64_t s1 = li + 1 < static_cast<int64_t>(starts.size()) ? starts[li + 1] - 1 : total_len;
+    if (s1 > s0 && s1 == total_len && buf[s1 - 1] == '\n') --s1;  // final newline ends the last line
+    line.assign(buf + s0, buf + s1);  // without the newline; NUL-terminated copy for strtod
+    bool blank = true;
+    for (char c : line)
+      if (!std::isspace(static_cast<unsigned char>(c))) {
+        blank = false;
+        break;
+      }
+    if (blank) continue;
+    const char* p = line.c_str();
+    char* end = nullptr;
+    auto fail_line = [&](const char* what) {
+      out.err_line = li + 1;
+      out.err = what;
+    };
+    const double label = std::strtod(p, &end);
+    if (end == p) {
+      fail_line("expected numeric label");
+      return;
+    }
+    p = end;
+    int64_t cnt = 0, last = -1;
+    for (;;) {
+      while (*p == ' ' || *p == '\t' || *p == '\r') ++p;
+      if (*p == '\0') break;
+      const long index = std::strtol(p, &end, 10);
+      if (end == p || *end != ':') {
+        fail_line("expected <index>:<value>");
+        return;
+      }
+      if (index < 1) {
+        fail_line("feature indices are 1-based");
+        return;
+      }
+      p = end + 1;
+      const double value = std::strtod(p, &end);
+      if (end == p) {
+        fail_line("expected numeric feature value");
+        return;
+      }
+      p = end;
+      const int32_t zb = static_cast<int32_t>(index - 1);
+      if (cnt > 0 && zb <= last) {
+        fail_line("feature indices must be strictly increasing");
+        return;
+      }
+      out.col.push_back(zb);
+      out.val.push_back(value);
+      last = zb;
+      ++cnt;
+    }
+    if (last > out.max_col) out.max_col = last;
+    out.row_nnz.push_back(cnt);
+    out.y.push_back(label);
+  }
+}
+}  // namespace
+
+int pkrrgpu_load_libsvm(const char* path, int threads, pkrrgpu_dataset** out) {
+  try {
+    if (!path || !out) fail(PKRRGPU_INVALID, "load_libsvm: null argument");
+    FILE* f = std::fopen(path, "rb");
+    if (!f) fail(PKRRGPU_IO, std::string("cannot open ") + path);
+    std::vector<char> buf;
+    {
+      std::fseek(f, 0, SEEK_END);
+      const long len = std::ftell(f);
+      std::fseek(f, 0, SEEK_SET);
+      buf.resize(static_cast<size_t>(len > 0 ? len : 0));
+      const size_t got = len > 0 ? std::fread(buf.data(), 1, buf.size(), f) : 0;
+      std::fclose(f);
+      buf.resize(got);
+    }
+    // line starts (std::getline semantics: a trailing newline does not open a line)
+    std::vector<int64_t> starts;
+    const int64_t L = static_cast<int64_t>(buf.size());
+    if (L > 0) starts.push_back(0);
+    for (int64_t i = 0; i < L; ++i)
+      if (buf[i] == '\n' && i + 1 < L) starts.push_back(i + 1);
+    const int64_t nl = static_cast<int64_t>(starts.size());
+    int T = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
+    if (T < 1) T = 1;
+    if (nl < 4096) T = 1;
+    std::vector<LibsvmChunk> parts(T);
+    std::vector<std::thread> pool;
+    for (int t = 0; t < T; ++t) {
+      const int64_t b = nl * t / T, e = nl * (t + 1) / T;
+      pool.emplace_back([&, b, e, t] { parse_libsvm_lines(buf.data(), starts, b, e, L, parts[t]); });
+    }
+    for (auto& th : pool) th.join();
+    // the sequential parser stops at the first failing line
+    for (const LibsvmChunk& c : parts)
+      if (c.err_line >= 0)
+        fail(PKRRGPU_IO, std::string(path) + ": parse error at line " + std::to_string(c.err_line) + ": " + c.err);
+    auto ds = std::make_unique<pkrrgpu_dataset>();
+    int64_t max_col = -1;
+    for (const LibsvmChunk& c : parts) {
+      for (int64_t k : c.row_nnz) ds->row_ptr.push_back(ds->row_ptr.back() + k);
+      ds->col.insert(ds->col.end(), c.col.begin(), c.col.end());
+      ds->val.insert(ds->val.end(), c.val.begin(), c.val.end());
+      ds->y.insert(ds->y.end(), c.y.begin(), c.y.end());
+      max_col = std::max(max_col, c.max_col);
+    }
+    ds->n = static_cast<int64_t>(ds->y.size());
+    ds->d = max_col + 1;
+    if (ds->n == 0) fail(PKRRGPU_IO, std::string(path) + ": empty dataset");
+    *out = ds.release();
+    return PKRRGPU_OK;
+  } catch (const Fail& f) {
+    return f.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return PKRRGPU_IO;
+  }
+}
+
+int pkrrgpu_dataset_shape(const pkrrgpu_dataset* ds, int64_t* n, int64_t* d, int64_t* nnz) {
+  if (!ds) return PKRRGPU_INVALID;
+  if (n) *n = ds->n;
+  if (d) *d = ds->d;
+  if (nnz) *nnz = static_cast<int64_t>(ds->col.size());
+  return PKRRGPU_OK;
+}
+
+int pkrrgpu_dataset_csr(const pkrrgpu_dataset* ds, int64_t* row_ptr, int32_t* col, double* val, double* y) {
+  if (!ds) return PKRRGPU_INVALID;
+  if (row_ptr) std::memcpy(row_ptr, ds->row_ptr.data(), sizeof(int64_t) * ds->row_ptr.size());
+  if (col) std::memcpy(col, ds->col.data(), sizeof(int32_t) * ds->col.size());
+  if (val) std::memcpy(val, ds->val.data(), sizeof(double) * ds->val.size());
+  if (y) std::memcpy(y, ds->y.data(), sizeof(double) * ds->y.size());
+  return PKRRGPU_OK;
+}
+
+int pkrrgpu_dataset_dense(pkrrgpu_ctx* ctx, pkrrgpu_dataset* ds, double* X, double* y) {
+  API_BEGIN
+  if (!ds || !X) fail(PKRRGPU_INVALID, "dataset_dense: null argument");
+  const int64_t n = ds->n, d = ds->d;
+  if (!ds->pinned) {
+    ck(cudaMallocHost(&ds->pinned, sizeof(double) * static_cast<size_t>(n * d > 0 ? n * d : 1)), "pinned");
+    // scatter the CSR rows into dense pinned rows, rows split across host threads
+    int T = static_cast<int>(std::thread::hardware_concurrency());
+    if (T < 1 || n < 4096) T = 1;
+    std::vector<std::thread> pool;
+    for (int t = 0; t < T; ++t)
+      pool.emplace_back([ds, n, d, t, T] {
+        for (int64_t i = n * t / T; i < n * (t + 1) / T; ++i) {
+          double* row = ds->pinned + i * d;
+          std::fill(row, row + d, 0.0);
+          for (int64_t k = ds->row_ptr[i]; k < ds->row_ptr[i + 1]; ++k) row[ds->col[k]] = ds->val[k];
+        }
+      });
+    for (auto& th : pool) th.join();
+  }
+  cudaStream_t s = ctx->main;
+  ck(cudaMemcpyAsync(X, ds->pinned, sizeof(double) * n * d, cudaMemcpyDefault, s), "dense copy");
+  if (y) ck(cudaMemcpyAsync(y, ds->y.data(), sizeof(double) * n, cudaMemcpyDefault, s), "label copy");
+  ck(cudaStreamSynchronize(s), "sync");
+  API_END
+}
+
+void pkrrgpu_dataset_free(pkrrgpu_dataset* ds) { delete ds; }
 
 // ---- kernel -----------------------------------------------------------------
 int pkrrgpu_gram(pkrrgpu_ctx* ctx, const double* A, int64_t na, const double* B, int64_t nb,

@@ -177,6 +177,23 @@ int main() {
     }
     CHECK(threw, "standardize: empty training set -> invalid_argument");
   }
+  // load_libsvm (dataset.cpp:83-125): the same Dataset, bitwise
+  {
+    const Dataset src = mixture(5000, 11, 4, 31);
+    const std::string path = "/tmp/pkrr_adapter_test.svm";
+    save_libsvm(src, path);
+    const Dataset g = gpu::load_libsvm(path);
+    const Dataset r = pkrr::load_libsvm(path);
+    CHECK(g.n == r.n && g.d == r.d && g.row_ptr == r.row_ptr && g.col == r.col && g.val == r.val && g.y == r.y,
+          "load_libsvm: identical Dataset");
+    bool threw = false;
+    try {
+      gpu::load_libsvm("/nonexistent.svm");
+    } catch (const std::runtime_error&) {
+      threw = true;
+    }
+    CHECK(threw, "load_libsvm: missing file -> runtime_error");
+  }
   std::printf("%d failure(s)\n", g_fail);
   return g_fail ? 1 : 0;
 }
