@@ -610,10 +610,15 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
           u.C = f.A;
           u.ldc = mp;
           u.c_row0 = u.c_col0 = kb * kNB;
-          u.tiles_m = nb - kb;
           u.tiles_n = 1;
           u.abort_flag = f.status;
-          gemm_launch<128, G_UPDATE>(f.tmA, f.tmA, u, nb - kb, s, c);
+          if (nb - kb < g_sms) {  // under one wave of 128-row tiles: 64-row tiles, twice the CTAs
+            u.tiles_m = 2 * (nb - kb);
+            gemm_launch<64, G_UPDATE>(f.tmA, f.tmA, u, u.tiles_m, s, c);
+          } else {
+            u.tiles_m = nb - kb;
+            gemm_launch<128, G_UPDATE>(f.tmA, f.tmA, u, u.tiles_m, s, c);
+          }
         });
       }
       cur = kb;
