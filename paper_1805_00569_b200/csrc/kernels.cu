@@ -217,15 +217,25 @@ __device__ __forceinline__ void mma_tile_rn(double (&acc)[2], const double* A, i
 }
 
 // lane i owns row i of the 32x32 block at Sd (stride kLS); returns the first
-// failing column or -1 (solver.cpp:18-33 per column: test, sqrt, divide, update)
-__device__ __noinline__ int warp_potrf32(double* Sd, int lane) {
+// failing column or -1 (solver.cpp:18-33 per column: test, sqrt, divide, update).
+// Column values are broadcast through shared memory (`col`: two 40-double buffers,
+// 16-byte aligned): one STS per lane, then LDS.128 reads of two values each, instead
+// of two SHFL.IDX per double.  Lane j+1 updates its own next pivot at once (its
+// a[j+1] -= l*l is exactly the general update with l_k = its own l) and publishes it
+// with the column, so the pivot chain is LDS -> rsqrt -> multiply -> STS -> syncwarp;
+// the buffers alternate so one __syncwarp per column suffices.
+__device__ __noinline__ int warp_potrf32(double* Sd, double* col, int lane) {
   double a[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = Sd[lane * kLS + c];
   int bad = -1;
+  if (lane == 0) col[32] = a[0];
+  __syncwarp();
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
-    double piv = __shfl_sync(0xffffffffu, a[j], j);
+    const double* cur = col + (j & 1) * 40;
+    double* nxt = col + ((j + 1) & 1) * 40;
+    double piv = cur[32];
     if (!(piv > 0.0) && bad < 0) bad = j;
     piv = bad >= 0 ? 1.0 : piv;  // keep the warp going; the result is discarded
     // one reciprocal square root on the pivot chain instead of sqrt + divide
@@ -233,10 +243,20 @@ __device__ __noinline__ int warp_potrf32(double* Sd, int lane) {
     const double dj = piv * rj;
     const double l = a[j] * rj;
     a[j] = lane == j ? dj : (lane > j ? l : 0.0);
+    if (j + 1 < 32) {
+      if (lane == j + 1) {
+        a[j + 1] = a[j + 1] - l * l;
+        nxt[32] = a[j + 1];
+      }
+      nxt[lane] = l;
+      __syncwarp();
+      // rows k > j: a[k] -= l_i * l_k for k <= i (lane j+1's own diagonal already done)
 #pragma unroll
-    for (int k = j + 1; k < 32; ++k) {
-      const double lkj = __shfl_sync(0xffffffffu, l, k);
-      a[k] = lane >= k ? a[k] - l * lkj : a[k];
+      for (int k = (j + 1) & ~1; k < 32; k += 2) {
+        const double2 lk = *reinterpret_cast<const double2*>(nxt + k);
+        if (k > j) a[k] = (lane >= k && !(k == j + 1 && lane == j + 1)) ? a[k] - l * lk.x : a[k];
+        if (k + 1 > j) a[k + 1] = lane >= k + 1 ? a[k + 1] - l * lk.y : a[k + 1];
+      }
     }
   }
   if (bad < 0) {
@@ -310,7 +330,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
     LEAF_MARK(2 + 5 * pb);
     if (factor && warp == 0) {
       // ---- warp Cholesky of the 32x32 diagonal block: lane i owns row i ----
-      const int bad = warp_potrf32(Sd, lane);
+      const int bad = warp_potrf32(Sd, Tt, lane);  // Tt is free until the blocked inverse
       const bool ok = bad < 0;
       if (!ok && lane == 0) {
         *flag = 1;
