@@ -1,3 +1,5 @@
+"""C1 grid once: per-part system residuals and the selection MSE (any PKRR_* mode,
+e.g. PKRR_SYRK=ozaki or PKRR_SHADOW=1)."""
 import sys
 sys.path.insert(0, ".")
 import numpy as np
