@@ -144,3 +144,44 @@ def test_sharded_grid_equals_single_process(engine):
     assert best == full.best_index
     emse, _, _ = sharding.combine(esse, failed, 300)
     assert emse.tobytes() == full.eval_mse.tobytes()
+
+
+def _check_grid_properties(res, sel_y, eval_y):
+    """Shared full-size properties: every cell's part systems solved (residual), the
+    reported MSEs equal the MSEs of the returned predictions, best = first strict
+    minimum over the non-failed cells (strategies.cpp:499-505)."""
+    assert not np.any(res.failed)
+    assert np.all(res.parts["part_residual"] <= 1e-8)
+    mse_val = float(np.mean((res.best_pred - sel_y) ** 2))
+    assert abs(mse_val - res.mse[res.best_index]) <= 1e-12 * mse_val
+    if eval_y is not None:
+        mse_tst = float(np.mean((res.best_eval_pred - eval_y) ** 2))
+        assert abs(mse_tst - res.eval_mse[res.best_index]) <= 1e-12 * mse_tst
+    best = 0
+    for c in range(1, len(res.mse)):
+        if res.mse[c] < res.mse[best]:
+            best = c
+    assert res.best_index == best
+
+
+def test_grid_full_c2_properties(engine, oracle):
+    """BASELINE configs[2]: BKRR2, k-balance p = 16 (8192 rows each), 3 sigma x 3 lambda."""
+    dd = datagen.config("c2")
+    lam, sig = [1e-6, 1e-4, 1e-2], [1.0, 3.0, 10.0]
+    res = engine.grid_search("bkrr2", dd["X_train"], dd["y_train"], dd["X_val"], dd["y_val"], 16, lam, sig, 1,
+                             eval_X=dd["X_test"], eval_y=dd["y_test"], want_partition=True)
+    assert res.mse.shape == (9,)
+    _check_grid_properties(res, dd["y_val"], dd["y_test"])
+    # the partition is the oracle's k-balance (default k-means parameters, strategies.cpp:93-96)
+    r = oracle.kbalance(dd["X_train"], 16, 1)
+    assert np.array_equal(res.parts["part_of"], r["membership"])
+    assert set(res.parts["part_sizes"].tolist()) == {8192}
+
+
+def test_grid_full_c4_properties(engine):
+    """BASELINE configs[4]: KKRR2 on 262144 x 784 clipped rows, p = 8 (~32768 rows per part)."""
+    dd = datagen.config("c4")
+    res = engine.grid_search("kkrr2", dd["X_train"], dd["y_train"], dd["X_test"], dd["y_test"], 8, [1e-4], [8.0],
+                             1, want_partition=True)
+    _check_grid_properties(res, dd["y_test"], None)
+    assert int(res.parts["part_sizes"].sum()) == 262144
