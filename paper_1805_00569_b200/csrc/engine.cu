@@ -566,12 +566,12 @@ void part_load(pkrrgpu_ctx* ctx, PartBuf& pb, const double* dX, const double* dy
 void part_solve(pkrrgpu_ctx* ctx, PartBuf& pb, double lambda, int* status, double* res_out,
                 cudaStream_t s, cudaStream_t s2) {
   const double shift = lambda * static_cast<double>(pb.m);
-  pk::launch_assemble(pb.K, pb.A, pb.mp, shift, status, s, ctx->counter);
+  pk::launch_assemble(pb.K, pb.A, pb.mp, shift, status, s, ctx->counter, /*lower_only=*/true);
   pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, status, s, ctx->counter, pb.slices, pb.exps,
                    s2);
   pk::launch_trsv(pb.A, pb.Linv, pb.mp, pb.yp, pb.z, pb.alpha, pb.scratch, status, s, ctx->counter);
   if (res_out) {
-    pk::launch_gemv_rows(pb.K, pb.mp, pb.m, pb.m, pb.alpha, pb.Ka, status, s, ctx->counter);
+    pk::launch_symv_lower(pb.K, pb.mp, pb.alpha, pb.Ka, status, s, ctx->counter);
     pk::launch_residual_finish(pb.Ka, pb.alpha, pb.yp, pb.m, shift, res_out, status, s, ctx->counter);
   }
 }
@@ -713,9 +713,9 @@ int pkrrgpu_probe_potrf(pkrrgpu_ctx* ctx, int64_t m, double* out) {
   ++ctx->counter.launches;
   pk::launch_gather_rows(dX, d, idx, m, pb.Xp, pb.mp, pb.dp, s, ctx->counter);
   pk::launch_row_norms(pb.Xp, pb.mp, pb.dp, pb.dp, pb.norms, s, ctx->counter);
-  pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, m, 3.0, pb.K, pb.mp, nullptr, s, ctx->counter);
+  pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, m, 3.0, pb.K, pb.mp, nullptr, s, ctx->counter, false);
   int* status = sc.zeros<int>(2, s);
-  pk::launch_assemble(pb.K, pb.A, pb.mp, 1e-4 * static_cast<double>(m), status, s, ctx->counter);
+  pk::launch_assemble(pb.K, pb.A, pb.mp, 1e-4 * static_cast<double>(m), status, s, ctx->counter, true);
   ck(cudaStreamSynchronize(s), "sync");
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
   std::vector<double> fl;
@@ -1196,7 +1196,7 @@ int pkrrgpu_train_krr(pkrrgpu_ctx* ctx, const double* X, const double* y, int64_
   iota_kernel<<<blocks_for(m), 256, 0, s>>>(idx, m);
   ++ctx->counter.launches;
   part_load(ctx, pb, dX, dy, d, idx, s);
-  pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, m, sigma, pb.K, pb.mp, nullptr, s, ctx->counter);
+  pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, m, sigma, pb.K, pb.mp, nullptr, s, ctx->counter, false);
   int* status = sc.zeros<int>(2, s);
   double* res = sc.zeros<double>(2, s);
   part_solve(ctx, pb, lambda, status, res, s, ctx->aux_main);
@@ -1368,7 +1368,7 @@ int pkrrgpu_train_partitions(pkrrgpu_ctx* ctx, int strategy, const double* X, co
     part_alloc(sc, pb, po.sizes[t], d, true, ws);
     part_load(ctx, pb, dX, dy, d, po.order + po.start[t], ws);
     pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws,
-                        ctx->counter);
+                        ctx->counter, false);
     part_solve(ctx, pb, lambda, status + 2 * t, res + 2 * t, ws, ctx->aux[t % ctx->aux.size()]);
   }
   ck(cudaDeviceSynchronize(), "train");
@@ -1691,7 +1691,8 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
         cudaStream_t ws = streams[sidx[q]];
         const double m = static_cast<double>(pb.m);
         cudaEvent_t g0 = ev_on(ws);
-        pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws, ctx->counter);
+        pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws, ctx->counter,
+                            false);
         if (tcount[q] > 0)
           pk::launch_gram_cross(qt[q].tmQ, pb.tmX, qt[q].norms, pb.norms, qt[q].qp, tcount[q], pb.mp, pb.m, pb.dp,
                                 sigma, qt[q].cross, ws, ctx->counter);
@@ -1713,7 +1714,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
           int* st = dstatus + (cell * p + q) * 2;
           double* rs = dres + (cell * p + q) * 4;
           cudaEvent_t c0 = ev_on(ws);
-          pk::launch_assemble(pb.K, pb.A, pb.mp, shift, st, ws, ctx->counter);
+          pk::launch_assemble(pb.K, pb.A, pb.mp, shift, st, ws, ctx->counter, true);
           pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, st, ws, ctx->counter, pb.slices, pb.exps,
                            look_streams[sidx[q]]);
           cudaEvent_t c1 = ev_on(ws);
@@ -1721,7 +1722,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
           if (li == 0 && si == 0) part_end[q] = c1, part_ev[q][2] = c0, part_ev[q][3] = c1;
           f_chol += chol_flops(pb.m);
           pk::launch_trsv(pb.A, pb.Linv, pb.mp, pb.yp, pb.z, pb.alpha, pb.scratch, st, ws, ctx->counter);
-          pk::launch_gemv_rows(pb.K, pb.mp, pb.m, pb.m, pb.alpha, pb.Ka, st, ws, ctx->counter);
+          pk::launch_symv_lower(pb.K, pb.mp, pb.alpha, pb.Ka, st, ws, ctx->counter);
           pk::launch_residual_finish(pb.Ka, pb.alpha, pb.yp, pb.m, shift, rs, st, ws, ctx->counter);
           f_other += 4.0 * m * m;
           if (tcount[q] > 0) {

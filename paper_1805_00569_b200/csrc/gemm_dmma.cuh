@@ -35,6 +35,8 @@ struct GemmParams {
   double denom;          // (2*sigma)*sigma, kernel.cpp:55
   double neg_inv_denom;  // -1 / denom (the epilogue multiplies; see below)
   const int* abort_flag; // per-part NPD flag: skip work once a pivot failed
+  int mirror;            // G_GRAM_SYM: 1 = also write the upper triangle (public gram API);
+                         // 0 = lower tiles only (the pipeline's K: nothing reads the upper half)
 };
 
 constexpr int kBK = 16;        // f64 per k-tile row = 128 B (one swizzle row)
@@ -239,7 +241,7 @@ __global__ void __launch_bounds__(gemm_threads<MODE>(), 1)
           dst[0] = acc[i][j][0];
         }
       }
-    if constexpr (MODE == G_GRAM_SYM) {
+    if (MODE == G_GRAM_SYM && p.mirror) {
       // mirrored write K[gj][gi] = K[gi][gj] through a transposed smem stage
       // (coalesced rows; bitwise symmetric like kernel.cpp:113-116)
       double* T = reinterpret_cast<double*>(smem);  // pipeline ring is drained

@@ -151,8 +151,9 @@ static void gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const GemmPa
 
 void launch_gram_sym(const CUtensorMap& tmX, const double* norms, int64_t mp, int64_t dp,
                      int64_t m, double sigma, double* K, int64_t ldk, const int* abort,
-                     cudaStream_t s, Counter& c) {
+                     cudaStream_t s, Counter& c, bool mirror) {
   GemmParams p{};
+  p.mirror = mirror ? 1 : 0;
   p.a_row0 = p.b_row0 = 0;
   p.a_k0 = p.b_k0 = 0;
   p.ktiles = static_cast<int>(dp / kBK);
@@ -964,13 +965,14 @@ void launch_trsv(const double* L, const double* Linv, int64_t mp, const double* 
 // assemble / GEMV / reductions
 // ---------------------------------------------------------------------------
 __global__ void assemble_kernel(const double2* __restrict__ K, double2* __restrict__ A, int64_t mp,
-                                double shift, const int* abort) {
+                                double shift, const int* abort, int lower) {
   if (abort && *reinterpret_cast<const volatile int*>(abort)) return;
   const int64_t total = mp * mp / 2;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    double2 v = K[e];
     const int64_t r = (2 * e) / mp, col = (2 * e) % mp;
+    if (lower && col > r) continue;  // the factorization reads the lower triangle only
+    double2 v = K[e];
     if (col == r) v.x += shift;
     if (col + 1 == r) v.y += shift;
     A[e] = v;
@@ -978,9 +980,89 @@ __global__ void assemble_kernel(const double2* __restrict__ K, double2* __restri
 }
 
 void launch_assemble(const double* K, double* A, int64_t mp, double shift, const int* abort,
-                     cudaStream_t s, Counter& c) {
+                     cudaStream_t s, Counter& c, bool lower_only) {
   assemble_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<const double2*>(K),
-                                         reinterpret_cast<double2*>(A), mp, shift, abort);
+                                         reinterpret_cast<double2*>(A), mp, shift, abort, lower_only ? 1 : 0);
+  ++c.launches;
+}
+
+// y = K alpha for a symmetric K of which only the lower 128x128 tiles are stored (the
+// pipeline's gram): CTA I streams its row tiles (I, J < I), the lower half of (I, I) and
+// its column tiles (J > I, I) -- T tiles per CTA, balanced -- with per-thread partials
+// (16 rows x 4 columns per thread, as in the triangular solves) reduced once, in a fixed
+// order: deterministic.  alpha's padding entries are 0.
+__global__ void __launch_bounds__(256) symv_lower_kernel(const double* __restrict__ K, int64_t ld, int nb,
+                                                         const double* __restrict__ alpha, double* __restrict__ y,
+                                                         const int* abort) {
+  if (abort && *reinterpret_cast<const volatile int*>(abort)) return;
+  __shared__ double red[8][kNB];
+  __shared__ double yrow[kNB];
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int I = blockIdx.x;
+  double ar[16];
+#pragma unroll
+  for (int rr = 0; rr < 16; ++rr) ar[rr] = 0.0;
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+  const int64_t r0 = static_cast<int64_t>(I) * kNB + w * 16;
+  for (int J = 0; J < I; ++J) {  // row part: full tiles left of the diagonal
+    double4 m[16];
+    load_block16(K + r0 * ld + J * kNB + lane * 4, ld, m);
+    const double4 v = ldg_d4(alpha + J * kNB + lane * 4);
+#pragma unroll
+    for (int rr = 0; rr < 16; ++rr)
+      ar[rr] = fma(m[rr].w, v.w, fma(m[rr].z, v.z, fma(m[rr].y, v.y, fma(m[rr].x, v.x, ar[rr]))));
+  }
+  {  // diagonal tile: element (r, c) with c <= r stands for itself and, if c < r, for (c, r)
+    double4 m[16];
+    load_block16(K + r0 * ld + I * kNB + lane * 4, ld, m);
+    const double4 v = ldg_d4(alpha + I * kNB + lane * 4);
+    const double xr = lane < 16 ? __ldg(alpha + r0 + lane) : 0.0;
+#pragma unroll
+    for (int rr = 0; rr < 16; ++rr) {
+      const int r = w * 16 + rr, c = lane * 4;
+      const double xa = __shfl_sync(0xffffffffu, xr, rr);
+      const double e0 = c <= r ? m[rr].x : 0.0, e1 = c + 1 <= r ? m[rr].y : 0.0;
+      const double e2 = c + 2 <= r ? m[rr].z : 0.0, e3 = c + 3 <= r ? m[rr].w : 0.0;
+      ar[rr] = fma(e3, v.w, fma(e2, v.z, fma(e1, v.y, fma(e0, v.x, ar[rr]))));
+      c0 = fma(c < r ? m[rr].x : 0.0, xa, c0);
+      c1 = fma(c + 1 < r ? m[rr].y : 0.0, xa, c1);
+      c2 = fma(c + 2 < r ? m[rr].z : 0.0, xa, c2);
+      c3 = fma(c + 3 < r ? m[rr].w : 0.0, xa, c3);
+    }
+  }
+  for (int J = I + 1; J < nb; ++J) {  // column part: tiles below the diagonal, transposed
+    double4 m[16];
+    const int64_t rj = static_cast<int64_t>(J) * kNB + w * 16;
+    load_block16(K + rj * ld + I * kNB + lane * 4, ld, m);
+    const double xr = lane < 16 ? __ldg(alpha + rj + lane) : 0.0;
+#pragma unroll
+    for (int rr = 0; rr < 16; ++rr) {
+      const double xa = __shfl_sync(0xffffffffu, xr, rr);
+      c0 = fma(m[rr].x, xa, c0);
+      c1 = fma(m[rr].y, xa, c1);
+      c2 = fma(m[rr].z, xa, c2);
+      c3 = fma(m[rr].w, xa, c3);
+    }
+  }
+#pragma unroll
+  for (int rr = 0; rr < 16; ++rr) {
+    const double sum = warp_sum(ar[rr]);
+    if (lane == 0) yrow[w * 16 + rr] = sum;
+  }
+  *reinterpret_cast<double4*>(&red[w][lane * 4]) = make_double4(c0, c1, c2, c3);
+  __syncthreads();
+  if (tid < kNB) {
+    double sum = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sum += red[q][tid];
+    y[static_cast<int64_t>(I) * kNB + tid] = yrow[tid] + sum;
+  }
+}
+
+void launch_symv_lower(const double* K, int64_t mp, const double* alpha, double* y, const int* abort,
+                       cudaStream_t s, Counter& c) {
+  symv_lower_kernel<<<static_cast<unsigned>(mp / kNB), 256, 0, s>>>(K, mp, static_cast<int>(mp / kNB), alpha, y,
+                                                                    abort);
   ++c.launches;
 }
 

@@ -35,7 +35,7 @@ void launch_gather_vec(const double* y, const int64_t* idx, int64_t cnt, double*
 // K (ldk x ldk, padded mp) = gaussian gram of Xp (mp x dp) ; valid = m
 void launch_gram_sym(const CUtensorMap& tmX, const double* norms, int64_t mp, int64_t dp,
                      int64_t m, double sigma, double* K, int64_t ldk, const int* abort,
-                     cudaStream_t s, Counter& c);
+                     cudaStream_t s, Counter& c, bool mirror = true);
 // Kc (qp x mp) = k(Q_q, X_i); valid rows q, valid cols m
 void launch_gram_cross(const CUtensorMap& tmQ, const CUtensorMap& tmX, const double* qnorms,
                        const double* xnorms, int64_t qp, int64_t q, int64_t mp, int64_t m,
@@ -74,8 +74,11 @@ void launch_trsv(const double* L, const double* Linv, int64_t mp, const double* 
                  double* x, int* scratch, const int* abort, cudaStream_t s, Counter& c);
 
 // ---- assemble: A = K + shift * I (full copy) ------------------------------
+// y = K alpha from the lower 128x128 tiles of a symmetric K (mp x mp, ld = mp); deterministic
+void launch_symv_lower(const double* K, int64_t mp, const double* alpha, double* y, const int* abort,
+                       cudaStream_t s, Counter& c);
 void launch_assemble(const double* K, double* A, int64_t mp, double shift, const int* abort,
-                     cudaStream_t s, Counter& c);
+                     cudaStream_t s, Counter& c, bool lower_only = false);
 
 // ---- GEMV rows: out[i] = sum_{j<cols} M[i][j] v[j], i < rows (deterministic)
 void launch_gemv_rows(const double* M, int64_t ld, int64_t rows, int64_t cols, const double* v,
