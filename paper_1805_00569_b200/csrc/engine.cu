@@ -257,7 +257,7 @@ struct PartBuf {
   double* alpha = nullptr;
   double* Ka = nullptr;
   int* scratch = nullptr;   // trsv tickets/flags
-  int8_t* slices = nullptr; // Ozaki SYRK scratch: int8 [8 x mp x 512]
+  int8_t* slices = nullptr; // Ozaki SYRK scratch: 2 x int8 [8 x mp x 512]
   int* exps = nullptr;      // [mp]
   CUtensorMap tmX, tmA, tmLinv;
 };
@@ -277,8 +277,8 @@ void part_alloc(Scope& sc, PartBuf& pb, int64_t m, int64_t d, bool need_K, cudaS
   pb.Ka = sc.alloc<double>(pb.mp);
   pb.scratch = sc.alloc<int>(2 * (pb.mp / kNB) + 2);
   if (pk::syrk_ozaki()) {
-    pb.slices = sc.alloc<int8_t>(8 * pb.mp * 512);
-    pb.exps = sc.alloc<int>(pb.mp);
+    pb.slices = sc.alloc<int8_t>(2 * 8 * pb.mp * 512);  // two buffers: lookahead alternates them
+    pb.exps = sc.alloc<int>(2 * pb.mp);
   }
   if (!pk::make_tmap(&pb.tmX, pb.Xp, pb.mp, pb.dp, pb.dp) ||
       !pk::make_tmap(&pb.tmA, pb.A, pb.mp, pb.mp, pb.mp) ||
@@ -1616,7 +1616,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
     };
     return 8.0 * static_cast<double>(mp * dp + 8 * mp + 2 * mp * mp + mp * kNB + qbytes(tcount[q]) +
                                      (te ? qbytes(ecount[q]) : 0)) +
-           (pk::syrk_ozaki() ? 8.0 * 512.0 * static_cast<double>(mp) : 0.0);
+           (pk::syrk_ozaki() ? 2.0 * 8.0 * 512.0 * static_cast<double>(mp) : 0.0);
   };
   std::vector<std::vector<int64_t>> batches;
   {

@@ -609,7 +609,7 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
   const bool int8_update = g_syrk_ozaki && slices && exps;
   const int G = g_panel_group > 0 ? g_panel_group : (int8_update || nb < 64 ? 4 : 8);
   // lookahead needs a second stream; not with the shadow checker or the int8 update
-  const bool look = s2 != nullptr && !shadow && !int8_update && nb > 2 * G;
+  const bool look = s2 != nullptr && !shadow && nb > 2 * G;
   cudaEvent_t ev_panel = nullptr, ev_b = nullptr;
   bool b_pending = false;
   if (look) {
@@ -678,7 +678,49 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
       cudaEventRecord(e0, s);
     }
     cur = kend;
-    if (g_syrk_ozaki && slices && exps && Kg == 512) {
+    if (int8_update && Kg == 512 && look) {
+      // int8 update with lookahead: the group's panel rows are sliced once (into one of
+      // two alternating slice buffers -- the previous group's (b) may still be reading
+      // the other), (a) updates the next G2 block columns on s, (b) the rest on s2;
+      // ordering as for the DMMA lookahead below.
+      const int R = rem * kNB;
+      const int buf = (kb0 / G) & 1;
+      int8_t* sl = slices + static_cast<int64_t>(buf) * kOzS * mp * 512;
+      int* ex = exps + static_cast<int64_t>(buf) * mp;
+      ozaki_slice_kernel<<<(R * 32 + 255) / 256, 256, 0, s>>>(A, mp, kend * kNB, kb0 * kNB, R, Kg, sl, ex, status,
+                                                              static_cast<int>(mp));
+      CUtensorMap ta, tb;
+      if (!make_tmap_slices(&ta, sl, mp, Kg, kOzM) || !make_tmap_slices(&tb, sl, mp, Kg, kOzN)) {
+        fprintf(stderr, "pkrr: slice tensor map failed\n");
+        abort();
+      }
+      const int G2 = rem < G ? rem : G;
+      cudaEventRecord(ev_panel, s);  // panel and slices ready
+      cudaStreamWaitEvent(s2, ev_panel, 0);
+      if (b_pending) cudaStreamWaitEvent(s, ev_b, 0);
+      OzParams op{};
+      op.row0 = kend * kNB;
+      op.R = R;
+      op.ksteps = Kg / kOzK;
+      op.exps = ex;
+      op.abort_flag = status;
+      op.srow = 0;
+      op.narrow = G2 < rem ? 2 * G2 : 0;
+      const int na = G2 < rem ? G2 * (G2 + 1) + (rem - G2) * 2 * G2 : rem * (rem + 1);
+      ozaki_syrk_kernel<<<na, kOzThreads, kOzSmem, s>>>(ta, tb, tmA, op);
+      c.launches += 2;
+      if (rem > G2) {
+        OzParams ob = op;
+        const int T2 = rem - G2;
+        ob.row0 = (kend + G2) * kNB;
+        ob.srow = G2 * kNB;
+        ob.narrow = 0;
+        ozaki_syrk_kernel<<<T2 * (T2 + 1), kOzThreads, kOzSmem, s2>>>(ta, tb, tmA, ob);
+        ++c.launches;
+        cudaEventRecord(ev_b, s2);
+        b_pending = true;
+      }
+    } else if (int8_update && Kg == 512) {
       // int8 tensor-core trailing update (Ozaki splitting), FP64-accurate; fixed
       // geometry per part (slice stride mp rows) -> the same descriptors every group
       const int R = rem * kNB;

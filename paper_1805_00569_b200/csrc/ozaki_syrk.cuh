@@ -34,11 +34,13 @@ constexpr int kOzSmem = kOzStages * kOzStageBytes + kOzCBytes + 1024 + 256;
 constexpr int kOzThreads = 256;
 
 struct OzParams {
-  int row0;     // first trailing row/col of A (C tiles start here)
+  int row0;     // first row/col of A covered by the C tiles
   int R;        // trailing rows (multiple of 128)
   int ksteps;   // K / 32
-  const int* exps;  // per trailing row: e_i
+  const int* exps;  // per sliced row: e_i
   const int* abort_flag;
+  int srow;     // row of the slice / exps arrays that corresponds to row0 (lookahead (b): 128 G)
+  int narrow;   // > 0: only the first `narrow` 64-column tiles (lookahead (a)); 0: whole triangle
 };
 
 __device__ __forceinline__ uint64_t oz_desc_sw32(uint32_t saddr) {
@@ -129,7 +131,17 @@ __global__ void __launch_bounds__(kOzThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
 
   int I, J;
-  oz_tile_coords(blockIdx.x, I, J);
+  if (p.narrow > 0) {  // the first `narrow` tile columns: the triangle of rows I < narrow/2, then full rows
+    const int g2 = p.narrow >> 1, tri = g2 * (g2 + 1);
+    if (static_cast<int>(blockIdx.x) < tri) {
+      oz_tile_coords(blockIdx.x, I, J);
+    } else {
+      I = g2 + (blockIdx.x - tri) / p.narrow;
+      J = (blockIdx.x - tri) % p.narrow;
+    }
+  } else {
+    oz_tile_coords(blockIdx.x, I, J);
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     OZ_MARK(0);
@@ -171,8 +183,8 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         mbar_arrive_expect_tx(&full[st], kOzStageBytes);
         unsigned char* sa = ring + st * kOzStageBytes;
         unsigned char* sb = sa + kOzABytes;
-        tma_load_3d(sa, &tmA8, ks * kOzK, I * kOzM, 0, &full[st]);
-        tma_load_3d(sb, &tmB8, ks * kOzK, J * kOzN, 0, &full[st]);
+        tma_load_3d(sa, &tmA8, ks * kOzK, p.srow + I * kOzM, 0, &full[st]);
+        tma_load_3d(sb, &tmB8, ks * kOzK, p.srow + J * kOzN, 0, &full[st]);
       }
     }
   } else if (warp == 1) {
@@ -213,7 +225,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     tc_fence_after();
     if (threadIdx.x == 128) OZ_MARK(3);
     mbar_wait(cfull, 0);
-    const double sci = __longlong_as_double(static_cast<long long>(1023 + p.exps[I * kOzM + r]) << 52);
+    const double sci = __longlong_as_double(static_cast<long long>(1023 + p.exps[p.srow + I * kOzM + r]) << 52);
     double acc[32];
 #pragma unroll
     for (int c = 0; c < 32; ++c) acc[c] = 0.0;
@@ -228,7 +240,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
       const int col = ch * 32 + c;
-      const double scj = __longlong_as_double(static_cast<long long>(1023 + p.exps[J * kOzN + col]) << 52);
+      const double scj = __longlong_as_double(static_cast<long long>(1023 + p.exps[p.srow + J * kOzN + col]) << 52);
       const uint32_t off = static_cast<uint32_t>((((col >> 4) * 2 + (r >> 6)) << 13)) + swz128(r & 63, col & 15);
       const uint32_t addr = smem_u32(cbuf) + off;
       sts_f64(addr, lds_f64_at(addr) - acc[c] * sci * scj);  // power-of-two scales: exact

@@ -34,8 +34,8 @@ int main(int argc, char** argv) {
     cudaMalloc(&b.A, K.size() * 8);
     cudaMalloc(&b.L, (size_t)mp * kNB * 8);
     cudaMalloc(&b.st, 64);
-    cudaMalloc(&b.sl, (size_t)8 * mp * 512);
-    cudaMalloc(&b.ex, (size_t)mp * 4);
+    cudaMalloc(&b.sl, (size_t)2 * 8 * mp * 512);
+    cudaMalloc(&b.ex, (size_t)2 * mp * 4);
     make_tmap(&b.tA, b.A, mp, mp, mp);
     make_tmap(&b.tL, b.L, mp, kNB, kNB);
     return b;
