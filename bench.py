@@ -73,6 +73,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sample-n", type=int, default=0, help="reference sample train rows (0 = auto)")
     ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
+    ap.add_argument("--update", default="fp64", choices=["fp64", "int8"],
+                    help="trailing Cholesky update: FP64 tensor cores (DMMA, default) or the opt-in "
+                         "FP64-accurate int8 Ozaki emulation (tcgen05 kind::i8)")
     return ap.parse_args()
 
 
@@ -322,6 +325,8 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (datagen.py seed 1, BASELINE {cfg['name'].split(':')[0]} shapes)",
         "config": {"workload": f"BASELINE {cfg['name']}", "strategy": cfg["strategy"],
+                   "trailing_update": ("int8 Ozaki emulation of FP64 (tcgen05 kind::i8, opt-in)"
+                                       if os.environ.get("PKRR_SYRK") == "ozaki" else "FP64 DMMA tensor cores"),
                    "n_train": n_train, "n_val": cfg["val"], "n_test": cfg["test"], "d": cfg["d"], "p": p,
                    "sigmas": cfg["sigmas"], "lambdas": cfg["lambdas"], "cells": ncell,
                    "samples_per_step": samples, "parallelism": f"parts sharded t % {world}",
@@ -388,6 +393,8 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.update == "int8":  # read by the library at context creation
+        os.environ["PKRR_SYRK"] = "ozaki"
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

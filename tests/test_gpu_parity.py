@@ -242,3 +242,19 @@ def test_indefinite_cells_are_failed_not_fatal(engine, oracle):
     r = oracle.grid_search("exact", X, y, Q, np.sin(Q[:, 0]), 1, lam, sig, 1)
     assert list(g.failed) == list(r["failed"])
     assert g.best_index == r["best"]
+
+
+def test_indefinite_cells_with_lookahead(engine, oracle):
+    """NPD inside lookahead factorizations (parts of ~1500 rows: 12 panels > 2 groups):
+    the failing slice aborts on both streams, the other cell of the part still solves,
+    and the failed set / best cell equal the oracle's."""
+    base = np.random.default_rng(4).uniform(-2, 2, size=(1000, 3))
+    X = np.repeat(base, 3, axis=0)  # every point three times: K is singular
+    y = np.sin(X[:, 0]) + X[:, 1]
+    Q = np.random.default_rng(5).uniform(-2, 2, size=(64, 3))
+    lam, sig = [1e-300, 1e-2], [1.5]
+    g = engine.grid_search("kkrr2", X, y, Q, np.sin(Q[:, 0]) + Q[:, 1], 2, lam, sig, 3)
+    r = oracle.grid_search("kkrr2", X, y, Q, np.sin(Q[:, 0]) + Q[:, 1], 2, lam, sig, 3)
+    assert list(g.failed) == list(r["failed"]) == [True, False]
+    assert g.best_index == r["best"] == 1
+    assert abs(g.mse[1] - r["mse"][1]) <= 1e-8 * abs(r["mse"][1])
