@@ -1589,10 +1589,6 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   for (size_t i = 0; i < S; ++i) order_by_load[i] = i;
   std::stable_sort(order_by_load.begin(), order_by_load.end(),
                    [&](size_t x, size_t y) { return load[x] > load[y]; });
-  static const int prio_mode = std::getenv("PKRR_PRIO") ? std::atoi(std::getenv("PKRR_PRIO")) : -1;
-  if (prio_mode == 2 && S > 2)  // the critical stream first, then the others shortest-first
-    std::stable_sort(order_by_load.begin() + 1, order_by_load.end(),
-                     [&](size_t x, size_t y) { return load[x] < load[y]; });
   std::vector<size_t> rank_of(S);
   for (size_t r = 0; r < S; ++r) rank_of[order_by_load[r]] = r;
   std::vector<double> nz;

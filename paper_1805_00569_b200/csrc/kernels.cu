@@ -1459,9 +1459,6 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // the sequential per-coordinate chains and frees slots through "empty" mbarriers.
 // The loaders run up to kMeansRing chunks ahead, so the DADD chain sets the pace.
 constexpr int kMeansLoaders = kMeansThreads - 32;
-#ifndef MEANS_EXP
-#define MEANS_EXP 0  // tools/means_probe only: 1 = consumer idle, 2 = producer without copies
-#endif
 
 __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
@@ -1515,7 +1512,7 @@ __global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __re
 #pragma unroll
         for (int u = 0; u < kSteps; ++u) {
           const int rr = 2 * w + half + 14 * u;
-          if (cur[u] >= 0 && MEANS_EXP != 2)
+          if (cur[u] >= 0)
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(b + rr * kMeansF + 2 * piece)),
                          "l"(X + cur[u] * d + f0 + 2 * piece)
                          : "memory");
@@ -1557,7 +1554,7 @@ __global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __re
   // the DADD latency.  A slot is released after the DADDs that consumed its last block
   // (their operands -- the LDS results -- have arrived, so the reads are complete).
   double s = 0.0;
-  const int64_t nfull = MEANS_EXP == 1 ? 0 : sz / kMeansRows;
+  const int64_t nfull = sz / kMeansRows;
   auto slot_of = [&](int64_t c) { return smem_u32(mbuf + (c % kMeansRing) * kMeansRows * kMeansF + threadIdx.x); };
   auto wait_full = [&](int64_t c) {
     mbar_wait(&full[c % kMeansRing], static_cast<uint32_t>((c / kMeansRing) & 1));
@@ -1593,19 +1590,13 @@ __global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __re
       if (threadIdx.x == 0) mbar_arrive(&empty[c % kMeansRing]);
     }
   }
-  if (MEANS_EXP != 1 && nfull < nchunks) {  // the partial last chunk
+  if (nfull < nchunks) {  // the partial last chunk
     const int64_t c = nfull;
     wait_full(c);
     const uint32_t b = slot_of(c);
     const int rows = static_cast<int>(sz - c * kMeansRows);
     for (int r = 0; r < rows; ++r) s = __dadd_rn(s, lds_f64_at(b + (r * kMeansF) * 8));
   }
-  if (MEANS_EXP == 1)
-    for (int64_t c = 0; c < nchunks; ++c) {
-      wait_full(c);
-      __syncwarp();
-      if (threadIdx.x == 0) mbar_arrive(&empty[c % kMeansRing]);
-    }
   if (threadIdx.x < fw)
     centers[static_cast<int64_t>(j) * d + f0 + threadIdx.x] =
         sz > 0 ? __dmul_rn(s, __ddiv_rn(1.0, static_cast<double>(sz))) : 0.0;
