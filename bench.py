@@ -7,7 +7,7 @@ Default workload ("step", --config c1) -- KKRR2 at BASELINE configs[1], syntheti
 one Gaussian KRR model per part (sigma 3, lambda 1e-4: gram + lambda*m_t*I +
 Cholesky + solves + residual), val and test rows routed to the nearest centroid's
 model, MSE, best cell selected on validation MSE.  Weak scaling: per-GPU work (8
-parts of ~8192 rows) is fixed as N grows; parts are sharded t % N == rank with no
+parts of ~8192 rows) is fixed as N grows; parts are sharded by LPT on m^3 with no
 data-path collective (per-part SSE combined in part order afterwards).
 --config c0|c2|c3|c4 runs the other BASELINE configs (see CONFIGS).
 
@@ -329,7 +329,7 @@ def run_ours(args):
                                        if os.environ.get("PKRR_SYRK") == "ozaki" else "FP64 DMMA tensor cores"),
                    "n_train": n_train, "n_val": cfg["val"], "n_test": cfg["test"], "d": cfg["d"], "p": p,
                    "sigmas": cfg["sigmas"], "lambdas": cfg["lambdas"], "cells": ncell,
-                   "samples_per_step": samples, "parallelism": f"parts sharded t % {world}",
+                   "samples_per_step": samples, "parallelism": f"parts sharded over {world} rank(s), LPT on m^3",
                    "l2": "256 MB buffer written between timed steps (per-step K/A working set >> L2)",
                    "part_sizes": [int(x) for x in res.parts["part_sizes"]]},
         "gpu_launches": int(launches),

@@ -178,7 +178,8 @@ typedef struct {
   uint64_t seed;
   double km_threshold; /* used when km_max_iters > 0; else reference defaults 0.01/100 */
   int km_max_iters;
-  int rank;  /* parts t with t % world == rank are trained by this context */
+  int rank;  /* this context trains the parts the LPT rule (m^3, largest first to the least-loaded
+              * rank) assigns to `rank` -- identical on every rank (sharding.owned_parts) */
   int world; /* 1 = single process */
 } pkrrgpu_grid_args;
 

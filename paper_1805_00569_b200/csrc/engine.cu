@@ -1543,9 +1543,27 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   hmark("routing returned");
 
   // ---- per-part buffers for the parts this rank owns ----
+  // Ownership across ranks: LPT on the Cholesky cost m^3 (largest part first to the
+  // least-loaded rank, ties to the lower index / rank) -- every rank holds the same
+  // partition, so every rank computes the same assignment (sharding.owned_parts).
   std::vector<int64_t> owned;
-  for (int64_t q = 0; q < p; ++q)
-    if (q % world == rank) owned.push_back(q);
+  {
+    std::vector<int64_t> ord(p);
+    for (int64_t q = 0; q < p; ++q) ord[q] = q;
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return po.sizes[x] > po.sizes[y]; });
+    std::vector<double> rload(world, 0.0);
+    std::vector<int> owner(p, 0);
+    for (int64_t q : ord) {
+      int best = 0;
+      for (int r = 1; r < world; ++r)
+        if (rload[r] < rload[best]) best = r;
+      owner[q] = best;
+      const double m = static_cast<double>(po.sizes[q]);
+      rload[best] += m * m * m;
+    }
+    for (int64_t q = 0; q < p; ++q)
+      if (owner[q] == rank) owned.push_back(q);
+  }
   const int64_t dp = round_up(d, 16);
   std::vector<PartBuf> parts(p);
   std::vector<QueryBuf> qt(p), qe(p);
@@ -1816,9 +1834,11 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   for (int64_t c = 0; c < ncell; ++c)
     for (int64_t q : owned) pfail[c * p + q] = st[(c * p + q) * 2] ? 1 : 0;
   if (o->part_failed) std::memcpy(o->part_failed, pfail.data(), ncell * p);
+  std::vector<uint8_t> is_mine(p, 0);
+  for (int64_t q : owned) is_mine[q] = 1;
   for (int64_t c = 0; c < ncell; ++c)
     for (int64_t q = 0; q < p; ++q) {
-      const bool mine = (q % world) == rank;
+      const bool mine = is_mine[q] != 0;
       if (o->part_sse) o->part_sse[c * p + q] = mine ? rs[(c * p + q) * 4 + 2] : 0.0;
       if (o->part_eval_sse) o->part_eval_sse[c * p + q] = mine ? rs[(c * p + q) * 4 + 3] : 0.0;
       if (o->part_residual) o->part_residual[c * p + q] = mine ? rs[(c * p + q) * 4 + 0] : 0.0;

@@ -1,7 +1,8 @@
 """One process per GPU: part ownership and the per-cell combine.
 
-The p per-part models are independent, so parts are sharded
-t % world == rank with no data-path collective.  After training, each rank holds
+The p per-part models are independent, so parts are sharded across
+ranks with no data-path collective: LPT on the Cholesky cost m^3 (largest part to the
+least-loaded rank), computed identically by every rank from the common partition.  After training, each rank holds
 per-(cell, part) SSE / failure flags for its own parts (zeros elsewhere).  One
 all-reduce (SUM for SSE -- the shards are disjoint, so every sum is x + 0 + ...
 = x exactly; MAX for flags) reconstructs the full table on every rank, which is
@@ -13,8 +14,19 @@ from __future__ import annotations
 import numpy as np
 
 
-def owned_parts(p: int, rank: int, world: int):
-    return [t for t in range(p) if t % world == rank]
+def owned_parts(sizes, rank: int, world: int):
+    """Parts owned by `rank`: the engine's LPT rule (csrc/engine.cu grid_search_ex) --
+    parts by size descending (stable), each to the least-loaded rank (lowest on ties),
+    load += m^3."""
+    sizes = [int(x) for x in sizes]
+    order = sorted(range(len(sizes)), key=lambda t: -sizes[t])  # stable: ties keep index order
+    load = [0.0] * world
+    owner = [0] * len(sizes)
+    for t in order:
+        r = min(range(world), key=lambda q: (load[q], q))
+        owner[t] = r
+        load[r] += float(sizes[t]) ** 3
+    return [t for t in range(len(sizes)) if owner[t] == rank]
 
 
 def allreduce_tables(part_sse, part_failed, dist, device=None):

@@ -133,7 +133,7 @@ def test_sharded_grid_equals_single_process(engine):
     for rank in range(2):
         r = engine.grid_search("kkrr2", dd["X_train"], dd["y_train"], dd["X_val"], dd["y_val"], 6, lam, sig, 3,
                                rank=rank, world=2, **kw)
-        mine = sharding.owned_parts(6, rank, 2)
+        mine = sharding.owned_parts(r.parts["part_sizes"], rank, 2)
         other = [t for t in range(6) if t not in mine]
         assert np.all(r.parts["part_sse"][:, other] == 0.0)
         sse += r.parts["part_sse"]

@@ -1,5 +1,5 @@
 """CPU, world_size 2 over gloo: the multi-GPU combine reproduces the
-single-process result bitwise (parts sharded t % world, disjoint SSE shards)."""
+single-process result bitwise (parts sharded by the LPT rule, disjoint SSE shards)."""
 import os
 import socket
 
@@ -17,13 +17,13 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, full_sse, full_failed, t, out):
+def _worker(rank, world, port, full_sse, full_failed, t, sizes, out):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     nc, p = full_sse.shape
-    mine = sharding.owned_parts(p, rank, world)
+    mine = sharding.owned_parts(sizes, rank, world)
     sse = np.zeros_like(full_sse)
     fl = np.zeros_like(full_failed)
     sse[:, mine] = full_sse[:, mine]
@@ -45,7 +45,8 @@ def test_two_rank_combine_is_bitwise_single_rank():
     manager = mp.Manager()
     out = manager.dict()
     port = _free_port()
-    mp.start_processes(_worker, args=(2, port, full_sse, full_failed, t, out), nprocs=2, join=True,
+    sizes = [8275, 4117, 4002, 4108, 20544, 4092, 12298, 8100]
+    mp.start_processes(_worker, args=(2, port, full_sse, full_failed, t, sizes, out), nprocs=2, join=True,
                        start_method="spawn")
     for rank in range(2):
         mse_b, failed_b, best = out[rank]
@@ -57,6 +58,11 @@ def test_two_rank_combine_is_bitwise_single_rank():
 
 
 def test_owned_parts_partition_the_parts():
+    rng = np.random.default_rng(1)
+    sizes = rng.integers(1000, 30000, 13).tolist()
     for world in (1, 2, 3, 8):
-        seen = sorted(t for r in range(world) for t in sharding.owned_parts(13, r, world))
-        assert seen == list(range(13))
+        owned = [sharding.owned_parts(sizes, r, world) for r in range(world)]
+        assert sorted(t for o in owned for t in o) == list(range(13))
+        # LPT: the heaviest rank carries at most the largest part above the lightest
+        loads = [sum(sizes[t] ** 3 for t in o) for o in owned]
+        assert max(loads) - min(loads) <= max(sizes) ** 3
