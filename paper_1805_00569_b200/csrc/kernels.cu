@@ -897,6 +897,9 @@ __global__ void __launch_bounds__(256) trsv_fwd_kernel(const double* __restrict_
   __syncthreads();
   const int I = sI;
   prefetch_l2_block(Linv + static_cast<int64_t>(I) * kNB * kNB, kNB, tid);
+  double bpre[16];  // b_I, loaded now: off the flag chain
+#pragma unroll
+  for (int rr = 0; rr < 16; ++rr) bpre[rr] = lane == 0 ? __ldg(b + I * kNB + w * 16 + rr) : 0.0;
   const double* rows = L + (static_cast<int64_t>(I) * kNB + w * 16) * ld + lane * 4;
   double acc[16];
 #pragma unroll
@@ -913,7 +916,7 @@ __global__ void __launch_bounds__(256) trsv_fwd_kernel(const double* __restrict_
 #pragma unroll
   for (int rr = 0; rr < 16; ++rr) {
     const double sum = warp_sum(acc[rr]);
-    if (lane == 0) sacc[w * 16 + rr] = b[I * kNB + w * 16 + rr] - sum;
+    if (lane == 0) sacc[w * 16 + rr] = bpre[rr] - sum;
   }
   __syncthreads();
   const double4 v = *reinterpret_cast<const double4*>(sacc + lane * 4);
@@ -944,6 +947,7 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(const double* __restrict_
   __syncthreads();
   const int I = sI;
   prefetch_l2_block(Linv + static_cast<int64_t>(I) * kNB * kNB, kNB, tid);
+  const double zI = tid < kNB ? __ldg(z + I * kNB + tid) : 0.0;  // z is final (previous kernel): load now
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // columns 4l..4l+3, partial over this warp's rows
   for (int K = nb - 1; K > I; --K) {
     double4 m[16];
@@ -965,7 +969,7 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(const double* __restrict_
     double sum = 0.0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) sum += red[q][tid];
-    sv[tid] = z[I * kNB + tid] - sum;
+    sv[tid] = zI - sum;
   }
   __syncthreads();
   // x_I = Linv_I^T sv: column sums over this warp's 16 rows, then across warps
