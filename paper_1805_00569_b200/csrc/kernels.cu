@@ -618,16 +618,36 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
   }
   for (int kb0 = 0; kb0 < nb; kb0 += G) {
     const int kend = kb0 + G < nb ? kb0 + G : nb;
+    // two-level blocking: a group of G > 4 panels is factored as halves of H = G / 2;
+    // once the first half is done, its contribution to the second half's block columns
+    // is applied by one narrow SYRK (K = 128 H) and column updates only span panels of
+    // the block's own half -- most of the intra-group update runs in the SYRK kernel
+    const int H = G > 4 ? G / 2 : G;
     for (int kb = kb0; kb < kend; ++kb) {
-      if (kb > kb0) {
-        // column block kb (rows >= kb) -= A[:, kb0:kb] A[kb, kb0:kb]^T
+      const int sub0 = kb < kb0 + H ? kb0 : kb0 + H;  // first panel of this block's half
+      if (kb == kb0 + H) {
+        cur = kb;
+        step("half-update", [&](FactorBufs& f) {
+          SyrkParams u{};
+          u.row0 = kb * kNB;
+          u.k0 = kb0 * kNB;
+          u.ktiles = H * (kNB / kBK);
+          u.T = nb - kb;
+          u.abort_flag = f.status;
+          u.narrow = kend - kb;
+          dsyrk_persistent_kernel<<<syrk_tile_count(u.T, u.narrow), kSyrkThreads, kSyrkSmem, s>>>(f.tmA, u);
+          ++c.launches;
+        });
+      }
+      if (kb > sub0) {
+        // column block kb (rows >= kb) -= A[:, sub0:kb] A[kb, sub0:kb]^T
         cur = kb;
         step("col-update", [&](FactorBufs& f) {
           GemmParams u{};
           u.a_row0 = kb * kNB;
           u.b_row0 = kb * kNB;
-          u.a_k0 = u.b_k0 = kb0 * kNB;
-          u.ktiles = (kb - kb0) * (kNB / kBK);
+          u.a_k0 = u.b_k0 = sub0 * kNB;
+          u.ktiles = (kb - sub0) * (kNB / kBK);
           u.C = f.A;
           u.ldc = mp;
           u.c_row0 = u.c_col0 = kb * kNB;
