@@ -41,7 +41,7 @@ METRIC = "train+predict samples/sec (FP64)"
 # DRAM bytes per 128x128 SYRK output tile from the committed ncu --set full captures of the
 # m=20544 factorization probe: K=512 (profiles/ncu_syrk_r01.txt, 8911 tiles, 2.98e9 read +
 # 1.14e9 write) and K=1024 (profiles/ncu_syrk_k1024_r01.txt, 11781 tiles, 9.87e9 + 1.53e9).
-SYRK_TRAFFIC_PER_TILE = {512: 462800, 1024: 967700}
+SYRK_TRAFFIC_PER_TILE = {512: 462800, 1024: 967700, 2048: 1646600}  # K=2048: ncu_syrk_k2048_r01 (10585 tiles)
 UNIT = "samples/s"
 
 # BASELINE.json configs (per GPU for the weak-scaled ones).  km_iters 20 = exactly
@@ -296,7 +296,8 @@ def run_ours(args):
     # --- dominant kernel, live: the largest part's factorization alone on one stream,
     # CUDA events around every trailing-SYRK launch (algorithmic flops / launch time)
     big = int(max(res.parts["part_sizes"]))
-    syrk_k = 1024 if big >= 8192 else 512  # the library's automatic panel group (kernels.cu launch_potrf)
+    nb_big = (big + 127) // 128  # the library's automatic panel group (kernels.cu launch_potrf)
+    syrk_k = 512 if (nb_big < 64 or os.environ.get("PKRR_SYRK") == "ozaki") else (1024 if nb_big < 128 else 2048)
     probe = eng.probe_potrf(big)
     syrk_tflops = probe["syrk_flops"] / (probe["syrk_ms"] / 1e3) / 1e12 if probe["syrk_ms"] > 0 else 0.0
 

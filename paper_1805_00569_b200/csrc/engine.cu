@@ -169,6 +169,9 @@ struct Scope {
   ~Scope() {
     cudaDeviceSynchronize();
     for (void* p : ptrs) ctx->release(p);
+    // bound the cache: a call that needed more than half of HBM (e.g. C4's 44 GB parts)
+    // returns it, so other processes on the device (or later large calls) can allocate
+    if (static_cast<double>(ctx->cached_bytes) > 0.5 * ctx->total_mem) ctx->trim();
   }
   template <typename T>
   T* alloc(int64_t count) {

@@ -466,7 +466,7 @@ void set_syrk_probe(std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* ev, std::v
 static int g_syrk_persistent = 0;  // 0: one tile per CTA (priority-responsive); 1: one CTA per SM
 static int g_syrk_ozaki = 0;       // 1: trailing SYRK on the int8 tensor cores (Ozaki splitting)
 
-void set_panel_group(int g) { g_panel_group = g < 0 ? 0 : (g > 8 ? 8 : g); }
+void set_panel_group(int g) { g_panel_group = g < 0 ? 0 : (g > 16 ? 16 : g); }
 void set_syrk_persistent(int on) { g_syrk_persistent = on; }
 void set_syrk_ozaki(int on) { g_syrk_ozaki = on; }
 int syrk_ozaki() { return g_syrk_ozaki; }
@@ -604,10 +604,11 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
   };
   const int nb = static_cast<int>(mp / kNB);
   // panels per trailing update: K = 512 for the int8 update and small systems (short
-  // panel chains), K = 1024 from m >= 8192 (half the passes over the trailing matrix;
-  // C1 -1.1 %, C2 -1.8 %, C3 -2 %, C0 +23 % if used there)
+  // panel chains), K = 1024 from m >= 8192, K = 2048 from m >= 16384 (fewer passes over
+  // the trailing matrix; the recursive blocking below keeps the intra-group work in
+  // the SYRK kernel)
   const bool int8_update = g_syrk_ozaki && slices && exps;
-  const int G = g_panel_group > 0 ? g_panel_group : (int8_update || nb < 64 ? 4 : 8);
+  const int G = g_panel_group > 0 ? g_panel_group : (int8_update || nb < 64 ? 4 : (nb < 128 ? 8 : 16));
   // lookahead needs a second stream; not with the shadow checker or the int8 update
   const bool look = s2 != nullptr && !shadow && nb > 2 * G;
   cudaEvent_t ev_panel = nullptr, ev_b = nullptr;
@@ -618,23 +619,26 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
   }
   for (int kb0 = 0; kb0 < nb; kb0 += G) {
     const int kend = kb0 + G < nb ? kb0 + G : nb;
-    // two-level blocking: a group of G > 4 panels is factored as halves of H = G / 2;
-    // once the first half is done, its contribution to the second half's block columns
-    // is applied by one narrow SYRK (K = 128 H) and column updates only span panels of
-    // the block's own half -- most of the intra-group update runs in the SYRK kernel
-    const int H = G > 4 ? G / 2 : G;
+    // Recursive blocking inside a group of G panels (leaf blocks of 4): when panel kb
+    // starts the right child of a node of 2S panels (S >= 4), the left child's S panels
+    // are applied to the right child's block columns in one narrow SYRK (K = 128 S);
+    // column updates only span panels of the block's own leaf block of 4.  Every
+    // (panel, block column) pair of the group is applied exactly once, most of them by
+    // the SYRK kernel.
     for (int kb = kb0; kb < kend; ++kb) {
-      const int sub0 = kb < kb0 + H ? kb0 : kb0 + H;  // first panel of this block's half
-      if (kb == kb0 + H) {
+      const int off = kb - kb0;
+      const int sub0 = kb0 + (off / 4) * 4;  // first panel of this block's leaf block
+      for (int S = 4; S < G; S *= 2) {
+        if (off % (2 * S) != S) continue;
         cur = kb;
         step("half-update", [&](FactorBufs& f) {
           SyrkParams u{};
           u.row0 = kb * kNB;
-          u.k0 = kb0 * kNB;
-          u.ktiles = H * (kNB / kBK);
+          u.k0 = (kb - S) * kNB;
+          u.ktiles = S * (kNB / kBK);
           u.T = nb - kb;
           u.abort_flag = f.status;
-          u.narrow = kend - kb;
+          u.narrow = std::min(S, kend - kb);
           dsyrk_persistent_kernel<<<syrk_tile_count(u.T, u.narrow), kSyrkThreads, kSyrkSmem, s>>>(f.tmA, u);
           ++c.launches;
         });

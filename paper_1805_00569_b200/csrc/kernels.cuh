@@ -52,7 +52,7 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
 // updated first on s and the rest of the trailing update runs on s2, overlapping the
 // next panel factorisation; the result is bitwise the same as without.
 // Number of 128-column panels per trailing update (K = 128 * G); 0 (default) = automatic:
-// 4 for m < 8192 or the int8 update, 8 otherwise.
+// 4 for m < 8192 or the int8 update, 8 below m = 16384, 16 above (max 16).
 void set_panel_group(int g);
 // SYRK grid: 0 = one 128x128 tile per CTA (default), 1 = persistent (one CTA per SM).
 void set_syrk_persistent(int on);
