@@ -305,6 +305,8 @@ def run_ours(args):
     h = {k: torch.from_numpy(v).pin_memory().numpy() for k, v in dd.items()}
     e2e_ms = []
     with torch.cuda.stream(stream):
+        step(h)  # untimed: the first host-input call allocates the engine's input staging buffers
+        torch.cuda.synchronize()
         for i in range(max(1, min(args.steps, 3))):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
