@@ -1471,7 +1471,7 @@ void launch_group(const int32_t* label, int64_t n, int k, int64_t* sizes, int64_
 // order) stream through a double-buffered shared-memory ring via cp.async; warp
 // 0 keeps one strictly sequential accumulator per feature, so every centre
 // coordinate is the same chain of roundings as the reference's loop.
-constexpr int kMeansRows = 64, kMeansF = 32, kMeansThreads = 256, kMeansRing = 10;
+constexpr int kMeansRows = 128, kMeansF = 32, kMeansThreads = 256, kMeansRing = 6;
 constexpr int kMeansSmem = kMeansRing * kMeansRows * kMeansF * 8;
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -1595,10 +1595,19 @@ __global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __re
 #pragma unroll
       for (int u = 0; u < 32; ++u) A[u] = lds_f64_at(b0 + (u * kMeansF) * 8);
     }
+    static_assert(kMeansRows == 128, "the block pipeline below assumes 4 blocks of 32 rows per chunk");
     for (int64_t c = 0; c < nfull; ++c) {
       const uint32_t b = slot_of(c);
 #pragma unroll
       for (int u = 0; u < 32; ++u) B[u] = lds_f64_at(b + ((32 + u) * kMeansF) * 8);
+#pragma unroll
+      for (int u = 0; u < 32; ++u) s = __dadd_rn(s, A[u]);
+#pragma unroll
+      for (int u = 0; u < 32; ++u) A[u] = lds_f64_at(b + ((64 + u) * kMeansF) * 8);
+#pragma unroll
+      for (int u = 0; u < 32; ++u) s = __dadd_rn(s, B[u]);
+#pragma unroll
+      for (int u = 0; u < 32; ++u) B[u] = lds_f64_at(b + ((96 + u) * kMeansF) * 8);
       // probe the next chunk's barrier now and branch on it only after this block's
       // DADDs, so the probe latency overlaps the chain
       const uint32_t ready = c + 1 < nfull ? mbar_test(&full[(c + 1) % kMeansRing],
