@@ -139,6 +139,20 @@ __global__ void __launch_bounds__(gemm_threads<MODE>(), 1)
   const int cwarp = warp - kFirstConsumer;
   const int wm = cwarp >> 2, wn = cwarp & 3;
   const int lr = lane >> 2, lk = lane & 3;
+  // gram modes: the row norms the epilogue needs are loaded before the mainloop, so
+  // their latency hides behind it (they were among the epilogue's top stalls)
+  constexpr bool kGram = MODE == G_GRAM_SYM || MODE == G_GRAM_CROSS;
+  double na[kGram ? Cfg::MT : 1], nb[kGram ? Cfg::NT : 1][2];
+  if constexpr (kGram) {
+    const int gi0 = tm * BM + (cwarp >> 2) * Cfg::WM + (lane >> 2), gj0 = tn * kBN + (cwarp & 3) * Cfg::WN + 2 * (lane & 3);
+#pragma unroll
+    for (int i = 0; i < Cfg::MT; ++i) na[i] = __ldg(p.norm_a + gi0 + i * 8);
+#pragma unroll
+    for (int j = 0; j < Cfg::NT; ++j) {
+      nb[j][0] = __ldg(p.norm_b + gj0 + j * 8);
+      nb[j][1] = __ldg(p.norm_b + gj0 + j * 8 + 1);
+    }
+  }
   double acc[Cfg::MT][Cfg::NT][2];
 #pragma unroll
   for (int i = 0; i < Cfg::MT; ++i)
@@ -197,14 +211,6 @@ __global__ void __launch_bounds__(gemm_threads<MODE>(), 1)
     // Gaussian kernel epilogue (kernel.cpp:52-56): dist2 = (n_a + n_b) - 2*dot,
     // clamp at 0, exp(-dist2 / ((2 s) s)).  Padding rows are identity (sym) / 0.
     const int gi0 = tm * BM, gj0 = tn * kBN;
-    double na[Cfg::MT], nb[Cfg::NT][2];
-#pragma unroll
-    for (int i = 0; i < Cfg::MT; ++i) na[i] = p.norm_a[gi0 + r0 + i * 8];
-#pragma unroll
-    for (int j = 0; j < Cfg::NT; ++j) {
-      nb[j][0] = p.norm_b[gj0 + c0 + j * 8];
-      nb[j][1] = p.norm_b[gj0 + c0 + j * 8 + 1];
-    }
 #pragma unroll
     for (int i = 0; i < Cfg::MT; ++i)
 #pragma unroll
