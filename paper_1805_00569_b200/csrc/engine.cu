@@ -294,17 +294,19 @@ struct QueryBuf {
   int64_t q = 0, qp = 0;
   double* Xq = nullptr;
   double* norms = nullptr;
-  double* cross = nullptr;  // qp x mp
-  double* pred = nullptr;   // qp
+  double* cross = nullptr;    // qp x mp (only the public cross-gram API materialises it)
+  double* partial = nullptr;  // fused-prediction scratch (predict_partial_elems)
+  double* pred = nullptr;     // qp
   CUtensorMap tmQ;
 };
 
-void query_alloc(Scope& sc, QueryBuf& qb, int64_t q, int64_t dp, int64_t mp) {
+void query_alloc(Scope& sc, QueryBuf& qb, int64_t q, int64_t dp, int64_t mp, bool cross = false) {
   qb.q = q;
   qb.qp = round_up(q > 0 ? q : 1, 64);
   qb.Xq = sc.alloc<double>(qb.qp * dp);
   qb.norms = sc.alloc<double>(qb.qp);
-  qb.cross = sc.alloc<double>(qb.qp * mp);
+  if (cross) qb.cross = sc.alloc<double>(qb.qp * mp);
+  else qb.partial = sc.alloc<double>(pk::predict_partial_elems(qb.qp, mp));
   qb.pred = sc.alloc<double>(qb.qp);
   if (!pk::make_tmap(&qb.tmQ, qb.Xq, qb.qp, dp, dp)) fail(PKRRGPU_CUDA, "tensor map (Q)");
 }
@@ -1088,7 +1090,7 @@ int pkrrgpu_gram(pkrrgpu_ctx* ctx, const double* A, int64_t na, const double* B,
        "copy K");
   } else {
     QueryBuf qb;
-    query_alloc(sc, qb, na, pb.dp, pb.mp);
+    query_alloc(sc, qb, na, pb.dp, pb.mp, true);
     int64_t* qidx = sc.alloc<int64_t>(na);
     iota_kernel<<<blocks_for(na), 256, 0, s>>>(qidx, na);
     ++ctx->counter.launches;
@@ -1240,9 +1242,8 @@ int pkrrgpu_predict(pkrrgpu_ctx* ctx, const double* S, const double* alpha, int6
   query_alloc(sc, qb, q, pb.dp, pb.mp);
   pk::launch_gather_rows(dQ, d, idx, q, qb.Xq, qb.qp, pb.dp, s, ctx->counter);
   pk::launch_row_norms(qb.Xq, qb.qp, pb.dp, pb.dp, qb.norms, s, ctx->counter);
-  pk::launch_gram_cross(qb.tmQ, pb.tmX, qb.norms, pb.norms, qb.qp, q, pb.mp, m, pb.dp, sigma, qb.cross,
-                        s, ctx->counter);
-  pk::launch_gemv_rows(qb.cross, pb.mp, q, m, pb.alpha, qb.pred, nullptr, s, ctx->counter);
+  pk::launch_predict_fused(qb.tmQ, pb.tmX, qb.norms, pb.norms, qb.qp, q, pb.mp, m, pb.dp, sigma, pb.alpha,
+                           qb.partial, qb.pred, nullptr, s, ctx->counter);
   copy_out(out, qb.pred, q, s);
   ck(cudaStreamSynchronize(s), "sync");
   API_END
@@ -1466,10 +1467,9 @@ int pkrrgpu_predict_nearest(pkrrgpu_ctx* ctx, const pkrrgpu_models* models, cons
     const int64_t* rows = ro.members + ro.start[t];
     pk::launch_gather_rows(dQ, d, rows, cnt, qb.Xq, qb.qp, dp, ws, ctx->counter);
     pk::launch_row_norms(qb.Xq, qb.qp, dp, dp, qb.norms, ws, ctx->counter);
-    pk::launch_gram_cross(qb.tmQ, models->tmX[t], qb.norms, models->norms[t], qb.qp, cnt,
-                          models->mp[t], models->m[t], dp, models->sigma, qb.cross, ws, ctx->counter);
-    pk::launch_gemv_rows(qb.cross, models->mp[t], cnt, models->m[t], models->alpha[t], qb.pred, nullptr,
-                         ws, ctx->counter);
+    pk::launch_predict_fused(qb.tmQ, models->tmX[t], qb.norms, models->norms[t], qb.qp, cnt, models->mp[t],
+                             models->m[t], dp, models->sigma, models->alpha[t], qb.partial, qb.pred, nullptr, ws,
+                             ctx->counter);
     pk::launch_sse_scatter(qb.pred, rows, cnt, ydummy, pred_all, sse + t, nullptr, ws, ctx->counter);
   }
   ck(cudaDeviceSynchronize(), "predict");
@@ -1710,13 +1710,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
         cudaEvent_t g0 = ev_on(ws);
         pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws, ctx->counter,
                             false);
-        if (tcount[q] > 0)
-          pk::launch_gram_cross(qt[q].tmQ, pb.tmX, qt[q].norms, pb.norms, qt[q].qp, tcount[q], pb.mp, pb.m, pb.dp,
-                                sigma, qt[q].cross, ws, ctx->counter);
-        if (te && ecount[q] > 0)
-          pk::launch_gram_cross(qe[q].tmQ, pb.tmX, qe[q].norms, pb.norms, qe[q].qp, ecount[q], pb.mp, pb.m, pb.dp,
-                                sigma, qe[q].cross, ws, ctx->counter);
-        f_gram += static_cast<double>(d) * m * (m + 1) + 2.0 * (tcount[q] + ecount[q]) * m * d;
+        f_gram += static_cast<double>(d) * m * (m + 1);
         gram_iv.push_back({g0, ev_on(ws)});
         if (si == 0) part_ev[q][0] = g0, part_ev[q][1] = gram_iv.back().b;
       }
@@ -1743,16 +1737,18 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
           pk::launch_residual_finish(pb.Ka, pb.alpha, pb.yp, pb.m, shift, rs, st, ws, ctx->counter);
           f_other += 4.0 * m * m;
           if (tcount[q] > 0) {
-            pk::launch_gemv_rows(qt[q].cross, pb.mp, tcount[q], pb.m, pb.alpha, qt[q].pred, st, ws, ctx->counter);
+            pk::launch_predict_fused(qt[q].tmQ, pb.tmX, qt[q].norms, pb.norms, qt[q].qp, tcount[q], pb.mp, pb.m,
+                                     pb.dp, sigma, pb.alpha, qt[q].partial, qt[q].pred, st, ws, ctx->counter);
             double* dst = pred_t + (cell * pp_parts + (pp_parts > 1 ? q : 0)) * t;
             pk::launch_sse_scatter(qt[q].pred, tpos[q], tcount[q], dyt, dst, rs + 2, st, ws, ctx->counter);
-            f_other += 2.0 * tcount[q] * m;
+            f_other += 2.0 * tcount[q] * m * (d + 1);
           }
           if (te && ecount[q] > 0) {
-            pk::launch_gemv_rows(qe[q].cross, pb.mp, ecount[q], pb.m, pb.alpha, qe[q].pred, st, ws, ctx->counter);
+            pk::launch_predict_fused(qe[q].tmQ, pb.tmX, qe[q].norms, pb.norms, qe[q].qp, ecount[q], pb.mp, pb.m,
+                                     pb.dp, sigma, pb.alpha, qe[q].partial, qe[q].pred, st, ws, ctx->counter);
             double* dst = pred_e + (cell * pp_parts + (pp_parts > 1 ? q : 0)) * te;
             pk::launch_sse_scatter(qe[q].pred, epos[q], ecount[q], dye, dst, rs + 3, st, ws, ctx->counter);
-            f_other += 2.0 * ecount[q] * m;
+            f_other += 2.0 * ecount[q] * m * (d + 1);
           }
           pred_iv.push_back({c1, ev_on(ws)});
           if (li == 0 && si == 0) part_ev[q][4] = pred_iv.back().b;

@@ -13,10 +13,13 @@
 #include "gemm_dmma.cuh"
 #include "syrk_persistent.cuh"
 #include "ozaki_syrk.cuh"
+#include "predict_fused.cuh"
 #include <string>
 #include "kernels.cuh"
 
 namespace pk {
+
+static int g_sms = 148;  // refreshed from the device by launch_potrf
 
 // ---------------------------------------------------------------------------
 // TMA descriptors (driver entry point fetched through the runtime)
@@ -186,6 +189,40 @@ void launch_gram_cross(const CUtensorMap& tmQ, const CUtensorMap& tmX, const dou
   p.denom = (2.0 * sigma) * sigma;
   p.neg_inv_denom = -1.0 / p.denom;
   gemm_launch<64, G_GRAM_CROSS>(tmQ, tmX, p, p.tiles_m * p.tiles_n, s, c);
+}
+
+int64_t predict_partial_elems(int64_t qp, int64_t mp) { return qp * (mp / 128); }
+
+void launch_predict_fused(const CUtensorMap& tmQ, const CUtensorMap& tmX, const double* qnorms,
+                          const double* xnorms, int64_t qp, int64_t q, int64_t mp, int64_t m, int64_t dp,
+                          double sigma, const double* alpha, double* partial, double* pred, const int* abort,
+                          cudaStream_t s, Counter& c) {
+  if (q <= 0) return;
+  PredictParams p{};
+  p.ktiles = static_cast<int>(dp / kBK);
+  p.tiles_q = static_cast<int>(qp / 64);
+  p.tiles_x = static_cast<int>(mp / 128);
+  // about two CTAs per SM over the whole launch, at least one support tile each
+  int nch = (2 * g_sms + p.tiles_q - 1) / p.tiles_q;
+  nch = nch < 1 ? 1 : (nch > p.tiles_x ? p.tiles_x : nch);
+  p.chunk = (p.tiles_x + nch - 1) / nch;
+  nch = (p.tiles_x + p.chunk - 1) / p.chunk;
+  p.valid_x = static_cast<int>(m);
+  p.qp = qp;
+  p.qnorms = qnorms;
+  p.xnorms = xnorms;
+  p.alpha = alpha;
+  p.neg_inv_denom = -1.0 / ((2.0 * sigma) * sigma);
+  p.partial = partial;
+  p.abort_flag = abort;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(predict_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<64>::SMEM);
+    attr_set = true;
+  }
+  predict_fused_kernel<<<p.tiles_q * nch, kGemmThreads, GemmCfg<64>::SMEM, s>>>(tmQ, tmX, p);
+  predict_reduce_kernel<<<static_cast<unsigned>((q + 255) / 256), 256, 0, s>>>(partial, qp, nch, q, pred, abort);
+  c.launches += 2;
 }
 
 // ---------------------------------------------------------------------------
@@ -449,7 +486,6 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
   LEAF_MARK(24);
 }
 
-static int g_sms = 148;
 
 // Panel-grouped blocked right-looking Cholesky.  G consecutive 128-column panels
 // are factored with narrow column updates restricted to the group (leaf + DMMA

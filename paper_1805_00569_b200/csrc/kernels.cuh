@@ -81,6 +81,13 @@ void launch_assemble(const double* K, double* A, int64_t mp, double shift, const
                      cudaStream_t s, Counter& c, bool lower_only = false);
 
 // ---- GEMV rows: out[i] = sum_{j<cols} M[i][j] v[j], i < rows (deterministic)
+// prediction with the cross kernel tile fused into the alpha contraction
+// (predict_fused.cuh); partial = predict_partial_elems(qp, mp) doubles of scratch
+int64_t predict_partial_elems(int64_t qp, int64_t mp);
+void launch_predict_fused(const CUtensorMap& tmQ, const CUtensorMap& tmX, const double* qnorms,
+                          const double* xnorms, int64_t qp, int64_t q, int64_t mp, int64_t m, int64_t dp,
+                          double sigma, const double* alpha, double* partial, double* pred, const int* abort,
+                          cudaStream_t s, Counter& c);
 void launch_gemv_rows(const double* M, int64_t ld, int64_t rows, int64_t cols, const double* v,
                       double* out, const int* abort, cudaStream_t s, Counter& c);
 // residual ratio of (K + shift I) alpha = y from Kalpha (strategies.cpp:310-320 and

@@ -135,6 +135,22 @@ def test_train_krr_matches_oracle(engine, oracle, m, d, sigma, lam):
     assert relnorm(model.predict(Q), oracle.predict(X, alpha, sigma, Q)) <= REL
 
 
+@pytest.mark.parametrize("m,q,d,sigma", [(1, 1, 3, 0.9), (129, 65, 7, 1.5), (20000, 1, 90, 3.0),
+                                         (3000, 4100, 90, 3.0), (5000, 700, 17, 0.3)])
+def test_predict_fused_matches_oracle(engine, oracle, m, q, d, sigma):
+    # predict_fused.cuh: the test-by-support tile folded into the alpha contraction,
+    # split over support chunks (1 .. tiles_x CTAs per query tile) and reduced in order
+    rng = np.random.default_rng(m + q)
+    S = rng.standard_normal((m, d))
+    Q = np.vstack([S[: min(q, m) // 2], rng.standard_normal((q - min(q, m) // 2, d))])
+    alpha = rng.standard_normal(m)
+    got = engine.predict(S, alpha, sigma, Q)
+    ref = oracle.predict(S, alpha, sigma, Q)
+    # per element, relative to sum_i |K(q, i) alpha_i| <= sum |alpha| (summation-order bound)
+    assert np.all(np.abs(got - ref) <= 1e-13 * np.abs(alpha).sum() + 1e-12 * np.abs(ref))
+    assert np.array_equal(got, engine.predict(S, alpha, sigma, Q))  # deterministic
+
+
 # ------------------------------------------------------------- clustering ----
 @pytest.mark.parametrize("n,d,k,seed", [(30, 2, 1, 99), (12, 1, 12, 55), (2000, 4, 3, 17), (5000, 90, 8, 2),
                                         (9000, 90, 16, 5), (4000, 33, 40, 11)])
