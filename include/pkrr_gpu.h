@@ -270,8 +270,10 @@ int pkrrgpu_fp64_peak(pkrrgpu_ctx* ctx, double* tflops);
 /* Roofline probe of the dominant kernel: factor an m x m SPD system alone on one
  * stream with CUDA events around every trailing-SYRK launch.  out[0] total ms,
  * out[1] Cholesky algorithmic flops, out[2] SYRK ms (sum over launches),
- * out[3] SYRK algorithmic flops, out[4] SYRK launches, out[5] NPD flag. */
-int pkrrgpu_probe_potrf(pkrrgpu_ctx* ctx, int64_t m, double* out);
+ * out[3] SYRK algorithmic flops, out[4] SYRK launches, out[5] NPD flag.
+ * alone != 0: the panel schedule of a system factorised alone (single-part grids,
+ * pkrrgpu_cholesky, pkrrgpu_train_krr), else the one of a part among several. */
+int pkrrgpu_probe_potrf(pkrrgpu_ctx* ctx, int64_t m, int alone, double* out);
 
 #ifdef __cplusplus
 }

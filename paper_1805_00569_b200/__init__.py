@@ -135,7 +135,7 @@ def load_library(path: str = LIB_PATH):
         "pkrrgpu_last_timings": (C.c_int, [C.c_void_p, _d, C.c_int]),
         "pkrrgpu_stream": (C.c_void_p, [C.c_void_p]),
         "pkrrgpu_fp64_peak": (C.c_int, [C.c_void_p, _d]),
-        "pkrrgpu_probe_potrf": (C.c_int, [C.c_void_p, C.c_int64, _d]),
+        "pkrrgpu_probe_potrf": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, _d]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -245,11 +245,12 @@ class Engine:
         _check(_lib.pkrrgpu_fp64_peak(self._h, C.byref(v)))
         return v.value
 
-    def probe_potrf(self, m: int) -> dict:
+    def probe_potrf(self, m: int, alone: bool = False) -> dict:
         """Standalone factorization of an m x m system with events around every
-        trailing-SYRK launch (the dominant kernel's live roofline)."""
+        trailing-SYRK launch (the dominant kernel's live roofline); `alone` selects the
+        panel schedule of a system factorised by itself (single-part grids)."""
         out = (C.c_double * 8)()
-        _check(_lib.pkrrgpu_probe_potrf(self._h, int(m), out))
+        _check(_lib.pkrrgpu_probe_potrf(self._h, int(m), 1 if alone else 0, out))
         return dict(total_ms=out[0], chol_flops=out[1], syrk_ms=out[2], syrk_flops=out[3],
                     syrk_launches=int(out[4]), npd=int(out[5]))
 

@@ -569,11 +569,11 @@ void part_load(pkrrgpu_ctx* ctx, PartBuf& pb, const double* dX, const double* dy
 }
 
 void part_solve(pkrrgpu_ctx* ctx, PartBuf& pb, double lambda, int* status, double* res_out,
-                cudaStream_t s, cudaStream_t s2) {
+                cudaStream_t s, cudaStream_t s2, bool alone) {
   const double shift = lambda * static_cast<double>(pb.m);
   pk::launch_assemble(pb.K, pb.A, pb.mp, shift, status, s, ctx->counter, /*lower_only=*/true);
   pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, status, s, ctx->counter, pb.slices, pb.exps,
-                   s2);
+                   s2, alone);
   pk::launch_trsv(pb.A, pb.Linv, pb.mp, pb.yp, pb.z, pb.alpha, pb.scratch, status, s, ctx->counter);
   if (res_out) {
     pk::launch_symv_lower(pb.K, pb.mp, pb.alpha, pb.Ka, status, s, ctx->counter);
@@ -699,7 +699,7 @@ int64_t pkrrgpu_launch_count(const pkrrgpu_ctx* ctx) { return ctx ? ctx->counter
 
 void* pkrrgpu_stream(pkrrgpu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->main) : nullptr; }
 
-int pkrrgpu_probe_potrf(pkrrgpu_ctx* ctx, int64_t m, double* out) {
+int pkrrgpu_probe_potrf(pkrrgpu_ctx* ctx, int64_t m, int alone, double* out) {
   API_BEGIN
   if (m <= 0 || !out) fail(PKRRGPU_INVALID, "probe_potrf: bad arguments");
   Scope sc(ctx);
@@ -727,7 +727,8 @@ int pkrrgpu_probe_potrf(pkrrgpu_ctx* ctx, int64_t m, double* out) {
   Timer tm;
   pk::set_syrk_probe(&ev, &fl);
   ck(cudaEventRecord(tm.a, s), "event");
-  pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, m, status, s, ctx->counter, pb.slices, pb.exps);
+  pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, m, status, s, ctx->counter, pb.slices, pb.exps,
+                   nullptr, alone != 0);
   ck(cudaEventRecord(tm.b, s), "event");
   pk::set_syrk_probe(nullptr, nullptr);
   ck(cudaStreamSynchronize(s), "sync");
@@ -1146,7 +1147,7 @@ int pkrrgpu_cholesky(pkrrgpu_ctx* ctx, const double* A, int64_t m, double* L, in
   }
   int* status = sc.zeros<int>(2, s);
   pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, m, status, s, ctx->counter, pb.slices, pb.exps,
-                   ctx->aux_main);
+                   ctx->aux_main, true);
   std::vector<int> st = to_host(status, 2, s);
   if (st[0]) {
     if (npd_pivot) *npd_pivot = st[1];
@@ -1204,7 +1205,7 @@ int pkrrgpu_train_krr(pkrrgpu_ctx* ctx, const double* X, const double* y, int64_
   pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, m, sigma, pb.K, pb.mp, nullptr, s, ctx->counter, false);
   int* status = sc.zeros<int>(2, s);
   double* res = sc.zeros<double>(2, s);
-  part_solve(ctx, pb, lambda, status, res, s, ctx->aux_main);
+  part_solve(ctx, pb, lambda, status, res, s, ctx->aux_main, true);
   std::vector<int> st = to_host(status, 2, s);
   if (st[0]) {
     if (npd_pivot) *npd_pivot = st[1];
@@ -1373,7 +1374,7 @@ int pkrrgpu_train_partitions(pkrrgpu_ctx* ctx, int strategy, const double* X, co
     part_load(ctx, pb, dX, dy, d, po.order + po.start[t], ws);
     pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws,
                         ctx->counter, false);
-    part_solve(ctx, pb, lambda, status + 2 * t, res + 2 * t, ws, ctx->aux[t % ctx->aux.size()]);
+    part_solve(ctx, pb, lambda, status + 2 * t, res + 2 * t, ws, ctx->aux[t % ctx->aux.size()], po.p == 1);
   }
   ck(cudaDeviceSynchronize(), "train");
   std::vector<int> st = to_host(status, 2 * po.p, s);
@@ -1727,7 +1728,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
           cudaEvent_t c0 = ev_on(ws);
           pk::launch_assemble(pb.K, pb.A, pb.mp, shift, st, ws, ctx->counter, true);
           pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, st, ws, ctx->counter, pb.slices, pb.exps,
-                           look_streams[sidx[q]]);
+                           look_streams[sidx[q]], p == 1);  // rank-independent: the same schedule at any world size
           cudaEvent_t c1 = ev_on(ws);
           chol_iv.push_back({c0, c1});
           if (li == 0 && si == 0) part_end[q] = c1, part_ev[q][2] = c0, part_ev[q][3] = c1;

@@ -46,9 +46,12 @@ constexpr int kGemmThreads = (kConsumerWarps + 1) * 32;
 constexpr int kStages = 4;
 
 
+// BM = 32 (latency-bound panel steps: twice the CTAs of BM = 64) still loads a
+// 64-row A box (the TMA box height); only its first 32 rows are used.
 template <int BM>
 struct GemmCfg {
-  static constexpr int A_BYTES = BM * kBK * 8;
+  static constexpr int A_ROWS = BM < 64 ? 64 : BM;
+  static constexpr int A_BYTES = A_ROWS * kBK * 8;
   static constexpr int B_BYTES = kBN * kBK * 8;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int WM = BM / 2;
@@ -126,7 +129,7 @@ __global__ void __launch_bounds__(gemm_threads<MODE>(), 1)
         unsigned char* sb = sa + Cfg::A_BYTES;
         const int ka = p.a_k0 + kt * kBK, kb = p.b_k0 + kt * kBK;
 #pragma unroll
-        for (int h = 0; h < BM / 64; ++h) tma_load_2d(sa + h * 8192, &tmA, ka, arow + h * 64, &full[s]);
+        for (int h = 0; h < Cfg::A_ROWS / 64; ++h) tma_load_2d(sa + h * 8192, &tmA, ka, arow + h * 64, &full[s]);
 #pragma unroll
         for (int h = 0; h < kBN / 64; ++h) tma_load_2d(sb + h * 8192, &tmB, kb, brow + h * 64, &full[s]);
       }

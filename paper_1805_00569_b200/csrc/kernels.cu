@@ -239,19 +239,40 @@ constexpr int kLS = 132;  // S stride (doubles): == 4 (mod 16) -> conflict-free 
 constexpr int kBS = 36;   // 32x32 block stride
 constexpr int kLeafSmem = (kNB * kLS + 4 * 32 * kBS + 3 * 32 * kBS) * 8 + 32;
 
-// acc(8x8) += A(rows a0.., k) * Bt(rows b0.., k)^T over k in [0, K), both row-major
-__device__ __forceinline__ void mma_tile_rt(double (&acc)[2], const double* A, int lda,
-                                            const double* Bt, int ldb, int K, int lr, int lk) {
-#pragma unroll 8
-  for (int k = 0; k < K; k += 4)
-    dmma(acc, A[lr * lda + k + lk], Bt[lr * ldb + k + lk]);
+// Register-blocked variants (one A fragment feeds several DMMAs: half the LDS traffic,
+// which otherwise co-limits with the single SM's DMMA rate):
+// acc[c] (8x8) += A(rows, k) * Bt(rows 8c.., k)^T, c < 4 (one row tile x 4 column tiles)
+__device__ __forceinline__ void mma_row4_rt(double (&acc)[4][2], const double* A, int lda, const double* Bt,
+                                            int ldb, int k0, int k1, int lr, int lk) {
+#pragma unroll 4
+  for (int k = k0; k < k1; k += 4) {
+    const double a = A[lr * lda + k + lk];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dmma(acc[c], a, Bt[(8 * c + lr) * ldb + k + lk]);
+  }
 }
-// acc(8x8) += A(rows, k) * B(k, cols) with B row-major [k][n]
-__device__ __forceinline__ void mma_tile_rn(double (&acc)[2], const double* A, int lda,
-                                            const double* B, int ldb, int K, int lr, int lk) {
-#pragma unroll 8
-  for (int k = 0; k < K; k += 4)
-    dmma(acc, A[lr * lda + k + lk], B[(k + lk) * ldb + lr]);
+// acc[r][c] (2x2 tiles of 8x8) += A(rows 8r.., k) * Bt(rows 8c.., k)^T
+__device__ __forceinline__ void mma_2x2_rt(double (&acc)[2][2][2], const double* A, const double* Bt, int ld,
+                                           int K, int lr, int lk) {
+#pragma unroll 4
+  for (int k = 0; k < K; k += 4) {
+    const double a0 = A[lr * ld + k + lk], a1 = A[(8 + lr) * ld + k + lk];
+    const double b0 = Bt[lr * ld + k + lk], b1 = Bt[(8 + lr) * ld + k + lk];
+    dmma(acc[0][0], a0, b0);
+    dmma(acc[0][1], a0, b1);
+    dmma(acc[1][0], a1, b0);
+    dmma(acc[1][1], a1, b1);
+  }
+}
+// acc[c] (8x8) += A(rows, k) * B(k, cols 8c..) with B row-major [k][n], k in [k0, k1)
+__device__ __forceinline__ void mma_row4_rn(double (&acc)[4][2], const double* A, int lda, const double* B,
+                                            int ldb, int k0, int k1, int lr, int lk) {
+#pragma unroll 4
+  for (int k = k0; k < k1; k += 4) {
+    const double a = A[lr * lda + k + lk];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dmma(acc[c], a, B[(k + lk) * ldb + 8 * c + lr]);
+  }
 }
 
 // lane i owns row i of the 32x32 block at Sd (stride kLS); returns the first
@@ -391,98 +412,109 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
     __syncthreads();
     LEAF_MARK(4 + 5 * pb);
     if (!factor || pb == 3) continue;
-    // ---- panel TRSM: P = A[R0:128, 32pb:+32] * D_pb^T (in place after a barrier) ----
+    // ---- panel TRSM: P = A[R0:128, 32pb:+32] * D_pb^T (in place after a barrier);
+    // warp w: row tiles w and w + 8, each against the 4 column tiles ----
     const int R0 = 32 * (pb + 1), nrt = (kNB - R0) / 8;
     const double* Db = D + pb * 32 * kBS;
-    double res[6][2];
+    double res[2][4][2];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      const int t = warp + 8 * q;
-      res[q][0] = res[q][1] = 0.0;
-      if (t < nrt * 4) {
-        const int rt = t >> 2, ct = t & 3;
-        mma_tile_rt(res[q], S + (R0 + 8 * rt) * kLS + 32 * pb, kLS, Db + (8 * ct) * kBS, kBS, 32, lr, lk);
-      }
+    for (int q = 0; q < 2; ++q) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) res[q][c][0] = res[q][c][1] = 0.0;
+      const int rt = warp + 8 * q;
+      if (rt < nrt) mma_row4_rt(res[q], S + (R0 + 8 * rt) * kLS + 32 * pb, kLS, Db, kBS, 0, 32, lr, lk);
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      const int t = warp + 8 * q;
-      if (t < nrt * 4) {
-        const int rt = t >> 2, ct = t & 3;
-        double* dst = S + (R0 + 8 * rt + lr) * kLS + 32 * pb + 8 * ct + 2 * lk;
-        dst[0] = res[q][0];
-        dst[1] = res[q][1];
+    for (int q = 0; q < 2; ++q) {
+      const int rt = warp + 8 * q;
+      if (rt < nrt) {
+        double* dst = S + (R0 + 8 * rt + lr) * kLS + 32 * pb + 2 * lk;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) *reinterpret_cast<double2*>(dst + 8 * c) = make_double2(res[q][c][0], res[q][c][1]);
       }
     }
     __syncthreads();
     LEAF_MARK(5 + 5 * pb);
-    // ---- trailing SYRK inside the block: S[R0:, R0:] -= P P^T (lower 8x8 tiles) ----
-    const int ntl = nrt * (nrt + 1) / 2;
-    for (int t = warp; t < ntl; t += 8) {
-      int rt = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-      while ((rt + 1) * (rt + 2) / 2 <= t) ++rt;
-      while (rt * (rt + 1) / 2 > t) --rt;
-      const int ct = t - rt * (rt + 1) / 2;
-      double acc[2] = {0.0, 0.0};
-      mma_tile_rt(acc, S + (R0 + 8 * rt) * kLS + 32 * pb, kLS, S + (R0 + 8 * ct) * kLS + 32 * pb, kLS, 32,
-                  lr, lk);
-      double* dst = S + (R0 + 8 * rt + lr) * kLS + R0 + 8 * ct + 2 * lk;
-      dst[0] -= acc[0];
-      dst[1] -= acc[1];
+    // ---- trailing SYRK inside the block: S[R0:, R0:] -= P P^T over lower 16x16
+    // blocks (2x2 DMMA tiles each; the upper tile of a diagonal block is not stored) ----
+    const int nbt = nrt / 2, nbl = nbt * (nbt + 1) / 2;
+    for (int t = warp; t < nbl; t += 8) {
+      int rb = 0;
+      while ((rb + 1) * (rb + 2) / 2 <= t) ++rb;
+      const int cb = t - rb * (rb + 1) / 2;
+      double acc[2][2][2] = {};
+      mma_2x2_rt(acc, S + (R0 + 16 * rb) * kLS + 32 * pb, S + (R0 + 16 * cb) * kLS + 32 * pb, kLS, 32, lr, lk);
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (rb == cb && j > i) continue;
+          double* dst = S + (R0 + 16 * rb + 8 * i + lr) * kLS + R0 + 16 * cb + 8 * j + 2 * lk;
+          const double2 v = *reinterpret_cast<double2*>(dst);
+          *reinterpret_cast<double2*>(dst) = make_double2(v.x - acc[i][j][0], v.y - acc[i][j][1]);
+        }
     }
     __syncthreads();
   }
 
   LEAF_MARK(22);
+  // L is final: its rows (lower part, 16-byte rounded -- the one extra column is a
+  // zero of a diagonal 32-block) go out with plain vector stores from all warps before
+  // the blocked inverse, which only writes S's upper 32-blocks, beyond every stored row
+  // (fire-and-forget STG.128 drain while the DMMAs run; the bulk-copy engine is slow
+  // for hundreds of small copies)
+  if (factor) {
+    for (int e = tid; e < kNB * 64; e += kLeafThreads) {
+      const int r = e >> 6, cp = e & 63;
+      if (2 * cp <= r)
+        *reinterpret_cast<double2*>(Ab + static_cast<int64_t>(r) * lda + 2 * cp) =
+            *reinterpret_cast<const double2*>(S + r * kLS + 2 * cp);
+    }
+  }
+  LEAF_MARK(21);
   // ---- blocked inverse: X_ij = -D_i * sum_{k=j}^{i-1} L_ik X_kj, X_ij stored (not
-  // transposed) in S's free upper block (j, i); T_j row-major in Tt[j]
+  // transposed) in S's free upper block (j, i); T_j row-major in Tt[j].  Work item =
+  // one 8-row tile x the 4 column tiles (the A fragment is loaded once per k step);
+  // the lower-triangular D blocks bound the k ranges ----
   for (int bi = 1; bi < 4; ++bi) {
-    for (int t = warp; t < bi * 16; t += 8) {
-      const int bj = t >> 4, rt = (t >> 2) & 3, ct = t & 3;
-      double acc[2] = {0.0, 0.0};
+    for (int t = warp; t < bi * 4; t += 8) {
+      const int bj = t >> 2, rt = t & 3;
+      double acc[4][2] = {};
       const double* Arow = S + (32 * bi + 8 * rt) * kLS;
-      mma_tile_rn(acc, Arow + 32 * bj, kLS, D + bj * 32 * kBS + 8 * ct, kBS, 32, lr, lk);  // X_jj = D_j
+      mma_row4_rn(acc, Arow + 32 * bj, kLS, D + bj * 32 * kBS, kBS, 0, 32, lr, lk);  // X_jj = D_j
       for (int bk = bj + 1; bk < bi; ++bk)
-        mma_tile_rn(acc, Arow + 32 * bk, kLS, S + (32 * bj) * kLS + 32 * bk + 8 * ct, kLS,
-                    32, lr, lk);
-      double* T = Tt + bj * 32 * kBS;
-      *reinterpret_cast<double2*>(T + (8 * rt + lr) * kBS + 8 * ct + 2 * lk) = make_double2(acc[0], acc[1]);
+        mma_row4_rn(acc, Arow + 32 * bk, kLS, S + (32 * bj) * kLS + 32 * bk, kLS, 0, 32, lr, lk);
+      double* T = Tt + bj * 32 * kBS + (8 * rt + lr) * kBS + 2 * lk;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) *reinterpret_cast<double2*>(T + 8 * c) = make_double2(acc[c][0], acc[c][1]);
     }
     __syncthreads();
-    for (int t = warp; t < bi * 16; t += 8) {
-      const int bj = t >> 4, rt = (t >> 2) & 3, ct = t & 3;
-      double acc[2] = {0.0, 0.0};
-      mma_tile_rn(acc, D + bi * 32 * kBS + (8 * rt) * kBS, kBS, Tt + bj * 32 * kBS + 8 * ct, kBS, 32, lr, lk);
-      *reinterpret_cast<double2*>(S + (32 * bj + 8 * rt + lr) * kLS + 32 * bi + 8 * ct + 2 * lk) =
-          make_double2(-acc[0], -acc[1]);
+    for (int t = warp; t < bi * 4; t += 8) {
+      const int bj = t >> 2, rt = t & 3;
+      double acc[4][2] = {};
+      // row tile rt of the lower-triangular D_i has nonzeros in k < 8 rt + 8 only
+      mma_row4_rn(acc, D + bi * 32 * kBS + (8 * rt) * kBS, kBS, Tt + bj * 32 * kBS, kBS, 0, 8 * rt + 8, lr, lk);
+      double* X = S + (32 * bj + 8 * rt + lr) * kLS + 32 * bi + 2 * lk;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) *reinterpret_cast<double2*>(X + 8 * c) = make_double2(-acc[c][0], -acc[c][1]);
     }
     __syncthreads();
   }
 
   LEAF_MARK(23);
-  // write-out by the bulk-copy engine: L rows (the strict upper part of the
-  // diagonal block is never read as data) and the 10 lower 32x32 blocks of
-  // inv(L) (the upper blocks of the Linv scratch are zeroed once at allocation)
-  fence_proxy_async();
-  __syncthreads();
-  if (warp == 0) {
-    if (factor)
-      for (int r = lane; r < kNB; r += 32) bulk_store(Ab + static_cast<int64_t>(r) * lda, S + r * kLS, kNB * 8);
-    bulk_commit();
-  } else {
-    // 10 lower 32x32 blocks of inv(L): warps 1..7, one 32-double row segment per warp step
-    double* Lo = Linv + base * kNB;
-    for (int q = warp - 1; q < 10 * 32; q += 7) {
-      const int blk = q >> 5, r = q & 31;
-      int bi = 0;
-      while ((bi + 1) * (bi + 2) / 2 <= blk) ++bi;
-      const int bj = blk - bi * (bi + 1) / 2;
-      const double* src = bi == bj ? D + bi * 32 * kBS + r * kBS : S + (32 * bj + r) * kLS + 32 * bi;
-      Lo[(32 * bi + r) * kNB + 32 * bj + lane] = src[lane];
-    }
+  // the 10 lower 32x32 blocks of inv(L), 16 double2 per row segment (the upper blocks
+  // of the Linv scratch are zeroed once at allocation)
+  double* Lo = Linv + base * kNB;
+  for (int e = tid; e < 10 * 32 * 16; e += kLeafThreads) {
+    const int q = e >> 4, cp = e & 15;
+    const int blk = q >> 5, r = q & 31;
+    const int bi = blk < 1 ? 0 : (blk < 3 ? 1 : (blk < 6 ? 2 : 3));
+    const int bj = blk - bi * (bi + 1) / 2;
+    const double* src = bi == bj ? D + bi * 32 * kBS + r * kBS : S + (32 * bj + r) * kLS + 32 * bi;
+    *reinterpret_cast<double2*>(Lo + (32 * bi + r) * kNB + 32 * bj + 2 * cp) =
+        *reinterpret_cast<const double2*>(src + 2 * cp);
   }
-  if (warp == 0) bulk_wait_read0();  // smem drained; global completion is ordered by the kernel boundary
   LEAF_MARK(24);
 }
 
@@ -598,7 +630,7 @@ struct FactorBufs {
 
 void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, double* Linv,
                   int64_t mp, int64_t m_valid, int* status, cudaStream_t s, Counter& c, int8_t* slices,
-                  int* exps, cudaStream_t s2) {
+                  int* exps, cudaStream_t s2, bool latency) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(potrf_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLeafSmem);
@@ -644,7 +676,47 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
   // the trailing matrix; the recursive blocking below keeps the intra-group work in
   // the SYRK kernel)
   const bool int8_update = g_syrk_ozaki && slices && exps;
-  const int G = g_panel_group > 0 ? g_panel_group : (int8_update || nb < 64 ? 4 : (nb < 128 ? 8 : 16));
+  // A lone small system (latency-bound panel chain) uses G = 1: each panel's next
+  // block column is updated at once by a 64-row-tile GEMM, the rest behind it.
+  const int G = g_panel_group > 0 ? g_panel_group
+                                  : (int8_update ? 4 : (nb < 64 ? (latency ? 1 : 4) : (nb < 128 ? 8 : 16)));
+  // (a) of the trailing update (the next group's block columns) as a column GEMM with
+  // 64-row tiles for narrow groups: K = 128 G is short, so spread it over more CTAs
+  const bool gemm_a = G <= 2;
+  // a lone system's panel steps (TRSM, next-column update) run on 32-row tiles: the
+  // chain is latency-bound and twice the CTAs halve each CTA's share of the step
+  const bool narrow_rows = latency && nb < 64;
+  auto update_next = [&](const FactorBufs& f, int kb0_, int kend_, int G2, cudaStream_t st) {
+    const int rem_ = nb - kend_;
+    if (gemm_a) {
+      GemmParams u{};
+      u.a_row0 = u.b_row0 = kend_ * kNB;
+      u.a_k0 = u.b_k0 = kb0_ * kNB;
+      u.ktiles = (kend_ - kb0_) * (kNB / kBK);
+      u.C = f.A;
+      u.ldc = mp;
+      u.c_row0 = u.c_col0 = kend_ * kNB;
+      u.tiles_n = G2;
+      u.abort_flag = f.status;
+      if (narrow_rows) {
+        u.tiles_m = 4 * rem_;
+        gemm_launch<32, G_UPDATE>(f.tmA, f.tmA, u, u.tiles_m * G2, st, c);
+      } else {
+        u.tiles_m = 2 * rem_;
+        gemm_launch<64, G_UPDATE>(f.tmA, f.tmA, u, u.tiles_m * G2, st, c);
+      }
+    } else {
+      SyrkParams u{};
+      u.row0 = kend_ * kNB;
+      u.k0 = kb0_ * kNB;
+      u.ktiles = (kend_ - kb0_) * (kNB / kBK);
+      u.T = rem_;
+      u.abort_flag = f.status;
+      u.narrow = G2;
+      dsyrk_persistent_kernel<<<syrk_tile_count(rem_, G2), kSyrkThreads, kSyrkSmem, st>>>(f.tmA, u);
+      ++c.launches;
+    }
+  };
   // lookahead needs a second stream; not with the shadow checker or the int8 update
   const bool look = s2 != nullptr && !shadow && nb > 2 * G;
   cudaEvent_t ev_panel = nullptr, ev_b = nullptr;
@@ -722,10 +794,15 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
         t.ldc = mp;
         t.c_row0 = (kb + 1) * kNB;
         t.c_col0 = kb * kNB;
-        t.tiles_m = rem * 2;
         t.tiles_n = 1;
         t.abort_flag = f.status;
-        gemm_launch<64, G_STORE>(f.tmA, f.tmLinv, t, rem * 2, s, c);
+        if (narrow_rows) {
+          t.tiles_m = rem * 4;
+          gemm_launch<32, G_STORE>(f.tmA, f.tmLinv, t, rem * 4, s, c);
+        } else {
+          t.tiles_m = rem * 2;
+          gemm_launch<64, G_STORE>(f.tmA, f.tmLinv, t, rem * 2, s, c);
+        }
       });
     }
     const int rem = nb - kend;
@@ -808,20 +885,23 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
       // and (b) of this group runs after (b) of the previous one on s2, (a) after it too,
       // so every element sees the panels in the same order: bitwise the same factor.
       const int G2 = rem < G ? rem : G;
-      cudaEventRecord(ev_panel, s);
-      cudaStreamWaitEvent(s2, ev_panel, 0);
       if (b_pending) cudaStreamWaitEvent(s, ev_b, 0);
-      SyrkParams u{};
-      u.row0 = kend * kNB;
-      u.k0 = kb0 * kNB;
-      u.ktiles = (kend - kb0) * (kNB / kBK);
-      u.T = rem;
-      u.abort_flag = status;
-      u.narrow = G2;
-      dsyrk_persistent_kernel<<<syrk_tile_count(rem, G2), kSyrkThreads, kSyrkSmem, s>>>(tmA, u);
-      ++c.launches;
+      if (!gemm_a) {
+        cudaEventRecord(ev_panel, s);
+        cudaStreamWaitEvent(s2, ev_panel, 0);
+      }
+      update_next(main, kb0, kend, G2, s);
+      if (gemm_a) {
+        // (b) behind (a): the short column GEMM gets the whole GPU (a persistent (b)
+        // started first would leave it the reserved SMs only), (b) overlaps the next leaf
+        cudaEventRecord(ev_panel, s);
+        cudaStreamWaitEvent(s2, ev_panel, 0);
+      }
       if (rem > G2) {
-        SyrkParams v = u;
+        SyrkParams v{};
+        v.k0 = kb0 * kNB;
+        v.ktiles = (kend - kb0) * (kNB / kBK);
+        v.abort_flag = status;
         v.row0 = (kend + G2) * kNB;
         v.T = rem - G2;
         v.narrow = 0;
@@ -838,6 +918,23 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
     } else {
       // trailing: A22 -= L21 L21^T over the whole group (K = 128 * group), C staged by TMA
       step("syrk", [&](FactorBufs& f) {
+        if (gemm_a) {
+          // same split as the lookahead path (bitwise-neutral): next columns, then the rest
+          const int G2 = rem < G ? rem : G;
+          update_next(f, kb0, kend, G2, s);
+          if (rem == G2) return;
+          SyrkParams v{};
+          v.row0 = (kend + G2) * kNB;
+          v.k0 = kb0 * kNB;
+          v.ktiles = (kend - kb0) * (kNB / kBK);
+          v.T = rem - G2;
+          v.abort_flag = f.status;
+          const int ntl = v.T * (v.T + 1) / 2;
+          const int grid = g_syrk_persistent ? (ntl < g_sms ? ntl : g_sms) : ntl;
+          dsyrk_persistent_kernel<<<grid, kSyrkThreads, kSyrkSmem, s>>>(f.tmA, v);
+          ++c.launches;
+          return;
+        }
         SyrkParams u{};
         u.row0 = kend * kNB;
         u.k0 = kb0 * kNB;

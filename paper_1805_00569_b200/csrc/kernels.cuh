@@ -47,10 +47,13 @@ void launch_gram_cross(const CUtensorMap& tmQ, const CUtensorMap& tmX, const dou
 void shadow_report();  // PKRR_SHADOW debug mode (see launch_potrf)
 void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, double* Linv,
                   int64_t mp, int64_t m_valid, int* status, cudaStream_t s, Counter& c,
-                  int8_t* slices = nullptr, int* exps = nullptr, cudaStream_t s2 = nullptr);
+                  int8_t* slices = nullptr, int* exps = nullptr, cudaStream_t s2 = nullptr,
+                  bool latency = false);
 // s2 (optional): a second stream for lookahead -- the next panel's columns are
 // updated first on s and the rest of the trailing update runs on s2, overlapping the
 // next panel factorisation; the result is bitwise the same as without.
+// latency: the system is factorised alone (nothing else to fill the GPU): small
+// systems (m < 8192) then use single-panel groups (see launch_potrf).
 // Number of 128-column panels per trailing update (K = 128 * G); 0 (default) = automatic:
 // 4 for m < 8192 or the int8 update, 8 below m = 16384, 16 above (max 16).
 void set_panel_group(int g);
