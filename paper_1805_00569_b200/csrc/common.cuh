@@ -37,6 +37,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Arrive without a compiler memory clobber: for a latency-critical unrolled loop whose
+// shared-memory writes are already ordered before it by a __syncwarp; the clobber
+// would stop the scheduler from overlapping independent work across the arrive.
+__device__ __forceinline__ void mbar_arrive_nomem(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)));
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint32_t done = 0;

@@ -78,8 +78,16 @@ constexpr int gemm_threads() {
   return MODE == G_GRAM_SYM ? 384 : kGemmThreads;
 }
 
+// The 64-row panel GEMMs (TRSM, column updates: K = 128..512, a few microseconds of
+// mainloop) fit two CTAs per SM at <= 112 registers, so one CTA's prologue / epilogue
+// overlaps the other's mainloop.
 template <int BM, int MODE>
-__global__ void __launch_bounds__(gemm_threads<MODE>(), 1)
+constexpr int gemm_min_blocks() {
+  return BM <= 64 && (MODE == G_UPDATE || MODE == G_STORE) ? 2 : 1;
+}
+
+template <int BM, int MODE>
+__global__ void __launch_bounds__(gemm_threads<MODE>(), gemm_min_blocks<BM, MODE>())
     dgemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     GemmParams p) {
   using Cfg = GemmCfg<BM>;

@@ -227,17 +227,19 @@ void launch_predict_fused(const CUtensorMap& tmQ, const CUtensorMap& tmX, const 
 
 // ---------------------------------------------------------------------------
 // Cholesky leaf (128 x 128 diagonal block), one CTA of 8 warps:
-//   for each 32-column panel: warp-level register Cholesky of the 32x32
-//   diagonal block (+ its inverse), DMMA panel TRSM and DMMA SYRK inside smem;
-//   then the blocked inverse of the whole 128 block (DMMA) for the panel TRSM
-//   of the outer algorithm and for the triangular solves.
+//   for each 32-column panel: warp 0 factors the 32x32 diagonal block in registers
+//   while warps 1..3-pb factor the rows below it column by column from the values
+//   warp 0 publishes (so no panel TRSM, and no 32x32 inverse, on the chain), then a
+//   register-blocked DMMA SYRK inside smem; warp 7 inverts each 32x32 diagonal block
+//   off the chain; finally the blocked inverse of the whole 128 block (DMMA) for the
+//   panel TRSM of the outer algorithm and for the triangular solves.
 // Pivot test / sqrt / column divide / rank-1 update per column follow
 // solver.cpp:18-33; only the blocking (summation order) differs.
 // ---------------------------------------------------------------------------
 constexpr int kLeafThreads = 256;
 constexpr int kLS = 132;  // S stride (doubles): == 4 (mod 16) -> conflict-free DMMA fragments
 constexpr int kBS = 36;   // 32x32 block stride
-constexpr int kLeafSmem = (kNB * kLS + 4 * 32 * kBS + 3 * 32 * kBS) * 8 + 32;
+constexpr int kLeafSmem = (kNB * kLS + 4 * 32 * kBS + 3 * 32 * kBS) * 8 + (1 + 32 + 4) * 8 + 16;
 
 // Register-blocked variants (one A fragment feeds several DMMAs: half the LDS traffic,
 // which otherwise co-limits with the single SM's DMMA rate):
@@ -282,8 +284,11 @@ __device__ __forceinline__ void mma_row4_rn(double (&acc)[4][2], const double* A
 // of two SHFL.IDX per double.  Lane j+1 updates its own next pivot at once (its
 // a[j+1] -= l*l is exactly the general update with l_k = its own l) and publishes it
 // with the column, so the pivot chain is LDS -> rsqrt -> multiply -> STS -> syncwarp;
-// the buffers alternate so one __syncwarp per column suffices.
-__device__ __noinline__ int warp_potrf32(double* Sd, double* col, int lane) {
+// the buffers alternate so one __syncwarp per column suffices.  With `pub`, each
+// column (l values, pivot at [32]) is also copied to its own 40-double slot and
+// lane 0 arrives on cbar[j]: the warps factoring the rows below the block
+// (warp_tall32) consume the slots without ever holding this warp up.
+__device__ __noinline__ int warp_potrf32(double* Sd, double* col, double* pub, uint64_t* cbar, int lane) {
   double a[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = Sd[lane * kLS + c];
@@ -302,6 +307,10 @@ __device__ __noinline__ int warp_potrf32(double* Sd, double* col, int lane) {
     const double dj = piv * rj;
     const double l = a[j] * rj;
     a[j] = lane == j ? dj : (lane > j ? l : 0.0);
+    if (pub) {
+      pub[j * 40 + lane] = l;
+      if (lane == 0) pub[j * 40 + 32] = piv;
+    }
     if (j + 1 < 32) {
       if (lane == j + 1) {
         a[j + 1] = a[j + 1] - l * l;
@@ -309,6 +318,7 @@ __device__ __noinline__ int warp_potrf32(double* Sd, double* col, int lane) {
       }
       nxt[lane] = l;
       __syncwarp();
+      if (pub && lane == 0) mbar_arrive_nomem(&cbar[j]);
       // rows k > j: a[k] -= l_i * l_k for k <= i (lane j+1's own diagonal already done)
 #pragma unroll
       for (int k = (j + 1) & ~1; k < 32; k += 2) {
@@ -316,6 +326,9 @@ __device__ __noinline__ int warp_potrf32(double* Sd, double* col, int lane) {
         if (k > j) a[k] = (lane >= k && !(k == j + 1 && lane == j + 1)) ? a[k] - l * lk.x : a[k];
         if (k + 1 > j) a[k + 1] = lane >= k + 1 ? a[k + 1] - l * lk.y : a[k + 1];
       }
+    } else if (pub) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive_nomem(&cbar[j]);
     }
   }
   if (bad < 0) {
@@ -323,6 +336,33 @@ __device__ __noinline__ int warp_potrf32(double* Sd, double* col, int lane) {
     for (int c = 0; c < 32; ++c) Sd[lane * kLS + c] = c <= lane ? a[c] : 0.0;
   }
   return bad;
+}
+
+// The rows below the diagonal block, factored along with it (the panel TRSM of the
+// reference's column loop, solver.cpp:21-33, on rows > the block): lane i owns one
+// row's 32 panel entries at P; per column j, after warp_potrf32's arrival on cbar[j],
+// l_i = a_ij * rsqrt(pivot_j) and a_ik -= l_i * l_kj for k > j.  The rsqrt repeats the
+// diagonal warp's (same bits; its failed pivots are already replaced by 1).
+__device__ __noinline__ void warp_tall32(double* P, const double* pub, uint64_t* cbar, uint32_t parity) {
+  double a[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) a[c] = P[c];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    mbar_wait(&cbar[j], parity);
+    const double* cj = pub + j * 40;
+    const double rj = rsqrt(cj[32]);
+    const double l = a[j] * rj;
+    a[j] = l;
+#pragma unroll
+    for (int k = (j + 1) & ~1; k < 32; k += 2) {
+      const double2 lk = *reinterpret_cast<const double2*>(cj + k);
+      if (k > j) a[k] -= l * lk.x;
+      if (k + 1 > j) a[k + 1] -= l * lk.y;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 32; c += 2) *reinterpret_cast<double2*>(P + c) = make_double2(a[c], a[c + 1]);
 }
 
 // inverse of the lower 32x32 block at Sd into Db (row-major, stride kBS);
@@ -350,8 +390,13 @@ __device__ __noinline__ void warp_trtri32(const double* Sd, double* Db, int lane
 
 #ifdef PKRR_LEAF_TRACE
 __device__ long long g_leaf_trace[64];
-#define LEAF_MARK(i) \
-  if (threadIdx.x == 0) g_leaf_trace[i] = clock64();
+// the __syncwarp keeps warp 0 converged (a lone-lane store left unreconverged would
+// send every later __syncwarp / shuffle of the warp down its divergent path)
+#define LEAF_MARK(i)                                   \
+  {                                                    \
+    if (threadIdx.x == 0) g_leaf_trace[i] = clock64(); \
+    __syncwarp();                                      \
+  }
 #else
 #define LEAF_MARK(i)
 #endif
@@ -365,7 +410,9 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
   double* D = S + kNB * kLS;             // 4 x [32][36]: inv(L_bb)
   double* Tt = D + 4 * 32 * kBS;         // 3 x [32][36]: temporaries (transposed)
   uint64_t* lbar = reinterpret_cast<uint64_t*>(Tt + 3 * 32 * kBS);
-  int* flag = reinterpret_cast<int*>(lbar + 1);
+  uint64_t* cbar = lbar + 1;  // [32] column j of the current panel published (warp_potrf32)
+  uint64_t* dbar = cbar + 32; // [4] diagonal block pb factored
+  int* flag = reinterpret_cast<int*>(dbar + 4);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int lr = lane >> 2, lk = lane & 3;
   const int64_t base = static_cast<int64_t>(kb) * kNB;
@@ -375,6 +422,8 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
   if (tid == 0) {
     *flag = 0;
     mbar_init(lbar, 1);
+    for (int j = 0; j < 32; ++j) mbar_init(&cbar[j], 1);
+    for (int j = 0; j < 4; ++j) mbar_init(&dbar[j], 1);
     fence_mbar_init();
     mbar_arrive_expect_tx(lbar, kNB * kNB * 8);
     for (int r = 0; r < kNB; ++r) bulk_load(S + r * kLS, Ab + static_cast<int64_t>(r) * lda, kNB * 8, lbar);
@@ -384,95 +433,94 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
   mbar_wait(lbar, 0);
   LEAF_MARK(1);
 
-  for (int pb = 0; pb < 4; ++pb) {
-    double* Sd = S + (32 * pb) * kLS + 32 * pb;
-    LEAF_MARK(2 + 5 * pb);
-    if (factor && warp == 0) {
-      // ---- warp Cholesky of the 32x32 diagonal block: lane i owns row i ----
-      const int bad = warp_potrf32(Sd, Tt, lane);  // Tt is free until the blocked inverse
-      const bool ok = bad < 0;
-      if (!ok && lane == 0) {
-        *flag = 1;
-        if (status) {
-          status[1] = static_cast<int>(base + 32 * pb + bad);
-          __threadfence();
-          atomicExch(&status[0], 1);
+  if (!factor) {
+    // diagonal-block inverses of a finished factor (launch_diag_inverses)
+    if (warp < 4) warp_trtri32(S + (32 * warp) * kLS + 32 * warp, D + warp * 32 * kBS, lane);
+    __syncthreads();
+  } else if (warp == 7) {
+    // ---- warp 7: the 32x32 diagonal-block inverses, each as soon as its block is
+    // factored, off the panel chain (they feed only the blocked inverse below) ----
+    for (int pb = 0; pb < 4; ++pb) {
+      mbar_wait(&dbar[pb], 0);
+      if (*reinterpret_cast<volatile int*>(flag)) return;
+      warp_trtri32(S + (32 * pb) * kLS + 32 * pb, D + pb * 32 * kBS, lane);
+    }
+    __syncthreads();
+  } else {
+    // ---- warps 0-6: four 32-column panels.  Warp 0 factors the diagonal block,
+    // warps 1..3-pb the rows below it in step (one column behind at most), then the
+    // trailing SYRK inside the block; barriers among these 7 warps only ----
+    for (int pb = 0; pb < 4; ++pb) {
+      double* Sd = S + (32 * pb) * kLS + 32 * pb;
+      const int R0 = 32 * (pb + 1);
+      LEAF_MARK(2 + 5 * pb);
+      if (warp == 0) {
+        // Tt is free until the blocked inverse: two column buffers, then 32 published slots
+        const int bad = warp_potrf32(Sd, Tt, pb < 3 ? Tt + 80 : nullptr, cbar, lane);
+#ifdef PKRR_LEAF_TRACE
+        if (lane == 0) g_leaf_trace[40 + pb] = clock64();
+        __syncwarp();
+#endif
+        if (bad >= 0 && lane == 0) {
+          *flag = 1;
+          if (status) {
+            status[1] = static_cast<int>(base + 32 * pb + bad);
+            __threadfence();
+            atomicExch(&status[0], 1);
+          }
         }
+        __threadfence_block();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dbar[pb]);
+      } else if (warp < 4 - pb) {
+        warp_tall32(S + (R0 + 32 * (warp - 1) + lane) * kLS + 32 * pb, Tt + 80, cbar, static_cast<uint32_t>(pb & 1));
+#ifdef PKRR_LEAF_TRACE
+        if (lane == 0) g_leaf_trace[44 + 4 * pb + warp] = clock64();
+        __syncwarp();
+#endif
       }
-    }
-    __syncthreads();
-    LEAF_MARK(3 + 5 * pb);
-    if (*flag) return;
-    if (warp == 0 || !factor) {
-      if (warp == (factor ? 0 : pb % 8)) {
-        // ---- warp inverse of the 32x32 lower block: lane c computes column c ----
-        warp_trtri32(Sd, D + pb * 32 * kBS, lane);
+      consumer_sync(7 * 32);
+      LEAF_MARK(3 + 5 * pb);
+      if (*flag) return;
+      if (pb == 3) break;
+      // ---- trailing SYRK inside the block: S[R0:, R0:] -= P P^T over lower 16x16
+      // blocks (2x2 DMMA tiles each; the upper tile of a diagonal block is not stored) ----
+      const int nbt = (kNB - R0) / 16, nbl = nbt * (nbt + 1) / 2;
+      for (int t = warp; t < nbl; t += 7) {
+        int rb = 0;
+        while ((rb + 1) * (rb + 2) / 2 <= t) ++rb;
+        const int cb = t - rb * (rb + 1) / 2;
+        double acc[2][2][2] = {};
+        mma_2x2_rt(acc, S + (R0 + 16 * rb) * kLS + 32 * pb, S + (R0 + 16 * cb) * kLS + 32 * pb, kLS, 32, lr, lk);
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            if (rb == cb && j > i) continue;
+            double* dst = S + (R0 + 16 * rb + 8 * i + lr) * kLS + R0 + 16 * cb + 8 * j + 2 * lk;
+            const double2 v = *reinterpret_cast<double2*>(dst);
+            *reinterpret_cast<double2*>(dst) = make_double2(v.x - acc[i][j][0], v.y - acc[i][j][1]);
+          }
       }
+      consumer_sync(7 * 32);
+      LEAF_MARK(4 + 5 * pb);
     }
-    __syncthreads();
-    LEAF_MARK(4 + 5 * pb);
-    if (!factor || pb == 3) continue;
-    // ---- panel TRSM: P = A[R0:128, 32pb:+32] * D_pb^T (in place after a barrier);
-    // warp w: row tiles w and w + 8, each against the 4 column tiles ----
-    const int R0 = 32 * (pb + 1), nrt = (kNB - R0) / 8;
-    const double* Db = D + pb * 32 * kBS;
-    double res[2][4][2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) res[q][c][0] = res[q][c][1] = 0.0;
-      const int rt = warp + 8 * q;
-      if (rt < nrt) mma_row4_rt(res[q], S + (R0 + 8 * rt) * kLS + 32 * pb, kLS, Db, kBS, 0, 32, lr, lk);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int rt = warp + 8 * q;
-      if (rt < nrt) {
-        double* dst = S + (R0 + 8 * rt + lr) * kLS + 32 * pb + 2 * lk;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) *reinterpret_cast<double2*>(dst + 8 * c) = make_double2(res[q][c][0], res[q][c][1]);
-      }
-    }
-    __syncthreads();
-    LEAF_MARK(5 + 5 * pb);
-    // ---- trailing SYRK inside the block: S[R0:, R0:] -= P P^T over lower 16x16
-    // blocks (2x2 DMMA tiles each; the upper tile of a diagonal block is not stored) ----
-    const int nbt = nrt / 2, nbl = nbt * (nbt + 1) / 2;
-    for (int t = warp; t < nbl; t += 8) {
-      int rb = 0;
-      while ((rb + 1) * (rb + 2) / 2 <= t) ++rb;
-      const int cb = t - rb * (rb + 1) / 2;
-      double acc[2][2][2] = {};
-      mma_2x2_rt(acc, S + (R0 + 16 * rb) * kLS + 32 * pb, S + (R0 + 16 * cb) * kLS + 32 * pb, kLS, 32, lr, lk);
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          if (rb == cb && j > i) continue;
-          double* dst = S + (R0 + 16 * rb + 8 * i + lr) * kLS + R0 + 16 * cb + 8 * j + 2 * lk;
-          const double2 v = *reinterpret_cast<double2*>(dst);
-          *reinterpret_cast<double2*>(dst) = make_double2(v.x - acc[i][j][0], v.y - acc[i][j][1]);
-        }
-    }
-    __syncthreads();
-  }
-
-  LEAF_MARK(22);
-  // L is final: its rows (lower part, 16-byte rounded -- the one extra column is a
-  // zero of a diagonal 32-block) go out with plain vector stores from all warps before
-  // the blocked inverse, which only writes S's upper 32-blocks, beyond every stored row
-  // (fire-and-forget STG.128 drain while the DMMAs run; the bulk-copy engine is slow
-  // for hundreds of small copies)
-  if (factor) {
-    for (int e = tid; e < kNB * 64; e += kLeafThreads) {
+    // L is final: its rows (lower part, 16-byte rounded -- the one extra column is a
+    // zero of a diagonal 32-block) go out with plain vector stores while warp 7
+    // finishes the last diagonal inverse; the blocked inverse below only writes S's
+    // upper 32-blocks, beyond every stored row (fire-and-forget STG.128 drain while
+    // the DMMAs run; the bulk-copy engine is slow for hundreds of small copies)
+    for (int e = tid; e < kNB * 64; e += 7 * 32) {
       const int r = e >> 6, cp = e & 63;
       if (2 * cp <= r)
         *reinterpret_cast<double2*>(Ab + static_cast<int64_t>(r) * lda + 2 * cp) =
             *reinterpret_cast<const double2*>(S + r * kLS + 2 * cp);
     }
+    LEAF_MARK(21);
+    __syncthreads();
   }
-  LEAF_MARK(21);
+
+  LEAF_MARK(22);
   // ---- blocked inverse: X_ij = -D_i * sum_{k=j}^{i-1} L_ik X_kj, X_ij stored (not
   // transposed) in S's free upper block (j, i); T_j row-major in Tt[j].  Work item =
   // one 8-row tile x the 4 column tiles (the A fragment is loaded once per k step);

@@ -34,4 +34,9 @@ int main() {
                          "p2", "potrf2", "trtri2", "trsm2", "p3", "potrf3", "trtri3", "trsm3"};
   for (int i = 1; i <= 24; ++i) printf("%2d %8lld\n", i, tr[i] - tr[i - 1]);
   printf("total %lld cycles\n", tr[24] - tr[0]);
+  for (int pb = 0; pb < 4; ++pb) {
+    printf("panel %d: diag warp %lld", pb, tr[40 + pb] - tr[2 + 5 * pb]);
+    for (int w = 1; w < 4 - pb; ++w) printf("  tall warp %d %lld", w, tr[44 + 4 * pb + w] - tr[2 + 5 * pb]);
+    printf("  all %lld\n", tr[3 + 5 * pb] - tr[2 + 5 * pb]);
+  }
 }
