@@ -719,6 +719,10 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
     shadow_diff(Linv, sh.Linv, mp * kNB, s, tag + " Linv");
   };
   const int nb = static_cast<int>(mp / kNB);
+  // leaf block of the recursive group blocking (panels whose column updates run as
+  // column GEMMs; larger spans go through the SYRK kernel); PKRR_LEAF_BLOCK=2|8 measured
+  // within 0.5% of 4 on C1 / C2
+  static const int kLB = std::getenv("PKRR_LEAF_BLOCK") ? std::atoi(std::getenv("PKRR_LEAF_BLOCK")) : 4;
   // panels per trailing update: K = 512 for the int8 update and small systems (short
   // panel chains), K = 1024 from m >= 8192, K = 2048 from m >= 16384 (fewer passes over
   // the trailing matrix; the recursive blocking below keeps the intra-group work in
@@ -783,8 +787,8 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
     // the SYRK kernel.
     for (int kb = kb0; kb < kend; ++kb) {
       const int off = kb - kb0;
-      const int sub0 = kb0 + (off / 4) * 4;  // first panel of this block's leaf block
-      for (int S = 4; S < G; S *= 2) {
+      const int sub0 = kb0 + (off / kLB) * kLB;  // first panel of this block's leaf block
+      for (int S = kLB; S < G; S *= 2) {
         if (off % (2 * S) != S) continue;
         cur = kb;
         step("half-update", [&](FactorBufs& f) {

@@ -90,3 +90,14 @@ def test_lookahead_is_bitwise_neutral():
     assert la[0]["pred"] == la[1]["pred"] == no[0]["pred"]
     assert la[0]["mse"] == no[0]["mse"]
     assert la[0]["res"] == no[0]["res"]
+
+
+def test_lookahead_is_bitwise_neutral_lone_system():
+    """A system factorised alone (m < 8192: single-panel groups, the trailing update
+    split three ways over two streams) gives bitwise the single-stream result."""
+    la, _ = _run({}, 4096, 1, reps=2)
+    no, _ = _run({"PKRR_LOOKAHEAD": "0"}, 4096, 1, reps=1)
+    assert la[0]["pred"] == la[1]["pred"] == no[0]["pred"]
+    assert la[0]["mse"] == no[0]["mse"]
+    assert la[0]["res"] == no[0]["res"]
+    assert max(la[0]["res"]) <= 1e-8
