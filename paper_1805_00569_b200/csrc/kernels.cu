@@ -319,12 +319,16 @@ __device__ __noinline__ int warp_potrf32(double* Sd, double* col, double* pub, u
       nxt[lane] = l;
       __syncwarp();
       if (pub && lane == 0) mbar_arrive_nomem(&cbar[j]);
-      // rows k > j: a[k] -= l_i * l_k for k <= i (lane j+1's own diagonal already done)
+      // rows k > j: a[k] -= l_i * l_k (lane j+1's own diagonal already done).  Applied
+      // to every lane: entries above a lane's diagonal (k > i) only collect values that
+      // are never read (a later column zeroes them, the final store drops them), and
+      // the valid entries combine valid values only -- no per-entry selects, about a
+      // third of the code (the leaf is instruction-fetch bound when its SM is cold).
 #pragma unroll
       for (int k = (j + 1) & ~1; k < 32; k += 2) {
         const double2 lk = *reinterpret_cast<const double2*>(nxt + k);
-        if (k > j) a[k] = (lane >= k && !(k == j + 1 && lane == j + 1)) ? a[k] - l * lk.x : a[k];
-        if (k + 1 > j) a[k + 1] = lane >= k + 1 ? a[k + 1] - l * lk.y : a[k + 1];
+        if (k > j) a[k] = (k == j + 1 && lane == j + 1) ? a[k] : a[k] - l * lk.x;
+        if (k + 1 > j) a[k + 1] -= l * lk.y;
       }
     } else if (pub) {
       __syncwarp();
