@@ -356,6 +356,8 @@ void kmeans_device(pkrrgpu_ctx* ctx, Scope& sc, const double* dX, int64_t n, int
   unsigned long long* changed = sc.alloc<unsigned long long>(2);
   unsigned long long* far = sc.alloc<unsigned long long>(2);
   std::vector<int64_t> sz(k);
+  cudaEvent_t ev_sizes;
+  ck(cudaEventCreateWithFlags(&ev_sizes, cudaEventDisableTiming), "event");
   int iter = 0;
   for (; iter < max_iters; ++iter) {
     pk::launch_row_norms(co.centers, k, d, d, cnorm, s, ctx->counter);
@@ -363,14 +365,19 @@ void kmeans_device(pkrrgpu_ctx* ctx, Scope& sc, const double* dX, int64_t n, int
     pk::launch_assign(dX, n, d, xnorm, co.centers, cnorm, k, 0, nullptr, 0, co.label, best, changed, s,
                       ctx->counter);
     group_labels(ctx, sc, co.label, n, k, co, s);
-    // one round trip per iteration: sizes and the changed count together
+    // one round trip per iteration: sizes and the changed count together.  The centroid
+    // update is enqueued before the host looks at them (speculatively: it only has to
+    // be redone when a cluster is empty and gets reseeded below), so the host decision
+    // overlaps the update instead of idling the GPU
     {
       auto* pin = static_cast<unsigned char*>(ctx->pinned);
       ck(cudaMemcpyAsync(pin, co.sizes, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s), "D2H");
       ck(cudaMemcpyAsync(pin + sizeof(int64_t) * k, changed, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                          s),
          "D2H");
-      ck(cudaStreamSynchronize(s), "sync");
+      ck(cudaEventRecord(ev_sizes, s), "event");
+      pk::launch_means(dX, d, co.members, co.start, co.sizes, k, co.centers, s, ctx->counter);
+      ck(cudaEventSynchronize(ev_sizes), "sync");
       std::memcpy(sz.data(), pin, sizeof(int64_t) * k);
     }
     unsigned long long ch = 0;
@@ -394,13 +401,16 @@ void kmeans_device(pkrrgpu_ctx* ctx, Scope& sc, const double* dX, int64_t n, int
       ++ch;
       reseeded = true;
     }
-    if (reseeded) group_labels(ctx, sc, co.label, n, k, co, s);
-    pk::launch_means(dX, d, co.members, co.start, co.sizes, k, co.centers, s, ctx->counter);
+    if (reseeded) {  // the speculative update saw an empty cluster: regroup and redo it
+      group_labels(ctx, sc, co.label, n, k, co, s);
+      pk::launch_means(dX, d, co.members, co.start, co.sizes, k, co.centers, s, ctx->counter);
+    }
     if (static_cast<double>(ch) / static_cast<double>(n) <= threshold) {
       ++iter;
       break;
     }
   }
+  cudaEventDestroy(ev_sizes);
   co.iterations = iter;
   co.h_sizes = to_host(co.sizes, k, s);
   co.h_start = to_host(co.start, k, s);
