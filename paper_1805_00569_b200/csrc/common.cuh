@@ -175,6 +175,12 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uin
                "r"(smem_u32(smem_src)), "r"(bytes)
                : "memory");
 }
+// Programmatic dependent launch: a kernel launched with programmatic stream
+// serialization may start while its predecessor in the stream drains; it must not
+// touch memory the predecessor writes or reads before this wait (a no-op for a
+// normally launched kernel).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }

@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(gemm_threads<MODE>(), gemm_min_blocks<BM, MODE
   constexpr bool kWG = MODE == G_GRAM_SYM;             // warpgroup-specialised layout
   constexpr int kProducerWarp = kWG ? 0 : kConsumerWarps;
   constexpr int kFirstConsumer = kWG ? 4 : 0;
+  pdl_wait();
   if (p.abort_flag && *reinterpret_cast<const volatile int*>(p.abort_flag)) return;
 
   extern __shared__ unsigned char smem_raw[];

@@ -138,6 +138,27 @@ void launch_gather_vec(const double* y, const int64_t* idx, int64_t cnt, double*
 // ---------------------------------------------------------------------------
 // DMMA GEMM launches
 // ---------------------------------------------------------------------------
+// Launch with programmatic stream serialization: the kernel's CTAs may be scheduled
+// while the previous kernel in the stream drains (every kernel of the factorisation
+// chain starts with pdl_wait), trimming the launch gap between dependent panel steps.
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  static const bool off = std::getenv("PKRR_PDL") && std::atoi(std::getenv("PKRR_PDL")) == 0;
+  cfg.numAttrs = off ? 0 : 1;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 template <int BM, int MODE>
 static void gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p,
                         int blocks, cudaStream_t s, Counter& c) {
@@ -148,7 +169,7 @@ static void gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const GemmPa
                          GemmCfg<BM>::SMEM);
     attr_set = true;
   }
-  dgemm_tn_kernel<BM, MODE><<<blocks, gemm_threads<MODE>(), GemmCfg<BM>::SMEM, s>>>(a, b, p);
+  launch_pdl(dgemm_tn_kernel<BM, MODE>, blocks, gemm_threads<MODE>(), GemmCfg<BM>::SMEM, s, a, b, p);
   ++c.launches;
 }
 
@@ -408,6 +429,7 @@ __device__ long long g_leaf_trace[64];
 __global__ void __launch_bounds__(kLeafThreads, 1)
     potrf_leaf_kernel(double* __restrict__ A, int64_t lda, int kb, double* __restrict__ Linv,
                       int* status, int64_t m_valid, int factor) {
+  pdl_wait();
   if (status && *reinterpret_cast<volatile int*>(status)) return;
   extern __shared__ double sm[];
   double* S = sm;                        // [128][132]: L (lower), X_ij^T in the upper blocks
@@ -832,7 +854,7 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
       }
       cur = kb;
       step("leaf", [&](FactorBufs& f) {
-        potrf_leaf_kernel<<<1, kLeafThreads, kLeafSmem, s>>>(f.A, mp, kb, f.Linv, f.status, m_valid, 1);
+        launch_pdl(potrf_leaf_kernel, 1, kLeafThreads, kLeafSmem, s, f.A, mp, kb, f.Linv, f.status, m_valid, 1);
         ++c.launches;
       });
       const int rem = nb - 1 - kb;

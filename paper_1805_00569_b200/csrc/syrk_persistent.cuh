@@ -38,6 +38,7 @@ __device__ __forceinline__ uint32_t c_off(int r, int c) {
 
 __global__ void __launch_bounds__(kSyrkThreads, 1)
     dsyrk_persistent_kernel(const __grid_constant__ CUtensorMap tmA, SyrkParams p) {
+  pdl_wait();
   if (p.abort_flag && *reinterpret_cast<const volatile int*>(p.abort_flag)) return;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
