@@ -1635,6 +1635,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   if (no_look) std::fill(look_streams.begin(), look_streams.end(), nullptr);
   std::vector<size_t> sidx(p, 0);
   for (int64_t q : owned) sidx[q] = rank_of[slot[q]];
+  std::vector<cudaEvent_t> res_done(p, nullptr);  // residual GEMV of the part's last cell done
   // ---- memory-aware batches of parts (largest first) ----
   auto part_bytes = [&](int64_t q) {
     const int64_t mp = round_up(po.sizes[q], kNB);
@@ -1718,6 +1719,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
         PartBuf& pb = parts[q];
         cudaStream_t ws = streams[sidx[q]];
         const double m = static_cast<double>(pb.m);
+        if (res_done[q]) ck(cudaStreamWaitEvent(ws, res_done[q], 0), "wait");  // K is rewritten
         cudaEvent_t g0 = ev_on(ws);
         pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws, ctx->counter,
                             false);
@@ -1743,9 +1745,15 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
           chol_iv.push_back({c0, c1});
           if (li == 0 && si == 0) part_end[q] = c1, part_ev[q][2] = c0, part_ev[q][3] = c1;
           f_chol += chol_flops(pb.m);
+          if (res_done[q]) ck(cudaStreamWaitEvent(ws, res_done[q], 0), "wait");  // alpha is rewritten
           pk::launch_trsv(pb.A, pb.Linv, pb.mp, pb.yp, pb.z, pb.alpha, pb.scratch, st, ws, ctx->counter);
-          pk::launch_symv_lower(pb.K, pb.mp, pb.alpha, pb.Ka, st, ws, ctx->counter);
-          pk::launch_residual_finish(pb.Ka, pb.alpha, pb.yp, pb.m, shift, rs, st, ws, ctx->counter);
+          // the residual GEMV (strategies.cpp:310-320) only feeds the reported residual:
+          // on the part's idle lookahead stream, overlapping the predictions
+          cudaStream_t rst = look_streams[sidx[q]] ? look_streams[sidx[q]] : ws;
+          if (rst != ws) ck(cudaStreamWaitEvent(rst, ev_on(ws), 0), "wait");
+          pk::launch_symv_lower(pb.K, pb.mp, pb.alpha, pb.Ka, st, rst, ctx->counter);
+          pk::launch_residual_finish(pb.Ka, pb.alpha, pb.yp, pb.m, shift, rs, st, rst, ctx->counter);
+          if (rst != ws) res_done[q] = ev_on(rst);
           f_other += 4.0 * m * m;
           if (tcount[q] > 0) {
             pk::launch_predict_fused(qt[q].tmQ, pb.tmX, qt[q].norms, pb.norms, qt[q].qp, tcount[q], pb.mp, pb.m,
@@ -1769,6 +1777,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
     for (int64_t q : batch) {
       cudaEvent_t e = ev_on(streams[sidx[q]]);
       ck(cudaStreamWaitEvent(s, e, 0), "wait");
+      if (res_done[q]) ck(cudaStreamWaitEvent(s, res_done[q], 0), "wait");
     }
     hmark("batch enqueued");
   }
