@@ -257,6 +257,7 @@ struct PartBuf {
   double* A = nullptr;      // mp x mp (factor)
   double* Linv = nullptr;   // mp x 128
   double* z = nullptr;
+  double* w = nullptr;      // fused forward-substitution accumulator (mp)
   double* alpha = nullptr;
   double* Ka = nullptr;
   int* scratch = nullptr;   // trsv tickets/flags
@@ -276,6 +277,7 @@ void part_alloc(Scope& sc, PartBuf& pb, int64_t m, int64_t d, bool need_K, cudaS
   pb.A = sc.alloc<double>(pb.mp * pb.mp);
   pb.Linv = sc.zeros<double>(pb.mp * kNB, s);  // upper 32x32 blocks stay zero (the leaf writes lower)
   pb.z = sc.alloc<double>(pb.mp);
+  pb.w = sc.alloc<double>(pb.mp);
   pb.alpha = sc.alloc<double>(pb.mp);
   pb.Ka = sc.alloc<double>(pb.mp);
   pb.scratch = sc.alloc<int>(2 * (pb.mp / kNB) + 2);
@@ -582,9 +584,12 @@ void part_solve(pkrrgpu_ctx* ctx, PartBuf& pb, double lambda, int* status, doubl
                 cudaStream_t s, cudaStream_t s2, bool alone) {
   const double shift = lambda * static_cast<double>(pb.m);
   pk::launch_assemble(pb.K, pb.A, pb.mp, shift, status, s, ctx->counter, /*lower_only=*/true);
-  pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, status, s, ctx->counter, pb.slices, pb.exps,
-                   s2, alone);
-  pk::launch_trsv(pb.A, pb.Linv, pb.mp, pb.yp, pb.z, pb.alpha, pb.scratch, status, s, ctx->counter);
+  const pk::FwdSolve fs{pb.yp, pb.w, pb.z};
+  if (pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, status, s, ctx->counter, pb.slices,
+                       pb.exps, s2, alone, &fs))
+    pk::launch_trsv_bwd(pb.A, pb.Linv, pb.mp, pb.z, pb.alpha, pb.scratch, status, s, ctx->counter);
+  else
+    pk::launch_trsv(pb.A, pb.Linv, pb.mp, pb.yp, pb.z, pb.alpha, pb.scratch, status, s, ctx->counter);
   if (res_out) {
     pk::launch_symv_lower(pb.K, pb.mp, pb.alpha, pb.Ka, status, s, ctx->counter);
     pk::launch_residual_finish(pb.Ka, pb.alpha, pb.yp, pb.m, shift, res_out, status, s, ctx->counter);
@@ -1739,14 +1744,19 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
           double* rs = dres + (cell * p + q) * 4;
           cudaEvent_t c0 = ev_on(ws);
           pk::launch_assemble(pb.K, pb.A, pb.mp, shift, st, ws, ctx->counter, true);
-          pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, st, ws, ctx->counter, pb.slices, pb.exps,
-                           look_streams[sidx[q]], p == 1);  // rank-independent: the same schedule at any world size
+          const pk::FwdSolve fs{pb.yp, pb.w, pb.z};
+          // rank-independent schedule (p == 1): the same at any world size
+          const bool fused = pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, st, ws, ctx->counter,
+                                              pb.slices, pb.exps, look_streams[sidx[q]], p == 1, &fs);
           cudaEvent_t c1 = ev_on(ws);
           chol_iv.push_back({c0, c1});
           if (li == 0 && si == 0) part_end[q] = c1, part_ev[q][2] = c0, part_ev[q][3] = c1;
           f_chol += chol_flops(pb.m);
           if (res_done[q]) ck(cudaStreamWaitEvent(ws, res_done[q], 0), "wait");  // alpha is rewritten
-          pk::launch_trsv(pb.A, pb.Linv, pb.mp, pb.yp, pb.z, pb.alpha, pb.scratch, st, ws, ctx->counter);
+          if (fused)
+            pk::launch_trsv_bwd(pb.A, pb.Linv, pb.mp, pb.z, pb.alpha, pb.scratch, st, ws, ctx->counter);
+          else
+            pk::launch_trsv(pb.A, pb.Linv, pb.mp, pb.yp, pb.z, pb.alpha, pb.scratch, st, ws, ctx->counter);
           // the residual GEMV (strategies.cpp:310-320) only feeds the reported residual:
           // on the part's idle lookahead stream, overlapping the predictions
           cudaStream_t rst = look_streams[sidx[q]] ? look_streams[sidx[q]] : ws;

@@ -37,6 +37,10 @@ struct GemmParams {
   const int* abort_flag; // per-part NPD flag: skip work once a pivot failed
   int mirror;            // G_GRAM_SYM: 1 = also write the upper triangle (public gram API);
                          // 0 = lower tiles only (the pipeline's K: nothing reads the upper half)
+  // G_STORE (panel TRSM) with the forward substitution fused into the factorization:
+  // fw[row] -= (C row) . fz over the tile's 128 columns, rows indexed like C (null: off)
+  const double* fz;
+  double* fw;
 };
 
 constexpr int kBK = 16;        // f64 per k-tile row = 128 B (one swizzle row)
@@ -219,6 +223,36 @@ __global__ void __launch_bounds__(gemm_threads<MODE>(), gemm_min_blocks<BM, MODE
           *dst = make_double2(acc[i][j][0], acc[i][j][1]);
         }
       }
+    if constexpr (MODE == G_STORE) {
+      if (p.fz) {
+        // right-looking forward substitution step of this panel: w_r -= L21[r, :] . z_panel,
+        // per-thread partial over its columns, then the 4 lanes of a row, then the 4
+        // column warps in a fixed order (deterministic)
+        __shared__ double fred[4][BM];
+        double zc[Cfg::NT][2];
+#pragma unroll
+        for (int j = 0; j < Cfg::NT; ++j) {
+          zc[j][0] = p.fz[tn * kBN + c0 + j * 8];
+          zc[j][1] = p.fz[tn * kBN + c0 + j * 8 + 1];
+        }
+#pragma unroll
+        for (int i = 0; i < Cfg::MT; ++i) {
+          double part = 0.0;
+#pragma unroll
+          for (int j = 0; j < Cfg::NT; ++j) part = fma(acc[i][j][1], zc[j][1], fma(acc[i][j][0], zc[j][0], part));
+          part += __shfl_xor_sync(0xffffffffu, part, 1);
+          part += __shfl_xor_sync(0xffffffffu, part, 2);
+          if (lk == 0) fred[wn][r0 + i * 8] = part;
+        }
+        consumer_sync(kConsumerWarps * 32);
+        if (cwarp * 32 + lane < BM) {
+          const int r = cwarp * 32 + lane;
+          const double sum = (fred[0][r] + fred[1][r]) + (fred[2][r] + fred[3][r]);
+          double* w = p.fw + p.c_row0 + tm * BM + r;
+          *w -= sum;
+        }
+      }
+    }
   } else {
     // Gaussian kernel epilogue (kernel.cpp:52-56): dist2 = (n_a + n_b) - 2*dot,
     // clamp at 0, exp(-dist2 / ((2 s) s)).  Padding rows are identity (sym) / 0.

@@ -428,7 +428,8 @@ __device__ long long g_leaf_trace[64];
 
 __global__ void __launch_bounds__(kLeafThreads, 1)
     potrf_leaf_kernel(double* __restrict__ A, int64_t lda, int kb, double* __restrict__ Linv,
-                      int* status, int64_t m_valid, int factor) {
+                      int* status, int64_t m_valid, int factor, const double* __restrict__ fw = nullptr,
+                      double* __restrict__ fz = nullptr) {
   pdl_wait();
   if (status && *reinterpret_cast<volatile int*>(status)) return;
   extern __shared__ double sm[];
@@ -443,6 +444,8 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
   const int lr = lane >> 2, lk = lane & 3;
   const int64_t base = static_cast<int64_t>(kb) * kNB;
   double* Ab = A + base * lda + base;
+  __shared__ double wsm[kNB];  // fused forward substitution: w_kb, final at kernel start
+  if (fz && tid < kNB) wsm[tid] = fw[base + tid];
   // stage the 128 x 128 block: 128 row copies of 1 KB in flight at once (the
   // strict upper triangle is stale but never read as data)
   if (tid == 0) {
@@ -577,6 +580,27 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
   }
 
   LEAF_MARK(23);
+  if (fz) {
+    // fused forward substitution (see launch_potrf): z_kb = inv(L_kk) w_kb, w_kb being
+    // final (every earlier panel's TRSM has subtracted its part); row i of inv(L_kk):
+    // diagonal 32-block from D, the others from the X blocks in S's upper half
+    if (tid < kNB) {
+      const int bi = tid >> 5, r = tid & 31;
+      double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
+      for (int bj = 0; bj <= bi; ++bj) {
+        const double* src = bi == bj ? D + bi * 32 * kBS + r * kBS : S + (32 * bj + r) * kLS + 32 * bi;
+        const double* wk = wsm + 32 * bj;
+#pragma unroll
+        for (int c = 0; c < 32; c += 4) {
+          z0 = fma(src[c], wk[c], z0);
+          z1 = fma(src[c + 1], wk[c + 1], z1);
+          z2 = fma(src[c + 2], wk[c + 2], z2);
+          z3 = fma(src[c + 3], wk[c + 3], z3);
+        }
+      }
+      fz[base + tid] = (z0 + z1) + (z2 + z3);
+    }
+  }
   // the 10 lower 32x32 blocks of inv(L), 16 double2 per row segment (the upper blocks
   // of the Linv scratch are zeroed once at allocation)
   double* Lo = Linv + base * kNB;
@@ -702,9 +726,9 @@ struct FactorBufs {
 };
 }  // namespace
 
-void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, double* Linv,
+bool launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, double* Linv,
                   int64_t mp, int64_t m_valid, int* status, cudaStream_t s, Counter& c, int8_t* slices,
-                  int* exps, cudaStream_t s2, bool latency) {
+                  int* exps, cudaStream_t s2, bool latency, const FwdSolve* fs) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(potrf_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLeafSmem);
@@ -730,6 +754,9 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
     make_tmap(&sh.tmA, sh.A, mp, mp, mp);
     make_tmap(&sh.tmLinv, sh.Linv, mp, kNB, kNB);
   }
+  // fused forward substitution (not with the shadow checker: its steps run twice)
+  const bool fused = fs != nullptr && !shadow;
+  if (fused) cudaMemcpyAsync(fs->w, fs->y, sizeof(double) * mp, cudaMemcpyDeviceToDevice, s);
   int cur = 0;  // block index of the current step (shadow report tag)
   auto step = [&](const char* name, auto&& fn) {
     if (!shadow) {
@@ -854,7 +881,8 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
       }
       cur = kb;
       step("leaf", [&](FactorBufs& f) {
-        launch_pdl(potrf_leaf_kernel, 1, kLeafThreads, kLeafSmem, s, f.A, mp, kb, f.Linv, f.status, m_valid, 1);
+        launch_pdl(potrf_leaf_kernel, 1, kLeafThreads, kLeafSmem, s, f.A, mp, kb, f.Linv, f.status, m_valid, 1,
+                   fused ? static_cast<const double*>(fs->w) : nullptr, fused ? fs->z : nullptr);
         ++c.launches;
       });
       const int rem = nb - 1 - kb;
@@ -874,6 +902,8 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
         t.c_col0 = kb * kNB;
         t.tiles_n = 1;
         t.abort_flag = f.status;
+        t.fz = fused ? fs->z + static_cast<int64_t>(kb) * kNB : nullptr;
+        t.fw = fused ? fs->w : nullptr;
         if (narrow_rows) {
           t.tiles_m = rem * 4;
           gemm_launch<32, G_STORE>(f.tmA, f.tmLinv, t, rem * 4, s, c);
@@ -1043,6 +1073,7 @@ void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
     cudaFreeAsync(sh.Linv, s);
     if (sh.status) cudaFreeAsync(sh.status, s);
   }
+  return fused;
 }
 
 void launch_diag_inverses(const double* L, int64_t mp, double* Linv, cudaStream_t s, Counter& c) {
@@ -1231,6 +1262,14 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(const double* __restrict_
   __threadfence();
   __syncthreads();
   if (tid == 0) st_release(&flags[I], 1);
+}
+
+void launch_trsv_bwd(const double* L, const double* Linv, int64_t mp, const double* z, double* x,
+                     int* scratch, const int* abort, cudaStream_t s, Counter& c) {
+  const int nb = static_cast<int>(mp / kNB);
+  cudaMemsetAsync(scratch, 0, sizeof(int) * (2 * nb + 2), s);
+  trsv_bwd_kernel<<<nb, 256, 0, s>>>(L, mp, Linv, z, x, nb, scratch + 1, scratch + 2 + nb, abort);
+  ++c.launches;
 }
 
 void launch_trsv(const double* L, const double* Linv, int64_t mp, const double* b, double* z,

@@ -45,10 +45,19 @@ void launch_gram_cross(const CUtensorMap& tmQ, const CUtensorMap& tmX, const dou
 // status[0] = abort flag, status[1] = first failing global column (int).
 // slices/exps: int8 [8 x mp x 512] and int [mp] scratch for the Ozaki SYRK mode (may be null).
 void shadow_report();  // PKRR_SHADOW debug mode (see launch_potrf)
-void launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, double* Linv,
+// Forward substitution fused into the factorization: w (mp) := y, then each panel's
+// leaf sets z_k = inv(L_kk) w_k and its TRSM subtracts L21 z_k from w below it, so
+// z = L^{-1} y is complete with the factor (launch_trsv_bwd finishes the solve).
+struct FwdSolve {
+  const double* y;
+  double* w;
+  double* z;
+};
+// Returns true when the forward solve was fused (fs given and not in PKRR_SHADOW mode).
+bool launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, double* Linv,
                   int64_t mp, int64_t m_valid, int* status, cudaStream_t s, Counter& c,
                   int8_t* slices = nullptr, int* exps = nullptr, cudaStream_t s2 = nullptr,
-                  bool latency = false);
+                  bool latency = false, const FwdSolve* fs = nullptr);
 // s2 (optional): a second stream for lookahead -- the next panel's columns are
 // updated first on s and the rest of the trailing update runs on s2, overlapping the
 // next panel factorisation; the result is bitwise the same as without.
@@ -75,6 +84,9 @@ void launch_zero_upper(double* A, int64_t mp, cudaStream_t s, Counter& c);
 // scratch: 2*nb + 2 ints (tickets + flags), zeroed by the launcher
 void launch_trsv(const double* L, const double* Linv, int64_t mp, const double* b, double* z,
                  double* x, int* scratch, const int* abort, cudaStream_t s, Counter& c);
+// backward half only (z from a fused forward substitution)
+void launch_trsv_bwd(const double* L, const double* Linv, int64_t mp, const double* z, double* x,
+                     int* scratch, const int* abort, cudaStream_t s, Counter& c);
 
 // ---- assemble: A = K + shift * I (full copy) ------------------------------
 // y = K alpha from the lower 128x128 tiles of a symmetric K (mp x mp, ld = mp); deterministic
