@@ -279,7 +279,7 @@ void part_alloc(Scope& sc, PartBuf& pb, int64_t m, int64_t d, bool need_K, cudaS
   pb.z = sc.alloc<double>(pb.mp);
   pb.w = sc.alloc<double>(pb.mp);
   pb.alpha = sc.alloc<double>(pb.mp);
-  pb.Ka = sc.alloc<double>(pb.mp);
+  pb.Ka = sc.alloc<double>(pb.mp * pk::kSymvSplit);
   pb.scratch = sc.alloc<int>(2 * (pb.mp / kNB) + 2);
   if (pk::syrk_ozaki()) {
     pb.slices = sc.alloc<int8_t>(2 * 8 * pb.mp * 512);  // two buffers: lookahead alternates them

@@ -1319,12 +1319,16 @@ __global__ void __launch_bounds__(256) symv_lower_kernel(const double* __restric
   __shared__ double yrow[kNB];
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int I = blockIdx.x;
+  // this CTA's share of the tile range (blockIdx.y of kSymvSplit): a partial y_I
+  const int J0 = static_cast<int>(blockIdx.y) * nb / kSymvSplit;
+  const int J1 = (static_cast<int>(blockIdx.y) + 1) * nb / kSymvSplit;
+  y += static_cast<int64_t>(blockIdx.y) * nb * kNB;
   double ar[16];
 #pragma unroll
   for (int rr = 0; rr < 16; ++rr) ar[rr] = 0.0;
   double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
   const int64_t r0 = static_cast<int64_t>(I) * kNB + w * 16;
-  for (int J = 0; J < I; ++J) {  // row part: full tiles left of the diagonal
+  for (int J = J0; J < (I < J1 ? I : J1); ++J) {  // row part: full tiles left of the diagonal
     double4 m[16];
     load_block16(K + r0 * ld + J * kNB + lane * 4, ld, m);
     const double4 v = ldg_d4(alpha + J * kNB + lane * 4);
@@ -1332,7 +1336,7 @@ __global__ void __launch_bounds__(256) symv_lower_kernel(const double* __restric
     for (int rr = 0; rr < 16; ++rr)
       ar[rr] = fma(m[rr].w, v.w, fma(m[rr].z, v.z, fma(m[rr].y, v.y, fma(m[rr].x, v.x, ar[rr]))));
   }
-  {  // diagonal tile: element (r, c) with c <= r stands for itself and, if c < r, for (c, r)
+  if (I >= J0 && I < J1) {  // diagonal tile: (r, c) with c <= r stands for itself and, if c < r, for (c, r)
     double4 m[16];
     load_block16(K + r0 * ld + I * kNB + lane * 4, ld, m);
     const double4 v = ldg_d4(alpha + I * kNB + lane * 4);
@@ -1350,7 +1354,7 @@ __global__ void __launch_bounds__(256) symv_lower_kernel(const double* __restric
       c3 = fma(c + 3 < r ? m[rr].w : 0.0, xa, c3);
     }
   }
-  for (int J = I + 1; J < nb; ++J) {  // column part: tiles below the diagonal, transposed
+  for (int J = (I + 1 > J0 ? I + 1 : J0); J < J1; ++J) {  // column part: tiles below the diagonal, transposed
     double4 m[16];
     const int64_t rj = static_cast<int64_t>(J) * kNB + w * 16;
     load_block16(K + rj * ld + I * kNB + lane * 4, ld, m);
@@ -1381,8 +1385,8 @@ __global__ void __launch_bounds__(256) symv_lower_kernel(const double* __restric
 
 void launch_symv_lower(const double* K, int64_t mp, const double* alpha, double* y, const int* abort,
                        cudaStream_t s, Counter& c) {
-  symv_lower_kernel<<<static_cast<unsigned>(mp / kNB), 256, 0, s>>>(K, mp, static_cast<int>(mp / kNB), alpha, y,
-                                                                    abort);
+  const dim3 grid(static_cast<unsigned>(mp / kNB), kSymvSplit);
+  symv_lower_kernel<<<grid, 256, 0, s>>>(K, mp, static_cast<int>(mp / kNB), alpha, y, abort);
   ++c.launches;
 }
 
@@ -1427,13 +1431,16 @@ __device__ double block_sum_1024(double v, double* red) {
 __global__ void __launch_bounds__(1024) residual_finish_kernel(const double* __restrict__ Ka,
                                                                const double* __restrict__ alpha,
                                                                const double* __restrict__ y,
-                                                               int64_t m, double shift,
+                                                               int64_t m, int64_t mp, double shift,
                                                                double* out, const int* abort) {
   if (abort && *reinterpret_cast<const volatile int*>(abort)) return;
   __shared__ double red[32];
   double rs = 0.0, ys = 0.0;
   for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
-    const double acc = (shift * alpha[i] - y[i]) + Ka[i];
+    double ka = Ka[i];  // the symmetric GEMV's partial vectors, summed in a fixed order
+#pragma unroll
+    for (int q = 1; q < kSymvSplit; ++q) ka += Ka[q * mp + i];
+    const double acc = (shift * alpha[i] - y[i]) + ka;
     rs += acc * acc;
     ys += y[i] * y[i];
   }
@@ -1448,7 +1455,8 @@ __global__ void __launch_bounds__(1024) residual_finish_kernel(const double* __r
 void launch_residual_finish(const double* Kalpha, const double* alpha, const double* y, int64_t m,
                             double shift, double* out, const int* abort, cudaStream_t s,
                             Counter& c) {
-  residual_finish_kernel<<<1, 1024, 0, s>>>(Kalpha, alpha, y, m, shift, out, abort);
+  const int64_t mp = (m + kNB - 1) / kNB * kNB;
+  residual_finish_kernel<<<1, 1024, 0, s>>>(Kalpha, alpha, y, m, mp, shift, out, abort);
   ++c.launches;
 }
 

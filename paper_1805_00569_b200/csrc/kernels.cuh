@@ -89,7 +89,11 @@ void launch_trsv_bwd(const double* L, const double* Linv, int64_t mp, const doub
                      int* scratch, const int* abort, cudaStream_t s, Counter& c);
 
 // ---- assemble: A = K + shift * I (full copy) ------------------------------
-// y = K alpha from the lower 128x128 tiles of a symmetric K (mp x mp, ld = mp); deterministic
+// y = K alpha from the lower 128x128 tiles of a symmetric K (mp x mp, ld = mp); deterministic.
+// y holds kSymvSplit partial vectors of mp (tile ranges split over that many CTAs per
+// block row, so the latency-bound GEMV occupies its SMs a quarter as long);
+// launch_residual_finish sums them in a fixed order.
+constexpr int kSymvSplit = 4;
 void launch_symv_lower(const double* K, int64_t mp, const double* alpha, double* y, const int* abort,
                        cudaStream_t s, Counter& c);
 void launch_assemble(const double* K, double* A, int64_t mp, double shift, const int* abort,
