@@ -169,9 +169,11 @@ struct Scope {
   ~Scope() {
     cudaDeviceSynchronize();
     for (void* p : ptrs) ctx->release(p);
-    // bound the cache: a call that needed more than half of HBM (e.g. C4's 44 GB parts)
-    // returns it, so other processes on the device (or later large calls) can allocate
-    if (static_cast<double>(ctx->cached_bytes) > 0.5 * ctx->total_mem) ctx->trim();
+    // bound the cache: a call that needed nearly all of HBM returns it, so other users
+    // of the device can allocate; below that the blocks stay cached for the next call
+    // (C4 holds ~0.8 of HBM: trimming it made every call re-allocate ~150 GB, ~0.2-0.5 s).
+    // A later call that does not fit trims on cudaMalloc failure (pkrrgpu_ctx::alloc).
+    if (static_cast<double>(ctx->cached_bytes) > 0.9 * ctx->total_mem) ctx->trim();
   }
   template <typename T>
   T* alloc(int64_t count) {
