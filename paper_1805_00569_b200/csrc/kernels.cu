@@ -1543,8 +1543,10 @@ __global__ void __launch_bounds__(kAssignRows)
                   const double* __restrict__ cnorm, int k, int mode,
                   const uint8_t* __restrict__ open, int64_t row0, int32_t* label,
                   double* best_dist, unsigned long long* changed) {
-  __shared__ double xs[kAssignRows][kChunk + 1];
-  __shared__ double cs[KP][kChunk + 1];
+  // feature chunk staged per step: 16 for 64 centres (static shared memory <= 48 KB)
+  constexpr int CH = KP > 32 ? 16 : kChunk;
+  __shared__ double xs[kAssignRows][CH + 1];
+  __shared__ double cs[KP][CH + 1];
   const int64_t rbase = row0 + static_cast<int64_t>(blockIdx.x) * kAssignRows;
   const int64_t i = rbase + threadIdx.x;
   bool need = i < n;
@@ -1560,23 +1562,23 @@ __global__ void __launch_bounds__(kAssignRows)
     double dot[KP];
 #pragma unroll
     for (int q = 0; q < KP; ++q) dot[q] = 0.0;
-    for (int64_t c0 = 0; c0 < d; c0 += kChunk) {
-      const int cw = static_cast<int>(d - c0 < kChunk ? d - c0 : kChunk);
+    for (int64_t c0 = 0; c0 < d; c0 += CH) {
+      const int cw = static_cast<int>(d - c0 < CH ? d - c0 : CH);
       __syncthreads();
       {
         // all 32 staging loads of this thread in flight before the first store
-        double v[kChunk];
-        const int cc = threadIdx.x & (kChunk - 1), r0 = threadIdx.x / kChunk;
+        double v[CH];
+        const int cc = threadIdx.x & (CH - 1), r0 = threadIdx.x / CH;
 #pragma unroll
-        for (int u = 0; u < kChunk; ++u) {
-          const int64_t gr = rbase + r0 + u * (kAssignRows / kChunk);
+        for (int u = 0; u < CH; ++u) {
+          const int64_t gr = rbase + r0 + u * (kAssignRows / CH);
           v[u] = (gr < n && cc < cw) ? __ldg(X + gr * d + c0 + cc) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < kChunk; ++u) xs[r0 + u * (kAssignRows / kChunk)][cc] = v[u];
+        for (int u = 0; u < CH; ++u) xs[r0 + u * (kAssignRows / CH)][cc] = v[u];
       }
-      for (int e = threadIdx.x; e < KP * kChunk; e += kAssignRows) {
-        const int q = e / kChunk, cc = e % kChunk;
+      for (int e = threadIdx.x; e < KP * CH; e += kAssignRows) {
+        const int q = e / CH, cc = e % CH;
         cs[q][cc] = (jb + q < k && cc < cw) ? centers[static_cast<int64_t>(jb + q) * d + c0 + cc] : 0.0;
       }
       __syncthreads();
@@ -1634,8 +1636,11 @@ void launch_assign(const double* X, int64_t n, int64_t d, const double* xnorm,
   else if (k <= 16)
     assign_kernel<16><<<blocks, kAssignRows, 0, s>>>(X, n, d, xnorm, centers, cnorm, k, mode, open,
                                                     row0, label, best_dist, changed);
-  else
+  else if (k <= 32)
     assign_kernel<32><<<blocks, kAssignRows, 0, s>>>(X, n, d, xnorm, centers, cnorm, k, mode, open,
+                                                    row0, label, best_dist, changed);
+  else  // one pass over X for up to 64 centres (the weak-scaled partitions: k = 8 per GPU)
+    assign_kernel<64><<<blocks, kAssignRows, 0, s>>>(X, n, d, xnorm, centers, cnorm, k, mode, open,
                                                     row0, label, best_dist, changed);
   ++c.launches;
 }
@@ -1654,35 +1659,50 @@ __global__ void group_count_kernel(const int32_t* __restrict__ label, int64_t n,
   for (int j = threadIdx.x; j < k; j += blockDim.x) counts[static_cast<int64_t>(blockIdx.x) * k + j] = cnt_s[j];
 }
 
-__global__ void group_scan_kernel(int64_t* counts, int64_t nblk, int k, int64_t* sizes,
-                                  int64_t* start) {
-  // warp w: exclusive scan of counts[:, j] over blocks (in place), 32 blocks per step
-  __shared__ int64_t tot[1024];
+// CTA j: exclusive scan of counts[:, j] over the nblk row blocks (in place), total in
+// sizes[j] (one CTA per cluster: the scan is latency-bound, so spread it)
+__global__ void __launch_bounds__(1024) group_scan_kernel(int64_t* counts, int64_t nblk, int k,
+                                                          int64_t* sizes) {
+  __shared__ int64_t wsum[32];
+  const int j = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int j = warp; j < k; j += nw) {
-    int64_t run = 0;
-    for (int64_t b0 = 0; b0 < nblk; b0 += 32) {
-      const int64_t b = b0 + lane;
-      const int64_t v = b < nblk ? counts[b * k + j] : 0;
-      int64_t incl = v;
+  int64_t carry = 0;
+  for (int64_t b0 = 0; b0 < nblk; b0 += blockDim.x) {
+    const int64_t b = b0 + threadIdx.x;
+    const int64_t v = b < nblk ? counts[b * k + j] : 0;
+    int64_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int64_t w = lane < nw ? wsum[lane] : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
+        const int64_t t = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += t;
       }
-      if (b < nblk) counts[b * k + j] = run + incl - v;
-      run += __shfl_sync(0xffffffffu, incl, 31);
+      if (lane < nw) wsum[lane] = w;  // inclusive over warps
     }
-    if (lane == 0) tot[j] = run;
+    __syncthreads();
+    incl += warp > 0 ? wsum[warp - 1] : 0;
+    if (b < nblk) counts[b * k + j] = carry + incl - v;
+    carry += wsum[nw - 1];
+    __syncthreads();
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t run = 0;
-    for (int j = 0; j < k; ++j) {
-      sizes[j] = tot[j];
-      start[j] = run;
-      run += tot[j];
-    }
+  if (threadIdx.x == 0) sizes[j] = carry;
+}
+
+// start[j] = sum of sizes[0..j) (k is the cluster count: a short serial scan)
+__global__ void group_start_kernel(const int64_t* __restrict__ sizes, int k, int64_t* start) {
+  if (threadIdx.x != 0) return;
+  int64_t run = 0;
+  for (int j = 0; j < k; ++j) {
+    start[j] = run;
+    run += sizes[j];
   }
 }
 
@@ -1718,10 +1738,11 @@ void launch_group(const int32_t* label, int64_t n, int k, int64_t* sizes, int64_
   if (n <= 0) return;
   const int64_t nblk = (n + kGroupRows - 1) / kGroupRows;
   group_count_kernel<<<static_cast<unsigned>(nblk), kGroupRows, sizeof(int) * k, s>>>(label, n, k, tmp);
-  group_scan_kernel<<<1, 1024, 0, s>>>(tmp, nblk, k, sizes, start);
+  group_scan_kernel<<<static_cast<unsigned>(k), 1024, 0, s>>>(tmp, nblk, k, sizes);
+  group_start_kernel<<<1, 32, 0, s>>>(sizes, k, start);
   group_scatter_kernel<<<static_cast<unsigned>(nblk), kGroupRows, sizeof(int) * 8 * k, s>>>(
       label, n, k, tmp, start, members);
-  c.launches += 3;
+  c.launches += 4;
 }
 
 // clustering.cpp:34-49: zero, row-order sums, then * (1.0 / size).

@@ -153,7 +153,7 @@ def test_predict_fused_matches_oracle(engine, oracle, m, q, d, sigma):
 
 # ------------------------------------------------------------- clustering ----
 @pytest.mark.parametrize("n,d,k,seed", [(30, 2, 1, 99), (12, 1, 12, 55), (2000, 4, 3, 17), (5000, 90, 8, 2),
-                                        (9000, 90, 16, 5), (4000, 33, 40, 11)])
+                                        (9000, 90, 16, 5), (4000, 33, 40, 11), (6000, 90, 64, 13)])
 def test_kmeans_bit_exact(engine, oracle, n, d, k, seed):
     X, _ = mixture(n, d, max(k, 2), seed=seed)
     g = engine.kmeans(X, k, seed)
@@ -178,7 +178,7 @@ def test_kmeans_forced_iterations_and_duplicates(engine, oracle):
 
 
 @pytest.mark.parametrize("n,d,k,seed", [(10, 2, 3, 5), (100, 2, 2, 66), (16000, 4, 8, 2), (5003, 90, 16, 3),
-                                        (777, 9, 7, 1)])
+                                        (777, 9, 7, 1), (3000, 90, 40, 4)])
 def test_kbalance_bit_exact(engine, oracle, n, d, k, seed):
     X, _ = mixture(n, d, 4, seed=seed)
     for recompute in (True, False):
