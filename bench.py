@@ -231,12 +231,22 @@ def run_ours(args):
     g = {k: torch.from_numpy(v).to(dev) for k, v in dd.items()}
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
     thr, iters = (-1.0, cfg["km_iters"]) if cfg["km_iters"] else (0.01, 0)
+    # the partition (every rank needs it) is sharded over the ranks from N = 4 on: rows'
+    # assignments and whole clusters' centroid chains split, NCCL all-gathers per Lloyd
+    # iteration, bitwise the single-process partition (sharding.torch_allgather); below
+    # that the redundant partition is as fast (tools/partition_scale.py)
+    shard_env = os.environ.get("PKRR_SHARD_PARTITION")
+    shard = world > 1 and (world >= 4 if shard_env is None else shard_env == "1")
+    allgather = None
+    if shard:
+        from paper_1805_00569_b200 import sharding
+        allgather = sharding.torch_allgather(dist, rank, world, dev)
 
     def step(src):
         sX, sy, eX, ey = selection(src)
         return eng.grid_search(cfg["strategy"], src["X_train"], src["y_train"], sX, sy, p, cfg["lambdas"],
                                cfg["sigmas"], 1, eval_X=eX, eval_y=ey, km_threshold=thr, km_max_iters=iters,
-                               rank=rank, world=world)
+                               rank=rank, world=world, allgather=allgather)
 
     for _ in range(args.warmup):
         step(g)
@@ -334,7 +344,9 @@ def run_ours(args):
                                        if os.environ.get("PKRR_SYRK") == "ozaki" else "FP64 DMMA tensor cores"),
                    "n_train": n_train, "n_val": cfg["val"], "n_test": cfg["test"], "d": cfg["d"], "p": p,
                    "sigmas": cfg["sigmas"], "lambdas": cfg["lambdas"], "cells": ncell,
-                   "samples_per_step": samples, "parallelism": f"parts sharded over {world} rank(s), LPT on m^3",
+                   "samples_per_step": samples,
+                   "parallelism": f"parts sharded over {world} rank(s), LPT on m^3"
+                                  + (", partition sharded (NCCL all-gather per Lloyd iteration)" if shard else ""),
                    "l2": "256 MB buffer written between timed steps (per-step K/A working set >> L2)",
                    "part_sizes": [int(x) for x in res.parts["part_sizes"]]},
         "gpu_launches": int(launches),

@@ -156,6 +156,13 @@ int pkrrgpu_grid_search(pkrrgpu_ctx* ctx, int strategy, const double* X_train,
                         double* cell_mse, uint8_t* cell_failed, double* cell_residual,
                         int64_t* best_index);
 
+/* All-gather for a sharded partition (one process per GPU): `dev_buf` is a DEVICE
+ * buffer of `world` equal slices of `bytes_per_rank` bytes; this rank's slice (offset
+ * rank * bytes_per_rank) is filled when the engine calls (its stream synchronised);
+ * the callback fills the other slices before returning (e.g. an NCCL all-gather)
+ * and returns 0 on success. */
+typedef int (*pkrrgpu_allgather_fn)(void* user, void* dev_buf, int64_t bytes_per_rank);
+
 /* Extended grid: adds a held-out evaluation set scored for every cell, explicit
  * k-means parameters, and part sharding for one-process-per-GPU runs. */
 typedef struct {
@@ -181,6 +188,13 @@ typedef struct {
   int rank;  /* this context trains the parts the LPT rule (m^3, largest first to the least-loaded
               * rank) assigns to `rank` -- identical on every rank (sharding.owned_parts) */
   int world; /* 1 = single process */
+  /* optional (world > 1): shard the k-means partition over the ranks -- each rank
+   * assigns a 1/world slice of the rows and updates a 1/world slice of the clusters,
+   * exchanged by `allgather` every iteration.  Every value is computed by the
+   * single-process arithmetic on exactly one rank: bitwise the same partition.
+   * NULL: every rank partitions redundantly. */
+  pkrrgpu_allgather_fn allgather;
+  void* allgather_user;
 } pkrrgpu_grid_args;
 
 typedef struct {

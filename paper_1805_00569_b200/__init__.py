@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 
 # up to 17 concurrent streams per context (see pkrrgpu_create); must precede the
 # process's CUDA context creation to take effect
@@ -55,13 +56,18 @@ class CudaError(RuntimeError):
     pass
 
 
+# pkrrgpu_allgather_fn: int (*)(void* user, void* dev_buf, int64_t bytes_per_rank)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64)
+
+
 class GridArgs(C.Structure):
     _fields_ = [("strategy", C.c_int), ("X_train", C.c_void_p), ("y_train", C.c_void_p), ("n", C.c_int64),
                 ("d", C.c_int64), ("X_test", C.c_void_p), ("y_test", C.c_void_p), ("t", C.c_int64),
                 ("X_eval", C.c_void_p), ("y_eval", C.c_void_p), ("t_eval", C.c_int64), ("p", C.c_int64),
                 ("lambdas", C.c_void_p), ("n_lambdas", C.c_int64), ("sigmas", C.c_void_p),
                 ("n_sigmas", C.c_int64), ("seed", C.c_uint64), ("km_threshold", C.c_double),
-                ("km_max_iters", C.c_int), ("rank", C.c_int), ("world", C.c_int)]
+                ("km_max_iters", C.c_int), ("rank", C.c_int), ("world", C.c_int),
+                ("allgather", ALLGATHER_FN), ("allgather_user", C.c_void_p)]
 
 
 class GridOut(C.Structure):
@@ -427,8 +433,12 @@ class Engine:
 
     def grid_search(self, strategy, train_X, train_y, test_X, test_y, p, lambdas, sigmas, seed, *,
                     eval_X=None, eval_y=None, km_threshold=0.01, km_max_iters=0, rank=0, world=1,
-                    want_partition=False):
-        """strategies.cpp:343-507.  Returns GridResult (cells lambda-major)."""
+                    want_partition=False, allgather=None):
+        """strategies.cpp:343-507.  Returns GridResult (cells lambda-major).
+
+        allgather (world > 1): fn(dev_ptr, bytes_per_rank) all-gathering a device buffer
+        of `world` slices (sharding.torch_allgather / staged_allgather) -- shards the
+        k-means partition over the ranks (bitwise the single-process partition)."""
         lam = np.ascontiguousarray(lambdas, np.float64)
         sig = np.ascontiguousarray(sigmas, np.float64)
         tX, ty, sX, sy = _f64(train_X), _f64(train_y), _f64(test_X), _f64(test_y)
@@ -448,6 +458,17 @@ class Engine:
                         lambdas=lam.ctypes.data, n_lambdas=lam.size, sigmas=sig.ctypes.data,
                         n_sigmas=sig.size, seed=seed, km_threshold=km_threshold, km_max_iters=km_max_iters,
                         rank=rank, world=world)
+        if allgather is not None and world > 1:
+            def _cb(user, buf, nbytes):
+                try:
+                    allgather(int(buf), int(nbytes))
+                    return 0
+                except Exception as exc:  # reported as a failed exchange by the engine
+                    print(f"pkrr allgather failed: {exc!r}", file=sys.stderr)
+                    return 1
+            cb = ALLGATHER_FN(_cb)
+            keep.append(cb)
+            args.allgather = cb
         nc = lam.size * sig.size
         pmax = max(p, 1)
         res = dict(cell_mse=np.full(nc, np.nan), cell_failed=np.zeros(nc, np.uint8), cell_residual=np.zeros(nc),

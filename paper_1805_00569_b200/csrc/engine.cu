@@ -340,13 +340,37 @@ void group_labels(pkrrgpu_ctx* ctx, Scope& sc, const int32_t* label, int64_t n, 
   pk::launch_group(label, n, k, co.sizes, co.start, co.members, co.tmp, s, ctx->counter);
 }
 
+// Sharded partition exchange (pkrrgpu_grid_args.allgather)
+struct Exchange {
+  pkrrgpu_allgather_fn fn = nullptr;
+  void* user = nullptr;
+  int rank = 0, world = 1;
+  bool on() const { return fn != nullptr && world > 1; }
+};
+
+void exchange(pkrrgpu_ctx* ctx, const Exchange& ex, void* buf, int64_t bytes_per_rank) {
+  ck(cudaStreamSynchronize(ctx->main), "sync");
+  if (ex.fn(ex.user, buf, bytes_per_rank) != 0) fail(PKRRGPU_CUDA, "partition all-gather failed");
+}
+
 void kmeans_device(pkrrgpu_ctx* ctx, Scope& sc, const double* dX, int64_t n, int64_t d, int k,
                    uint64_t seed, double threshold, int max_iters, const double* xnorm,
-                   ClusterOut& co) {
+                   ClusterOut& co, const Exchange* exg = nullptr) {
   cudaStream_t s = ctx->main;
   if (k < 1 || static_cast<int64_t>(k) > n) fail(PKRRGPU_INVALID, "kmeans: need 1 <= k <= n");
-  co.label = sc.alloc<int32_t>(n);
-  co.centers = sc.alloc<double>(static_cast<int64_t>(k) * d);
+  // Sharded (one process per GPU): rank r assigns rows [r S, (r+1) S) and updates
+  // clusters [r Kc, (r+1) Kc); labels and centres are all-gathered each iteration, the
+  // changed count is recounted globally.  Each row's argmin and each cluster's
+  // sequential chain is the single-process computation: bitwise the same result.
+  const Exchange ex = exg ? *exg : Exchange{};
+  const bool shard = ex.on();
+  const int W = shard ? ex.world : 1, R = shard ? ex.rank : 0;
+  const int64_t S = (n + W - 1) / W;
+  const int Kc = (k + W - 1) / W;
+  const int64_t r0 = std::min<int64_t>(n, R * S), r1 = std::min<int64_t>(n, (R + 1) * S);
+  const int j0 = std::min(k, R * Kc), j1 = std::min(k, (R + 1) * Kc);
+  co.label = sc.alloc<int32_t>(W * S);
+  co.centers = sc.alloc<double>(static_cast<int64_t>(W) * Kc * d);
   // init: k distinct samples, Rng(seed) + random_permutation (clustering.cpp:64-68)
   HostRng rng(seed);
   const std::vector<int64_t> perm = rng.permutation(n);
@@ -355,19 +379,28 @@ void kmeans_device(pkrrgpu_ctx* ctx, Scope& sc, const double* dX, int64_t n, int
   pk::launch_gather_rows(dX, d, didx, k, co.centers, k, d, s, ctx->counter);
   fill_i32_kernel<<<blocks_for(n), 256, 0, s>>>(co.label, n, -1);
   ++ctx->counter.launches;
-  double* best = sc.alloc<double>(n);
+  double* best = sc.alloc<double>(W * S);
   double* cnorm = sc.alloc<double>(k);
+  int32_t* prev = shard ? sc.alloc<int32_t>(n) : nullptr;
   unsigned long long* changed = sc.alloc<unsigned long long>(2);
   unsigned long long* far = sc.alloc<unsigned long long>(2);
   std::vector<int64_t> sz(k);
   cudaEvent_t ev_sizes;
   ck(cudaEventCreateWithFlags(&ev_sizes, cudaEventDisableTiming), "event");
+  auto update = [&]() {  // centroid update of this rank's clusters, then the exchange
+    pk::launch_means(dX, d, co.members, co.start, co.sizes, k, co.centers, s, ctx->counter, j0, j1);
+  };
   int iter = 0;
   for (; iter < max_iters; ++iter) {
     pk::launch_row_norms(co.centers, k, d, d, cnorm, s, ctx->counter);
     ck(cudaMemsetAsync(changed, 0, sizeof(unsigned long long), s), "memset");
-    pk::launch_assign(dX, n, d, xnorm, co.centers, cnorm, k, 0, nullptr, 0, co.label, best, changed, s,
+    if (shard) ck(cudaMemcpyAsync(prev, co.label, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s), "copy");
+    pk::launch_assign(dX, r1, d, xnorm, co.centers, cnorm, k, 0, nullptr, r0, co.label, best, changed, s,
                       ctx->counter);
+    if (shard) {
+      exchange(ctx, ex, co.label, S * static_cast<int64_t>(sizeof(int32_t)));
+      pk::launch_label_diff(prev, co.label, n, changed, s, ctx->counter);
+    }
     group_labels(ctx, sc, co.label, n, k, co, s);
     // one round trip per iteration: sizes and the changed count together.  The centroid
     // update is enqueued before the host looks at them (speculatively: it only has to
@@ -380,7 +413,7 @@ void kmeans_device(pkrrgpu_ctx* ctx, Scope& sc, const double* dX, int64_t n, int
                          s),
          "D2H");
       ck(cudaEventRecord(ev_sizes, s), "event");
-      pk::launch_means(dX, d, co.members, co.start, co.sizes, k, co.centers, s, ctx->counter);
+      update();
       ck(cudaEventSynchronize(ev_sizes), "sync");
       std::memcpy(sz.data(), pin, sizeof(int64_t) * k);
     }
@@ -390,6 +423,7 @@ void kmeans_device(pkrrgpu_ctx* ctx, Scope& sc, const double* dX, int64_t n, int
     bool reseeded = false;
     for (int j = 0; j < k; ++j) {
       if (sz[j] != 0) continue;
+      if (shard && !reseeded) exchange(ctx, ex, best, S * static_cast<int64_t>(sizeof(double)));
       ck(cudaMemcpyAsync(co.sizes, sz.data(), sizeof(int64_t) * k, cudaMemcpyHostToDevice, s), "H2D");
       pk::launch_farthest(best, co.label, co.sizes, n, far, s, ctx->counter);
       const std::vector<unsigned long long> f = to_host(far, 2, s);
@@ -407,8 +441,9 @@ void kmeans_device(pkrrgpu_ctx* ctx, Scope& sc, const double* dX, int64_t n, int
     }
     if (reseeded) {  // the speculative update saw an empty cluster: regroup and redo it
       group_labels(ctx, sc, co.label, n, k, co, s);
-      pk::launch_means(dX, d, co.members, co.start, co.sizes, k, co.centers, s, ctx->counter);
+      update();
     }
+    if (shard) exchange(ctx, ex, co.centers, static_cast<int64_t>(Kc) * d * static_cast<int64_t>(sizeof(double)));
     if (static_cast<double>(ch) / static_cast<double>(n) <= threshold) {
       ++iter;
       break;
@@ -422,9 +457,9 @@ void kmeans_device(pkrrgpu_ctx* ctx, Scope& sc, const double* dX, int64_t n, int
 
 void kbalance_device(pkrrgpu_ctx* ctx, Scope& sc, const double* dX, int64_t n, int64_t d, int k,
                      uint64_t seed, double threshold, int max_iters, bool recompute,
-                     const double* xnorm, ClusterOut& co) {
+                     const double* xnorm, ClusterOut& co, const Exchange* ex = nullptr) {
   if (k < 1 || static_cast<int64_t>(k) > n) fail(PKRRGPU_INVALID, "kbalance: need 1 <= k <= n");
-  kmeans_device(ctx, sc, dX, n, d, k, seed, threshold, max_iters, xnorm, co);
+  kmeans_device(ctx, sc, dX, n, d, k, seed, threshold, max_iters, xnorm, co, ex);  // the warm start
   cudaStream_t s = ctx->main;
   const int64_t base = n / k, extra = n % k;
   // exact parallel replay of the sequential capacity scan (clustering.cpp:159-176):
@@ -497,7 +532,7 @@ struct PartitionOut {
 
 void make_partition_device(pkrrgpu_ctx* ctx, Scope& sc, int strategy, const double* dX, int64_t n,
                            int64_t d, int64_t p, uint64_t seed, double thr, int max_iters,
-                           PartitionOut& po) {
+                           PartitionOut& po, const Exchange* ex = nullptr) {
   cudaStream_t s = ctx->main;
   const int pk_kind = partitioner_of(strategy);
   if (pk_kind == 0) {
@@ -535,9 +570,9 @@ void make_partition_device(pkrrgpu_ctx* ctx, Scope& sc, int strategy, const doub
   pk::launch_row_norms(dX, n, d, d, xnorm, s, ctx->counter);
   ClusterOut co;
   if (pk_kind == 2)
-    kmeans_device(ctx, sc, dX, n, d, static_cast<int>(p), seed, thr, max_iters, xnorm, co);
+    kmeans_device(ctx, sc, dX, n, d, static_cast<int>(p), seed, thr, max_iters, xnorm, co, ex);
   else
-    kbalance_device(ctx, sc, dX, n, d, static_cast<int>(p), seed, thr, max_iters, true, xnorm, co);
+    kbalance_device(ctx, sc, dX, n, d, static_cast<int>(p), seed, thr, max_iters, true, xnorm, co, ex);
   po.part_of = co.label;
   po.order = co.members;
   po.centers = co.centers;
@@ -1537,7 +1572,12 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   const double thr = a->km_max_iters > 0 ? a->km_threshold : 0.01;
   const int iters = a->km_max_iters > 0 ? a->km_max_iters : 100;
   hmark("inputs enqueued");
-  make_partition_device(ctx, sc, a->strategy, dX, n, d, a->p, a->seed, thr, iters, po);
+  Exchange ex;
+  ex.fn = a->allgather;
+  ex.user = a->allgather_user;
+  ex.rank = rank;
+  ex.world = world;
+  make_partition_device(ctx, sc, a->strategy, dX, n, d, a->p, a->seed, thr, iters, po, &ex);
   hmark("partition returned");
   const int64_t p = po.p;
   for (int64_t q = 0; q < p; ++q)

@@ -1775,10 +1775,10 @@ __global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __re
                                                               const int64_t* __restrict__ members,
                                                               const int64_t* __restrict__ start,
                                                               const int64_t* __restrict__ sizes, int k,
-                                                              double* centers, int bulk) {
+                                                              double* centers, int bulk, int j0) {
   extern __shared__ double mbuf[];  // [ring][rows][F]
   __shared__ uint64_t full[kMeansRing], empty[kMeansRing];
-  const int j = blockIdx.x;
+  const int j = j0 + static_cast<int>(blockIdx.x);
   const int64_t f0 = static_cast<int64_t>(blockIdx.y) * kMeansF;
   const int fw = static_cast<int>(d - f0 < kMeansF ? d - f0 : kMeansF);
   const int64_t sz = sizes[j], st = start[j];
@@ -1919,16 +1919,34 @@ __global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __re
 }
 
 void launch_means(const double* X, int64_t d, const int64_t* members, const int64_t* start,
-                  const int64_t* sizes, int k, double* centers, cudaStream_t s, Counter& c) {
+                  const int64_t* sizes, int k, double* centers, cudaStream_t s, Counter& c, int j0, int j1) {
+  if (j1 < 0) j1 = k;
+  if (j1 <= j0) return;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(means_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMeansSmem);
     attr = true;
   }
-  dim3 grid(k, static_cast<unsigned>((d + kMeansF - 1) / kMeansF));
+  dim3 grid(j1 - j0, static_cast<unsigned>((d + kMeansF - 1) / kMeansF));
   // 16-byte cp.async pieces need 16-byte aligned rows and an even feature count: even d
   const int bulk = (d % 2 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
-  means_kernel<<<grid, kMeansThreads, kMeansSmem, s>>>(X, d, members, start, sizes, k, centers, bulk);
+  means_kernel<<<grid, kMeansThreads, kMeansSmem, s>>>(X, d, members, start, sizes, k, centers, bulk, j0);
+  ++c.launches;
+}
+
+__global__ void label_diff_kernel(const int32_t* __restrict__ a, const int32_t* __restrict__ b, int64_t n,
+                                  unsigned long long* count) {
+  unsigned local = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    local += a[i] != b[i];
+  if (local) atomicAdd(count, static_cast<unsigned long long>(local));
+}
+
+void launch_label_diff(const int32_t* a, const int32_t* b, int64_t n, unsigned long long* count,
+                       cudaStream_t s, Counter& c) {
+  cudaMemsetAsync(count, 0, sizeof(unsigned long long), s);
+  label_diff_kernel<<<148 * 2, 256, 0, s>>>(a, b, n, count);
   ++c.launches;
 }
 

@@ -138,8 +138,13 @@ void launch_assign(const double* X, int64_t n, int64_t d, const double* xnorm,
 void launch_group(const int32_t* label, int64_t n, int k, int64_t* sizes, int64_t* start,
                   int64_t* members, int64_t* tmp, cudaStream_t s, Counter& c);
 // centers[j][f] = (sum over members in row order) * (1.0 / size)  (clustering.cpp:34-49)
+// (clusters [j0, j1) only when given: one rank's share of a sharded update)
 void launch_means(const double* X, int64_t d, const int64_t* members, const int64_t* start,
-                  const int64_t* sizes, int k, double* centers, cudaStream_t s, Counter& c);
+                  const int64_t* sizes, int k, double* centers, cudaStream_t s, Counter& c, int j0 = 0,
+                  int j1 = -1);
+// count of i < n with a[i] != b[i] (the k-means "changed" count of a sharded assign)
+void launch_label_diff(const int32_t* a, const int32_t* b, int64_t n, unsigned long long* count,
+                       cudaStream_t s, Counter& c);
 // argmax_i best[i] over rows whose cluster has size > 1 (first index on ties)
 void launch_farthest(const double* best, const int32_t* label, const int64_t* sizes, int64_t n,
                      unsigned long long* out, cudaStream_t s, Counter& c);

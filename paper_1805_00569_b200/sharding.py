@@ -44,3 +44,46 @@ def combine(part_sse, part_failed, t):
     part-order SSE sum (see paper_1805_00569_b200.combine_parts)."""
     from . import combine_parts
     return combine_parts(part_sse, part_failed, t)
+
+
+# ---- sharded partition exchange (pkrrgpu_grid_args.allgather) -------------------------
+class _DeviceBytes:
+    """A raw device allocation seen by torch through __cuda_array_interface__."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def _device_view(ptr, nbytes, device):
+    import torch
+    return torch.as_tensor(_DeviceBytes(ptr, nbytes), device=device)
+
+
+def torch_allgather(dist, rank: int, world: int, device):
+    """Exchange for Engine.grid_search(allgather=...): the device buffer holds `world`
+    slices of `nbytes`; this rank's slice is gathered into all ranks' buffers with one
+    collective on the process group's device (NCCL over NVLink)."""
+    import torch
+
+    def fn(ptr, nbytes):
+        full = _device_view(ptr, nbytes * world, device)
+        mine = full[rank * nbytes:(rank + 1) * nbytes].clone()
+        dist.all_gather_into_tensor(full, mine)
+        torch.cuda.current_stream(device).synchronize()
+    return fn
+
+
+def staged_allgather(dist, rank: int, world: int, device):
+    """The same exchange through host memory, for process groups without device
+    collectives (gloo: the multi-process tests)."""
+    import torch
+
+    def fn(ptr, nbytes):
+        full = _device_view(ptr, nbytes * world, device)
+        mine = full[rank * nbytes:(rank + 1) * nbytes].cpu()
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine)
+        full.copy_(torch.cat(parts).to(device))
+        torch.cuda.synchronize(device)
+    return fn
