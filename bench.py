@@ -37,11 +37,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "train+predict samples/sec (FP64)"
-# DRAM read+write bytes per 128x128 trailing-SYRK output tile, from the committed
-# DRAM bytes per 128x128 SYRK output tile from the committed ncu --set full captures of the
-# m=20544 factorization probe: K=512 (profiles/ncu_syrk_r01.txt, 8911 tiles, 2.98e9 read +
-# 1.14e9 write) and K=1024 (profiles/ncu_syrk_k1024_r01.txt, 11781 tiles, 9.87e9 + 1.53e9).
-SYRK_TRAFFIC_PER_TILE = {512: 462800, 1024: 967700, 2048: 1646600}  # K=2048: ncu_syrk_k2048_r01 (10585 tiles)
+# DRAM bytes (read, write) and 128x128 tiles of one trailing-SYRK launch per K, from the
+# committed ncu --set full captures of the m = 20544 factorization probe:
+# K=512 profiles/ncu_syrk_r01.txt, K=1024 ncu_syrk_k1024_r01.txt, K=2048 ncu_syrk_k2048_r01.txt;
+# K=128 (a lone 4096-row system, C0): ncu_syrk_k128_r01.txt (tools/syrk_probe_alone.py).
+SYRK_NCU_LAUNCH = {128: (351, 49.44e6, 1.77e6), 512: (8911, 2.98e9, 1.14e9), 1024: (11781, 9.87e9, 1.53e9),
+                   2048: (10585, 16.05e9, 1.38e9)}
 UNIT = "samples/s"
 
 # BASELINE.json configs (per GPU for the weak-scaled ones).  km_iters 20 = exactly
@@ -361,10 +362,14 @@ def run_ours(args):
                                   if syrk_k == 128 else ""),
                      "achieved": syrk_tflops, "peak": peak, "unit": "TFLOP/s",
                      "frac": syrk_tflops / peak if peak else None,
-                     "traffic": SYRK_TRAFFIC_PER_TILE.get(syrk_k),
-                     "traffic_note": f"DRAM bytes per 128x128 output tile (K={syrk_k}) from the committed ncu "
-                                     "--set full capture (profiles/); algorithmic operand+C bytes per tile = "
-                                     f"{2 * 128 * syrk_k * 8 + 2 * 128 * 128 * 8} (panels are L2 hits)",
+                     "traffic": (SYRK_NCU_LAUNCH[syrk_k][1] + SYRK_NCU_LAUNCH[syrk_k][2]
+                                 if syrk_k in SYRK_NCU_LAUNCH else None),
+                     "traffic_note": (f"DRAM read+write bytes of the captured K={syrk_k} launch "
+                                      f"({SYRK_NCU_LAUNCH[syrk_k][0]} tiles of 128x128, ncu --set full, profiles/) "
+                                      f"vs its algorithmic operand+C bytes "
+                                      f"{SYRK_NCU_LAUNCH[syrk_k][0] * (2 * 128 * syrk_k * 8 + 2 * 128 * 128 * 8):.3e} "
+                                      "(panels are L2 hits: traffic below the algorithmic bytes)"
+                                      if syrk_k in SYRK_NCU_LAUNCH else "no ncu capture for this K"),
                      "peak_source": "measured live after the warm-up, best of 3: FP64 DMMA (mma.sync m8n8k4) "
                                     "probe over 148 SMs; MEASURED_PEAKS.json has no FP64 entry",
                      "algorithmic": "per launch rows(rows+1)*K flops (lower triangle incl. diagonal) / launch time; "
