@@ -300,16 +300,15 @@ __device__ __forceinline__ void mma_row4_rn(double (&acc)[4][2], const double* A
 
 // lane i owns row i of the 32x32 block at Sd (stride kLS); returns the first
 // failing column or -1 (solver.cpp:18-33 per column: test, sqrt, divide, update).
-// Column values are broadcast through shared memory (`col`: two 40-double buffers,
-// 16-byte aligned): one STS per lane, then LDS.128 reads of two values each, instead
-// of two SHFL.IDX per double.  Lane j+1 updates its own next pivot at once (its
-// a[j+1] -= l*l is exactly the general update with l_k = its own l) and publishes it
-// with the column, so the pivot chain is LDS -> rsqrt -> multiply -> STS -> syncwarp;
-// the buffers alternate so one __syncwarp per column suffices.  With `pub`, each
-// column (l values, pivot at [32]) is also copied to its own 40-double slot and
-// lane 0 arrives on cbar[j]: the warps factoring the rows below the block
-// (warp_tall32) consume the slots without ever holding this warp up.
-__device__ __noinline__ int warp_potrf32(double* Sd, double* col, double* pub, uint64_t* cbar, int lane) {
+// Column values are broadcast through shared memory, one 40-double slot per column
+// (`col`, 16-byte aligned; slot j+1 holds column j's l values and pivot j+1): one STS
+// per lane, then LDS.128 reads of two values each, instead of two SHFL.IDX per double.
+// Lane j+1 updates its own next pivot at once (its a[j+1] -= l*l is exactly the
+// general update with l_k = its own l) and publishes it with the column, so the pivot
+// chain is LDS -> rsqrt -> multiply -> STS -> syncwarp.  After each column lane 0
+// arrives on cbar[j] (when given): the warps factoring the rows below the block
+// (warp_tall32) read the same slots without ever holding this warp up.
+__device__ __noinline__ int warp_potrf32(double* Sd, double* col, uint64_t* cbar, int lane) {
   double a[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = Sd[lane * kLS + c];
@@ -318,8 +317,8 @@ __device__ __noinline__ int warp_potrf32(double* Sd, double* col, double* pub, u
   __syncwarp();
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
-    const double* cur = col + (j & 1) * 40;
-    double* nxt = col + ((j + 1) & 1) * 40;
+    const double* cur = col + j * 40;
+    double* nxt = col + (j + 1) * 40;
     double piv = cur[32];
     if (!(piv > 0.0) && bad < 0) bad = j;
     piv = bad >= 0 ? 1.0 : piv;  // keep the warp going; the result is discarded
@@ -328,18 +327,14 @@ __device__ __noinline__ int warp_potrf32(double* Sd, double* col, double* pub, u
     const double dj = piv * rj;
     const double l = a[j] * rj;
     a[j] = lane == j ? dj : (lane > j ? l : 0.0);
-    if (pub) {
-      pub[j * 40 + lane] = l;
-      if (lane == 0) pub[j * 40 + 32] = piv;
+    if (lane == j + 1) {
+      a[j + 1] = a[j + 1] - l * l;
+      nxt[32] = a[j + 1];
     }
+    nxt[lane] = l;
+    __syncwarp();
+    if (cbar && lane == 0) mbar_arrive_nomem(&cbar[j]);
     if (j + 1 < 32) {
-      if (lane == j + 1) {
-        a[j + 1] = a[j + 1] - l * l;
-        nxt[32] = a[j + 1];
-      }
-      nxt[lane] = l;
-      __syncwarp();
-      if (pub && lane == 0) mbar_arrive_nomem(&cbar[j]);
       // rows k > j: a[k] -= l_i * l_k (lane j+1's own diagonal already done).  Applied
       // to every lane: entries above a lane's diagonal (k > i) only collect values that
       // are never read (a later column zeroes them, the final store drops them), and
@@ -351,9 +346,6 @@ __device__ __noinline__ int warp_potrf32(double* Sd, double* col, double* pub, u
         if (k > j) a[k] = (k == j + 1 && lane == j + 1) ? a[k] : a[k] - l * lk.x;
         if (k + 1 > j) a[k + 1] -= l * lk.y;
       }
-    } else if (pub) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive_nomem(&cbar[j]);
     }
   }
   if (bad < 0) {
@@ -367,7 +359,8 @@ __device__ __noinline__ int warp_potrf32(double* Sd, double* col, double* pub, u
 // reference's column loop, solver.cpp:21-33, on rows > the block): lane i owns one
 // row's 32 panel entries at P; per column j, after warp_potrf32's arrival on cbar[j],
 // l_i = a_ij * rsqrt(pivot_j) and a_ik -= l_i * l_kj for k > j.  The rsqrt repeats the
-// diagonal warp's (same bits; its failed pivots are already replaced by 1).
+// diagonal warp's (same bits).  After a failed pivot the values are garbage, and the
+// leaf is abandoned right after this phase (the abort flag).
 __device__ __noinline__ void warp_tall32(double* P, const double* pub, uint64_t* cbar, uint32_t parity) {
   double a[32];
 #pragma unroll
@@ -375,8 +368,8 @@ __device__ __noinline__ void warp_tall32(double* P, const double* pub, uint64_t*
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     mbar_wait(&cbar[j], parity);
-    const double* cj = pub + j * 40;
-    const double rj = rsqrt(cj[32]);
+    const double* cj = pub + (j + 1) * 40;  // column j's l values (and pivot j + 1)
+    const double rj = rsqrt(pub[j * 40 + 32]);
     const double l = a[j] * rj;
     a[j] = l;
 #pragma unroll
@@ -485,7 +478,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
       LEAF_MARK(2 + 5 * pb);
       if (warp == 0) {
         // Tt is free until the blocked inverse: two column buffers, then 32 published slots
-        const int bad = warp_potrf32(Sd, Tt, pb < 3 ? Tt + 80 : nullptr, cbar, lane);
+        const int bad = warp_potrf32(Sd, Tt, cbar, lane);  // 33 column slots in Tt
 #ifdef PKRR_LEAF_TRACE
         if (lane == 0) g_leaf_trace[40 + pb] = clock64();
         __syncwarp();
@@ -502,7 +495,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&dbar[pb]);
       } else if (warp < 4 - pb) {
-        warp_tall32(S + (R0 + 32 * (warp - 1) + lane) * kLS + 32 * pb, Tt + 80, cbar, static_cast<uint32_t>(pb & 1));
+        warp_tall32(S + (R0 + 32 * (warp - 1) + lane) * kLS + 32 * pb, Tt, cbar, static_cast<uint32_t>(pb & 1));
 #ifdef PKRR_LEAF_TRACE
         if (lane == 0) g_leaf_trace[44 + 4 * pb + warp] = clock64();
         __syncwarp();
