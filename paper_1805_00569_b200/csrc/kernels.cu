@@ -298,6 +298,19 @@ __device__ __forceinline__ void mma_row4_rn(double (&acc)[4][2], const double* A
   }
 }
 
+// the same with a lower-triangular B (B[k][n] = 0 for n > k, a D block): column tile c
+// only meets k >= 8 c, so those DMMAs are not issued (K = 32)
+__device__ __forceinline__ void mma_row4_rn_lowB(double (&acc)[4][2], const double* A, int lda, const double* B,
+                                                 int ldb, int lr, int lk) {
+#pragma unroll
+  for (int k = 0; k < 32; k += 4) {
+    const double a = A[lr * lda + k + lk];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (k + 4 > 8 * c) dmma(acc[c], a, B[(k + lk) * ldb + 8 * c + lr]);
+  }
+}
+
 // lane i owns row i of the 32x32 block at Sd (stride kLS); returns the first
 // failing column or -1 (solver.cpp:18-33 per column: test, sqrt, divide, update).
 // Column values are broadcast through shared memory, one 40-double slot per column
@@ -552,7 +565,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
       const int bj = t >> 2, rt = t & 3;
       double acc[4][2] = {};
       const double* Arow = S + (32 * bi + 8 * rt) * kLS;
-      mma_row4_rn(acc, Arow + 32 * bj, kLS, D + bj * 32 * kBS, kBS, 0, 32, lr, lk);  // X_jj = D_j
+      mma_row4_rn_lowB(acc, Arow + 32 * bj, kLS, D + bj * 32 * kBS, kBS, lr, lk);  // X_jj = D_j
       for (int bk = bj + 1; bk < bi; ++bk)
         mma_row4_rn(acc, Arow + 32 * bk, kLS, S + (32 * bj) * kLS + 32 * bk, kLS, 0, 32, lr, lk);
       double* T = Tt + bj * 32 * kBS + (8 * rt + lr) * kBS + 2 * lk;
