@@ -1,15 +1,21 @@
 #!/usr/bin/env python
 """Benchmark of the partitioned Gaussian KRR hot path (BASELINE.json configs[1]).
 
-Default workload ("step", --config c1) -- KKRR2 at BASELINE configs[1], synthetic
-(datagen.py, seed 1): n_train = 65536*N, n_val = 2048, n_test = 2048, d = 90,
-16*N-component mixture; Lloyd k-means into p = 8*N parts (exactly 20 iterations),
-one Gaussian KRR model per part (sigma 3, lambda 1e-4: gram + lambda*m_t*I +
-Cholesky + solves + residual), val and test rows routed to the nearest centroid's
-model, MSE, best cell selected on validation MSE.  Weak scaling: per-GPU work (8
-parts of ~8192 rows) is fixed as N grows; parts are sharded by LPT on m^3 with no
-data-path collective (per-part SSE combined in part order afterwards).
---config c0|c2|c3|c4 runs the other BASELINE configs (see CONFIGS).
+Default workload ("step"):
+  N = 1: BASELINE configs[1] (--config c1) -- KKRR2, synthetic (datagen.py, seed 1):
+      n_train = 65536, n_val = 2048, n_test = 2048, d = 90, 16-component mixture; Lloyd
+      k-means into p = 8 parts (exactly 20 iterations), one Gaussian KRR model per part
+      (sigma 3, lambda 1e-4: gram + lambda*m_t*I + Cholesky + solves + residual), val and
+      test rows routed to the nearest centroid's model, MSE, best cell selected on
+      validation MSE.
+  N > 1: BASELINE configs[3] (--config c3), the reference's weak-scaling config -- BKRR2
+      with 16384 rows per part and p = 8 N parts (n_train = 131072 N), sigma 3,
+      lambda 1e-5; parts sharded by LPT on m^3 with no data-path collective, the ranks'
+      per-cell predictions summed (disjoint) and combined once.
+--config c0|c1|c2|c3|c4 picks a config explicitly (CONFIGS): c1 / c3 scale n and p
+with N (weak), c2 keeps its 16 parts of 8192 rows over N GPUs (strong), c0 / c4 are
+single-GPU configs.  `--gpus N` without torchrun re-launches this script under
+torch.distributed.run with N ranks (and fails if fewer than N GPUs are visible).
 
 Metric: train+predict samples/s = (n_train + n_val + n_test) * cells / step time.
 `value` times the engine with inputs resident in HBM (CUDA events on the engine's
@@ -55,10 +61,10 @@ CONFIGS = {
                scale_n=True),
     "c2": dict(name="configs[2]: BKRR2, k-balance p=16, 3 sigma x 3 lambda", strategy="bkrr2", n=131072, val=2048,
                test=2048, d=90, comps=32, p=16, sigmas=[1.0, 3.0, 10.0], lambdas=[1e-6, 1e-4, 1e-2], bump=3.0,
-               clipped=False, km_iters=0, scale_n=True),
+               clipped=False, km_iters=0, scale_n=False),
     "c3": dict(name="configs[3]: weak-scaling BKRR2, 16384 rows/part, p=8 per GPU", strategy="bkrr2", n=131072,
                val=2048, test=2048, d=90, comps=64, p=8, sigmas=[3.0], lambdas=[1e-5], bump=3.0, clipped=False,
-               km_iters=0, scale_n=True),
+               km_iters=0, scale_n=True, scale_comps=False),
     "c4": dict(name="configs[4]: wide-feature KKRR2, d=784, p=8", strategy="kkrr2", n=262144, val=0, test=4096,
                d=784, comps=10, p=8, sigmas=[8.0], lambdas=[1e-4], bump=8.0, clipped=True, km_iters=0,
                scale_n=False),
@@ -73,7 +79,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sample-n", type=int, default=0, help="reference sample train rows (0 = auto)")
-    ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="default: c1 at N = 1, c3 (the weak-scaling config) at N > 1")
     ap.add_argument("--update", default="fp64", choices=["fp64", "int8"],
                     help="trailing Cholesky update: FP64 tensor cores (DMMA, default) or the opt-in "
                          "FP64-accurate int8 Ozaki emulation (tcgen05 kind::i8)")
@@ -88,7 +95,8 @@ def dist_env():
 def workload(cfg, world):
     from paper_1805_00569_b200 import datagen
     mult = world if cfg["scale_n"] else 1
-    return datagen.make(cfg["n"] * mult, cfg["val"], cfg["test"], cfg["d"], cfg["comps"] * mult,
+    comps = cfg["comps"] * (mult if cfg.get("scale_comps", True) else 1)
+    return datagen.make(cfg["n"] * mult, cfg["val"], cfg["test"], cfg["d"], comps,
                         bumps=32 if cfg["clipped"] else 16, bump_sigma=cfg["bump"], clipped=cfg["clipped"], seed=1)
 
 
@@ -163,6 +171,43 @@ def reference_sample(cfg, dd, n_s, workers):
     return r, dt, (Xs, ys, Xq, yq)
 
 
+def _lpt_makespan(costs, workers):
+    """run_partitions (runtime.hpp:70-112) hands parts to `workers` threads in index
+    order as they free up; the makespan of that list schedule."""
+    import heapq
+    free = [0.0] * max(1, min(workers, len(costs)))
+    for c in costs:
+        t = heapq.heappop(free)
+        heapq.heappush(free, t + c)
+    return max(free)
+
+
+def cpu_extrapolation(cfg, dd, n_s, workers):
+    """Full-size / sample CPU-time ratio of the reference grid: each part's reference
+    cost is its Cholesky (m(m+1)(2m+1)/6 at the reference's measured 1.75 GFLOP/s per
+    core) plus its gram and cross kernel (d m(m+1) + 2 t_t m d at
+    0.68 GFLOP/s), per cell / per sigma, scheduled over `workers` threads like
+    run_partitions.  The parts come from the reference's own make_partition of the
+    sample and of the full training set.  Validated against full-size reference runs in
+    profiles/cpu_fullsize_*_r02.json."""
+    from oracle import Reference
+    ref = Reference()
+    ns, ncell = len(cfg["sigmas"]), len(cfg["sigmas"]) * len(cfg["lambdas"])
+    tq = cfg["val"] + cfg["test"]
+
+    def makespan(X):
+        part, _ = ref.make_partition(cfg["strategy"], X, cfg["p"], 1)
+        sizes = np.bincount(part).astype(float)
+        d = cfg["d"]
+        costs = [ncell * m * (m + 1) * (2 * m + 1) / 6 / 1.75e9
+                 + ns * (d * m * (m + 1) + 2 * tq * m * d * (m / sizes.sum())) / 0.68e9 for m in sizes]
+        return _lpt_makespan(costs, workers), sizes
+
+    full, fs = makespan(dd["X_train"])
+    samp, ss = makespan(dd["X_train"][:n_s])
+    return full / samp, [int(x) for x in fs], [int(x) for x in ss]
+
+
 def sample_rows(cfg, steps, warmup, override):
     """Bounded CPU sample: parts of ~2048 rows (1024 for multi-cell grids), so one
     reference step is a few seconds on the host's cores."""
@@ -195,14 +240,20 @@ def run_reference(args):
     sample = (f"first {n_s} of {cfg['n']} train rows, {cfg['strategy']} p={cfg['p']} (parts ~{n_s // cfg['p']} rows "
               f"vs ~{cfg['n'] // cfg['p']} at full size), {ncell} cell(s), {cfg['val'] + cfg['test']} val+test "
               f"rows; reference grid_search with GridOptions.workers={cores}")
+    ratio, full_sizes, sample_sizes = cpu_extrapolation(cfg, dd, n_s, cores)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "weak" if cfg["scale_n"] else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": {"workload": f"BASELINE {cfg['name']} (bounded CPU sample)", "n_train_sample": n_s,
                        "n_train": cfg["n"], "n_val": cfg["val"], "n_test": cfg["test"], "d": cfg["d"],
                        "p": cfg["p"]},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample,
-                             "extrapolated_full_value": value * (n_s / cfg["n"]) ** 2},
+                             "extrapolated_full_value": value * (cfg["n"] + cfg["val"] + cfg["test"])
+                             / (n_s + cfg["val"] + cfg["test"]) / ratio,
+                             "extrapolation": "sample time x (full / sample) makespan of per-part reference "
+                                              "costs over the cores (bench.cpu_extrapolation)",
+                             "full_part_sizes": full_sizes, "sample_part_sizes": sample_sizes},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -291,11 +342,12 @@ def run_ours(args):
         dist.all_reduce(tms, op=dist.ReduceOp.MAX)
         ms = float(tms.item())
         parts = res.parts
-        sse, fl = sharding.allreduce_tables(parts["part_sse"], parts["part_failed"], dist, device=dev)
-        sel_mse, failed, best = sharding.combine(sse, fl, n_sel)
+        sX, sy, eX, ey = selection(dd)
+        pred, fcell = sharding.allreduce_predictions(parts["cell_pred"], parts["part_failed"], dist, device=dev)
+        sel_mse, best, _ = sharding.combine(eng, cfg["strategy"], p, pred, fcell, sy)
         if n_eval:
-            esse, _ = sharding.allreduce_tables(parts["part_eval_sse"], parts["part_failed"], dist, device=dev)
-            eval_mse, _, _ = sharding.combine(esse, fl, n_eval)
+            epred, _ = sharding.allreduce_predictions(parts["cell_eval_pred"], parts["part_failed"], dist, device=dev)
+            eval_mse, _, _ = sharding.combine(eng, cfg["strategy"], p, epred, fcell, ey)
         else:
             eval_mse = sel_mse
     else:
@@ -339,7 +391,8 @@ def run_ours(args):
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak" if cfg["scale_n"] else "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (datagen.py seed 1, BASELINE {cfg['name'].split(':')[0]} shapes)",
         "config": {"workload": f"BASELINE {cfg['name']}", "strategy": cfg["strategy"],
@@ -402,7 +455,8 @@ def run_ours(args):
                 "sample": f"first {n_s} train rows, {cfg['strategy']} p={cfg['p']}, {ncell} cell(s), "
                           f"{cfg['val'] + cfg['test']} val+test rows, reference grid_search workers={cores}, "
                           f"{dt:.2f} s",
-                "extrapolated_full_value": cpu_v * (n_s / cfg["n"]) ** 2,
+                "extrapolated_full_value": cpu_v * (cfg["n"] + cfg["val"] + cfg["test"])
+                / (n_s + cfg["val"] + cfg["test"]) / cpu_extrapolation(cfg, dd, n_s, cores)[0],
                 "mse_reference": [float(x) for x in r["mse"]], "mse_gpu_same_sample": [float(x) for x in gs.mse],
                 "mse_max_rel_diff": rel, "best_cell_equal": bool(gs.best_index == r["best"])}
         except Exception as e:  # noqa: BLE001
@@ -417,12 +471,58 @@ def run_ours(args):
     return 0
 
 
+def visible_gpus():
+    fake = os.environ.get("PKRR_BENCH_FAKE_GPUS")  # CPU tests of the launcher only
+    if fake is not None:
+        return int(fake)
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:  # noqa: BLE001
+        return 0
+
+
+def _free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch(args):
+    """`bench.py --gpus N` outside torchrun: N ranks, one per GPU, under
+    torch.distributed.run (the driver's own launch shape).  Fails loudly when fewer
+    than N GPUs are visible."""
+    have = visible_gpus()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}", file=sys.stderr)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=dict(os.environ, PKRR_BENCH_LAUNCHED="1"))
+
+
 def main():
     args = parse()
+    if args.config is None:
+        args.config = "c1" if args.gpus <= 1 else "c3"
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.gpus > 1 and world == 0:
+        return relaunch(args)
+    if world and world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
+    if os.environ.get("PKRR_BENCH_DRYRUN"):  # launcher test: report the rank layout only
+        rank, world, local = dist_env()
+        print(json.dumps({"rank": rank, "world": world, "local_rank": local, "config": args.config}), flush=True)
+        return 0
     if args.update == "int8":  # read by the library at context creation
         os.environ["PKRR_SYRK"] = "ozaki"
     if args.impl == "reference":
         return run_reference(args)
+    if visible_gpus() < max(1, world):
+        print(f"bench.py: needs {max(1, world)} visible GPU(s), found {visible_gpus()}", file=sys.stderr)
+        return 2
     return run_ours(args)
 
 

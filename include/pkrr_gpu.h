@@ -58,6 +58,8 @@ typedef struct pkrrgpu_ctx pkrrgpu_ctx;
  * rank, see pkrrgpu_grid_args.rank/world). */
 int pkrrgpu_create(int device, pkrrgpu_ctx** out);
 void pkrrgpu_destroy(pkrrgpu_ctx* ctx);
+/* number of visible CUDA devices (0 when there is none) */
+int pkrrgpu_device_count(void);
 const char* pkrrgpu_last_error(void);
 /* Kernel launches made by this context since creation (evidence counter). */
 int64_t pkrrgpu_launch_count(const pkrrgpu_ctx* ctx);
@@ -135,6 +137,29 @@ int pkrrgpu_train_partitions(pkrrgpu_ctx* ctx, int strategy, const double* X, co
                              int64_t n, int64_t d, int64_t p, uint64_t seed, double sigma,
                              double lambda, pkrrgpu_models** out, int64_t* failed_part,
                              int64_t* npd_pivot);
+/* train_partitions(ps, train, spec, lambda, workers) -- strategies.cpp:104-133 with the
+ * CALLER's PartitionSet (strategies.hpp:31-36, :50-52): rows = ps.parts concatenated
+ * part by part (each part's rows in the caller's order -- make_partition keeps train
+ * row order, strategies.cpp:97-99), sizes[p] = the parts' lengths; centers [p*d] or
+ * NULL (then predict_nearest raises, like a PartitionSet without centers).  All parts
+ * train concurrently on the context's streams, largest first at the highest priority.
+ * Errors as pkrrgpu_train_partitions; an empty part or a row outside [0, n) is
+ * PKRRGPU_INVALID. */
+int pkrrgpu_train_parts(pkrrgpu_ctx* ctx, const double* X, const double* y, int64_t n, int64_t d,
+                        const int64_t* rows, const int64_t* sizes, int64_t p, const double* centers, double sigma,
+                        double lambda, pkrrgpu_models** out, int64_t* failed_part, int64_t* npd_pivot);
+/* Models from host (or device) KrrModels (solver.hpp:37-49): p models of sizes[t] support
+ * rows, S = the support rows concatenated model by model (sum(sizes) x d, dense),
+ * alpha concatenated the same way, centers [p*d] or NULL, Gaussian sigma. */
+int pkrrgpu_models_import(pkrrgpu_ctx* ctx, int64_t p, int64_t d, const int64_t* sizes, const double* S,
+                          const double* alpha, const double* centers, double sigma, pkrrgpu_models** out);
+/* KrrModel::predict (solver.cpp:74-87) of q rows: model `part` -> out[q]; part = -1:
+ * every model, out[t * q + j] (what predict_average / predict_oracle combine,
+ * strategies.cpp:135-140 / :151-166). */
+int pkrrgpu_models_predict(pkrrgpu_ctx* ctx, const pkrrgpu_models* models, int64_t part, const double* Q,
+                           int64_t q, double* out);
+/* centers of the partition the models were trained on (p*d), PKRRGPU_INVALID if none */
+int pkrrgpu_models_centers(const pkrrgpu_models* models, double* centers);
 int64_t pkrrgpu_models_count(const pkrrgpu_models* models);
 int64_t pkrrgpu_models_size(const pkrrgpu_models* models, int64_t part);
 int pkrrgpu_models_alpha(const pkrrgpu_models* models, int64_t part, double* alpha);
@@ -224,10 +249,47 @@ typedef struct {
   double flops_chol;
   double flops_gram;
   double flops_other;
+  /* optional: this rank's per-cell predictions, [ncell x pred_rows x t] (and t_eval).
+   * pred_rows = 1 for the whole / nearest predictors (test-row order; rows routed to
+   * parts this rank does not own are 0), = p for average / oracle (one row per part;
+   * parts not owned are 0).  Summing them over ranks is exact (disjoint), and
+   * pkrrgpu_combine on the sum gives the single-process cell MSEs / best cell bitwise. */
+  double* cell_pred;
+  double* cell_eval_pred;
+  int64_t pred_rows;
 } pkrrgpu_grid_out;
 
 int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* args,
                            pkrrgpu_grid_out* out);
+
+/* Cell combine + MSE + best cell -- strategies.cpp:458-505 (+ mse :168-177): pred is
+ * [ncell x P x t] with P = 1 (whole / nearest: test-row order) or p (average / oracle:
+ * one row per part), e.g. the sum over ranks of pkrrgpu_grid_out.cell_pred.  The MSE
+ * is summed sequentially in test-row order (the reference's own arithmetic), failed
+ * cells (cell_failed may be NULL) get NaN and never win; best = first strict minimum
+ * (-1 if none); best_pred (t entries, may be NULL) = the best cell's combined
+ * prediction.  grid_search_ex uses the same code for one process. */
+int pkrrgpu_combine(pkrrgpu_ctx* ctx, int strategy, int64_t p, int64_t t, int64_t ncell, const double* pred,
+                    const double* y, const uint8_t* cell_failed, double* cell_mse, int64_t* best_index,
+                    double* best_pred);
+
+/* ---- several GPUs in one process (one host thread per GPU) ----------- */
+
+/* A group of n contexts on devices[0..n) (NULL: 0..n-1), driven by one host thread per
+ * GPU.  A device may appear more than once (two contexts sharing one GPU).  Peer
+ * access is enabled between distinct devices (NVLink / NVSwitch). */
+typedef struct pkrrgpu_multi pkrrgpu_multi;
+int pkrrgpu_multi_create(const int* devices, int n, pkrrgpu_multi** out);
+void pkrrgpu_multi_destroy(pkrrgpu_multi* m);
+int pkrrgpu_multi_size(const pkrrgpu_multi* m);
+pkrrgpu_ctx* pkrrgpu_multi_context(pkrrgpu_multi* m, int i);
+/* grid_search (strategies.cpp:343-507) over every GPU of the group: each device trains
+ * the parts the LPT rule on m^3 gives it (no data-path collective); from 4 devices on
+ * (PKRR_SHARD_PARTITION=0/1 forces it) the k-means partition is sharded bit-exactly with a
+ * peer-memory all-gather per Lloyd iteration; the devices' per-cell predictions are
+ * summed and combined once (pkrrgpu_combine).  args->rank / world / allgather are
+ * ignored; `out` is filled as by a one-context call, and is bitwise equal to it. */
+int pkrrgpu_multi_grid_search(pkrrgpu_multi* m, const pkrrgpu_grid_args* args, pkrrgpu_grid_out* out);
 
 /* ---- data preparation (dataset.hpp standardize, strategies.hpp auto_sigma_grid) */
 
@@ -276,6 +338,11 @@ int pkrrgpu_last_timings(const pkrrgpu_ctx* ctx, double* ms, int n);
 /* The context's launch stream (cudaStream_t), so callers can time calls with
  * CUDA events on the stream the engine launches on. */
 void* pkrrgpu_stream(pkrrgpu_ctx* ctx);
+
+/* Order the context's launch stream after all work already queued on `stream` (a
+ * cudaStream_t of the caller, e.g. torch's current stream) -- for device-pointer inputs
+ * still being produced there.  Every call reads its inputs on the launch stream. */
+int pkrrgpu_wait_stream(pkrrgpu_ctx* ctx, void* stream);
 
 /* FP64 tensor-core peak probe: a DMMA (mma.sync m8n8k4 f64) loop over every
  * SM; *tflops = measured dense FP64 TFLOP/s (roofline denominator). */

@@ -13,15 +13,31 @@
 //   int           nearest_center(centers, x)                clustering.hpp:44-45
 //   PartitionSet  make_partition(kind, train, p, seed)      strategies.hpp:40-41
 //   TrainedPartitions train_partitions(ps, train, spec, lambda, workers)  :50-52
+//   double        predict_nearest(models, centers, x, ops)  strategies.hpp:56-58
+//   double        predict_average(models, x, ops)           :54-55
+//   pair          predict_oracle(models, x, y_true, ops)    :59-62
 //   GridResult    grid_search(kind, train, test, p, lambdas, sigmas, seed, options)  :117-120
 //
+// Batched GPU-resident forms of the predict stage: DeviceModels (train_partitions_device)
+// with predict_nearest(DeviceModels, Q) / predict(DeviceModels, t, Q), and
+// predict_nearest(models, centers, const Dataset& Q) over host KrrModels.
+//
+// Devices: every call runs on default_group() -- one engine context per GPU (env
+// PKRR_GPUS = a count "4" or a device list "0,1,2,3"; default: every visible GPU) with
+// one host thread per GPU.  grid_search shards the parts over the group's GPUs (bitwise
+// the one-GPU result), so the reference's multi-worker callers (cmd_run, cmd_weak_scaling,
+// experiment.cpp:107-110,272-274) scale over the GPUs unchanged.  Single-matrix calls use
+// the group's first GPU.
 // The analytic OpCount charges follow the reference accounting exactly
 // (kernel.cpp:68-79, solver.cpp:39-42/67-70, strategies.cpp:285-329/420-452), so
 // counters, messages, bytes and modeled_seconds in GridResult are identical.
 // Requires the reference headers on the include path and libpkrr_gpu.so at link.
 #pragma once
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <span>
 #include <stdexcept>
@@ -38,26 +54,62 @@
 
 namespace pkrr::gpu {
 
-// ---- engine handle (one per device; the default engine uses device 0) -------
-class Engine {
+// ---- engine handles ----------------------------------------------------------
+// One context per GPU, one host thread per GPU inside the library (pkrrgpu_multi).
+class Group {
  public:
-  explicit Engine(int device = 0) {
-    if (pkrrgpu_create(device, &ctx_) != PKRRGPU_OK)
+  explicit Group(const std::vector<int>& devices) {
+    if (pkrrgpu_multi_create(devices.data(), static_cast<int>(devices.size()), &m_) != PKRRGPU_OK)
       throw std::runtime_error(std::string("pkrr-gpu: ") + pkrrgpu_last_error());
   }
-  ~Engine() { pkrrgpu_destroy(ctx_); }
-  Engine(const Engine&) = delete;
-  Engine& operator=(const Engine&) = delete;
-  pkrrgpu_ctx* get() const { return ctx_; }
+  ~Group() { pkrrgpu_multi_destroy(m_); }
+  Group(const Group&) = delete;
+  Group& operator=(const Group&) = delete;
+  pkrrgpu_multi* get() const { return m_; }
+  int size() const { return pkrrgpu_multi_size(m_); }
+  pkrrgpu_ctx* context(int i = 0) const { return pkrrgpu_multi_context(m_, i); }
 
  private:
-  pkrrgpu_ctx* ctx_ = nullptr;
+  pkrrgpu_multi* m_ = nullptr;
 };
 
-inline Engine& default_engine() {
-  static Engine e(0);
-  return e;
+namespace detail {
+inline std::vector<int> default_devices() {
+  std::vector<int> devs;
+  if (const char* e = std::getenv("PKRR_GPUS")) {
+    const std::string s(e);
+    if (s.find(',') == std::string::npos) {
+      const int n = std::atoi(s.c_str());
+      for (int i = 0; i < n; ++i) devs.push_back(i);
+    } else {
+      std::size_t at = 0;
+      while (at <= s.size()) {
+        const std::size_t c = s.find(',', at);
+        devs.push_back(std::atoi(s.substr(at, c == std::string::npos ? std::string::npos : c - at).c_str()));
+        if (c == std::string::npos) break;
+        at = c + 1;
+      }
+    }
+  }
+  if (devs.empty()) {
+    const int n = pkrrgpu_device_count();
+    for (int i = 0; i < (n > 0 ? n : 1); ++i) devs.push_back(i);
+  }
+  return devs;
 }
+}  // namespace detail
+
+inline Group& default_group() {
+  static Group g(detail::default_devices());
+  return g;
+}
+
+// the group's first context (single-matrix primitives)
+struct EngineRef {
+  pkrrgpu_ctx* ctx;
+  pkrrgpu_ctx* get() const { return ctx; }
+};
+inline EngineRef default_engine() { return EngineRef{default_group().context(0)}; }
 
 namespace detail {
 
@@ -328,27 +380,256 @@ inline PartitionSet make_partition(StrategyKind kind, const Dataset& train, std:
   return ps;
 }
 
-inline TrainedPartitions train_partitions(const PartitionSet& ps, const Dataset& train, const KernelSpec& spec,
-                                          double lambda, std::size_t workers = 1) {
-  (void)workers;  // one GPU engine; parts run concurrently on device streams
+namespace detail {
+// OpCount charges of train_krr (solver.cpp:89-125): gram + shift + factor + solves
+inline OpCount train_ops(const Dataset& data) {
+  OpCount local;
+  std::uint64_t f = 0;
+  for (std::size_t i = 0; i < data.n; ++i) f += 2 * data.row(i).nnz();
+  for (std::size_t i = 0; i < data.n; ++i)
+    for (std::size_t j = i; j < data.n; ++j) f += gauss_pair_flops(data.row(i).nnz(), data.row(j).nnz());
+  local.gram_flops = f;
+  const std::uint64_t mu = data.n;
+  local.solve_flops = mu + mu * (mu + 1) * (2 * mu + 1) / 6 + 2 * mu * mu;
+  return local;
+}
+
+// KrrModel::predict charges for one row (solver.cpp:74-87)
+inline std::uint64_t predict_row_flops(const KrrModel& m, SparseRow x) {
+  std::uint64_t f = 2 * x.nnz();
+  for (std::size_t i = 0; i < m.support.n; ++i) f += gauss_pair_flops(m.support.row(i).nnz(), x.nnz()) + 2;
+  return f;
+}
+
+// ps.parts concatenated + their sizes (the C ABI's PartitionSet)
+inline void part_lists(const PartitionSet& ps, std::vector<int64_t>& rows, std::vector<int64_t>& sizes) {
+  for (const auto& part : ps.parts) {
+    sizes.push_back(static_cast<int64_t>(part.size()));
+    for (std::size_t i : part) rows.push_back(static_cast<int64_t>(i));
+  }
+}
+
+inline std::vector<double> flat_centers(const std::vector<std::vector<double>>& centers) {
+  std::vector<double> C;
+  for (const auto& c : centers) C.insert(C.end(), c.begin(), c.end());
+  return C;
+}
+}  // namespace detail
+
+// GPU-resident TrainedPartitions: support rows, norms and alpha stay in HBM for the
+// batched predict stage (pkrrgpu_models).
+class DeviceModels {
+ public:
+  DeviceModels(pkrrgpu_ctx* ctx, pkrrgpu_models* h, std::size_t d) : ctx_(ctx), h_(h), d_(d) {}
+  ~DeviceModels() { pkrrgpu_models_free(h_); }
+  DeviceModels(const DeviceModels&) = delete;
+  DeviceModels& operator=(const DeviceModels&) = delete;
+  DeviceModels(DeviceModels&& o) noexcept : ctx_(o.ctx_), h_(o.h_), d_(o.d_) { o.h_ = nullptr; }
+  pkrrgpu_models* get() const { return h_; }
+  pkrrgpu_ctx* context() const { return ctx_; }
+  std::size_t d() const { return d_; }
+  std::size_t size() const { return static_cast<std::size_t>(pkrrgpu_models_count(h_)); }
+  std::vector<double> alpha(std::size_t t) const {
+    std::vector<double> a(static_cast<std::size_t>(pkrrgpu_models_size(h_, static_cast<int64_t>(t))));
+    detail::check(pkrrgpu_models_alpha(h_, static_cast<int64_t>(t), a.data()));
+    return a;
+  }
+  double residual(std::size_t t) const {
+    double r = 0.0;
+    detail::check(pkrrgpu_models_residual(h_, static_cast<int64_t>(t), &r));
+    return r;
+  }
+
+ private:
+  pkrrgpu_ctx* ctx_;
+  pkrrgpu_models* h_;
+  std::size_t d_;
+};
+
+// train_partitions with the caller's PartitionSet, every part concurrently on the GPU
+// (strategies.cpp:104-133); the models stay on the device.
+inline DeviceModels train_partitions_device(const PartitionSet& ps, const Dataset& train, const KernelSpec& spec,
+                                            double lambda) {
+  detail::require_gaussian(spec);
+  if (!(lambda > 0.0)) throw std::invalid_argument("train_krr: lambda must be > 0");
   for (const auto& part : ps.parts)
     if (part.empty()) throw std::invalid_argument("train_partitions: empty part");
+  const std::vector<double> X = detail::dense(train);
+  std::vector<int64_t> rows, sizes;
+  detail::part_lists(ps, rows, sizes);
+  const std::vector<double> C = detail::flat_centers(ps.centers);
+  pkrrgpu_models* h = nullptr;
+  int64_t failed = -1, piv = -1;
+  pkrrgpu_ctx* ctx = default_engine().get();
+  const int rc = pkrrgpu_train_parts(ctx, X.data(), train.y.data(), train.n, train.d, rows.data(), sizes.data(),
+                                     ps.p, ps.has_centers() ? C.data() : nullptr, spec.sigma, lambda, &h, &failed,
+                                     &piv);
+  if (rc == PKRRGPU_NPD)  // train_partitions aggregates solver failures by part (strategies.cpp:119-125)
+    throw std::runtime_error("partition " + std::to_string(failed) + ": " + pkrrgpu_last_error());
+  detail::check(rc, piv);
+  return DeviceModels(ctx, h, train.d);
+}
+
+inline TrainedPartitions train_partitions(const PartitionSet& ps, const Dataset& train, const KernelSpec& spec,
+                                          double lambda, std::size_t workers = 1) {
+  (void)workers;  // every part runs concurrently on the device's streams
+  const DeviceModels dm = train_partitions_device(ps, train, spec, lambda);
   TrainedPartitions out;
-  std::string failures;
   out.stats.per_task.resize(ps.p);
   for (std::size_t t = 0; t < ps.p; ++t) {
-    try {
-      out.models.push_back(gpu::train_krr(subset(train, ps.parts[t]), spec, lambda, &out.stats.per_task[t].ops));
-    } catch (const std::exception& e) {
-      out.models.emplace_back();
-      if (!failures.empty()) failures += "; ";
-      failures += "partition " + std::to_string(t) + ": " + e.what();
-    }
+    KrrModel model;
+    model.support = subset(train, ps.parts[t]);
+    model.support_sq_norms.resize(model.support.n);
+    for (std::size_t i = 0; i < model.support.n; ++i) model.support_sq_norms[i] = squared_norm(model.support.row(i));
+    model.alpha = dm.alpha(t);
+    model.residual_ratio = dm.residual(t);
+    model.kernel = spec;
+    model.lambda = lambda;
+    model.train_ops = detail::train_ops(model.support);
+    out.stats.per_task[t].ops = model.train_ops;
+    if (ps.has_centers()) model.center = ps.centers[t];
+    out.models.push_back(std::move(model));
   }
-  if (!failures.empty()) throw std::runtime_error(failures);
   out.stats.finalize();
-  if (ps.has_centers())
-    for (std::size_t t = 0; t < ps.p; ++t) out.models[t].center = ps.centers[t];
+  return out;
+}
+
+// ---- predict stage (strategies.hpp:54-62, solver.hpp:48), batched on the GPU --------
+namespace detail {
+inline std::vector<double> dense_rows(const Dataset& Q, std::size_t d) {
+  std::vector<double> X(Q.n * d, 0.0);
+  for (std::size_t i = 0; i < Q.n; ++i) {
+    const SparseRow r = Q.row(i);
+    for (std::size_t k = 0; k < r.nnz(); ++k)
+      if (static_cast<std::size_t>(r.idx[k]) < d) X[i * d + r.idx[k]] = r.val[k];
+  }
+  return X;
+}
+
+// host KrrModels -> device models (support rows, alpha, centers)
+inline DeviceModels import_models(std::span<const KrrModel> models, const std::vector<std::vector<double>>* centers) {
+  if (models.empty()) throw std::invalid_argument("predict: no models");
+  const std::size_t d = models[0].support.d;
+  std::vector<int64_t> sizes;
+  std::vector<double> S, A;
+  double sigma = models[0].kernel.sigma;
+  for (const KrrModel& m : models) {
+    require_gaussian(m.kernel);
+    if (m.kernel.sigma != sigma) throw std::invalid_argument("pkrr-gpu: models with different kernels");
+    sizes.push_back(static_cast<int64_t>(m.support.n));
+    const std::vector<double> X = dense_rows(m.support, d);
+    S.insert(S.end(), X.begin(), X.end());
+    A.insert(A.end(), m.alpha.begin(), m.alpha.end());
+  }
+  const std::vector<double> C = centers ? flat_centers(*centers) : std::vector<double>{};
+  pkrrgpu_models* h = nullptr;
+  pkrrgpu_ctx* ctx = default_engine().get();
+  check(pkrrgpu_models_import(ctx, static_cast<int64_t>(models.size()), d, sizes.data(), S.data(), A.data(),
+                              centers ? C.data() : nullptr, sigma, &h));
+  return DeviceModels(ctx, h, d);
+}
+}  // namespace detail
+
+// nearest-centre routed predictions of every row of Q over GPU-resident models
+inline std::vector<double> predict_nearest(const DeviceModels& models, const Dataset& Q) {
+  std::vector<double> out(Q.n);
+  if (Q.n == 0) return out;
+  const std::vector<double> X = detail::dense_rows(Q, models.d());
+  detail::check(pkrrgpu_predict_nearest(models.context(), models.get(), X.data(), Q.n, out.data()));
+  return out;
+}
+
+// KrrModel::predict of model t over every row of Q
+inline std::vector<double> predict(const DeviceModels& models, std::size_t t, const Dataset& Q) {
+  std::vector<double> out(Q.n);
+  if (Q.n == 0) return out;
+  const std::vector<double> X = detail::dense_rows(Q, models.d());
+  detail::check(pkrrgpu_models_predict(models.context(), models.get(), static_cast<int64_t>(t), X.data(), Q.n,
+                                       out.data()));
+  return out;
+}
+
+// predict_nearest (strategies.cpp:142-149) over host models, every row of Q at once;
+// OpCount charged as the reference's per-row calls would
+inline std::vector<double> predict_nearest(std::span<const KrrModel> models,
+                                           const std::vector<std::vector<double>>& centers, const Dataset& Q,
+                                           OpCount* ops = nullptr) {
+  if (models.empty()) throw std::invalid_argument("predict_nearest: no models");
+  if (centers.size() != models.size())
+    throw std::invalid_argument("predict_nearest: centers undefined for this partitioning");
+  const DeviceModels dm = detail::import_models(models, &centers);
+  std::vector<double> out = predict_nearest(dm, Q);
+  if (ops) {
+    const std::vector<double> C = detail::flat_centers(centers), X = detail::dense_rows(Q, dm.d());
+    std::vector<int32_t> route(Q.n);
+    detail::check(pkrrgpu_nearest_center(dm.context(), C.data(), static_cast<int>(centers.size()), dm.d(), X.data(),
+                                         Q.n, route.data()));
+    for (std::size_t j = 0; j < Q.n; ++j) ops->predict_flops += detail::predict_row_flops(models[route[j]], Q.row(j));
+  }
+  return out;
+}
+
+// drop-in single-row form (strategies.hpp:56-58)
+inline double predict_nearest(std::span<const KrrModel> models, const std::vector<std::vector<double>>& centers,
+                              SparseRow x, OpCount* ops = nullptr) {
+  Dataset q;
+  q.d = models.empty() ? 0 : models[0].support.d;
+  q.add_row(std::vector<int>(x.idx.begin(), x.idx.end()), std::span<const double>(x.val.data(), x.val.size()), 0.0);
+  q.d = models.empty() ? 0 : models[0].support.d;
+  return predict_nearest(models, centers, q, ops)[0];
+}
+
+// predict_average (strategies.cpp:135-140): the models' predictions summed in model order / p
+inline std::vector<double> predict_average(std::span<const KrrModel> models, const Dataset& Q, OpCount* ops = nullptr) {
+  if (models.empty()) throw std::invalid_argument("predict_average: no models");
+  const DeviceModels dm = detail::import_models(models, nullptr);
+  const std::vector<double> X = detail::dense_rows(Q, dm.d());
+  std::vector<double> pp(models.size() * Q.n);
+  if (Q.n) detail::check(pkrrgpu_models_predict(dm.context(), dm.get(), -1, X.data(), Q.n, pp.data()));
+  std::vector<double> out(Q.n);
+  for (std::size_t j = 0; j < Q.n; ++j) {
+    double sum = 0.0;
+    for (std::size_t t = 0; t < models.size(); ++t) {
+      sum += pp[t * Q.n + j];
+      if (ops) ops->predict_flops += detail::predict_row_flops(models[t], Q.row(j));
+    }
+    out[j] = sum / static_cast<double>(models.size());
+  }
+  return out;
+}
+
+inline double predict_average(std::span<const KrrModel> models, SparseRow x, OpCount* ops = nullptr) {
+  Dataset q;
+  q.d = models.empty() ? 0 : models[0].support.d;
+  q.add_row(std::vector<int>(x.idx.begin(), x.idx.end()), std::span<const double>(x.val.data(), x.val.size()), 0.0);
+  q.d = models.empty() ? 0 : models[0].support.d;
+  return predict_average(models, q, ops)[0];
+}
+
+// predict_oracle (strategies.cpp:151-166): the least-squared-error model per row
+inline std::vector<std::pair<double, std::size_t>> predict_oracle(std::span<const KrrModel> models, const Dataset& Q,
+                                                                  OpCount* ops = nullptr) {
+  if (models.empty()) throw std::invalid_argument("predict_oracle: no models");
+  const DeviceModels dm = detail::import_models(models, nullptr);
+  const std::vector<double> X = detail::dense_rows(Q, dm.d());
+  std::vector<double> pp(models.size() * Q.n);
+  if (Q.n) detail::check(pkrrgpu_models_predict(dm.context(), dm.get(), -1, X.data(), Q.n, pp.data()));
+  std::vector<std::pair<double, std::size_t>> out(Q.n);
+  for (std::size_t j = 0; j < Q.n; ++j) {
+    double best_pred = 0.0, best_err = std::numeric_limits<double>::infinity();
+    std::size_t best_t = 0;
+    for (std::size_t t = 0; t < models.size(); ++t) {
+      const double pred = pp[t * Q.n + j];
+      const double err = (pred - Q.y[j]) * (pred - Q.y[j]);
+      if (ops) ops->predict_flops += detail::predict_row_flops(models[t], Q.row(j));
+      if (err < best_err) {
+        best_err = err;
+        best_pred = pred;
+        best_t = t;
+      }
+    }
+    out[j] = {best_pred, best_t};
+  }
   return out;
 }
 
@@ -356,7 +637,7 @@ inline TrainedPartitions train_partitions(const PartitionSet& ps, const Dataset&
 // the counters reproduce the reference's accounting (:285-329, :420-452).
 inline GridResult grid_search(StrategyKind kind, const Dataset& train, const Dataset& test, std::size_t p,
                               std::span<const double> lambdas, std::span<const double> sigmas, std::uint64_t seed,
-                              const GridOptions& options = {}) {
+                              const GridOptions& options = {}, Group& group = default_group()) {
   if (lambdas.empty() || sigmas.empty()) throw std::invalid_argument("grid_search: empty grid");
   if (train.n == 0 || test.n == 0) throw std::invalid_argument("grid_search: empty dataset");
   detail::require_gaussian(options.base_kernel);
@@ -381,7 +662,7 @@ inline GridResult grid_search(StrategyKind kind, const Dataset& train, const Dat
   a.sigmas = sigmas.data();
   a.n_sigmas = static_cast<int64_t>(ns);
   a.seed = seed;
-  a.world = 1;
+  a.world = 1;  // the group shards the parts over its GPUs itself
   pkrrgpu_grid_out o{};
   o.cell_mse = cmse.data();
   o.cell_failed = cfail.data();
@@ -390,9 +671,13 @@ inline GridResult grid_search(StrategyKind kind, const Dataset& train, const Dat
   o.part_residual = pres.data();
   o.part_sizes = psizes.data();
   o.part_test_count = ptest.data();
-  detail::check(pkrrgpu_grid_search_ex(default_engine().get(), &a, &o));
+  detail::check(pkrrgpu_multi_grid_search(group.get(), &a, &o));
   double ms[8] = {0};
-  pkrrgpu_last_timings(default_engine().get(), ms, 8);
+  for (int g = 0; g < group.size(); ++g) {  // device time: the slowest GPU's
+    double mg[8] = {0};
+    pkrrgpu_last_timings(group.context(g), mg, 8);
+    if (mg[3] > ms[3]) std::copy(mg, mg + 8, ms);
+  }
 
   GridResult r;
   r.kind = kind;

@@ -333,6 +333,27 @@ class Reference(_Base):
                                      _d, _d)
         self._sigma_grid = self._fn("auto_sigma_grid", C.c_int, _d, C.c_int64, C.c_int64, C.c_uint64, _d)
         self._libsvm = self._fn("load_libsvm", C.c_int, C.c_char_p, _i64, _i64, _i64, _i64, _i32, _d, _d)
+        self._tpp = self._fn("train_partitions_predict", C.c_int, _d, _d, C.c_int64, C.c_int64, _i32, C.c_int64,
+                             _d, C.c_double, C.c_double, C.c_int64, _d, C.c_int64, _d, _d, _d, _d)
+
+    def train_partitions_predict(self, Xtr, ytr, part_of, p, centers, sigma, lam, Q, workers=1):
+        """strategies.cpp:104-149 with a caller-given partition: train_partitions(ps, ...)
+        then predict_nearest (centers given) / the single model.  Returns (alpha
+        concatenated part by part, residual[p], predictions[q], task seconds[p])."""
+        Xtr, ytr, Q = _f64(Xtr), _f64(ytr), _f64(Q)
+        part_of = np.ascontiguousarray(part_of, np.int32)
+        n, d = Xtr.shape
+        cen = None if centers is None else _f64(centers)
+        alpha, res, sec = np.empty(n), np.empty(p), np.empty(p)
+        pred = np.empty(Q.shape[0])
+        st = self._tpp(_p(Xtr, _d), _p(ytr, _d), n, d, _p(part_of, _i32), p, None if cen is None else _p(cen, _d),
+                       sigma, lam, workers, _p(Q, _d), Q.shape[0], _p(alpha, _d), _p(res, _d), _p(pred, _d),
+                       _p(sec, _d))
+        if st == 2:
+            raise NotPositiveDefinite(-1)
+        if st:
+            raise RuntimeError(self._err().decode())
+        return alpha, res, pred, sec
 
     def load_libsvm(self, path):
         """dataset.cpp:83-125: (row_ptr, col, val, y, d) exactly as the reference's Dataset."""

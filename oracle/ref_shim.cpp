@@ -276,6 +276,49 @@ int ref_train_predict_nearest(int kind, const double* Xtr, const double* ytr, in
   }
 }
 
+// The 4-stage API with a caller-given partition (strategies.hpp:50-58): the PartitionSet
+// is rebuilt from part_of (rows in train row order, strategies.cpp:97-99), trained by the
+// reference's train_partitions(ps, train, spec, lambda, workers), and q query rows are
+// predicted by predict_nearest (centers given) or the single model (p == 1, no centers).
+// alpha_out: the parts' alphas concatenated in part order (n entries); residual_out[p],
+// seconds_out[p] (the per-task wall clocks of run_partitions, runtime.hpp:85-90).
+int ref_train_partitions_predict(const double* Xtr, const double* ytr, int64_t n, int64_t d,
+                                 const int32_t* part_of, int64_t p, const double* centers,
+                                 double sigma, double lambda, int64_t workers, const double* Q,
+                                 int64_t q, double* alpha_out, double* residual_out,
+                                 double* pred_out, double* seconds_out) {
+  try {
+    const Dataset train = dense(Xtr, ytr, n, d);
+    PartitionSet ps;
+    ps.p = static_cast<std::size_t>(p);
+    ps.parts.assign(ps.p, {});
+    for (int64_t i = 0; i < n; ++i) ps.parts[part_of[i]].push_back(static_cast<std::size_t>(i));
+    if (centers)
+      for (int64_t t = 0; t < p; ++t) ps.centers.emplace_back(centers + t * d, centers + (t + 1) * d);
+    const TrainedPartitions tp =
+        train_partitions(ps, train, gauss(sigma), lambda, static_cast<std::size_t>(workers < 1 ? 1 : workers));
+    int64_t at = 0;
+    for (int64_t t = 0; t < p; ++t) {
+      const auto& a = tp.models[t].alpha;
+      std::memcpy(alpha_out + at, a.data(), sizeof(double) * a.size());
+      at += static_cast<int64_t>(a.size());
+      if (residual_out) residual_out[t] = tp.models[t].residual_ratio;
+      if (seconds_out) seconds_out[t] = tp.stats.per_task[t].wall_seconds;
+    }
+    const Dataset qs = dense(Q, nullptr, q, d);
+    for (int64_t j = 0; j < q; ++j)
+      pred_out[j] = centers ? predict_nearest(tp.models, ps.centers, qs.row(j))
+                            : tp.models[0].predict(qs.row(j));
+    return 0;
+  } catch (const NotPositiveDefinite& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
 // dataset.cpp:199-232 through the reference's own standardize (dense rows in)
 int ref_standardize(const double* Xtr, int64_t n, int64_t d, const double* Xte, int64_t t, double* Xtr_out,
                     double* Xte_out, double* mean, double* stddev) {

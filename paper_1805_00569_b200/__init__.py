@@ -77,7 +77,8 @@ class GridOut(C.Structure):
                 ("part_test_count", C.c_void_p), ("part_eval_count", C.c_void_p), ("part_of", C.c_void_p),
                 ("centers", C.c_void_p), ("part_sizes", C.c_void_p), ("best_pred", C.c_void_p),
                 ("best_eval_pred", C.c_void_p), ("p_effective", C.c_int64), ("flops_chol", C.c_double),
-                ("flops_gram", C.c_double), ("flops_other", C.c_double)]
+                ("flops_gram", C.c_double), ("flops_other", C.c_double), ("cell_pred", C.c_void_p),
+                ("cell_eval_pred", C.c_void_p), ("pred_rows", C.c_int64)]
 
 
 _lib = None
@@ -142,6 +143,23 @@ def load_library(path: str = LIB_PATH):
         "pkrrgpu_stream": (C.c_void_p, [C.c_void_p]),
         "pkrrgpu_fp64_peak": (C.c_int, [C.c_void_p, _d]),
         "pkrrgpu_probe_potrf": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, _d]),
+        "pkrrgpu_wait_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
+        "pkrrgpu_train_parts": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
+                                          C.c_void_p, C.c_int64, C.c_void_p, C.c_double, C.c_double,
+                                          C.POINTER(C.c_void_p), _i64, _i64]),
+        "pkrrgpu_device_count": (C.c_int, []),
+        "pkrrgpu_models_import": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.c_void_p, C.c_double, C.POINTER(C.c_void_p)]),
+        "pkrrgpu_models_predict": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                             C.c_void_p]),
+        "pkrrgpu_models_centers": (C.c_int, [C.c_void_p, C.c_void_p]),
+        "pkrrgpu_combine": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p, _i64, C.c_void_p]),
+        "pkrrgpu_multi_create": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+        "pkrrgpu_multi_destroy": (None, [C.c_void_p]),
+        "pkrrgpu_multi_size": (C.c_int, [C.c_void_p]),
+        "pkrrgpu_multi_context": (C.c_void_p, [C.c_void_p, C.c_int]),
+        "pkrrgpu_multi_grid_search": (C.c_int, [C.c_void_p, C.POINTER(GridArgs), C.POINTER(GridOut)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -184,10 +202,21 @@ def _ptr(a):
     return a.ctypes.data, a
 
 
-def _f64(a):
-    if a is None or hasattr(a, "data_ptr"):
-        return a
-    return np.ascontiguousarray(a, dtype=np.float64)
+def _f64(a, device=None, dtype=np.float64):
+    """An FP64 (or `dtype`) C-contiguous view the engine can read: numpy arrays are
+    converted on the host; torch CUDA tensors are converted to `dtype` on the engine's
+    device (a float32 tensor or a tensor on another GPU is never reinterpreted); torch
+    CPU tensors become numpy arrays."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        import torch
+        tdt = {np.float64: torch.float64, np.int32: torch.int32}[dtype]
+        if a.is_cuda:
+            dev = torch.device("cuda", a.device.index if device is None else device)
+            return a.to(device=dev, dtype=tdt).contiguous()
+        return np.ascontiguousarray(a.numpy(), dtype=dtype)
+    return np.ascontiguousarray(a, dtype=dtype)
 
 
 def _open_libsvm(path, threads=0):
@@ -227,6 +256,8 @@ class Engine:
         self.device = device
 
     def close(self):
+        if getattr(self, "_borrowed", False):  # a Group's context: the group destroys it
+            self._h = None
         if getattr(self, "_h", None):
             _lib.pkrrgpu_destroy(self._h)
             self._h = None
@@ -236,6 +267,16 @@ class Engine:
             self.close()
         except Exception:
             pass
+
+    def _in(self, a, dtype=np.float64):
+        """Caller array -> engine input.  A CUDA tensor may still be written by work
+        queued on torch's current stream: the engine's launch stream is ordered after it
+        (pkrrgpu_wait_stream) before any kernel reads the tensor."""
+        a = self._in(a, self.device, dtype)
+        if a is not None and hasattr(a, "data_ptr"):
+            import torch
+            _check(_lib.pkrrgpu_wait_stream(self._h, torch.cuda.current_stream(a.device).cuda_stream))
+        return a
 
     @property
     def launches(self) -> int:
@@ -273,9 +314,9 @@ class Engine:
 
     # ---- kernel.hpp ---------------------------------------------------------
     def gram(self, X, Y, sigma):
-        X = _f64(X)
+        X = self._in(X)
         same = Y is None or Y is X
-        Y = X if same else _f64(Y)
+        Y = X if same else self._in(Y)
         na, d = X.shape
         nb = Y.shape[0]
         K = np.empty((na, nb))
@@ -285,14 +326,14 @@ class Engine:
         return K
 
     def assemble_system(self, K, lam, m):
-        K = _f64(K)
+        K = self._in(K)
         A = np.empty_like(K)
         _check(_lib.pkrrgpu_assemble(self._h, K.ctypes.data, K.shape[0], float(lam), int(m), A.ctypes.data))
         return A
 
     # ---- solver.hpp ---------------------------------------------------------
     def cholesky(self, A):
-        A = _f64(A)
+        A = self._in(A)
         L = np.empty_like(A)
         piv = C.c_int64(-1)
         rc = _lib.pkrrgpu_cholesky(self._h, A.ctypes.data, A.shape[0], L.ctypes.data, C.byref(piv))
@@ -300,13 +341,13 @@ class Engine:
         return L
 
     def solve_spd(self, L, b):
-        L, b = _f64(L), _f64(b)
+        L, b = self._in(L), self._in(b)
         x = np.empty(L.shape[0])
         _check(_lib.pkrrgpu_solve_spd(self._h, L.ctypes.data, L.shape[0], b.ctypes.data, x.ctypes.data))
         return x
 
     def train_krr(self, X, y, sigma, lam):
-        X, y = _f64(X), _f64(y)
+        X, y = self._in(X), self._in(y)
         m, d = X.shape
         alpha = np.empty(m)
         res = C.c_double(0)
@@ -320,7 +361,7 @@ class Engine:
                         alpha=alpha, sigma=float(sigma), lam=float(lam), residual_ratio=res.value, engine=self)
 
     def predict(self, S, alpha, sigma, Q):
-        S, alpha, Q = _f64(S), _f64(alpha), _f64(Q)
+        S, alpha, Q = self._in(S), self._in(alpha), self._in(Q)
         out = np.empty(Q.shape[0])
         _check(_lib.pkrrgpu_predict(self._h, S.ctypes.data, alpha.ctypes.data, S.shape[0], S.shape[1],
                                     float(sigma), Q.ctypes.data, Q.shape[0], out.ctypes.data))
@@ -328,7 +369,7 @@ class Engine:
 
     # ---- clustering.hpp -----------------------------------------------------
     def kmeans(self, X, k, seed, threshold=0.01, max_iters=100):
-        X = _f64(X)
+        X = self._in(X)
         n, d = X.shape
         mem = np.empty(n, np.int32)
         cen = np.empty((k, d))
@@ -340,7 +381,7 @@ class Engine:
         return Clustering(k=k, centers=cen, membership=mem, sizes=sz, iterations=it.value)
 
     def kbalance(self, X, k, seed, threshold=0.01, max_iters=100, recompute_centers=True):
-        X = _f64(X)
+        X = self._in(X)
         n, d = X.shape
         mem = np.empty(n, np.int32)
         cen = np.empty((k, d))
@@ -351,7 +392,7 @@ class Engine:
         return Clustering(k=k, centers=cen, membership=mem, sizes=sz)
 
     def nearest_center(self, centers, Q):
-        centers, Q = _f64(centers), _f64(Q)
+        centers, Q = self._in(centers), self._in(Q)
         single = Q.ndim == 1
         Q2 = Q.reshape(1, -1) if single else Q
         out = np.empty(Q2.shape[0], np.int32)
@@ -381,9 +422,9 @@ class Engine:
     # ---- dataset.hpp / strategies.hpp data preparation ------------------------
     def standardize(self, X_train, X_test=None):
         """dataset.cpp:199-232: (train_std, test_std, mean, stddev), bitwise the reference's."""
-        X = _f64(X_train)
+        X = self._in(X_train)
         n, d = X.shape
-        T = np.zeros((0, d)) if X_test is None else _f64(X_test)
+        T = np.zeros((0, d)) if X_test is None else self._in(X_test)
         tr, te = np.empty_like(X), np.empty_like(T)
         mean, sd = np.empty(d), np.empty(d)
         _check(_lib.pkrrgpu_standardize(self._h, X.ctypes.data, n, d, T.ctypes.data if T.size else None,
@@ -393,7 +434,7 @@ class Engine:
 
     def auto_sigma_grid(self, X, seed):
         """strategies.cpp:204-234: the 9-point sigma grid around the median distance."""
-        X = _f64(X)
+        X = self._in(X)
         g = np.empty(9)
         _check(_lib.pkrrgpu_auto_sigma_grid(self._h, X.ctypes.data if X.size else None, X.shape[0],
                                             X.shape[1] if X.ndim == 2 else 0, int(seed), g.ctypes.data))
@@ -401,7 +442,7 @@ class Engine:
 
     # ---- strategies.hpp -----------------------------------------------------
     def make_partition(self, strategy, X, p, seed):
-        X = _f64(X)
+        X = self._in(X)
         n, d = X.shape
         part = np.empty(n, np.int32)
         order = np.empty(n, np.int64)
@@ -420,7 +461,7 @@ class Engine:
         return PartitionSet(p=pe, parts=parts, centers=cen[:pe] if has_c else None)
 
     def train_partitions(self, strategy, X, y, p, seed, sigma, lam):
-        X, y = _f64(X), _f64(y)
+        X, y = self._in(X), self._in(y)
         n, d = X.shape
         h = C.c_void_p()
         fp, piv = C.c_int64(-1), C.c_int64(-1)
@@ -431,9 +472,45 @@ class Engine:
         _check(rc, piv.value)
         return TrainedPartitions(self, h)
 
+    def train_parts(self, X, y, parts, sigma, lam, centers=None):
+        """train_partitions(ps, train, spec, lambda) with the caller's PartitionSet
+        (strategies.cpp:104-133): `parts` = a list of row-index arrays (ps.parts, each in
+        its own order) or a PartitionSet."""
+        if isinstance(parts, PartitionSet):
+            centers = parts.centers if centers is None else centers
+            parts = parts.parts
+        X, y = self._in(X), self._in(y)
+        rows = np.ascontiguousarray(np.concatenate([np.asarray(q, np.int64) for q in parts]), np.int64)
+        sizes = np.ascontiguousarray([len(q) for q in parts], np.int64)
+        cen = self._in(centers) if centers is not None else None
+        n, d = X.shape
+        h = C.c_void_p()
+        fp, piv = C.c_int64(-1), C.c_int64(-1)
+        px, kx = _ptr(X)
+        py, ky = _ptr(y)
+        pc, kc = _ptr(cen)
+        rc = _lib.pkrrgpu_train_parts(self._h, px, py, n, d, rows.ctypes.data, sizes.ctypes.data, len(parts), pc,
+                                      float(sigma), float(lam), C.byref(h), C.byref(fp), C.byref(piv))
+        _check(rc, piv.value)
+        return TrainedPartitions(self, h)
+
+    def combine(self, strategy, p, pred, y, failed=None):
+        """pkrrgpu_combine: cell combine + reference-order MSE + best cell over gathered
+        per-cell predictions pred [ncell, P, t].  Returns (mse[ncell], best, best_pred)."""
+        pred = np.ascontiguousarray(pred, np.float64)
+        y = np.ascontiguousarray(y, np.float64)
+        nc, t = pred.shape[0], pred.shape[-1]
+        fl = np.zeros(nc, np.uint8) if failed is None else np.ascontiguousarray(failed, np.uint8)
+        mse_c = np.empty(nc)
+        best = C.c_int64(-1)
+        bp = np.zeros(t)
+        _check(_lib.pkrrgpu_combine(self._h, STRATEGIES[strategy], int(p), t, nc, pred.ctypes.data, y.ctypes.data,
+                                    fl.ctypes.data, mse_c.ctypes.data, C.byref(best), bp.ctypes.data))
+        return mse_c, int(best.value), bp
+
     def grid_search(self, strategy, train_X, train_y, test_X, test_y, p, lambdas, sigmas, seed, *,
                     eval_X=None, eval_y=None, km_threshold=0.01, km_max_iters=0, rank=0, world=1,
-                    want_partition=False, allgather=None):
+                    want_partition=False, allgather=None, group=None):
         """strategies.cpp:343-507.  Returns GridResult (cells lambda-major).
 
         allgather (world > 1): fn(dev_ptr, bytes_per_rank) all-gathering a device buffer
@@ -441,8 +518,8 @@ class Engine:
         k-means partition over the ranks (bitwise the single-process partition)."""
         lam = np.ascontiguousarray(lambdas, np.float64)
         sig = np.ascontiguousarray(sigmas, np.float64)
-        tX, ty, sX, sy = _f64(train_X), _f64(train_y), _f64(test_X), _f64(test_y)
-        eX, ey = _f64(eval_X), _f64(eval_y)
+        tX, ty, sX, sy = self._in(train_X), self._in(train_y), self._in(test_X), self._in(test_y)
+        eX, ey = self._in(eval_X), self._in(eval_y)
         n, d = tX.shape
         t = sX.shape[0]
         te = 0 if eX is None else eX.shape[0]
@@ -476,13 +553,22 @@ class Engine:
                    part_eval_sse=np.zeros(nc * pmax), part_failed=np.zeros(nc * pmax, np.uint8),
                    part_residual=np.zeros(nc * pmax), part_test_count=np.zeros(pmax, np.int64),
                    part_eval_count=np.zeros(pmax, np.int64), part_sizes=np.zeros(pmax, np.int64),
-                   best_pred=np.zeros(t), best_eval_pred=np.zeros(max(te, 1)))
+                   best_pred=np.zeros(t), best_eval_pred=np.zeros(max(te, 1)),
+                   cell_pred=np.zeros(nc * pmax * t), cell_eval_pred=np.zeros(nc * pmax * max(te, 1)))
         if want_partition:
             res["part_of"] = np.zeros(n, np.int32)
             res["centers"] = np.zeros((pmax, d))
         out = GridOut(**{k: v.ctypes.data for k, v in res.items()})
-        _check(_lib.pkrrgpu_grid_search_ex(self._h, C.byref(args), C.byref(out)))
+        if te == 0:
+            out.cell_eval_pred = None
+        if group is None:
+            _check(_lib.pkrrgpu_grid_search_ex(self._h, C.byref(args), C.byref(out)))
+        else:
+            _check(_lib.pkrrgpu_multi_grid_search(group, C.byref(args), C.byref(out)))
         pe = out.p_effective
+        P = out.pred_rows
+        res["cell_pred"] = res["cell_pred"][: nc * P * t].reshape(nc, P, t)
+        res["cell_eval_pred"] = res["cell_eval_pred"][: nc * P * te].reshape(nc, P, te) if te else None
         for k in ("part_sse", "part_eval_sse", "part_failed", "part_residual"):
             res[k] = res[k][: nc * pe].reshape(nc, pe)
         for k in ("part_test_count", "part_eval_count", "part_sizes"):
@@ -492,6 +578,47 @@ class Engine:
                           residual=res["cell_residual"], eval_mse=res["cell_eval_mse"] if te else None,
                           best_pred=res["best_pred"], best_eval_pred=res["best_eval_pred"][:te] if te else None,
                           parts=res, flops=dict(chol=out.flops_chol, gram=out.flops_gram, other=out.flops_other))
+
+
+class Group:
+    """Several GPUs in ONE process (pkrrgpu_multi): one engine context and one host
+    thread per device; grid_search shards the parts over the devices (LPT on m^3) and
+    returns the one-context result bitwise.  A device may repeat (two contexts on one GPU)."""
+
+    def __init__(self, devices):
+        lib = load_library()
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        _check(lib.pkrrgpu_multi_create(devs, len(devices), C.byref(h)))
+        self._h = h
+        self.devices = list(devices)
+        # engine facade on the first context (argument conversion, combine)
+        self.first = Engine.__new__(Engine)
+        self.first._borrowed = True
+        self.first._h = C.c_void_p(lib.pkrrgpu_multi_context(h, 0))
+        self.first.device = devices[0]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.first._h = None
+            _lib.pkrrgpu_multi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launches(self) -> int:
+        return sum(int(_lib.pkrrgpu_launch_count(_lib.pkrrgpu_multi_context(self._h, i)))
+                   for i in range(len(self.devices)))
+
+    def grid_search(self, strategy, train_X, train_y, test_X, test_y, p, lambdas, sigmas, seed, **kw):
+        kw.pop("rank", None), kw.pop("world", None), kw.pop("allgather", None)
+        return self.first.grid_search(strategy, train_X, train_y, test_X, test_y, p, lambdas, sigmas, seed,
+                                      group=self._h, **kw)
 
 
 @dataclass
@@ -558,10 +685,47 @@ class TrainedPartitions:
         return r.value
 
     def predict_nearest(self, Q):
+        """strategies.cpp:142-149 batched: route by nearest_center, predict with that model."""
         Q = np.ascontiguousarray(Q, np.float64)
         out = np.empty(Q.shape[0])
         _check(_lib.pkrrgpu_predict_nearest(self.engine._h, self._h, Q.ctypes.data, Q.shape[0], out.ctypes.data))
         return out
+
+    def predict(self, Q, part=-1):
+        """KrrModel::predict (solver.cpp:74-87) of model `part`, or of every model
+        ([p, q]) when part = -1."""
+        Q = np.ascontiguousarray(Q, np.float64)
+        rows = len(self) if part < 0 else 1
+        out = np.empty((rows, Q.shape[0]))
+        _check(_lib.pkrrgpu_models_predict(self.engine._h, self._h, int(part), Q.ctypes.data, Q.shape[0],
+                                           out.ctypes.data))
+        return out if part < 0 else out[0]
+
+    def predict_average(self, Q):
+        """strategies.cpp:135-140: sum of the models' predictions in model order / p."""
+        pp = self.predict(Q)
+        s = np.zeros(pp.shape[1])
+        for row in pp:
+            s = s + row
+        return s / float(pp.shape[0])
+
+    def predict_oracle(self, Q, y_true):
+        """strategies.cpp:151-166: per row, the model prediction with the least squared
+        error (first on ties).  Returns (predictions, chosen model)."""
+        pp = self.predict(Q)
+        err = (pp - np.asarray(y_true)[None, :]) ** 2
+        best = np.zeros(pp.shape[1], np.int64)
+        be = np.full(pp.shape[1], np.inf)
+        for t in range(pp.shape[0]):
+            better = err[t] < be
+            be[better] = err[t][better]
+            best[better] = t
+        return pp[best, np.arange(pp.shape[1])], best
+
+    def centers(self, d):
+        c = np.empty((len(self), d))
+        _check(_lib.pkrrgpu_models_centers(self._h, c.ctypes.data))
+        return c
 
 
 @dataclass
@@ -597,29 +761,3 @@ def mse(pred, truth):
     for a, b in zip(pred, truth):
         s += (a - b) * (a - b)
     return s / pred.size
-
-
-def combine_parts(part_sse, part_failed, t):
-    """Multi-rank combine (one process per GPU): per-part SSE gathered from all
-    ranks is summed in PART ORDER, exactly like the single-process engine does,
-    so results are bitwise independent of the GPU count.  Returns (mse, failed,
-    best_index) with the reference's best rule (strategies.cpp:499-505)."""
-    part_sse = np.asarray(part_sse, np.float64)
-    part_failed = np.asarray(part_failed).astype(bool)
-    nc = part_sse.shape[0]
-    mse_c = np.full(nc, np.nan)
-    failed = part_failed.any(axis=1)
-    for c in range(nc):
-        if failed[c]:
-            continue
-        s = 0.0
-        for v in part_sse[c]:
-            s += float(v)
-        mse_c[c] = s / float(t)
-    best = -1
-    for c in range(nc):
-        if failed[c]:
-            continue
-        if best < 0 or mse_c[c] < mse_c[best]:
-            best = c
-    return mse_c, failed, best

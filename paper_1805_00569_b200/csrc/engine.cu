@@ -378,7 +378,7 @@ void kmeans_device(pkrrgpu_ctx* ctx, Scope& sc, const double* dX, int64_t n, int
   int64_t* didx = sc.upload(first, s);
   pk::launch_gather_rows(dX, d, didx, k, co.centers, k, d, s, ctx->counter);
   fill_i32_kernel<<<blocks_for(n), 256, 0, s>>>(co.label, n, -1);
-  ++ctx->counter.launches;
+  ctx->counter.launched();
   double* best = sc.alloc<double>(W * S);
   double* cnorm = sc.alloc<double>(k);
   int32_t* prev = shard ? sc.alloc<int32_t>(n) : nullptr;
@@ -467,7 +467,7 @@ void kbalance_device(pkrrgpu_ctx* ctx, Scope& sc, const double* dX, int64_t n, i
   // a fixed open set; the next event is the first position where some open
   // cluster reaches its cap.  <= k+1 rounds.
   fill_i32_kernel<<<blocks_for(n), 256, 0, s>>>(co.label, n, -1);
-  ++ctx->counter.launches;
+  ctx->counter.launched();
   double* cnorm = sc.alloc<double>(k);
   pk::launch_row_norms(co.centers, k, d, d, cnorm, s, ctx->counter);
   std::vector<int64_t> sizes(k, 0), thr(k);
@@ -540,7 +540,7 @@ void make_partition_device(pkrrgpu_ctx* ctx, Scope& sc, int strategy, const doub
     po.part_of = sc.zeros<int32_t>(n, s);
     po.order = sc.alloc<int64_t>(n);
     iota_kernel<<<blocks_for(n), 256, 0, s>>>(po.order, n);
-    ++ctx->counter.launches;
+    ctx->counter.launched();
     po.sizes = {n};
     po.start = {0};
     return;
@@ -563,7 +563,7 @@ void make_partition_device(pkrrgpu_ctx* ctx, Scope& sc, int strategy, const doub
     int64_t* db = sc.upload(bounds, s);
     po.part_of = sc.alloc<int32_t>(n);
     part_labels_kernel<<<blocks_for(n), 256, 0, s>>>(po.order, db, p, po.part_of, n);
-    ++ctx->counter.launches;
+    ctx->counter.launched();
     return;
   }
   double* xnorm = sc.alloc<double>(n);
@@ -597,7 +597,7 @@ void route_rows(pkrrgpu_ctx* ctx, Scope& sc, const double* dQ, int64_t q, int64_
   pk::launch_row_norms(centers, k, d, d, cn, s, ctx->counter);
   ro.route = sc.alloc<int32_t>(q);
   fill_i32_kernel<<<blocks_for(q), 256, 0, s>>>(ro.route, q, -1);
-  ++ctx->counter.launches;
+  ctx->counter.launched();
   pk::launch_assign(dQ, q, d, qn, centers, cn, k, 0, nullptr, 0, ro.route, nullptr, nullptr, s,
                     ctx->counter);
   ClusterOut co;
@@ -650,13 +650,47 @@ double chol_flops(int64_t m) {
   return mu * (mu + 1) * (2 * mu + 1) / 6.0;
 }
 
+// Cell combine + reference-order MSE + best cell (strategies.cpp:458-505) on device:
+// pred [ncell x P x t]; failed cells get NaN and never win; best = first strict
+// minimum in trace order.  Returns the best index (-1 when every cell failed) and
+// copies its combined prediction to best_pred (host or device, may be null).
+int64_t combine_cells(pkrrgpu_ctx* ctx, Scope& sc, int predictor, int64_t P, int64_t t, int64_t ncell,
+                      const double* pred, const double* y, const std::vector<uint8_t>& cfail,
+                      std::vector<double>& cmse, double* best_pred) {
+  cudaStream_t s = ctx->main;
+  double* comb = sc.alloc<double>(ncell * t);
+  double* dm = sc.alloc<double>(ncell);
+  pk::launch_combine_cells(pred, P, t, ncell, predictor, y, comb, dm, s, ctx->counter);
+  cmse = to_host(dm, ncell, s);
+  int64_t best = -1;
+  for (int64_t c = 0; c < ncell; ++c) {
+    if (cfail[c]) {
+      cmse[c] = std::numeric_limits<double>::quiet_NaN();
+      continue;
+    }
+    if (best < 0 || cmse[c] < cmse[best]) best = c;
+  }
+  if (best >= 0 && best_pred) copy_out(best_pred, comb + best * t, t, s);
+  return best;
+}
+
 int guard(pkrrgpu_ctx* ctx) {
   if (!ctx) {
     g_err = "null context";
     return PKRRGPU_INVALID;
   }
   ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  ctx->counter.reset();
   return 0;
+}
+
+// Every kernel launch of the call was checked (pk::Counter::launched): a failed launch
+// turns the call's status into PKRRGPU_CUDA even though later work was enqueued.
+int launch_status(pkrrgpu_ctx* ctx) {
+  if (ctx->counter.err == cudaSuccess) return PKRRGPU_OK;
+  g_err = std::string("kernel launch failed (launch #") + std::to_string(ctx->counter.err_at) +
+          "): " + cudaGetErrorString(ctx->counter.err);
+  return PKRRGPU_CUDA;
 }
 
 }  // namespace
@@ -664,8 +698,9 @@ int guard(pkrrgpu_ctx* ctx) {
 #define API_BEGIN \
   try {           \
     if (int g_ = guard(ctx)) return g_;
+#define API_RETURN_OK return launch_status(ctx)
 #define API_END                                      \
-  return PKRRGPU_OK;                                 \
+  return launch_status(ctx);                         \
   }                                                  \
   catch (const Fail& f) {                            \
     return f.code;                                   \
@@ -679,6 +714,8 @@ extern "C" {
 
 const char* pkrrgpu_version(void) { return "pkrr-b200 0.1 (sm_100a, DMMA f64 + TMA)"; }
 const char* pkrrgpu_last_error(void) { return g_err.c_str(); }
+// internal (multi.cu): a worker thread's error reported on the calling thread
+void pkrrgpu_set_last_error_(const char* msg) { g_err = msg ? msg : ""; }
 
 int pkrrgpu_create(int device, pkrrgpu_ctx** out) {
   try {
@@ -699,6 +736,7 @@ int pkrrgpu_create(int device, pkrrgpu_ctx** out) {
     auto* c = new pkrrgpu_ctx();
     c->device = device;
     c->total_mem = total_mem;
+    if (const char* f = std::getenv("PKRR_FAULT_LAUNCH")) c->counter.fault_at = std::atoll(f);
     if (const char* g = std::getenv("PKRR_PANEL_GROUP")) pk::set_panel_group(std::atoi(g));
     if (const char* g = std::getenv("PKRR_SYRK_PERSISTENT")) pk::set_syrk_persistent(std::atoi(g));
     if (const char* g = std::getenv("PKRR_SYRK")) pk::set_syrk_ozaki(std::strcmp(g, "ozaki") == 0 ? 1 : 0);
@@ -747,9 +785,28 @@ void pkrrgpu_destroy(pkrrgpu_ctx* ctx) {
   delete ctx;
 }
 
+int pkrrgpu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 int64_t pkrrgpu_launch_count(const pkrrgpu_ctx* ctx) { return ctx ? ctx->counter.launches : 0; }
 
 void* pkrrgpu_stream(pkrrgpu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->main) : nullptr; }
+
+int pkrrgpu_wait_stream(pkrrgpu_ctx* ctx, void* stream) {
+  API_BEGIN
+  cudaEvent_t e;
+  ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  ck(cudaEventRecord(e, static_cast<cudaStream_t>(stream)), "event");
+  ck(cudaStreamWaitEvent(ctx->main, e, 0), "wait");
+  ck(cudaEventDestroy(e), "event");
+  API_END
+}
 
 int pkrrgpu_probe_potrf(pkrrgpu_ctx* ctx, int64_t m, int alone, double* out) {
   API_BEGIN
@@ -767,7 +824,7 @@ int pkrrgpu_probe_potrf(pkrrgpu_ctx* ctx, int64_t m, int alone, double* out) {
   const double* dX = sc.in(X.data(), m * d, s);
   int64_t* idx = sc.alloc<int64_t>(m);
   iota_kernel<<<blocks_for(m), 256, 0, s>>>(idx, m);
-  ++ctx->counter.launches;
+  ctx->counter.launched();
   pk::launch_gather_rows(dX, d, idx, m, pb.Xp, pb.mp, pb.dp, s, ctx->counter);
   pk::launch_row_norms(pb.Xp, pb.mp, pb.dp, pb.dp, pb.norms, s, ctx->counter);
   pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, m, 3.0, pb.K, pb.mp, nullptr, s, ctx->counter, false);
@@ -1133,7 +1190,7 @@ int pkrrgpu_gram(pkrrgpu_ctx* ctx, const double* A, int64_t na, const double* B,
   part_alloc(sc, pb, nb, d, true, s);
   int64_t* idx = sc.alloc<int64_t>(nb);
   iota_kernel<<<blocks_for(nb), 256, 0, s>>>(idx, nb);
-  ++ctx->counter.launches;
+  ctx->counter.launched();
   pk::launch_gather_rows(dB, d, idx, nb, pb.Xp, pb.mp, pb.dp, s, ctx->counter);
   pk::launch_row_norms(pb.Xp, pb.mp, pb.dp, pb.dp, pb.norms, s, ctx->counter);
   if (same) {
@@ -1146,7 +1203,7 @@ int pkrrgpu_gram(pkrrgpu_ctx* ctx, const double* A, int64_t na, const double* B,
     query_alloc(sc, qb, na, pb.dp, pb.mp, true);
     int64_t* qidx = sc.alloc<int64_t>(na);
     iota_kernel<<<blocks_for(na), 256, 0, s>>>(qidx, na);
-    ++ctx->counter.launches;
+    ctx->counter.launched();
     pk::launch_gather_rows(dA, d, qidx, na, qb.Xq, qb.qp, pb.dp, s, ctx->counter);
     pk::launch_row_norms(qb.Xq, qb.qp, pb.dp, pb.dp, qb.norms, s, ctx->counter);
     pk::launch_gram_cross(qb.tmQ, pb.tmX, qb.norms, pb.norms, qb.qp, na, pb.mp, nb, pb.dp, sigma,
@@ -1195,7 +1252,7 @@ int pkrrgpu_cholesky(pkrrgpu_ctx* ctx, const double* A, int64_t m, double* L, in
      "copy A");
   if (pb.mp > m) {
     set_diag_kernel<<<blocks_for(pb.mp - m), 256, 0, s>>>(pb.A, m, pb.mp, 1.0);
-    ++ctx->counter.launches;
+    ctx->counter.launched();
   }
   int* status = sc.zeros<int>(2, s);
   pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, m, status, s, ctx->counter, pb.slices, pb.exps,
@@ -1226,7 +1283,7 @@ int pkrrgpu_solve_spd(pkrrgpu_ctx* ctx, const double* L, int64_t m, const double
      "copy L");
   if (pb.mp > m) {
     set_diag_kernel<<<blocks_for(pb.mp - m), 256, 0, s>>>(pb.A, m, pb.mp, 1.0);
-    ++ctx->counter.launches;
+    ctx->counter.launched();
   }
   ck(cudaMemsetAsync(pb.yp, 0, sizeof(double) * pb.mp, s), "memset");
   ck(cudaMemcpyAsync(pb.yp, b, sizeof(double) * m, cudaMemcpyDefault, s), "copy b");
@@ -1252,7 +1309,7 @@ int pkrrgpu_train_krr(pkrrgpu_ctx* ctx, const double* X, const double* y, int64_
   part_alloc(sc, pb, m, d, true, s);
   int64_t* idx = sc.alloc<int64_t>(m);
   iota_kernel<<<blocks_for(m), 256, 0, s>>>(idx, m);
-  ++ctx->counter.launches;
+  ctx->counter.launched();
   part_load(ctx, pb, dX, dy, d, idx, s);
   pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, m, sigma, pb.K, pb.mp, nullptr, s, ctx->counter, false);
   int* status = sc.zeros<int>(2, s);
@@ -1288,7 +1345,7 @@ int pkrrgpu_predict(pkrrgpu_ctx* ctx, const double* S, const double* alpha, int6
   ck(cudaMemcpyAsync(pb.alpha, alpha, sizeof(double) * m, cudaMemcpyDefault, s), "copy alpha");
   int64_t* idx = sc.alloc<int64_t>(std::max(m, q));
   iota_kernel<<<blocks_for(std::max(m, q)), 256, 0, s>>>(idx, std::max(m, q));
-  ++ctx->counter.launches;
+  ctx->counter.launched();
   pk::launch_gather_rows(dS, d, idx, m, pb.Xp, pb.mp, pb.dp, s, ctx->counter);
   pk::launch_row_norms(pb.Xp, pb.mp, pb.dp, pb.dp, pb.norms, s, ctx->counter);
   QueryBuf qb;
@@ -1391,6 +1448,112 @@ struct pkrrgpu_models {
 
 extern "C" {
 
+}  // extern "C"
+
+namespace {
+
+// train_partitions core (strategies.cpp:104-133): every part of `po` trained
+// concurrently, largest first on the highest-priority streams (LPT over the context's
+// 8 part streams, each with its lookahead companion); the support rows, norms and
+// alpha are kept resident as the models (KrrModel, solver.hpp:37-49).
+pkrrgpu_models* train_models(pkrrgpu_ctx* ctx, Scope& sc, const double* dX, const double* dy, int64_t d,
+                             const PartitionOut& po, double sigma, double lambda, int predictor,
+                             int64_t* failed_part, int64_t* npd_pivot) {
+  cudaStream_t s = ctx->main;
+  for (int64_t t = 0; t < po.p; ++t)
+    if (po.sizes[t] == 0) fail(PKRRGPU_INVALID, "train_partitions: empty part");
+  std::vector<PartBuf> parts(po.p);
+  int* status = sc.zeros<int>(2 * po.p, s);
+  double* res = sc.zeros<double>(2 * po.p, s);
+  cudaEvent_t ready;
+  ck(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
+  ck(cudaEventRecord(ready, s), "event");
+  std::vector<int64_t> by_size(po.p);
+  for (int64_t t = 0; t < po.p; ++t) by_size[t] = t;
+  std::stable_sort(by_size.begin(), by_size.end(), [&](int64_t x, int64_t y) { return po.sizes[x] > po.sizes[y]; });
+  const size_t S = ctx->work.size();
+  for (size_t i = 0; i < by_size.size(); ++i) {
+    const int64_t t = by_size[i];
+    cudaStream_t ws = ctx->work[i % S];
+    ck(cudaStreamWaitEvent(ws, ready, 0), "wait");
+    PartBuf& pb = parts[t];
+    part_alloc(sc, pb, po.sizes[t], d, true, ws);
+    part_load(ctx, pb, dX, dy, d, po.order + po.start[t], ws);
+    pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws, ctx->counter, false);
+    part_solve(ctx, pb, lambda, status + 2 * t, res + 2 * t, ws, ctx->aux[i % S], po.p == 1);
+  }
+  ck(cudaEventDestroy(ready), "event");
+  ck(cudaDeviceSynchronize(), "train");
+  std::vector<int> st = to_host(status, 2 * po.p, s);
+  std::vector<double> rh = to_host(res, 2 * po.p, s);
+  for (int64_t t = 0; t < po.p; ++t)
+    if (st[2 * t]) {
+      if (failed_part) *failed_part = t;
+      if (npd_pivot) *npd_pivot = st[2 * t + 1];
+      fail(PKRRGPU_NPD, "partition " + std::to_string(t) + ": matrix not positive definite: pivot " +
+                            std::to_string(st[2 * t + 1]));
+    }
+  auto mod = std::make_unique<pkrrgpu_models>();
+  mod->ctx = ctx;
+  mod->p = po.p;
+  mod->d = d;
+  mod->dp = round_up(d, 16);
+  mod->sigma = sigma;
+  mod->predictor = predictor;
+  for (int64_t t = 0; t < po.p; ++t) {
+    PartBuf& pb = parts[t];
+    mod->m.push_back(pb.m);
+    mod->mp.push_back(pb.mp);
+    double* x = static_cast<double*>(ctx->alloc(sizeof(double) * pb.mp * pb.dp));
+    double* nm = static_cast<double*>(ctx->alloc(sizeof(double) * pb.mp));
+    double* al = static_cast<double*>(ctx->alloc(sizeof(double) * pb.mp));
+    mod->Xp.push_back(x);
+    mod->norms.push_back(nm);
+    mod->alpha.push_back(al);
+    ck(cudaMemcpyAsync(x, pb.Xp, sizeof(double) * pb.mp * pb.dp, cudaMemcpyDeviceToDevice, s), "copy");
+    ck(cudaMemcpyAsync(nm, pb.norms, sizeof(double) * pb.mp, cudaMemcpyDeviceToDevice, s), "copy");
+    ck(cudaMemcpyAsync(al, pb.alpha, sizeof(double) * pb.mp, cudaMemcpyDeviceToDevice, s), "copy");
+    CUtensorMap tm;
+    if (!pk::make_tmap(&tm, x, pb.mp, pb.dp, pb.dp)) fail(PKRRGPU_CUDA, "tensor map");
+    mod->tmX.push_back(tm);
+    mod->residual.push_back(rh[2 * t + 1]);
+  }
+  if (po.centers) {
+    mod->centers = static_cast<double*>(ctx->alloc(sizeof(double) * po.p * d));
+    ck(cudaMemcpyAsync(mod->centers, po.centers, sizeof(double) * po.p * d, cudaMemcpyDeviceToDevice, s), "copy");
+  }
+  ck(cudaStreamSynchronize(s), "sync");
+  return mod.release();
+}
+
+// the caller's PartitionSet (strategies.hpp:31-36) as a device PartitionOut: part t =
+// rows[start_t .. start_t + sizes[t]) in the caller's order (make_partition keeps train
+// row order, strategies.cpp:97-99; a random partition keeps its permutation order)
+void partition_from_lists(pkrrgpu_ctx* ctx, Scope& sc, const int64_t* rows, const int64_t* sizes, int64_t p,
+                          int64_t n, const double* centers, int64_t d, PartitionOut& po) {
+  cudaStream_t s = ctx->main;
+  if (p < 1) fail(PKRRGPU_INVALID, "partition: need p >= 1");
+  po.p = p;
+  po.sizes.assign(sizes, sizes + p);
+  po.start.assign(p, 0);
+  int64_t total = 0;
+  for (int64_t t = 0; t < p; ++t) {
+    if (sizes[t] <= 0) fail(PKRRGPU_INVALID, "train_partitions: empty part");
+    po.start[t] = total;
+    total += sizes[t];
+  }
+  std::vector<int64_t> h(total);
+  ck(cudaMemcpy(h.data(), rows, sizeof(int64_t) * total, cudaMemcpyDefault), "copy rows");
+  for (int64_t i = 0; i < total; ++i)
+    if (h[i] < 0 || h[i] >= n) fail(PKRRGPU_INVALID, "train_partitions: row index out of range");
+  po.order = sc.upload(h, s);
+  po.centers = centers ? const_cast<double*>(sc.in(centers, p * d, s)) : nullptr;
+}
+
+}  // namespace
+
+extern "C" {
+
 int pkrrgpu_train_partitions(pkrrgpu_ctx* ctx, int strategy, const double* X, const double* y,
                              int64_t n, int64_t d, int64_t p, uint64_t seed, double sigma,
                              double lambda, pkrrgpu_models** out, int64_t* failed_part,
@@ -1399,72 +1562,86 @@ int pkrrgpu_train_partitions(pkrrgpu_ctx* ctx, int strategy, const double* X, co
   if (!out) fail(PKRRGPU_INVALID, "null out");
   if (!(lambda > 0.0)) fail(PKRRGPU_INVALID, "train_krr: lambda must be > 0");
   if (!(sigma > 0.0)) fail(PKRRGPU_INVALID, "gaussian kernel needs sigma > 0");
+  if (strategy < 0 || strategy > 7) fail(PKRRGPU_INVALID, "unknown strategy");
   Scope sc(ctx);
   cudaStream_t s = ctx->main;
   const double* dX = sc.in(X, n * d, s);
   const double* dy = sc.in(y, n, s);
   PartitionOut po;
   make_partition_device(ctx, sc, strategy, dX, n, d, p, seed, 0.01, 100, po);
-  for (int64_t t = 0; t < po.p; ++t)
-    if (po.sizes[t] == 0) fail(PKRRGPU_INVALID, "train_partitions: empty part");
-  auto* mod = new pkrrgpu_models();
+  *out = train_models(ctx, sc, dX, dy, d, po, sigma, lambda, predictor_of(strategy), failed_part, npd_pivot);
+  API_END
+}
+
+int pkrrgpu_train_parts(pkrrgpu_ctx* ctx, const double* X, const double* y, int64_t n, int64_t d,
+                        const int64_t* rows, const int64_t* sizes, int64_t p, const double* centers, double sigma,
+                        double lambda, pkrrgpu_models** out, int64_t* failed_part, int64_t* npd_pivot) {
+  API_BEGIN
+  if (!out || !rows || !sizes) fail(PKRRGPU_INVALID, "null argument");
+  if (n <= 0 || d <= 0) fail(PKRRGPU_INVALID, "train_partitions: empty dataset");
+  if (!(lambda > 0.0)) fail(PKRRGPU_INVALID, "train_krr: lambda must be > 0");
+  if (!(sigma > 0.0)) fail(PKRRGPU_INVALID, "gaussian kernel needs sigma > 0");
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  const double* dX = sc.in(X, n * d, s);
+  const double* dy = sc.in(y, n, s);
+  PartitionOut po;
+  partition_from_lists(ctx, sc, rows, sizes, p, n, centers, d, po);
+  *out = train_models(ctx, sc, dX, dy, d, po, sigma, lambda, centers ? 2 : 0, failed_part, npd_pivot);
+  API_END
+}
+
+int pkrrgpu_models_import(pkrrgpu_ctx* ctx, int64_t p, int64_t d, const int64_t* sizes, const double* S,
+                          const double* alpha, const double* centers, double sigma, pkrrgpu_models** out) {
+  API_BEGIN
+  if (!out || !sizes || !S || !alpha || p < 1 || d <= 0) fail(PKRRGPU_INVALID, "models_import: bad arguments");
+  if (!(sigma > 0.0)) fail(PKRRGPU_INVALID, "gaussian kernel needs sigma > 0");
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  int64_t total = 0;
+  for (int64_t t = 0; t < p; ++t) {
+    if (sizes[t] <= 0) fail(PKRRGPU_INVALID, "models_import: empty model");
+    total += sizes[t];
+  }
+  const double* dS = sc.in(S, total * d, s);
+  const double* dA = sc.in(alpha, total, s);
+  auto mod = std::make_unique<pkrrgpu_models>();
   mod->ctx = ctx;
-  mod->p = po.p;
+  mod->p = p;
   mod->d = d;
   mod->dp = round_up(d, 16);
   mod->sigma = sigma;
-  mod->predictor = predictor_of(strategy);
-  std::vector<PartBuf> parts(po.p);
-  int* status = sc.zeros<int>(2 * po.p, s);
-  double* res = sc.zeros<double>(2 * po.p, s);
-  ck(cudaStreamSynchronize(s), "sync");
-  std::vector<cudaEvent_t> done;
-  for (int64_t t = 0; t < po.p; ++t) {
-    cudaStream_t ws = ctx->work[t % ctx->work.size()];
-    PartBuf& pb = parts[t];
-    part_alloc(sc, pb, po.sizes[t], d, true, ws);
-    part_load(ctx, pb, dX, dy, d, po.order + po.start[t], ws);
-    pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws,
-                        ctx->counter, false);
-    part_solve(ctx, pb, lambda, status + 2 * t, res + 2 * t, ws, ctx->aux[t % ctx->aux.size()], po.p == 1);
-  }
-  ck(cudaDeviceSynchronize(), "train");
-  std::vector<int> st = to_host(status, 2 * po.p, s);
-  std::vector<double> rh = to_host(res, 2 * po.p, s);
-  for (int64_t t = 0; t < po.p; ++t)
-    if (st[2 * t]) {
-      if (failed_part) *failed_part = t;
-      if (npd_pivot) *npd_pivot = st[2 * t + 1];
-      delete mod;
-      fail(PKRRGPU_NPD, "partition " + std::to_string(t) + ": matrix not positive definite: pivot " +
-                            std::to_string(st[2 * t + 1]));
-    }
-  // keep support rows, norms, alpha (KrrModel, solver.hpp:37-49)
-  for (int64_t t = 0; t < po.p; ++t) {
-    PartBuf& pb = parts[t];
-    mod->m.push_back(pb.m);
-    mod->mp.push_back(pb.mp);
-    double* x = static_cast<double*>(ctx->alloc(sizeof(double) * pb.mp * pb.dp));
-    double* nm = static_cast<double*>(ctx->alloc(sizeof(double) * pb.mp));
-    double* al = static_cast<double*>(ctx->alloc(sizeof(double) * pb.mp));
-    ck(cudaMemcpyAsync(x, pb.Xp, sizeof(double) * pb.mp * pb.dp, cudaMemcpyDeviceToDevice, s), "copy");
-    ck(cudaMemcpyAsync(nm, pb.norms, sizeof(double) * pb.mp, cudaMemcpyDeviceToDevice, s), "copy");
-    ck(cudaMemcpyAsync(al, pb.alpha, sizeof(double) * pb.mp, cudaMemcpyDeviceToDevice, s), "copy");
+  mod->predictor = centers ? 2 : 0;
+  int64_t at = 0;
+  for (int64_t t = 0; t < p; ++t) {
+    const int64_t m = sizes[t], mp = round_up(m, kNB);
+    double* x = static_cast<double*>(ctx->alloc(sizeof(double) * mp * mod->dp));
+    double* nm = static_cast<double*>(ctx->alloc(sizeof(double) * mp));
+    double* al = static_cast<double*>(ctx->alloc(sizeof(double) * mp));
+    mod->m.push_back(m);
+    mod->mp.push_back(mp);
     mod->Xp.push_back(x);
     mod->norms.push_back(nm);
     mod->alpha.push_back(al);
+    int64_t* idx = sc.alloc<int64_t>(m);
+    iota_kernel<<<blocks_for(m), 256, 0, s>>>(idx, m);
+    ctx->counter.launched();
+    pk::launch_gather_rows(dS + at * d, d, idx, m, x, mp, mod->dp, s, ctx->counter);
+    pk::launch_row_norms(x, mp, mod->dp, mod->dp, nm, s, ctx->counter);
+    ck(cudaMemsetAsync(al, 0, sizeof(double) * mp, s), "memset");
+    ck(cudaMemcpyAsync(al, dA + at, sizeof(double) * m, cudaMemcpyDeviceToDevice, s), "copy alpha");
     CUtensorMap tm;
-    if (!pk::make_tmap(&tm, x, pb.mp, pb.dp, pb.dp)) fail(PKRRGPU_CUDA, "tensor map");
+    if (!pk::make_tmap(&tm, x, mp, mod->dp, mod->dp)) fail(PKRRGPU_CUDA, "tensor map");
     mod->tmX.push_back(tm);
-    mod->residual.push_back(rh[2 * t + 1]);
+    mod->residual.push_back(0.0);
+    at += m;
   }
-  if (po.centers) {
-    mod->centers = static_cast<double*>(ctx->alloc(sizeof(double) * po.p * d));
-    ck(cudaMemcpyAsync(mod->centers, po.centers, sizeof(double) * po.p * d, cudaMemcpyDeviceToDevice, s),
-       "copy");
+  if (centers) {
+    mod->centers = static_cast<double*>(ctx->alloc(sizeof(double) * p * d));
+    ck(cudaMemcpyAsync(mod->centers, centers, sizeof(double) * p * d, cudaMemcpyDefault, s), "copy centers");
   }
   ck(cudaStreamSynchronize(s), "sync");
-  *out = mod;
+  *out = mod.release();
   API_END
 }
 
@@ -1501,6 +1678,8 @@ int pkrrgpu_predict_nearest(pkrrgpu_ctx* ctx, const pkrrgpu_models* models, cons
   if (!models || models->p < 1) fail(PKRRGPU_INVALID, "predict_nearest: no models");
   if (!models->centers)
     fail(PKRRGPU_INVALID, "predict_nearest: centers undefined for this partitioning");
+  if (models->ctx->device != ctx->device) fail(PKRRGPU_INVALID, "predict_nearest: models live on another device");
+  if (q <= 0) API_RETURN_OK;
   Scope sc(ctx);
   cudaStream_t s = ctx->main;
   const int64_t d = models->d, dp = models->dp;
@@ -1510,11 +1689,14 @@ int pkrrgpu_predict_nearest(pkrrgpu_ctx* ctx, const pkrrgpu_models* models, cons
   double* pred_all = sc.alloc<double>(q);
   double* ydummy = sc.zeros<double>(q, s);
   double* sse = sc.alloc<double>(models->p);
-  ck(cudaStreamSynchronize(s), "sync");
+  cudaEvent_t ready;
+  ck(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
+  ck(cudaEventRecord(ready, s), "event");
   for (int64_t t = 0; t < models->p; ++t) {
     const int64_t cnt = ro.sizes[t];
     if (cnt == 0) continue;
     cudaStream_t ws = ctx->work[t % ctx->work.size()];
+    ck(cudaStreamWaitEvent(ws, ready, 0), "wait");
     QueryBuf qb;
     query_alloc(sc, qb, cnt, dp, models->mp[t]);
     const int64_t* rows = ro.members + ro.start[t];
@@ -1525,8 +1707,78 @@ int pkrrgpu_predict_nearest(pkrrgpu_ctx* ctx, const pkrrgpu_models* models, cons
                              ctx->counter);
     pk::launch_sse_scatter(qb.pred, rows, cnt, ydummy, pred_all, sse + t, nullptr, ws, ctx->counter);
   }
+  ck(cudaEventDestroy(ready), "event");
   ck(cudaDeviceSynchronize(), "predict");
   copy_out(out, pred_all, q, s);
+  ck(cudaStreamSynchronize(s), "sync");
+  API_END
+}
+
+int pkrrgpu_models_predict(pkrrgpu_ctx* ctx, const pkrrgpu_models* models, int64_t part, const double* Q,
+                           int64_t q, double* out) {
+  API_BEGIN
+  if (!models || models->p < 1) fail(PKRRGPU_INVALID, "predict: no models");
+  if (part < -1 || part >= models->p) fail(PKRRGPU_INVALID, "predict: no such model");
+  if (models->ctx->device != ctx->device) fail(PKRRGPU_INVALID, "predict: models live on another device");
+  if (q <= 0) API_RETURN_OK;
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  const int64_t d = models->d, dp = models->dp;
+  const double* dQ = sc.in(Q, q * d, s);
+  const int64_t t0 = part < 0 ? 0 : part, t1 = part < 0 ? models->p : part + 1;
+  double* dout = sc.alloc<double>((t1 - t0) * q);
+  int64_t* idx = sc.alloc<int64_t>(q);
+  iota_kernel<<<blocks_for(q), 256, 0, s>>>(idx, q);
+  ctx->counter.launched();
+  QueryBuf qb0;
+  query_alloc(sc, qb0, q, dp, kNB);
+  pk::launch_gather_rows(dQ, d, idx, q, qb0.Xq, qb0.qp, dp, s, ctx->counter);
+  pk::launch_row_norms(qb0.Xq, qb0.qp, dp, dp, qb0.norms, s, ctx->counter);
+  cudaEvent_t ready;
+  ck(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
+  ck(cudaEventRecord(ready, s), "event");
+  for (int64_t t = t0; t < t1; ++t) {
+    cudaStream_t ws = ctx->work[(t - t0) % ctx->work.size()];
+    ck(cudaStreamWaitEvent(ws, ready, 0), "wait");
+    double* partial = sc.alloc<double>(pk::predict_partial_elems(qb0.qp, models->mp[t]));
+    pk::launch_predict_fused(qb0.tmQ, models->tmX[t], qb0.norms, models->norms[t], qb0.qp, q, models->mp[t],
+                             models->m[t], dp, models->sigma, models->alpha[t], partial, dout + (t - t0) * q,
+                             nullptr, ws, ctx->counter);
+  }
+  ck(cudaEventDestroy(ready), "event");
+  ck(cudaDeviceSynchronize(), "predict");
+  copy_out(out, dout, (t1 - t0) * q, s);
+  ck(cudaStreamSynchronize(s), "sync");
+  API_END
+}
+
+int pkrrgpu_models_centers(const pkrrgpu_models* m, double* centers) {
+  if (!m || !centers) return PKRRGPU_INVALID;
+  if (!m->centers) return PKRRGPU_INVALID;
+  cudaSetDevice(m->ctx->device);
+  return cudaMemcpy(centers, m->centers, sizeof(double) * m->p * m->d, cudaMemcpyDefault) == cudaSuccess
+             ? PKRRGPU_OK
+             : PKRRGPU_CUDA;
+}
+
+int pkrrgpu_combine(pkrrgpu_ctx* ctx, int strategy, int64_t p, int64_t t, int64_t ncell, const double* pred,
+                    const double* y, const uint8_t* cell_failed, double* cell_mse, int64_t* best_index,
+                    double* best_pred) {
+  API_BEGIN
+  if (strategy < 0 || strategy > 7) fail(PKRRGPU_INVALID, "unknown strategy");
+  if (t <= 0 || ncell <= 0 || p < 1 || !pred || !y) fail(PKRRGPU_INVALID, "combine: bad arguments");
+  const int predictor = predictor_of(strategy);
+  const int64_t P = predictor == 0 || predictor == 2 ? 1 : p;
+  Scope sc(ctx);
+  cudaStream_t s = ctx->main;
+  const double* dp = sc.in(pred, ncell * P * t, s);
+  const double* dy = sc.in(y, t, s);
+  std::vector<uint8_t> cfail(ncell, 0);
+  if (cell_failed) std::memcpy(cfail.data(), cell_failed, ncell);
+  std::vector<double> cmse;
+  const int64_t b = combine_cells(ctx, sc, predictor, P, t, ncell, dp, dy, cfail, cmse, best_pred);
+  if (cell_mse) std::memcpy(cell_mse, cmse.data(), sizeof(double) * ncell);
+  if (best_index) *best_index = b;
   ck(cudaStreamSynchronize(s), "sync");
   API_END
 }
@@ -1593,11 +1845,11 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   } else {
     iota_t = sc.alloc<int64_t>(t);
     iota_kernel<<<blocks_for(t), 256, 0, s>>>(iota_t, t);
-    ++ctx->counter.launches;
+    ctx->counter.launched();
     if (te) {
       iota_e = sc.alloc<int64_t>(te);
       iota_kernel<<<blocks_for(te), 256, 0, s>>>(iota_e, te);
-      ++ctx->counter.launches;
+      ctx->counter.launched();
     }
   }
   ck(cudaEventRecord(t_part.b, s), "event");
@@ -1834,10 +2086,6 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
     hmark("batch enqueued");
   }
   pk::shadow_report();
-  // combine for average/oracle predictors (world == 1)
-  double* dmse = sc.zeros<double>(2 * ncell, s);
-  double* comb_t = sc.alloc<double>(t);
-  double* comb_e = te ? sc.alloc<double>(te) : nullptr;
   ck(cudaEventRecord(t_all.b, s), "event");
   ck(cudaDeviceSynchronize(), "grid");
 
@@ -1928,64 +2176,36 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
     for (int64_t q = 0; q < p; ++q) o->part_sizes[q] = po.sizes[q];
 
   o->best_index = -1;
+  o->pred_rows = pp_parts;
+  // this rank's predictions (rows / part slices it does not own are zero): the
+  // multi-rank caller sums them over ranks (exact: disjoint) and runs pkrrgpu_combine
+  if (o->cell_pred) copy_out(o->cell_pred, pred_t, ncell * pp_parts * t, s);
+  if (o->cell_eval_pred && te) copy_out(o->cell_eval_pred, pred_e, ncell * pp_parts * te, s);
   if (world == 1) {
-    std::vector<double> cmse(ncell, std::numeric_limits<double>::quiet_NaN()), cemse(ncell,
-                                                                                       std::numeric_limits<double>::quiet_NaN());
     std::vector<uint8_t> cfail(ncell, 0);
     std::vector<double> cres(ncell, 0.0);
-    for (int64_t c = 0; c < ncell; ++c) {
+    for (int64_t c = 0; c < ncell; ++c)
       for (int64_t q = 0; q < p; ++q) {
         if (pfail[c * p + q]) cfail[c] = 1;
         const double r = rs[(c * p + q) * 4 + 0];
         if (!pfail[c * p + q] && r > cres[c]) cres[c] = r;
       }
-      if (cfail[c]) continue;
-      if (predictor == 0 || predictor == 2) {
-        // per-part SSE summed in part order (GPU-count independent)
-        double se = 0.0, ee = 0.0;
-        for (int64_t q = 0; q < p; ++q) {
-          se += rs[(c * p + q) * 4 + 2];
-          ee += rs[(c * p + q) * 4 + 3];
-        }
-        cmse[c] = se / static_cast<double>(t);
-        if (te) cemse[c] = ee / static_cast<double>(te);
-      } else {
-        pk::launch_combine(pred_t + c * p * t, p, t, predictor, nullptr, dyt, comb_t, dmse + 2 * c, s,
-                           ctx->counter);
-        if (te)
-          pk::launch_combine(pred_e + c * p * te, p, te, predictor, nullptr, dye, comb_e, dmse + 2 * c + 1,
-                             s, ctx->counter);
-        const std::vector<double> mm = to_host(dmse + 2 * c, 2, s);
-        cmse[c] = mm[0];
-        if (te) cemse[c] = mm[1];
-      }
-    }
-    for (int64_t c = 0; c < ncell; ++c) {
-      if (cfail[c]) continue;
-      if (o->best_index < 0 || cmse[c] < cmse[o->best_index]) o->best_index = c;
+    std::vector<double> cmse, cemse;
+    o->best_index = combine_cells(ctx, sc, predictor, pp_parts, t, ncell, pred_t, dyt, cfail, cmse, o->best_pred);
+    if (te) {
+      // the eval set's predictions of the cell chosen on the selection set
+        double* comb_e = sc.alloc<double>(ncell * te);
+      double* dm = sc.alloc<double>(ncell);
+      pk::launch_combine_cells(pred_e, pp_parts, te, ncell, predictor, dye, comb_e, dm, s, ctx->counter);
+      cemse = to_host(dm, ncell, s);
+      for (int64_t c = 0; c < ncell; ++c)
+        if (cfail[c]) cemse[c] = std::numeric_limits<double>::quiet_NaN();
+      if (o->best_index >= 0 && o->best_eval_pred) copy_out(o->best_eval_pred, comb_e + o->best_index * te, te, s);
     }
     if (o->cell_mse) std::memcpy(o->cell_mse, cmse.data(), sizeof(double) * ncell);
     if (o->cell_failed) std::memcpy(o->cell_failed, cfail.data(), ncell);
     if (o->cell_residual) std::memcpy(o->cell_residual, cres.data(), sizeof(double) * ncell);
     if (o->cell_eval_mse && te) std::memcpy(o->cell_eval_mse, cemse.data(), sizeof(double) * ncell);
-    const int64_t b = o->best_index;
-    if (b >= 0 && o->best_pred) {
-      if (pp_parts == 1) {
-        copy_out(o->best_pred, pred_t + b * t, t, s);
-      } else {
-        pk::launch_combine(pred_t + b * p * t, p, t, predictor, nullptr, dyt, comb_t, dmse, s, ctx->counter);
-        copy_out(o->best_pred, comb_t, t, s);
-      }
-    }
-    if (b >= 0 && o->best_eval_pred && te) {
-      if (pp_parts == 1) {
-        copy_out(o->best_eval_pred, pred_e + b * te, te, s);
-      } else {
-        pk::launch_combine(pred_e + b * p * te, p, te, predictor, nullptr, dye, comb_e, dmse + 1, s,
-                           ctx->counter);
-        copy_out(o->best_eval_pred, comb_e, te, s);
-      }
-    }
   }
   ck(cudaStreamSynchronize(s), "sync");
   API_END

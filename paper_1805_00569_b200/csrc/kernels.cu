@@ -9,6 +9,7 @@
 #include <cmath>
 #include <vector>
 #include <cstdlib>
+#include <atomic>
 
 #include "gemm_dmma.cuh"
 #include "syrk_persistent.cuh"
@@ -19,7 +20,59 @@
 
 namespace pk {
 
-static int g_sms = 148;  // refreshed from the device by launch_potrf
+// ---------------------------------------------------------------------------
+// per-device state.  Several contexts (one host thread per GPU, pkrrgpu_multi) can
+// launch concurrently on different devices: the SM count and the >48 KB dynamic
+// shared-memory opt-ins are per device, never per process.
+// ---------------------------------------------------------------------------
+static int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev & 63;
+}
+
+int sm_count() {
+  static std::atomic<int> sms[64];
+  const int dev = current_device();
+  int v = sms[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+    sms[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+#define g_sms (::pk::sm_count())
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device).  The bit
+// is set after the call, so a concurrent first launch on the same device sets it too.
+template <typename F>
+static void smem_optin(std::atomic<uint64_t>& done, F* kernel, int bytes) {
+  const uint64_t bit = 1ull << current_device();
+  if (done.load(std::memory_order_acquire) & bit) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done.fetch_or(bit, std::memory_order_acq_rel);
+}
+
+__global__ void fault_probe_kernel() {}
+
+void Counter::launched(int k) {
+  const int64_t before = launches;
+  launches += k;
+  if (fault_at > 0 && before < fault_at && launches >= fault_at)
+    fault_probe_kernel<<<1, 4096>>>();  // 4096 threads per block: cudaErrorInvalidConfiguration
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && err == cudaSuccess) {
+    err = e;
+    err_at = launches;
+  }
+}
+
+void Counter::reset() {
+  cudaGetLastError();  // a stale error of an earlier call is not this call's
+  err = cudaSuccess;
+  err_at = 0;
+}
 
 // ---------------------------------------------------------------------------
 // TMA descriptors (driver entry point fetched through the runtime)
@@ -95,7 +148,7 @@ void launch_row_norms(const double* X, int64_t rows, int64_t d, int64_t ld, doub
   if (rows <= 0) return;
   row_norms_kernel<<<static_cast<unsigned>((rows + kNormRows - 1) / kNormRows), kNormRows, 0, s>>>(
       X, rows, d, ld, out);
-  ++c.launches;
+  c.launched();
 }
 
 // ---------------------------------------------------------------------------
@@ -119,7 +172,7 @@ void launch_gather_rows(const double* X, int64_t d, const int64_t* idx, int64_t 
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   gather_rows_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(X, d, idx, cnt, dst, rows_pad, dp);
-  ++c.launches;
+  c.launched();
 }
 
 __global__ void gather_vec_kernel(const double* __restrict__ y, const int64_t* __restrict__ idx,
@@ -132,7 +185,7 @@ void launch_gather_vec(const double* y, const int64_t* idx, int64_t cnt, double*
                        cudaStream_t s, Counter& c) {
   if (pad <= 0) return;
   gather_vec_kernel<<<static_cast<unsigned>((pad + 255) / 256), 256, 0, s>>>(y, idx, cnt, dst, pad);
-  ++c.launches;
+  c.launched();
 }
 
 // ---------------------------------------------------------------------------
@@ -163,14 +216,10 @@ template <int BM, int MODE>
 static void gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const GemmParams& p,
                         int blocks, cudaStream_t s, Counter& c) {
   if (blocks <= 0) return;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(dgemm_tn_kernel<BM, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         GemmCfg<BM>::SMEM);
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  smem_optin(attr, dgemm_tn_kernel<BM, MODE>, GemmCfg<BM>::SMEM);
   launch_pdl(dgemm_tn_kernel<BM, MODE>, blocks, gemm_threads<MODE>(), GemmCfg<BM>::SMEM, s, a, b, p);
-  ++c.launches;
+  c.launched();
 }
 
 void launch_gram_sym(const CUtensorMap& tmX, const double* norms, int64_t mp, int64_t dp,
@@ -236,14 +285,11 @@ void launch_predict_fused(const CUtensorMap& tmQ, const CUtensorMap& tmX, const 
   p.neg_inv_denom = -1.0 / ((2.0 * sigma) * sigma);
   p.partial = partial;
   p.abort_flag = abort;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(predict_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<64>::SMEM);
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  smem_optin(attr, predict_fused_kernel, GemmCfg<64>::SMEM);
   predict_fused_kernel<<<p.tiles_q * nch, kGemmThreads, GemmCfg<64>::SMEM, s>>>(tmQ, tmX, p);
   predict_reduce_kernel<<<static_cast<unsigned>((q + 255) / 256), 256, 0, s>>>(partial, qp, nch, q, pred, abort);
-  c.launches += 2;
+  c.launched(2);
 }
 
 // ---------------------------------------------------------------------------
@@ -629,8 +675,8 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
 // trailing matrix is streamed through HBM nb/G times instead of nb times.
 static int g_panel_group = 0;  // 0: automatic (see launch_potrf)
 // optional per-launch timing of the trailing SYRK (bench probe only)
-static std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* g_syrk_events = nullptr;
-static std::vector<double>* g_syrk_flops = nullptr;
+static thread_local std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* g_syrk_events = nullptr;
+static thread_local std::vector<double>* g_syrk_flops = nullptr;
 void set_syrk_probe(std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* ev, std::vector<double>* fl) {
   g_syrk_events = ev;
   g_syrk_flops = fl;
@@ -735,16 +781,10 @@ struct FactorBufs {
 bool launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, double* Linv,
                   int64_t mp, int64_t m_valid, int* status, cudaStream_t s, Counter& c, int8_t* slices,
                   int* exps, cudaStream_t s2, bool latency, const FwdSolve* fs) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(potrf_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLeafSmem);
-    cudaFuncSetAttribute(dsyrk_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSyrkSmem);
-    cudaFuncSetAttribute(ozaki_syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzSmem);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr_leaf{0}, attr_syrk{0}, attr_oz{0};
+  smem_optin(attr_leaf, potrf_leaf_kernel, kLeafSmem);
+  smem_optin(attr_syrk, dsyrk_persistent_kernel, kSyrkSmem);
+  smem_optin(attr_oz, ozaki_syrk_kernel, kOzSmem);
   // Debug (PKRR_SHADOW): every step is run twice -- on A and on a copy taken just
   // before it -- and the two outputs compared (reported by shadow_report): a step
   // whose result depends on timing/concurrency shows up by name.
@@ -825,7 +865,7 @@ bool launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
       u.abort_flag = f.status;
       u.narrow = G2;
       dsyrk_persistent_kernel<<<syrk_tile_count(rem_, G2), kSyrkThreads, kSyrkSmem, st>>>(f.tmA, u);
-      ++c.launches;
+      c.launched();
     }
   };
   // lookahead needs a second stream; not with the shadow checker or the int8 update
@@ -859,7 +899,7 @@ bool launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
           u.abort_flag = f.status;
           u.narrow = std::min(S, kend - kb);
           dsyrk_persistent_kernel<<<syrk_tile_count(u.T, u.narrow), kSyrkThreads, kSyrkSmem, s>>>(f.tmA, u);
-          ++c.launches;
+          c.launched();
         });
       }
       if (kb > sub0) {
@@ -889,7 +929,7 @@ bool launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
       step("leaf", [&](FactorBufs& f) {
         launch_pdl(potrf_leaf_kernel, 1, kLeafThreads, kLeafSmem, s, f.A, mp, kb, f.Linv, f.status, m_valid, 1,
                    fused ? static_cast<const double*>(fs->w) : nullptr, fused ? fs->z : nullptr);
-        ++c.launches;
+        c.launched();
       });
       const int rem = nb - 1 - kb;
       if (rem <= 0) continue;
@@ -959,7 +999,7 @@ bool launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
       op.narrow = G2 < rem ? 2 * G2 : 0;
       const int na = G2 < rem ? G2 * (G2 + 1) + (rem - G2) * 2 * G2 : rem * (rem + 1);
       ozaki_syrk_kernel<<<na, kOzThreads, kOzSmem, s>>>(ta, tb, tmA, op);
-      c.launches += 2;
+      c.launched(2);
       if (rem > G2) {
         OzParams ob = op;
         const int T2 = rem - G2;
@@ -967,7 +1007,7 @@ bool launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
         ob.srow = G2 * kNB;
         ob.narrow = 0;
         ozaki_syrk_kernel<<<T2 * (T2 + 1), kOzThreads, kOzSmem, s2>>>(ta, tb, tmA, ob);
-        ++c.launches;
+        c.launched();
         cudaEventRecord(ev_b, s2);
         b_pending = true;
       }
@@ -990,7 +1030,7 @@ bool launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
         op.exps = exps;
         op.abort_flag = f.status;
         ozaki_syrk_kernel<<<rem * (rem + 1), kOzThreads, kOzSmem, s>>>(ta, tb, f.tmA, op);
-        c.launches += 2;
+        c.launched(2);
       });
     } else if (look) {
       // lookahead: (a) the next panel's G tile columns now, on s, so the next panel
@@ -1025,7 +1065,7 @@ bool launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
         const int nt = syrk_tile_count(v.T, 0);
         const int cap = g_sms - reserve;
         dsyrk_persistent_kernel<<<reserve > 0 && nt > cap ? cap : nt, kSyrkThreads, kSyrkSmem, s2>>>(tmA, v);
-        ++c.launches;
+        c.launched();
         cudaEventRecord(ev_b, s2);
         b_pending = true;
       }
@@ -1046,7 +1086,7 @@ bool launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
           const int ntl = v.T * (v.T + 1) / 2;
           const int grid = g_syrk_persistent ? (ntl < g_sms ? ntl : g_sms) : ntl;
           dsyrk_persistent_kernel<<<grid, kSyrkThreads, kSyrkSmem, s>>>(f.tmA, v);
-          ++c.launches;
+          c.launched();
           return;
         }
         SyrkParams u{};
@@ -1058,7 +1098,7 @@ bool launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
         const int ntl = rem * (rem + 1) / 2;
         const int grid = g_syrk_persistent ? (ntl < g_sms ? ntl : g_sms) : ntl;
         dsyrk_persistent_kernel<<<grid, kSyrkThreads, kSyrkSmem, s>>>(f.tmA, u);
-        ++c.launches;
+        c.launched();
       });
     }
     if (g_syrk_events) {
@@ -1083,16 +1123,13 @@ bool launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
 }
 
 void launch_diag_inverses(const double* L, int64_t mp, double* Linv, cudaStream_t s, Counter& c) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(potrf_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLeafSmem);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  smem_optin(attr, potrf_leaf_kernel, kLeafSmem);
   const int nb = static_cast<int>(mp / kNB);
   for (int kb = 0; kb < nb; ++kb) {
     potrf_leaf_kernel<<<1, kLeafThreads, kLeafSmem, s>>>(const_cast<double*>(L), mp, kb, Linv,
                                                          nullptr, mp, 0);
-    ++c.launches;
+    c.launched();
   }
 }
 
@@ -1106,7 +1143,7 @@ __global__ void zero_upper_kernel(double* A, int64_t mp) {
 
 void launch_zero_upper(double* A, int64_t mp, cudaStream_t s, Counter& c) {
   zero_upper_kernel<<<148 * 8, 256, 0, s>>>(A, mp);
-  ++c.launches;
+  c.launched();
 }
 
 // ---------------------------------------------------------------------------
@@ -1275,7 +1312,7 @@ void launch_trsv_bwd(const double* L, const double* Linv, int64_t mp, const doub
   const int nb = static_cast<int>(mp / kNB);
   cudaMemsetAsync(scratch, 0, sizeof(int) * (2 * nb + 2), s);
   trsv_bwd_kernel<<<nb, 256, 0, s>>>(L, mp, Linv, z, x, nb, scratch + 1, scratch + 2 + nb, abort);
-  ++c.launches;
+  c.launched();
 }
 
 void launch_trsv(const double* L, const double* Linv, int64_t mp, const double* b, double* z,
@@ -1284,7 +1321,7 @@ void launch_trsv(const double* L, const double* Linv, int64_t mp, const double* 
   cudaMemsetAsync(scratch, 0, sizeof(int) * (2 * nb + 2), s);
   trsv_fwd_kernel<<<nb, 256, 0, s>>>(L, mp, Linv, b, z, nb, scratch, scratch + 2, abort);
   trsv_bwd_kernel<<<nb, 256, 0, s>>>(L, mp, Linv, z, x, nb, scratch + 1, scratch + 2 + nb, abort);
-  c.launches += 2;
+  c.launched(2);
 }
 
 // ---------------------------------------------------------------------------
@@ -1309,7 +1346,7 @@ void launch_assemble(const double* K, double* A, int64_t mp, double shift, const
                      cudaStream_t s, Counter& c, bool lower_only) {
   assemble_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<const double2*>(K),
                                          reinterpret_cast<double2*>(A), mp, shift, abort, lower_only ? 1 : 0);
-  ++c.launches;
+  c.launched();
 }
 
 // y = K alpha for a symmetric K of which only the lower 128x128 tiles are stored (the
@@ -1393,7 +1430,7 @@ void launch_symv_lower(const double* K, int64_t mp, const double* alpha, double*
                        cudaStream_t s, Counter& c) {
   const dim3 grid(static_cast<unsigned>(mp / kNB), kSymvSplit);
   symv_lower_kernel<<<grid, 256, 0, s>>>(K, mp, static_cast<int>(mp / kNB), alpha, y, abort);
-  ++c.launches;
+  c.launched();
 }
 
 __global__ void __launch_bounds__(256) gemv_rows_kernel(const double* __restrict__ M, int64_t ld,
@@ -1416,7 +1453,7 @@ void launch_gemv_rows(const double* M, int64_t ld, int64_t rows, int64_t cols, c
   if (rows <= 0) return;
   gemv_rows_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(M, ld, rows, cols, v, out,
                                                                         abort);
-  ++c.launches;
+  c.launched();
 }
 
 // fixed-shape block tree reduction (deterministic)
@@ -1463,7 +1500,7 @@ void launch_residual_finish(const double* Kalpha, const double* alpha, const dou
                             Counter& c) {
   const int64_t mp = (m + kNB - 1) / kNB * kNB;
   residual_finish_kernel<<<1, 1024, 0, s>>>(Kalpha, alpha, y, m, mp, shift, out, abort);
-  ++c.launches;
+  c.launched();
 }
 
 __global__ void __launch_bounds__(1024) sse_scatter_kernel(const double* __restrict__ pred,
@@ -1490,7 +1527,7 @@ void launch_sse_scatter(const double* pred, const int64_t* pos, int64_t cnt, con
                         double* pred_all, double* out, const int* abort, cudaStream_t s,
                         Counter& c) {
   sse_scatter_kernel<<<1, 1024, 0, s>>>(pred, pos, cnt, ytest, pred_all, out, abort);
-  ++c.launches;
+  c.launched();
 }
 
 // predictor: 0 whole, 1 average, 2 nearest, 3 oracle (strategies.cpp:458-495)
@@ -1533,7 +1570,69 @@ void launch_combine(const double* pp, int64_t p, int64_t t, int predictor, const
                     const double* ytest, double* pred, double* mse_out, cudaStream_t s,
                     Counter& c) {
   combine_kernel<<<1, 1024, 0, s>>>(pp, p, t, predictor, route, ytest, pred, mse_out);
-  ++c.launches;
+  c.launched();
+}
+
+// Cell combine + MSE of every cell at once (strategies.cpp:458-495 + mse :168-177).
+// pp: per cell P x t predictions (P = 1: whole / nearest, already in test order; P = p:
+// average / oracle, one row per part).  comb[cell][j] = the combined prediction;
+// mse[cell] = sum_j (comb - y)^2 / t summed SEQUENTIALLY in test-row order with
+// explicit round-to-nearest multiplies / adds (no FMA contraction): the arithmetic of
+// the reference's mse(), so equal predictions give a bitwise equal MSE (and best cell).
+// predictor 4: average by division (predict_average, strategies.cpp:135-140).
+__global__ void combine_cells_kernel(const double* __restrict__ pp, int64_t P, int64_t t, int64_t ncell,
+                                     int predictor, const double* __restrict__ y, double* __restrict__ comb) {
+  const int64_t total = ncell * t;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = e / t, j = e % t;
+    const double* base = pp + c * P * t;
+    double v = 0.0;
+    if (predictor == 0 || predictor == 2) {
+      v = base[j];
+    } else if (predictor == 1 || predictor == 4) {
+      for (int64_t q = 0; q < P; ++q) v = __dadd_rn(v, base[q * t + j]);
+      v = predictor == 1 ? __dmul_rn(v, 1.0 / static_cast<double>(P)) : __ddiv_rn(v, static_cast<double>(P));
+    } else {
+      double be = INFINITY;
+      for (int64_t q = 0; q < P; ++q) {
+        const double u = base[q * t + j];
+        const double diff = __dsub_rn(u, y[j]);
+        const double err = __dmul_rn(diff, diff);
+        if (err < be) {
+          be = err;
+          v = u;
+        }
+      }
+    }
+    comb[e] = v;
+  }
+}
+
+__global__ void mse_rows_kernel(const double* __restrict__ comb, const double* __restrict__ y, int64_t t,
+                                int64_t ncell, double* __restrict__ mse) {
+  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (c >= ncell) return;
+  const double* v = comb + c * t;
+  double s = 0.0;
+  for (int64_t j = 0; j < t; ++j) {
+    const double diff = __dsub_rn(v[j], y[j]);
+    s = __dadd_rn(s, __dmul_rn(diff, diff));
+  }
+  mse[c] = __ddiv_rn(s, static_cast<double>(t));
+}
+
+void launch_combine_cells(const double* pp, int64_t P, int64_t t, int64_t ncell, int predictor, const double* y,
+                          double* comb, double* mse, cudaStream_t s, Counter& c) {
+  if (t <= 0 || ncell <= 0) return;
+  int64_t blocks = (ncell * t + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  combine_cells_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(pp, P, t, ncell, predictor, y, comb);
+  c.launched();
+  if (mse) {
+    mse_rows_kernel<<<static_cast<unsigned>((ncell + 31) / 32), 32, 0, s>>>(comb, y, t, ncell, mse);
+    c.launched();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1648,7 +1747,7 @@ void launch_assign(const double* X, int64_t n, int64_t d, const double* xnorm,
   else  // one pass over X for up to 64 centres (the weak-scaled partitions: k = 8 per GPU)
     assign_kernel<64><<<blocks, kAssignRows, 0, s>>>(X, n, d, xnorm, centers, cnorm, k, mode, open,
                                                     row0, label, best_dist, changed);
-  ++c.launches;
+  c.launched();
 }
 
 // ---- stable grouping: block counts -> scan -> scatter ----------------------
@@ -1748,7 +1847,7 @@ void launch_group(const int32_t* label, int64_t n, int k, int64_t* sizes, int64_
   group_start_kernel<<<1, 32, 0, s>>>(sizes, k, start);
   group_scatter_kernel<<<static_cast<unsigned>(nblk), kGroupRows, sizeof(int) * 8 * k, s>>>(
       label, n, k, tmp, start, members);
-  c.launches += 4;
+  c.launched(4);
 }
 
 // clustering.cpp:34-49: zero, row-order sums, then * (1.0 / size).
@@ -1928,16 +2027,13 @@ void launch_means(const double* X, int64_t d, const int64_t* members, const int6
                   const int64_t* sizes, int k, double* centers, cudaStream_t s, Counter& c, int j0, int j1) {
   if (j1 < 0) j1 = k;
   if (j1 <= j0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(means_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMeansSmem);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  smem_optin(attr, means_kernel, kMeansSmem);
   dim3 grid(j1 - j0, static_cast<unsigned>((d + kMeansF - 1) / kMeansF));
   // 16-byte cp.async pieces need 16-byte aligned rows and an even feature count: even d
   const int bulk = (d % 2 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
   means_kernel<<<grid, kMeansThreads, kMeansSmem, s>>>(X, d, members, start, sizes, k, centers, bulk, j0);
-  ++c.launches;
+  c.launched();
 }
 
 __global__ void label_diff_kernel(const int32_t* __restrict__ a, const int32_t* __restrict__ b, int64_t n,
@@ -1953,7 +2049,7 @@ void launch_label_diff(const int32_t* a, const int32_t* b, int64_t n, unsigned l
                        cudaStream_t s, Counter& c) {
   cudaMemsetAsync(count, 0, sizeof(unsigned long long), s);
   label_diff_kernel<<<148 * 2, 256, 0, s>>>(a, b, n, count);
-  ++c.launches;
+  c.launched();
 }
 
 // clustering.cpp:101-110: farthest sample among clusters of size > 1, first index
@@ -1993,7 +2089,7 @@ void launch_farthest(const double* best, const int32_t* label, const int64_t* si
   cudaMemsetAsync(out + 1, 0xff, sizeof(unsigned long long), s);
   farthest_max_kernel<<<148 * 4, 256, 0, s>>>(best, label, sizes, n, out);
   farthest_idx_kernel<<<148 * 4, 256, 0, s>>>(best, label, sizes, n, out);
-  c.launches += 2;
+  c.launched(2);
 }
 
 __global__ void hist_kernel(const int32_t* __restrict__ label, int64_t row0, int64_t row1, int k,
@@ -2019,7 +2115,7 @@ void launch_hist(const int32_t* label, int64_t row0, int64_t row1, int k, int64_
   if (blocks > 148 * 4) blocks = 148 * 4;
   hist_kernel<<<static_cast<unsigned>(blocks), 256, sizeof(int) * k, s>>>(
       label, row0, row1, k, reinterpret_cast<unsigned long long*>(hist));
-  ++c.launches;
+  c.launched();
 }
 
 // one CTA per cluster: position of the thr[j]-th occurrence of j in label[row0, n)
@@ -2065,7 +2161,7 @@ __global__ void __launch_bounds__(1024) events_kernel(const int32_t* __restrict_
 void launch_events(const int32_t* label, int64_t row0, int64_t n, int k, const int64_t* thr,
                    int64_t* pos, cudaStream_t s, Counter& c) {
   events_kernel<<<k, 1024, 0, s>>>(label, row0, n, thr, pos);
-  ++c.launches;
+  c.launched();
 }
 
 // ---------------------------------------------------------------------------
@@ -2088,7 +2184,7 @@ __global__ void dmma_probe_kernel(double* sink, int iters) {
 
 void launch_dmma_probe(int blocks, int threads, int iters, double* sink, cudaStream_t s, Counter& c) {
   dmma_probe_kernel<<<blocks, threads, 0, s>>>(sink, iters);
-  ++c.launches;
+  c.launched();
 }
 
 }  // namespace pk
@@ -2208,16 +2304,13 @@ __global__ void standardize_apply_kernel(const double* __restrict__ X, int64_t n
 
 bool launch_standardize_stats(const double* X, int64_t n, int64_t d, int64_t ld, double* mean, double* stddev,
                               cudaStream_t s, Counter& c) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(colstats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kStatSmem);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  smem_optin(attr, colstats_kernel, kStatSmem);
   CUtensorMap tm;  // needs a 16-byte aligned base and row pitch (ld even)
   if (!make_tmap_rows(&tm, X, n, d, ld, kStatCols, kStatRows)) return false;
   colstats_kernel<<<static_cast<unsigned>((d + kStatCols - 1) / kStatCols), 64, kStatSmem, s>>>(tm, n, d, mean,
                                                                                               stddev);
-  ++c.launches;
+  c.launched();
   return true;
 }
 
@@ -2227,7 +2320,7 @@ void launch_standardize_apply(const double* X, int64_t n, int64_t d, const doubl
   const int64_t total = n * d;
   const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
   standardize_apply_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(X, n, d, mean, stddev, out);
-  ++c.launches;
+  c.launched();
 }
 
 // auto_sigma_grid distances (strategies.cpp:214-222): pair (i, j), i < j, at the
@@ -2259,7 +2352,7 @@ void launch_pair_dist(const double* G, const double* norms, int64_t cnt, int64_t
   if (total <= 0) return;
   const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 8);
   pair_dist_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(G, norms, cnt, d, out);
-  ++c.launches;
+  c.launched();
 }
 
 }  // namespace pk

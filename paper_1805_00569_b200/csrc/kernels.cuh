@@ -14,8 +14,19 @@ namespace pk {
 
 constexpr int kNB = 128;  // Cholesky block (leaf / panel) size; parts are padded to it
 
+// Launch evidence + launch-error capture.  Every launcher calls launched() right after
+// its kernel launch(es): the count feeds bench.py's gpu_launches, and the first
+// launch error since reset() (cudaGetLastError: bad configuration, missing smem
+// attribute, ...) is kept so the C ABI returns PKRRGPU_CUDA instead of OK with
+// garbage outputs.  fault_at (PKRR_FAULT_LAUNCH, test hook) turns the launch with
+// that running count into an invalid one.
 struct Counter {
   int64_t launches = 0;
+  cudaError_t err = cudaSuccess;
+  int64_t err_at = 0;    // launch count at which err was seen
+  int64_t fault_at = 0;
+  void launched(int k = 1);
+  void reset();
 };
 
 // ---- TMA descriptors -------------------------------------------------------
@@ -121,6 +132,11 @@ void launch_sse_scatter(const double* pred, const int64_t* pos, int64_t cnt, con
                         Counter& c);
 // combine per-part predictions (average / oracle / nearest / whole) in part order
 // into pred[t] and mse over all rows (strategies.cpp:458-495)
+// every cell's combined prediction and its reference-order MSE (strategies.cpp:458-495,
+// mse :168-177): pp [ncell x P x t]; predictor 0 whole, 1 average (x 1/p), 2 nearest,
+// 3 oracle, 4 average by division (predict_average); comb [ncell x t], mse [ncell]
+void launch_combine_cells(const double* pp, int64_t P, int64_t t, int64_t ncell, int predictor, const double* y,
+                          double* comb, double* mse, cudaStream_t s, Counter& c);
 void launch_combine(const double* pp, int64_t p, int64_t t, int predictor, const int32_t* route,
                     const double* ytest, double* pred, double* mse_out, cudaStream_t s,
                     Counter& c);

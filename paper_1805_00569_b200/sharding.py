@@ -2,12 +2,16 @@
 
 The p per-part models are independent, so parts are sharded across
 ranks with no data-path collective: LPT on the Cholesky cost m^3 (largest part to the
-least-loaded rank), computed identically by every rank from the common partition.  After training, each rank holds
-per-(cell, part) SSE / failure flags for its own parts (zeros elsewhere).  One
-all-reduce (SUM for SSE -- the shards are disjoint, so every sum is x + 0 + ...
-= x exactly; MAX for flags) reconstructs the full table on every rank, which is
-then combined in PART ORDER exactly like the single-process engine does.  The
-result is therefore bitwise independent of the number of GPUs.
+least-loaded rank), computed identically by every rank from the common partition.
+After training, each rank holds its parts' per-cell predictions
+(pkrrgpu_grid_out.cell_pred: test rows routed to its parts for the nearest predictor,
+its parts' rows for average / oracle; zeros elsewhere) and per-(cell, part) failure
+flags.  One all-reduce (SUM for the predictions -- the shards are disjoint, so every
+sum is x + 0 + ... = x exactly; MAX for the flags) reconstructs the full predictions
+on every rank, and pkrrgpu_combine (Engine.combine) -- the very code the
+single-process grid runs -- combines them and sums the MSE in test-row order
+(strategies.cpp:458-505).  The result is bitwise independent of the number of GPUs,
+for every predictor (average and oracle included).
 """
 from __future__ import annotations
 
@@ -29,21 +33,22 @@ def owned_parts(sizes, rank: int, world: int):
     return [t for t in range(len(sizes)) if owner[t] == rank]
 
 
-def allreduce_tables(part_sse, part_failed, dist, device=None):
-    """SUM-reduce the disjoint SSE shards and MAX-reduce the failure flags."""
+def allreduce_predictions(cell_pred, part_failed, dist, device=None):
+    """SUM-reduce the disjoint per-cell prediction shards ([ncell, P, t]) and
+    MAX-reduce the per-(cell, part) failure flags; returns (predictions, failed
+    cells) identical on every rank."""
     import torch
-    sse = torch.as_tensor(np.ascontiguousarray(part_sse, np.float64), device=device).clone()
+    pred = torch.as_tensor(np.ascontiguousarray(cell_pred, np.float64), device=device).clone()
     fl = torch.as_tensor(np.ascontiguousarray(part_failed, np.float64), device=device).clone()
-    dist.all_reduce(sse, op=dist.ReduceOp.SUM)
+    dist.all_reduce(pred, op=dist.ReduceOp.SUM)
     dist.all_reduce(fl, op=dist.ReduceOp.MAX)
-    return sse.cpu().numpy(), fl.cpu().numpy() > 0
+    return pred.cpu().numpy(), (fl.cpu().numpy() > 0).any(axis=1)
 
 
-def combine(part_sse, part_failed, t):
-    """(mse per cell, failed per cell, best index): strategies.cpp:495-505 over the
-    part-order SSE sum (see paper_1805_00569_b200.combine_parts)."""
-    from . import combine_parts
-    return combine_parts(part_sse, part_failed, t)
+def combine(engine, strategy, p, cell_pred, failed_cells, y):
+    """(mse per cell, best index, best prediction) of the all-reduced predictions, by
+    the engine's own combine (pkrrgpu_combine): bitwise the single-process result."""
+    return engine.combine(strategy, p, cell_pred, y, failed_cells)
 
 
 # ---- sharded partition exchange (pkrrgpu_grid_args.allgather) -------------------------

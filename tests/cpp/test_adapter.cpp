@@ -3,6 +3,8 @@
 // build container (needs /root/reference headers); run on the GPU box by
 // tests/test_gpu_adapter.py.  Exit status 0 iff every check passes.
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <cstdio>
 #include <vector>
 
@@ -134,6 +136,97 @@ int main() {
       pn = pn && std::fabs(a - b) <= 1e-8 * std::fabs(b) + 1e-12;
     }
     CHECK(pn, "predict_nearest over GPU-trained models agrees");
+  }
+  // train_partitions with the caller's PartitionSet (random partition: rows in permutation
+  // order), GPU predict stage vs the reference's predict_nearest / predict_average /
+  // predict_oracle (strategies.cpp:135-166)
+  {
+    const Dataset Q = mixture(60, 12, 5, 8);
+    for (StrategyKind k : {StrategyKind::kk2, StrategyKind::dc, StrategyKind::bk2}) {
+      const PartitionSet ps = pkrr::make_partition(k, X, 4, 13);
+      const TrainedPartitions g = gpu::train_partitions(ps, X, spec, 1e-3);
+      const TrainedPartitions r = pkrr::train_partitions(ps, X, spec, 1e-3);
+      bool ok = g.models.size() == r.models.size();
+      for (std::size_t t = 0; ok && t < r.models.size(); ++t)
+        ok = rel(g.models[t].alpha, r.models[t].alpha) <= 1e-8 && g.models[t].support.val == r.models[t].support.val &&
+             g.models[t].train_ops.solve_flops == r.models[t].train_ops.solve_flops;
+      std::string what = std::string("train_partitions(") + strategy_name(k) + "): alpha rel <= 1e-8, same supports";
+      CHECK(ok, what.c_str());
+      // batched GPU predict over the GPU-resident models, and over the host models
+      const gpu::DeviceModels dm = gpu::train_partitions_device(ps, X, spec, 1e-3);
+      std::vector<double> ref_avg(Q.n), ref_or(Q.n);
+      std::vector<std::size_t> ref_or_t(Q.n);
+      OpCount oa, ob;
+      for (std::size_t j = 0; j < Q.n; ++j) {
+        ref_avg[j] = pkrr::predict_average(r.models, Q.row(j), &ob);
+        const auto pr = pkrr::predict_oracle(r.models, Q.row(j), Q.y[j]);
+        ref_or[j] = pr.first;
+        ref_or_t[j] = pr.second;
+      }
+      const std::vector<double> avg = gpu::predict_average(g.models, Q, &oa);
+      CHECK(rel(avg, ref_avg) <= 1e-8 && oa.predict_flops == ob.predict_flops,
+            "predict_average: GPU batched vs reference per row, rel <= 1e-8, OpCount identical");
+      const auto orc = gpu::predict_oracle(g.models, Q);
+      bool oc = true;
+      std::vector<double> orv;
+      for (std::size_t j = 0; j < Q.n; ++j) orv.push_back(orc[j].first), oc = oc && orc[j].second == ref_or_t[j];
+      CHECK(oc && rel(orv, ref_or) <= 1e-8, "predict_oracle: same chosen models, rel <= 1e-8");
+      for (std::size_t t = 0; t < ps.p; ++t) {
+        std::vector<double> want(Q.n);
+        for (std::size_t j = 0; j < Q.n; ++j) want[j] = r.models[t].predict(Q.row(j));
+        CHECK(rel(gpu::predict(dm, t, Q), want) <= 1e-8, "KrrModel::predict batched on device models, rel <= 1e-8");
+      }
+      if (!ps.has_centers()) continue;
+      std::vector<double> want(Q.n);
+      OpCount rc_ops, gc_ops;
+      for (std::size_t j = 0; j < Q.n; ++j) want[j] = pkrr::predict_nearest(r.models, ps.centers, Q.row(j), &rc_ops);
+      CHECK(rel(gpu::predict_nearest(dm, Q), want) <= 1e-8, "predict_nearest: device models vs reference, rel <= 1e-8");
+      CHECK(rel(gpu::predict_nearest(g.models, ps.centers, Q, &gc_ops), want) <= 1e-8 &&
+                gc_ops.predict_flops == rc_ops.predict_flops,
+            "predict_nearest: host models batched on the GPU, rel <= 1e-8, OpCount identical");
+      const double one = gpu::predict_nearest(std::span<const KrrModel>(g.models), ps.centers, Q.row(3));
+      CHECK(std::fabs(one - want[3]) <= 1e-8 * std::fabs(want[3]) + 1e-12, "predict_nearest: drop-in single row");
+    }
+  }
+  // a failed kernel launch is reported, never OK with garbage (PKRR_FAULT_LAUNCH test hook)
+  {
+    setenv("PKRR_FAULT_LAUNCH", "3", 1);
+    pkrrgpu_ctx* c = nullptr;
+    const int rc0 = pkrrgpu_create(0, &c);
+    unsetenv("PKRR_FAULT_LAUNCH");
+    std::vector<double> Xd = gpu::detail::dense(X), alpha(X.n);
+    double res = 0;
+    int64_t piv = -1;
+    const int rc = rc0 == PKRRGPU_OK ? pkrrgpu_train_krr(c, Xd.data(), X.y.data(), X.n, X.d, 2.5, 1e-4,
+                                                         alpha.data(), &res, &piv)
+                                     : rc0;
+    const std::string msg = pkrrgpu_last_error();
+    std::printf("  forced bad launch: rc=%d \"%s\"\n", rc, msg.c_str());
+    CHECK(rc == PKRRGPU_CUDA && msg.find("launch") != std::string::npos, "forced bad launch -> PKRRGPU_CUDA");
+    const int rc2 = pkrrgpu_train_krr(c, Xd.data(), X.y.data(), X.n, X.d, 2.5, 1e-4, alpha.data(), &res, &piv);
+    CHECK(rc2 == PKRRGPU_OK, "the context recovers: the next call (no fault) is OK");
+    pkrrgpu_destroy(c);
+  }
+  // two contexts on one GPU (one host thread each) == one context, bitwise; the sharded
+  // partition's peer all-gather included
+  {
+    setenv("PKRR_SHARD_PARTITION", "1", 1);
+    gpu::Group two({0, 0});
+    const Dataset tr = mixture(2400, 10, 6, 41), te = mixture(300, 10, 6, 42);
+    const std::vector<double> lam{1e-4, 1e-2}, sig{1.5, 4.0};
+    for (StrategyKind k : {StrategyKind::kk2, StrategyKind::bk2, StrategyKind::kk, StrategyKind::kk3,
+                           StrategyKind::dc, StrategyKind::exact}) {
+      const GridResult a = gpu::grid_search(k, tr, te, 6, lam, sig, 9);
+      const GridResult b = gpu::grid_search(k, tr, te, 6, lam, sig, 9, GridOptions{}, two);
+      bool same = a.best_index == b.best_index && a.cells.size() == b.cells.size();
+      for (std::size_t c = 0; same && c < a.cells.size(); ++c)
+        same = std::memcmp(&a.cells[c].mse, &b.cells[c].mse, sizeof(double)) == 0 &&
+               a.cells[c].failed == b.cells[c].failed && a.cells[c].max_residual == b.cells[c].max_residual &&
+               a.cells[c].flops == b.cells[c].flops;
+      std::string what = std::string("grid_search ") + strategy_name(k) + ": 2 contexts on one GPU == 1, bitwise";
+      CHECK(same, what.c_str());
+    }
+    unsetenv("PKRR_SHARD_PARTITION");
   }
   // grid_search
   {

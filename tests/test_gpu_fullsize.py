@@ -118,31 +118,36 @@ def test_degenerate_sizes(engine, oracle):
         assert abs(g.mse[0] - r["mse"][0]) <= 1e-8 * abs(r["mse"][0])
 
 
-def test_sharded_grid_equals_single_process(engine):
-    """The one-process-per-GPU path: each rank trains parts t % world == rank; the
-    disjoint per-part tables, combined in part order, give bitwise the
-    single-process result (run here as both ranks' shares on one GPU)."""
+@pytest.mark.parametrize("strategy", ["kkrr2", "bkrr", "kkrr3", "dckrr"])
+def test_sharded_grid_equals_single_process(engine, strategy):
+    """The one-process-per-GPU path: each rank trains the parts the LPT rule gives it;
+    the ranks' disjoint per-cell predictions, summed and combined by the engine's own
+    combine, give bitwise the single-process result -- for the nearest, average and
+    oracle predictors (run here as both ranks' shares on one GPU)."""
     from paper_1805_00569_b200 import sharding
     dd = datagen.make(6000, 300, 300, 20, 8, seed=21)
     kw = dict(eval_X=dd["X_test"], eval_y=dd["y_test"])
     lam, sig = [1e-4, 1e-2], [1.5, 4.0]
-    full = engine.grid_search("kkrr2", dd["X_train"], dd["y_train"], dd["X_val"], dd["y_val"], 6, lam, sig, 3, **kw)
-    sse = np.zeros_like(full.parts["part_sse"])
-    esse = np.zeros_like(sse)
-    failed = np.zeros(sse.shape, bool)
+    full = engine.grid_search(strategy, dd["X_train"], dd["y_train"], dd["X_val"], dd["y_val"], 6, lam, sig, 3,
+                              **kw)
+    pred = np.zeros_like(full.parts["cell_pred"])
+    epred = np.zeros_like(full.parts["cell_eval_pred"])
+    failed = np.zeros(full.parts["part_failed"].shape, bool)
     for rank in range(2):
-        r = engine.grid_search("kkrr2", dd["X_train"], dd["y_train"], dd["X_val"], dd["y_val"], 6, lam, sig, 3,
+        r = engine.grid_search(strategy, dd["X_train"], dd["y_train"], dd["X_val"], dd["y_val"], 6, lam, sig, 3,
                                rank=rank, world=2, **kw)
         mine = sharding.owned_parts(r.parts["part_sizes"], rank, 2)
         other = [t for t in range(6) if t not in mine]
         assert np.all(r.parts["part_sse"][:, other] == 0.0)
-        sse += r.parts["part_sse"]
-        esse += r.parts["part_eval_sse"]
+        pred += r.parts["cell_pred"]
+        epred += r.parts["cell_eval_pred"]
         failed |= r.parts["part_failed"].astype(bool)
-    mse, cell_failed, best = sharding.combine(sse, failed, 300)
+    assert pred.tobytes() == full.parts["cell_pred"].tobytes()
+    mse, best, best_pred = sharding.combine(engine, strategy, 6, pred, failed.any(axis=1), dd["y_val"])
     assert mse.tobytes() == full.mse.tobytes()
     assert best == full.best_index
-    emse, _, _ = sharding.combine(esse, failed, 300)
+    assert best_pred.tobytes() == full.best_pred.tobytes()
+    emse, _, _ = sharding.combine(engine, strategy, 6, epred, failed.any(axis=1), dd["y_test"])
     assert emse.tobytes() == full.eval_mse.tobytes()
 
 

@@ -3,8 +3,8 @@
 Two ranks (processes) share cuda:0 over a gloo process group with the host-staged
 exchange (sharding.staged_allgather): each rank assigns half the rows and updates
 half the clusters per Lloyd iteration.  The partition (labels, centres, sizes) must be
-bitwise the single-process one, and the per-part tables combined in part order must
-give bitwise the single-process cell MSEs -- for k-means (KKRR2), the k-balance warm
+bitwise the single-process one, and the ranks' per-cell predictions summed and combined
+must give bitwise the single-process cell MSEs -- for k-means (KKRR2), the k-balance warm
 start (BKRR2) and the empty-cluster reseed path.  (The ranks only meet in host-side
 collectives; no kernel waits on another rank.)
 """
@@ -40,7 +40,7 @@ r = eng.grid_search({strategy!r}, z["Xtr"], z["ytr"], z["Xs"], z["ys"], {p}, [1e
                     km_threshold={thr}, km_max_iters={iters}, rank=rank, world=world, want_partition=True,
                     allgather=ag)
 np.savez({out!r} + f".{{rank}}.npz", part_of=r.parts["part_of"], centers=r.parts["centers"],
-         sizes=r.parts["part_sizes"], sse=r.parts["part_sse"], failed=r.parts["part_failed"])
+         sizes=r.parts["part_sizes"], pred=r.parts["cell_pred"], failed=r.parts["part_failed"])
 dist.destroy_process_group()
 """
 
@@ -79,9 +79,9 @@ def test_sharded_partition_is_bitwise_the_single_process_one(engine, tmp_path, s
         assert np.array_equal(z["part_of"], full.parts["part_of"])
         assert np.array_equal(z["centers"], full.parts["centers"])
         assert np.array_equal(z["sizes"], full.parts["part_sizes"])
-    sse = sum(z["sse"] for z in ranks)
+    pred = sum(z["pred"] for z in ranks)
     failed = np.logical_or.reduce([z["failed"].astype(bool) for z in ranks])
-    mse, cell_failed, best = sharding.combine(sse, failed, Xs.shape[0])
+    mse, best, _ = sharding.combine(engine, strategy, p, pred, failed.any(axis=1), ys)
     assert mse.tobytes() == full.mse.tobytes()
     assert best == full.best_index
 

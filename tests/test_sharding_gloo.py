@@ -1,5 +1,7 @@
-"""CPU, world_size 2 over gloo: the multi-GPU combine reproduces the
-single-process result bitwise (parts sharded by the LPT rule, disjoint SSE shards)."""
+"""CPU, world_size 2 over gloo: the multi-GPU exchange reconstructs the
+single-process predictions bitwise (parts sharded by the LPT rule, disjoint
+prediction shards summed, failure flags max-reduced).  The combine that follows is
+the engine's own pkrrgpu_combine, checked on the GPU (test_gpu_fullsize.py)."""
 import os
 import socket
 
@@ -17,44 +19,57 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, full_sse, full_failed, t, sizes, out):
+def _shard(full_pred, route, full_failed, sizes, rank, world, per_part):
+    """This rank's share: its parts' rows (nearest: rows routed to its parts; average /
+    oracle: its parts' prediction rows), zeros elsewhere."""
+    mine = sharding.owned_parts(sizes, rank, world)
+    pred = np.zeros_like(full_pred)
+    if per_part:
+        pred[:, mine, :] = full_pred[:, mine, :]
+    else:
+        rows = np.isin(route, mine)
+        pred[:, 0, rows] = full_pred[:, 0, rows]
+    fl = np.zeros_like(full_failed)
+    fl[:, mine] = full_failed[:, mine]
+    return pred, fl
+
+
+def _worker(rank, world, port, cases, sizes, out):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    nc, p = full_sse.shape
-    mine = sharding.owned_parts(sizes, rank, world)
-    sse = np.zeros_like(full_sse)
-    fl = np.zeros_like(full_failed)
-    sse[:, mine] = full_sse[:, mine]
-    fl[:, mine] = full_failed[:, mine]
-    s, f = sharding.allreduce_tables(sse, fl, dist)
-    mse, failed, best = sharding.combine(s, f, t)
-    out[rank] = (mse.tobytes(), failed.tobytes(), best)
+    res = []
+    for full_pred, route, full_failed, per_part in cases:
+        pred, fl = _shard(full_pred, route, full_failed, sizes, rank, world, per_part)
+        p, f = sharding.allreduce_predictions(pred, fl, dist)
+        res.append((p.tobytes(), f.tobytes()))
+    out[rank] = res
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_two_rank_combine_is_bitwise_single_rank():
+def test_two_rank_prediction_exchange_is_bitwise_single_rank():
     rng = np.random.default_rng(0)
     nc, p, t = 6, 8, 2048
-    full_sse = rng.random((nc, p)) * 10.0 ** rng.integers(-3, 3, (nc, p))
-    full_failed = np.zeros((nc, p), bool)
-    full_failed[2, 5] = True  # one part of cell 2 failed (NPD) -> cell failed
-    ref_mse, ref_failed, ref_best = sharding.combine(full_sse, full_failed, t)
+    sizes = [8275, 4117, 4002, 4108, 20544, 4092, 12298, 8100]
+    route = rng.integers(0, p, t)
+    failed = np.zeros((nc, p), bool)
+    failed[2, 5] = True  # one part of cell 2 failed (NPD) -> cell failed
+    near = rng.standard_normal((nc, 1, t)) * 10.0 ** rng.integers(-3, 3, (nc, 1, t))
+    near[0, 0, :5] = -0.0  # signed zeros survive the sum only as +0: same squared error
+    avg = rng.standard_normal((nc, p, t))
+    cases = [(near, route, failed, False), (avg, route, failed, True)]
     manager = mp.Manager()
     out = manager.dict()
-    port = _free_port()
-    sizes = [8275, 4117, 4002, 4108, 20544, 4092, 12298, 8100]
-    mp.start_processes(_worker, args=(2, port, full_sse, full_failed, t, sizes, out), nprocs=2, join=True,
+    mp.start_processes(_worker, args=(2, _free_port(), cases, sizes, out), nprocs=2, join=True,
                        start_method="spawn")
     for rank in range(2):
-        mse_b, failed_b, best = out[rank]
-        assert mse_b == ref_mse.tobytes()
-        assert failed_b == ref_failed.tobytes()
-        assert best == ref_best
-    assert ref_failed[2] and not ref_failed[0]
-    assert np.isnan(ref_mse[2])
+        for (full_pred, _, full_failed, _), (pb, fb) in zip(cases, out[rank]):
+            got = np.frombuffer(pb, np.float64).reshape(full_pred.shape)
+            assert np.array_equal(got, full_pred)  # -0.0 == +0.0 compares equal
+            assert np.array_equal(np.abs(got).tobytes(), np.abs(full_pred).tobytes())
+            assert np.frombuffer(fb, bool).tolist() == full_failed.any(axis=1).tolist()
 
 
 def test_owned_parts_partition_the_parts():
