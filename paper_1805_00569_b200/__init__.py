@@ -272,7 +272,7 @@ class Engine:
         """Caller array -> engine input.  A CUDA tensor may still be written by work
         queued on torch's current stream: the engine's launch stream is ordered after it
         (pkrrgpu_wait_stream) before any kernel reads the tensor."""
-        a = self._in(a, self.device, dtype)
+        a = _f64(a, self.device, dtype)
         if a is not None and hasattr(a, "data_ptr"):
             import torch
             _check(_lib.pkrrgpu_wait_stream(self._h, torch.cuda.current_stream(a.device).cuda_stream))
