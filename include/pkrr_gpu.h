@@ -290,6 +290,15 @@ pkrrgpu_ctx* pkrrgpu_multi_context(pkrrgpu_multi* m, int i);
  * summed and combined once (pkrrgpu_combine).  args->rank / world / allgather are
  * ignored; `out` is filled as by a one-context call, and is bitwise equal to it. */
 int pkrrgpu_multi_grid_search(pkrrgpu_multi* m, const pkrrgpu_grid_args* args, pkrrgpu_grid_out* out);
+/* DKRR (the reference's whole-data baseline, runtime.cpp:54-57):
+ * train_krr (solver.cpp:89-125) of ONE n-row Gaussian system factorised ACROSS the
+ * group's GPUs -- block-cyclic super-columns of 128 G columns stored compactly per GPU
+ * (each holds ~1/W of the matrix), each factored panel peer-copied to the other GPUs,
+ * lookahead on the next panel's owner, forward substitution fused, backward solve along
+ * the owner chain.  alpha (n), residual ||(K + lambda n I) alpha - y|| / ||y||;
+ * PKRRGPU_NPD with *npd_pivot = the first failing column.  PKRR_DIST_GROUP sets G. */
+int pkrrgpu_multi_train_krr(pkrrgpu_multi* m, const double* X, const double* y, int64_t n, int64_t d,
+                            double sigma, double lambda, double* alpha, double* residual, int64_t* npd_pivot);
 
 /* ---- data preparation (dataset.hpp standardize, strategies.hpp auto_sigma_grid) */
 

@@ -160,6 +160,8 @@ def load_library(path: str = LIB_PATH):
         "pkrrgpu_multi_size": (C.c_int, [C.c_void_p]),
         "pkrrgpu_multi_context": (C.c_void_p, [C.c_void_p, C.c_int]),
         "pkrrgpu_multi_grid_search": (C.c_int, [C.c_void_p, C.POINTER(GridArgs), C.POINTER(GridOut)]),
+        "pkrrgpu_multi_train_krr": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_double,
+                                              C.c_double, C.c_void_p, _d, _i64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -614,6 +616,19 @@ class Group:
     def launches(self) -> int:
         return sum(int(_lib.pkrrgpu_launch_count(_lib.pkrrgpu_multi_context(self._h, i)))
                    for i in range(len(self.devices)))
+
+    def train_krr(self, X, y, sigma, lam):
+        """DKRR: train_krr (solver.cpp:89-125) of ONE system factorised across the group's
+        GPUs (pkrrgpu_multi_train_krr).  Returns (alpha, residual)."""
+        X = np.ascontiguousarray(X, np.float64)
+        y = np.ascontiguousarray(y, np.float64)
+        alpha = np.empty(X.shape[0])
+        res = C.c_double(0)
+        piv = C.c_int64(-1)
+        rc = _lib.pkrrgpu_multi_train_krr(self._h, X.ctypes.data, y.ctypes.data, X.shape[0], X.shape[1],
+                                          float(sigma), float(lam), alpha.ctypes.data, C.byref(res), C.byref(piv))
+        _check(rc, piv.value)
+        return alpha, res.value
 
     def grid_search(self, strategy, train_X, train_y, test_X, test_y, p, lambdas, sigmas, seed, **kw):
         kw.pop("rank", None), kw.pop("world", None), kw.pop("allgather", None)

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpkrr_gpu.so")
-SOURCES = ["kernels.cu", "engine.cu", "multi.cu"]
+SOURCES = ["kernels.cu", "engine.cu", "multi.cu", "dist.cu"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "-Xptxas", "-O3"]

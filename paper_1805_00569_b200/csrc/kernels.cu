@@ -517,7 +517,6 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
   if (!factor) {
     // diagonal-block inverses of a finished factor (launch_diag_inverses)
     if (warp < 4) warp_trtri32(S + (32 * warp) * kLS + 32 * warp, D + warp * 32 * kBS, lane);
-    __syncthreads();
   } else if (warp == 7) {
     // ---- warp 7: the 32x32 diagonal-block inverses, each as soon as its block is
     // factored, off the panel chain (they feed only the blocked inverse below) ----
@@ -526,7 +525,6 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
       if (*reinterpret_cast<volatile int*>(flag)) return;
       warp_trtri32(S + (32 * pb) * kLS + 32 * pb, D + pb * 32 * kBS, lane);
     }
-    __syncthreads();
   } else {
     // ---- warps 0-6: four 32-column panels.  Warp 0 factors the diagonal block,
     // warps 1..3-pb the rows below it in step (one column behind at most), then the
@@ -598,8 +596,9 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
             *reinterpret_cast<const double2*>(S + r * kLS + 2 * cp);
     }
     LEAF_MARK(21);
-    __syncthreads();
   }
+  // one barrier for every branch above (all warps reach this same call site)
+  __syncthreads();
 
   LEAF_MARK(22);
   // ---- blocked inverse: X_ij = -D_i * sum_{k=j}^{i-1} L_ik X_kj, X_ij stored (not
@@ -1246,13 +1245,15 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(const double* __restrict_
                                                        const double* __restrict__ Linv,
                                                        const double* __restrict__ z, double* x,
                                                        int nb, int* ticket, int* flags,
-                                                       const int* abort) {
+                                                       const int* abort, int ihi) {
   if (abort && *reinterpret_cast<const volatile int*>(abort)) return;
   __shared__ double red[8][kNB];
   __shared__ double sv[kNB];
   __shared__ int sI;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  if (tid == 0) sI = nb - 1 - atomicAdd(ticket, 1);
+  // blocks ihi-1, ihi-2, ... in ticket order (ihi = nb: the whole solve; the distributed
+  // solve runs one super-column's blocks with the later x blocks already final)
+  if (tid == 0) sI = ihi - 1 - atomicAdd(ticket, 1);
   __syncthreads();
   const int I = sI;
   prefetch_l2_block(Linv + static_cast<int64_t>(I) * kNB * kNB, kNB, tid);
@@ -1311,7 +1312,7 @@ void launch_trsv_bwd(const double* L, const double* Linv, int64_t mp, const doub
                      int* scratch, const int* abort, cudaStream_t s, Counter& c) {
   const int nb = static_cast<int>(mp / kNB);
   cudaMemsetAsync(scratch, 0, sizeof(int) * (2 * nb + 2), s);
-  trsv_bwd_kernel<<<nb, 256, 0, s>>>(L, mp, Linv, z, x, nb, scratch + 1, scratch + 2 + nb, abort);
+  trsv_bwd_kernel<<<nb, 256, 0, s>>>(L, mp, Linv, z, x, nb, scratch + 1, scratch + 2 + nb, abort, nb);
   c.launched();
 }
 
@@ -1320,7 +1321,7 @@ void launch_trsv(const double* L, const double* Linv, int64_t mp, const double* 
   const int nb = static_cast<int>(mp / kNB);
   cudaMemsetAsync(scratch, 0, sizeof(int) * (2 * nb + 2), s);
   trsv_fwd_kernel<<<nb, 256, 0, s>>>(L, mp, Linv, b, z, nb, scratch, scratch + 2, abort);
-  trsv_bwd_kernel<<<nb, 256, 0, s>>>(L, mp, Linv, z, x, nb, scratch + 1, scratch + 2 + nb, abort);
+  trsv_bwd_kernel<<<nb, 256, 0, s>>>(L, mp, Linv, z, x, nb, scratch + 1, scratch + 2 + nb, abort, nb);
   c.launched(2);
 }
 
@@ -2353,6 +2354,116 @@ void launch_pair_dist(const double* G, const double* norms, int64_t cnt, int64_t
   const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 8);
   pair_dist_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(G, norms, cnt, d, out);
   c.launched();
+}
+
+// ---------------------------------------------------------------------------
+// building blocks of the distributed (DKRR) factorization, csrc/dist.cu: the same
+// kernels as launch_potrf, addressed through explicit row / column origins so that a
+// device can work on its own compact column slabs (row-major, ld = its slab width).
+// ---------------------------------------------------------------------------
+void launch_gemm_update(const CUtensorMap& tmA, const CUtensorMap& tmB, int a_row0, int a_k0, int b_row0, int b_k0,
+                        int ktiles, double* C, int64_t ldc, int c_row0, int c_col0, int tiles_m128, int tiles_n,
+                        const int* abort, cudaStream_t s, Counter& c) {
+  if (tiles_m128 <= 0 || tiles_n <= 0 || ktiles <= 0) return;
+  GemmParams u{};
+  u.a_row0 = a_row0;
+  u.b_row0 = b_row0;
+  u.a_k0 = a_k0;
+  u.b_k0 = b_k0;
+  u.ktiles = ktiles;
+  u.C = C;
+  u.ldc = ldc;
+  u.c_row0 = c_row0;
+  u.c_col0 = c_col0;
+  u.tiles_n = tiles_n;
+  u.abort_flag = abort;
+  if (tiles_m128 * tiles_n < g_sms) {  // under one wave of 128-row tiles: 64-row tiles
+    u.tiles_m = 2 * tiles_m128;
+    gemm_launch<64, G_UPDATE>(tmA, tmB, u, u.tiles_m * tiles_n, s, c);
+  } else {
+    u.tiles_m = tiles_m128;
+    gemm_launch<128, G_UPDATE>(tmA, tmB, u, u.tiles_m * tiles_n, s, c);
+  }
+}
+
+void launch_gemm_trsm(const CUtensorMap& tmA, const CUtensorMap& tmLinv, int row0, int col0, int kb, int rows128,
+                      double* C, int64_t ldc, const double* fz, double* fw, const int* abort, cudaStream_t s,
+                      Counter& c) {
+  if (rows128 <= 0) return;
+  GemmParams t{};
+  t.a_row0 = row0;
+  t.a_k0 = col0;
+  t.b_row0 = kb * kNB;
+  t.b_k0 = 0;
+  t.ktiles = kNB / kBK;
+  t.C = C;
+  t.ldc = ldc;
+  t.c_row0 = row0;
+  t.c_col0 = col0;
+  t.tiles_n = 1;
+  t.tiles_m = rows128 * 2;
+  t.abort_flag = abort;
+  t.fz = fz;
+  t.fw = fw;
+  gemm_launch<64, G_STORE>(tmA, tmLinv, t, t.tiles_m, s, c);
+}
+
+void launch_leaf_at(double* A_shifted, int64_t lda, int kb, double* Linv, int* status, int64_t m_valid,
+                    const double* w, double* z, cudaStream_t s, Counter& c) {
+  static std::atomic<uint64_t> attr{0};
+  smem_optin(attr, potrf_leaf_kernel, kLeafSmem);
+  launch_pdl(potrf_leaf_kernel, 1, kLeafThreads, kLeafSmem, s, A_shifted, lda, kb, Linv, status, m_valid, 1, w, z);
+  c.launched();
+}
+
+// Gaussian kernel block K[row0 : row0 + rows, col0 : col0 + cols] (global indices,
+// rows % 64 == 0, cols % 128 == 0) written at Cblk (ld ldc); padding rows / columns
+// (>= m_valid) are 0 -- the caller sets the diagonal
+void launch_gram_block(const CUtensorMap& tmX, const double* norms, int64_t dp, int row0, int col0, int rows,
+                       int cols, int64_t m_valid, double sigma, double* Cblk, int64_t ldc, cudaStream_t s,
+                       Counter& c) {
+  if (rows <= 0 || cols <= 0) return;
+  GemmParams p{};
+  p.ktiles = static_cast<int>(dp / kBK);
+  p.a_row0 = row0;
+  p.b_row0 = col0;
+  p.C = Cblk;
+  p.ldc = ldc;
+  p.tiles_m = rows / 64;
+  p.tiles_n = cols / 128;
+  p.norm_a = norms + row0;
+  p.norm_b = norms + col0;
+  p.valid_a = static_cast<int>(m_valid - row0 < 0 ? 0 : m_valid - row0);
+  p.valid_b = static_cast<int>(m_valid - col0 < 0 ? 0 : m_valid - col0);
+  p.denom = (2.0 * sigma) * sigma;
+  p.neg_inv_denom = -1.0 / p.denom;
+  gemm_launch<64, G_GRAM_CROSS>(tmX, tmX, p, p.tiles_m * p.tiles_n, s, c);
+}
+
+__global__ void set_diag_ld_kernel(double* A, int64_t ld, int64_t row0, int64_t col0, int64_t count, double v) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < count) A[(row0 + i) * ld + col0 + i] = v;
+}
+
+void launch_set_diag(double* A, int64_t ld, int64_t row0, int64_t col0, int64_t count, double v, cudaStream_t s,
+                     Counter& c) {
+  if (count <= 0) return;
+  set_diag_ld_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, s>>>(A, ld, row0, col0, count, v);
+  c.launched();
+}
+
+__global__ void fill_flags_kernel(int* f, int n, int lo, int hi) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) f[i] = i >= lo && i < hi ? 0 : 1;
+}
+
+void launch_trsv_bwd_range(const double* L_shifted, int64_t ld, const double* Linv, const double* z, double* x, int nb,
+                           int ilo, int ihi, int* scratch, const int* abort, cudaStream_t s, Counter& c) {
+  // scratch: [0] ticket, [1 ..] flags: the blocks >= ihi are final (x from later super-columns)
+  cudaMemsetAsync(scratch, 0, sizeof(int), s);
+  fill_flags_kernel<<<(nb + 255) / 256, 256, 0, s>>>(scratch + 1, nb, ilo, ihi);
+  trsv_bwd_kernel<<<ihi - ilo, 256, 0, s>>>(L_shifted, ld, Linv, z, x, nb, scratch, scratch + 1, abort, ihi);
+  c.launched(2);
 }
 
 }  // namespace pk

@@ -186,4 +186,27 @@ void launch_standardize_apply(const double* X, int64_t n, int64_t d, const doubl
 void launch_pair_dist(const double* G, const double* norms, int64_t cnt, int64_t d, double* out, cudaStream_t s,
                       Counter& c);
 
+// ---- distributed factorization building blocks (csrc/dist.cu) ----------------
+// C[c_row0 + .., c_col0 + ..] -= A[a_row0 + .., a_k0 ..] B[b_row0 + .., b_k0 ..]^T over
+// tiles_m128 x tiles_n tiles of 128 x 128, K = 16 ktiles
+void launch_gemm_update(const CUtensorMap& tmA, const CUtensorMap& tmB, int a_row0, int a_k0, int b_row0, int b_k0,
+                        int ktiles, double* C, int64_t ldc, int c_row0, int c_col0, int tiles_m128, int tiles_n,
+                        const int* abort, cudaStream_t s, Counter& c);
+// panel TRSM in place: C[row0 .., col0 .. +128] = A[row0 .., col0 ..] inv(L_kb)^T over
+// rows128 128-row blocks; fused forward substitution fw -= C fz (fz = z + 128 kb)
+void launch_gemm_trsm(const CUtensorMap& tmA, const CUtensorMap& tmLinv, int row0, int col0, int kb, int rows128,
+                      double* C, int64_t ldc, const double* fz, double* fw, const int* abort, cudaStream_t s,
+                      Counter& c);
+// the Cholesky leaf of global block kb of a matrix whose block (kb, kb) sits at
+// A_shifted + 128 kb (lda + 1)
+void launch_leaf_at(double* A_shifted, int64_t lda, int kb, double* Linv, int* status, int64_t m_valid,
+                    const double* w, double* z, cudaStream_t s, Counter& c);
+void launch_gram_block(const CUtensorMap& tmX, const double* norms, int64_t dp, int row0, int col0, int rows,
+                       int cols, int64_t m_valid, double sigma, double* Cblk, int64_t ldc, cudaStream_t s,
+                       Counter& c);
+void launch_set_diag(double* A, int64_t ld, int64_t row0, int64_t col0, int64_t count, double v, cudaStream_t s,
+                     Counter& c);
+// backward solve of blocks [ilo, ihi) (x blocks >= ihi final); scratch: nb + 1 ints
+void launch_trsv_bwd_range(const double* L_shifted, int64_t ld, const double* Linv, const double* z, double* x, int nb,
+                           int ilo, int ihi, int* scratch, const int* abort, cudaStream_t s, Counter& c);
 }  // namespace pk

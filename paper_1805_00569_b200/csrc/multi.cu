@@ -140,6 +140,9 @@ void pkrrgpu_multi_destroy(pkrrgpu_multi* m) {
 
 int pkrrgpu_multi_size(const pkrrgpu_multi* m) { return m ? static_cast<int>(m->g.ctx.size()) : 0; }
 
+// internal (dist.cu)
+int pkrrgpu_multi_device_(const pkrrgpu_multi* m, int i) { return m->g.devices[i]; }
+
 pkrrgpu_ctx* pkrrgpu_multi_context(pkrrgpu_multi* m, int i) {
   return (m && i >= 0 && i < static_cast<int>(m->g.ctx.size())) ? m->g.ctx[i] : nullptr;
 }

@@ -139,3 +139,46 @@ def test_torch_inputs_converted_and_stream_ordered(engine, oracle):
         yd = torch.from_numpy(y).cuda()
         m2 = engine.train_krr(Xd, yd, 2.0, 1e-3)
     assert _rel(m2.alpha, a_ref) <= 1e-8
+
+
+def _dkrr_run(devices, n, d, sigma, lam, group=None, seed=3):
+    env = "" if group is None else f'os.environ["PKRR_DIST_GROUP"] = "{group}"'
+    code = f"""
+import os, sys
+{env}
+sys.path.insert(0, {ROOT!r})
+import numpy as np
+import paper_1805_00569_b200 as pk
+from paper_1805_00569_b200 import datagen
+dd = datagen.make({n}, 0, 10, {d}, 6, seed={seed})
+g = pk.Group({devices!r})
+a, r = g.train_krr(dd["X_train"], dd["y_train"], {sigma}, {lam})
+np.save(sys.argv[1], np.concatenate([a, [r]]))
+"""
+    import tempfile
+    out = tempfile.mktemp(suffix=".npy")
+    r = subprocess.run([sys.executable, "-c", code, out], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    v = np.load(out)
+    os.unlink(out)
+    return v[:-1], float(v[-1])
+
+
+@pytest.mark.parametrize("devices,group", [([0, 0], None), ([0, 0], 1), ([0], None), ([0, 0, 0], 2)])
+def test_dkrr_matches_oracle(oracle, devices, group):
+    """DKRR (one system across the group's contexts) vs the oracle at m = 3000."""
+    dd = datagen.make(3000, 0, 10, 12, 6, seed=3)
+    a_ref, _ = oracle.train_krr(dd["X_train"], dd["y_train"], 2.0, 1e-3)
+    a, res = _dkrr_run(devices, 3000, 12, 2.0, 1e-3, group)
+    assert res <= 1e-8
+    assert _rel(a, a_ref) <= 1e-8, _rel(a, a_ref)
+
+
+def test_dkrr_two_contexts_match_one_gpu(engine):
+    """2 contexts on one GPU (super-columns alternating, panels exchanged by peer copies)
+    against the one-GPU train_krr at m = 12000 (G = 8: 12 super-columns)."""
+    dd = datagen.make(12000, 0, 10, 90, 16, seed=5)
+    m = engine.train_krr(dd["X_train"], dd["y_train"], 3.0, 1e-4)
+    a, res = _dkrr_run([0, 0], 12000, 90, 3.0, 1e-4, seed=5)
+    assert res <= 1e-8
+    assert _rel(a, m.alpha) <= 1e-8, _rel(a, m.alpha)
