@@ -141,7 +141,7 @@ def test_torch_inputs_converted_and_stream_ordered(engine, oracle):
     assert _rel(m2.alpha, a_ref) <= 1e-8
 
 
-def _dkrr_run(devices, n, d, sigma, lam, group=None, seed=3):
+def _dkrr_run(devices, n, d, sigma, lam, group=None, seed=3, comps=6):
     env = "" if group is None else f'os.environ["PKRR_DIST_GROUP"] = "{group}"'
     code = f"""
 import os, sys
@@ -150,7 +150,7 @@ sys.path.insert(0, {ROOT!r})
 import numpy as np
 import paper_1805_00569_b200 as pk
 from paper_1805_00569_b200 import datagen
-dd = datagen.make({n}, 0, 10, {d}, 6, seed={seed})
+dd = datagen.make({n}, 0, 10, {d}, {comps}, seed={seed})
 g = pk.Group({devices!r})
 a, r = g.train_krr(dd["X_train"], dd["y_train"], {sigma}, {lam})
 np.save(sys.argv[1], np.concatenate([a, [r]]))
@@ -179,6 +179,6 @@ def test_dkrr_two_contexts_match_one_gpu(engine):
     against the one-GPU train_krr at m = 12000 (G = 8: 12 super-columns)."""
     dd = datagen.make(12000, 0, 10, 90, 16, seed=5)
     m = engine.train_krr(dd["X_train"], dd["y_train"], 3.0, 1e-4)
-    a, res = _dkrr_run([0, 0], 12000, 90, 3.0, 1e-4, seed=5)
+    a, res = _dkrr_run([0, 0], 12000, 90, 3.0, 1e-4, seed=5, comps=16)
     assert res <= 1e-8
     assert _rel(a, m.alpha) <= 1e-8, _rel(a, m.alpha)
