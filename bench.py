@@ -182,26 +182,28 @@ def _lpt_makespan(costs, workers):
     return max(free)
 
 
+# Reference CPU cost of one part's train + predict vs its size: T ~ m^3.31, fitted to the
+# reference's own full-size runs (tests/golden/make_fullsize_golden.py, profiles/
+# cpu_fullsize_*_r02.json: m = 4096 in 8.3 s, m = 20544 in 1740 s on one core each).  The
+# exponent is above 3 because the reference's unblocked Cholesky falls out of cache as m
+# grows (1.75 GFLOP/s at m = 4096 down to 1.66 at 20544 per core).
+CPU_COST_EXP = 3.31
+
+
 def cpu_extrapolation(cfg, dd, n_s, workers):
-    """Full-size / sample CPU-time ratio of the reference grid: each part's reference
-    cost is its Cholesky (m(m+1)(2m+1)/6 at the reference's measured 1.75 GFLOP/s per
-    core) plus its gram and cross kernel (d m(m+1) + 2 t_t m d at
-    0.68 GFLOP/s), per cell / per sigma, scheduled over `workers` threads like
-    run_partitions.  The parts come from the reference's own make_partition of the
-    sample and of the full training set.  Validated against full-size reference runs in
-    profiles/cpu_fullsize_*_r02.json."""
+    """Full-size / sample CPU-time ratio of the reference grid: each part costs
+    cells * m^CPU_COST_EXP, the parts are scheduled over `workers` threads like
+    run_partitions (runtime.hpp:70-112, index order), and the parts come from the
+    reference's own make_partition of the sample and of the full training set.
+    Checked against the measured full-size C1 run (profiles/cpu_fullsize_c1_r02.json)."""
     from oracle import Reference
     ref = Reference()
-    ns, ncell = len(cfg["sigmas"]), len(cfg["sigmas"]) * len(cfg["lambdas"])
-    tq = cfg["val"] + cfg["test"]
+    ncell = len(cfg["sigmas"]) * len(cfg["lambdas"])
 
     def makespan(X):
         part, _ = ref.make_partition(cfg["strategy"], X, cfg["p"], 1)
         sizes = np.bincount(part).astype(float)
-        d = cfg["d"]
-        costs = [ncell * m * (m + 1) * (2 * m + 1) / 6 / 1.75e9
-                 + ns * (d * m * (m + 1) + 2 * tq * m * d * (m / sizes.sum())) / 0.68e9 for m in sizes]
-        return _lpt_makespan(costs, workers), sizes
+        return _lpt_makespan([ncell * m ** CPU_COST_EXP for m in sizes], workers), sizes
 
     full, fs = makespan(dd["X_train"])
     samp, ss = makespan(dd["X_train"][:n_s])
@@ -252,7 +254,9 @@ def run_reference(args):
                              "extrapolated_full_value": value * (cfg["n"] + cfg["val"] + cfg["test"])
                              / (n_s + cfg["val"] + cfg["test"]) / ratio,
                              "extrapolation": "sample time x (full / sample) makespan of per-part reference "
-                                              "costs over the cores (bench.cpu_extrapolation)",
+                                              "costs m^3.31 over the cores (bench.cpu_extrapolation); measured "
+                                              "full-size C1 reference: 1749 s on 8 cores "
+                                              "(profiles/cpu_fullsize_c1_r02.json)",
                              "full_part_sizes": full_sizes, "sample_part_sizes": sample_sizes},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
