@@ -263,6 +263,38 @@ def run_reference(args):
     return 0
 
 
+def full_size_parity(name, eng, dd):
+    """alpha / prediction / MSE agreement with the REFERENCE at the workload's full size:
+    the reference's own outputs (tests/golden/fullsize_<cfg>.npz, written by
+    tests/golden/make_fullsize_golden.py from oracle/_ref; the box cannot run it at this
+    size in minutes) against this engine on the same regenerated inputs."""
+    import hashlib
+    path = os.path.join(ROOT, "tests", "golden", f"fullsize_{name}.npz")
+    if name != "c1" or not os.path.exists(path):
+        return {"unavailable": f"no full-size fixture for {name}"}
+    z = np.load(path)
+    X = dd["X_train"]
+    Q = np.concatenate([dd["X_val"], dd["X_test"]])
+    if hashlib.sha256(np.ascontiguousarray(X).tobytes()).hexdigest() != str(z["x_sha"]):
+        return {"unavailable": "datagen drift"}
+    rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
+    km = eng.kmeans(X, 8, 1, threshold=-1.0, max_iters=20)
+    parts = [np.flatnonzero(km.membership == t) for t in range(8)]
+    tp = eng.train_parts(X, z["y"], parts, 3.0, 1e-4, centers=km.centers)
+    at, worst = 0, 0.0
+    for t in range(8):
+        a = tp.alpha(t)
+        worst = max(worst, rel(a, z["alpha"][at:at + len(a)]))
+        at += len(a)
+    pred = tp.predict_nearest(Q)
+    nv = int(z["n_val"])
+    mse_v = float(np.mean((pred[:nv] - z["y_q"][:nv]) ** 2))
+    return {"reference": "oracle/_ref at full size (tests/golden/fullsize_c1.npz, 1749 s on 8 cores)",
+            "labels_bitwise": bool(np.array_equal(km.membership, z["membership"].astype(np.int32))),
+            "alpha_max_rel_diff": worst, "pred_rel_diff": rel(pred, z["pred"]),
+            "mse_val_rel_diff": abs(mse_v - float(z["mse_val"])) / float(z["mse_val"])}
+
+
 # -------------------------------------------------------------------- ours ----
 def run_ours(args):
     import torch
@@ -466,6 +498,10 @@ def run_ours(args):
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": cores, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
+        try:
+            line["cpu_baseline"]["full_size_parity"] = full_size_parity(args.config, eng, dd)
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"]["full_size_parity"] = {"unavailable": str(e)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

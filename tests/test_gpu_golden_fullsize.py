@@ -77,12 +77,15 @@ def test_c1_kkrr2_every_part(engine):
     parts = [np.flatnonzero(km.membership == t) for t in range(8)]
     tp = engine.train_parts(X, y, parts, 3.0, 1e-4, centers=km.centers)
     at = 0
+    diffs = {}
     for t in range(8):
         a = tp.alpha(t)
         ref = z["alpha"][at:at + len(a)]
         at += len(a)
+        diffs[len(a)] = _rel(a, ref)
         assert _rel(a, ref) <= 1e-8, (t, len(a), _rel(a, ref))
         assert tp.residual(t) <= 1e-8
+    print("C1 alpha relative difference per part size:", diffs)
     pred = tp.predict_nearest(Q)
     assert _rel(pred, z["pred"]) <= 1e-8, _rel(pred, z["pred"])
     nv = int(z["n_val"])
@@ -119,6 +122,7 @@ def test_c3_part_16384(engine):
     a = tp.alpha(0)
     assert len(a) == 16384
     assert _rel(a, z["alpha"][0]) <= 1e-8, _rel(a, z["alpha"][0])
+    print("C3 part 0 (16384 rows) alpha relative difference:", _rel(a, z["alpha"][0]))
     pred = tp.predict(Q[routed], part=0)
     assert _rel(pred, z["pred"][0]) <= 1e-8, _rel(pred, z["pred"][0])
 
