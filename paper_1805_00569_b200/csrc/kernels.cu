@@ -1729,12 +1729,136 @@ __global__ void __launch_bounds__(kAssignRows)
   }
 }
 
+// Lloyd assign / routing (mode 0) with the rows streamed by the bulk-copy engine: a
+// persistent CTA of 64 threads (one row each) walks 64-row tiles of X, each tile one
+// contiguous cp.async.bulk (64 d doubles: rows are contiguous in row-major X) into a
+// two-stage shared-memory ring, so the next tile's HBM read overlaps this tile's dot
+// products.  Each thread reads its own row with 16-byte shared loads (row stride 8 d
+// bytes: conflict-free wavefronts) and the centres by broadcast.  Arithmetic exactly
+// assign_kernel's: sequential __dmul_rn / __dadd_rn in feature order, (xn + cn) - 2 dot,
+// clamp, strict < (bitwise the reference's labels, clustering.cpp:79-96, 182-195).
+constexpr int kBulkRows = 64, kBulkStages = 2;
+
+template <int KP>
+__global__ void __launch_bounds__(kBulkRows, 2)
+    assign_bulk_kernel(const double* __restrict__ X, int64_t n, int d, const double* __restrict__ xnorm,
+                       const double* __restrict__ centers, const double* __restrict__ cnorm, int k,
+                       int64_t row0, int32_t* label, double* best_dist, unsigned long long* changed) {
+  extern __shared__ __align__(16) unsigned char bulk_smem[];
+  double* tiles = reinterpret_cast<double*>(bulk_smem);
+  double* cs = tiles + kBulkStages * kBulkRows * d;  // [KP][d] centres (zero beyond k)
+  __shared__ uint64_t full[kBulkStages];
+  __shared__ double cn_s[KP];
+  const int tid = threadIdx.x;
+  const int64_t rows = n - row0;
+  const int64_t ntiles = (rows + kBulkRows - 1) / kBulkRows;
+  auto tile_bytes = [&](int64_t t) {
+    const int64_t r = rows - t * kBulkRows;
+    return static_cast<uint32_t>((r < kBulkRows ? r : kBulkRows) * d * 8);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < kBulkStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    for (int s = 0; s < kBulkStages; ++s) {
+      const int64_t t = blockIdx.x + static_cast<int64_t>(s) * gridDim.x;
+      if (t < ntiles) {
+        mbar_arrive_expect_tx(&full[s], tile_bytes(t));
+        bulk_load(tiles + s * kBulkRows * d, X + (row0 + t * kBulkRows) * d, tile_bytes(t), &full[s]);
+      }
+    }
+  }
+  for (int e = tid; e < KP * d; e += kBulkRows) {
+    const int q = e / d;
+    cs[e] = q < k ? centers[e] : 0.0;
+  }
+  if (tid < KP) cn_s[tid] = tid < k ? cnorm[tid] : 0.0;
+  __syncthreads();
+  unsigned ch = 0;
+  int it = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int s = it % kBulkStages;
+    mbar_wait(&full[s], static_cast<uint32_t>((it / kBulkStages) & 1));
+    const int64_t i = row0 + t * kBulkRows + tid;
+    if (i < n) {
+      const double* xr = tiles + s * kBulkRows * d + tid * d;
+      double dot[KP];
+#pragma unroll
+      for (int q = 0; q < KP; ++q) dot[q] = 0.0;
+      for (int c = 0; c < d; c += 2) {
+        const double2 x = *reinterpret_cast<const double2*>(xr + c);
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+          const double2 cv = *reinterpret_cast<const double2*>(cs + q * d + c);
+          dot[q] = __dadd_rn(dot[q], __dmul_rn(x.x, cv.x));
+          dot[q] = __dadd_rn(dot[q], __dmul_rn(x.y, cv.y));
+        }
+      }
+      const double xn = xnorm[i];
+      double min_d = INFINITY;
+      int min_j = 0;
+#pragma unroll
+      for (int q = 0; q < KP; ++q) {
+        if (q >= k) break;
+        double dist = __dsub_rn(__dadd_rn(xn, cn_s[q]), __dmul_rn(2.0, dot[q]));
+        if (dist < 0.0) dist = 0.0;
+        if (dist < min_d) {
+          min_d = dist;
+          min_j = q;
+        }
+      }
+      if (label[i] != min_j) {
+        label[i] = min_j;
+        ch += 1;
+      }
+      if (best_dist) best_dist[i] = min_d;
+    }
+    __syncthreads();  // every row of stage s consumed: refill it
+    if (tid == 0) {
+      const int64_t tn = t + static_cast<int64_t>(kBulkStages) * gridDim.x;
+      if (tn < ntiles) {
+        mbar_arrive_expect_tx(&full[s], tile_bytes(tn));
+        bulk_load(tiles + s * kBulkRows * d, X + (row0 + tn * kBulkRows) * d, tile_bytes(tn), &full[s]);
+      }
+    }
+  }
+  if (changed) {
+    const unsigned w = __reduce_add_sync(0xffffffffu, ch);
+    if ((tid & 31) == 0 && w) atomicAdd(changed, static_cast<unsigned long long>(w));
+  }
+}
+
+template <int KP>
+static bool try_assign_bulk(const double* X, int64_t n, int64_t d, const double* xnorm, const double* centers,
+                            const double* cnorm, int k, int64_t row0, int32_t* label, double* best_dist,
+                            unsigned long long* changed, cudaStream_t s, Counter& c) {
+  static const bool off = std::getenv("PKRR_ASSIGN_BULK") && std::atoi(std::getenv("PKRR_ASSIGN_BULK")) == 0;
+  const size_t smem = sizeof(double) * (static_cast<size_t>(kBulkStages) * kBulkRows * d + KP * d);
+  if (off || d % 2 || (reinterpret_cast<uintptr_t>(X) & 15) || smem > 110 * 1024) return false;
+  static std::atomic<uint64_t> attr{0};
+  smem_optin(attr, assign_bulk_kernel<KP>, 110 * 1024);
+  const int64_t ntiles = (n - row0 + kBulkRows - 1) / kBulkRows;
+  const int64_t grid = ntiles < 2 * g_sms ? ntiles : 2 * g_sms;
+  assign_bulk_kernel<KP><<<static_cast<unsigned>(grid), kBulkRows, smem, s>>>(X, n, static_cast<int>(d), xnorm,
+                                                                            centers, cnorm, k, row0, label,
+                                                                            best_dist, changed);
+  c.launched();
+  return true;
+}
+
 void launch_assign(const double* X, int64_t n, int64_t d, const double* xnorm,
                    const double* centers, const double* cnorm, int k, int mode,
                    const uint8_t* open, int64_t row0, int32_t* label, double* best_dist,
                    unsigned long long* changed, cudaStream_t s, Counter& c) {
   const int64_t rows = n - row0;
   if (rows <= 0) return;
+  // mode 0 (Lloyd assign, routing): bulk-copy row streaming (k-balance rounds, mode 1, skip
+  // whole blocks of settled rows and keep the per-chunk kernel below)
+  if (mode == 0 && k <= 8 &&
+      try_assign_bulk<8>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
+    return;
+  if (mode == 0 && k > 8 && k <= 16 &&
+      try_assign_bulk<16>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
+    return;
   const unsigned blocks = static_cast<unsigned>((rows + kAssignRows - 1) / kAssignRows);
   if (k <= 8)
     assign_kernel<8><<<blocks, kAssignRows, 0, s>>>(X, n, d, xnorm, centers, cnorm, k, mode, open,
