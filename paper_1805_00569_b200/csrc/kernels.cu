@@ -1747,7 +1747,7 @@ __global__ void __launch_bounds__(kBulkRows, 2)
   extern __shared__ __align__(16) unsigned char bulk_smem[];
   double* tiles = reinterpret_cast<double*>(bulk_smem);
   double* cs = tiles + kBulkStages * kBulkRows * d;  // [KP][d] centres (zero beyond k)
-  __shared__ uint64_t full[kBulkStages];
+  __shared__ uint64_t full[kBulkStages + 1];  // + the centres' barrier
   __shared__ double cn_s[KP];
   const int tid = threadIdx.x;
   const int64_t rows = n - row0;
@@ -1757,8 +1757,11 @@ __global__ void __launch_bounds__(kBulkRows, 2)
     return static_cast<uint32_t>((r < kBulkRows ? r : kBulkRows) * d * 8);
   };
   if (tid == 0) {
-    for (int s = 0; s < kBulkStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s <= kBulkStages; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
+    // the k centres (contiguous k d doubles) by one bulk copy, ahead of the first tile
+    mbar_arrive_expect_tx(&full[kBulkStages], static_cast<uint32_t>(k * d * 8));
+    bulk_load(cs, centers, static_cast<uint32_t>(k * d * 8), &full[kBulkStages]);
     for (int s = 0; s < kBulkStages; ++s) {
       const int64_t t = blockIdx.x + static_cast<int64_t>(s) * gridDim.x;
       if (t < ntiles) {
@@ -1767,18 +1770,19 @@ __global__ void __launch_bounds__(kBulkRows, 2)
       }
     }
   }
-  for (int e = tid; e < KP * d; e += kBulkRows) {
-    const int q = e / d;
-    cs[e] = q < k ? centers[e] : 0.0;
-  }
+  for (int e = k * d + tid; e < KP * d; e += kBulkRows) cs[e] = 0.0;  // centres beyond k
   if (tid < KP) cn_s[tid] = tid < k ? cnorm[tid] : 0.0;
   __syncthreads();
+  mbar_wait(&full[kBulkStages], 0);
   unsigned ch = 0;
   int it = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
     const int s = it % kBulkStages;
-    mbar_wait(&full[s], static_cast<uint32_t>((it / kBulkStages) & 1));
     const int64_t i = row0 + t * kBulkRows + tid;
+    // the row's norm and label are read before waiting for its tile
+    const double xn = i < n ? xnorm[i] : 0.0;
+    const int lab = i < n ? label[i] : 0;
+    mbar_wait(&full[s], static_cast<uint32_t>((it / kBulkStages) & 1));
     if (i < n) {
       const double* xr = tiles + s * kBulkRows * d + tid * d;
       double dot[KP];
@@ -1793,7 +1797,6 @@ __global__ void __launch_bounds__(kBulkRows, 2)
           dot[q] = __dadd_rn(dot[q], __dmul_rn(x.y, cv.y));
         }
       }
-      const double xn = xnorm[i];
       double min_d = INFINITY;
       int min_j = 0;
 #pragma unroll
@@ -1806,7 +1809,7 @@ __global__ void __launch_bounds__(kBulkRows, 2)
           min_j = q;
         }
       }
-      if (label[i] != min_j) {
+      if (lab != min_j) {
         label[i] = min_j;
         ch += 1;
       }
@@ -1833,7 +1836,9 @@ static bool try_assign_bulk(const double* X, int64_t n, int64_t d, const double*
                             unsigned long long* changed, cudaStream_t s, Counter& c) {
   static const bool off = std::getenv("PKRR_ASSIGN_BULK") && std::atoi(std::getenv("PKRR_ASSIGN_BULK")) == 0;
   const size_t smem = sizeof(double) * (static_cast<size_t>(kBulkStages) * kBulkRows * d + KP * d);
-  if (off || d % 2 || (reinterpret_cast<uintptr_t>(X) & 15) || smem > 110 * 1024) return false;
+  if (off || d % 2 || (reinterpret_cast<uintptr_t>(X) & 15) || (reinterpret_cast<uintptr_t>(centers) & 15) ||
+      smem > 110 * 1024)
+    return false;
   static std::atomic<uint64_t> attr{0};
   smem_optin(attr, assign_bulk_kernel<KP>, 110 * 1024);
   const int64_t ntiles = (n - row0 + kBulkRows - 1) / kBulkRows;
