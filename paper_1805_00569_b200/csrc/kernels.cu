@@ -1764,9 +1764,10 @@ __global__ void __launch_bounds__((kTWarps + 1) * 32, 1)
     }
     fence_mbar_init();
   }
+  const uint32_t cbase = smem_u32(cs);  // explicit shared-window accesses (not generic)
   for (int e = tid; e < KP * dch; e += blockDim.x) {
     const int q = e / dch, f = e % dch;
-    cs[e] = (q < k && f < d) ? centers[static_cast<int64_t>(q) * d + f] : 0.0;
+    sts_f64(cbase + 8u * e, (q < k && f < d) ? __ldg(centers + static_cast<int64_t>(q) * d + f) : 0.0);
   }
   if (tid < KP) cn_s[tid] = tid < k ? cnorm[tid] : 0.0;
   __syncthreads();
@@ -1811,13 +1812,13 @@ __global__ void __launch_bounds__((kTWarps + 1) * 32, 1)
       if (lane == 0) mbar_arrive(&empty[(u - 1) % kTS]);
     }
     const uint32_t st = sbase + s * kTStage;
-    const double* cc = cs + c * kTF;
+    const uint32_t cc = cbase + 8u * (c * kTF);
 #pragma unroll
     for (int p = 0; p < kTF / 2; ++p) {
       const double2 x = lds_f64x2(st + swz128(tid, 2 * p));
 #pragma unroll
       for (int q = 0; q < KP; ++q) {
-        const double2 cv = *reinterpret_cast<const double2*>(cc + q * dch + 2 * p);
+        const double2 cv = lds_f64x2(cc + 8u * (q * dch + 2 * p));
         dot[q] = __dadd_rn(dot[q], __dmul_rn(x.x, cv.x));
         dot[q] = __dadd_rn(dot[q], __dmul_rn(x.y, cv.y));
       }
