@@ -1737,11 +1737,11 @@ __global__ void __launch_bounds__(kAssignRows)
 // Arithmetic exactly assign_kernel's: sequential __dmul_rn / __dadd_rn in feature order
 // (the zero padding adds +0), (xn + cn) - 2 dot, clamp, strict < -- bitwise the
 // reference's labels (clustering.cpp:79-96, 182-195).
-constexpr int kTR = 256, kTS = 4, kTF = 16, kTWarps = kTR / 32;
-constexpr int kTStage = kTR * kTF * 8;  // 32 KB
+constexpr int kTR = 128, kTS = 4, kTF = 16, kTWarps = kTR / 32, kTBlocksPerSM = 3;
+constexpr int kTStage = kTR * kTF * 8;  // 16 KB
 
 template <int KP>
-__global__ void __launch_bounds__((kTWarps + 1) * 32, 1)
+__global__ void __launch_bounds__((kTWarps + 1) * 32, kTBlocksPerSM)
     assign_tma_kernel(const __grid_constant__ CUtensorMap tmX, int64_t n, int d, const double* __restrict__ xnorm,
                       const double* __restrict__ centers, const double* __restrict__ cnorm, int k, int64_t row0,
                       int32_t* label, double* best_dist, unsigned long long* changed) {
@@ -1764,13 +1764,8 @@ __global__ void __launch_bounds__((kTWarps + 1) * 32, 1)
     }
     fence_mbar_init();
   }
+  __syncthreads();  // barriers initialised: the producer starts streaming at once
   const uint32_t cbase = smem_u32(cs);  // explicit shared-window accesses (not generic)
-  for (int e = tid; e < KP * dch; e += blockDim.x) {
-    const int q = e / dch, f = e % dch;
-    sts_f64(cbase + 8u * e, (q < k && f < d) ? __ldg(centers + static_cast<int64_t>(q) * d + f) : 0.0);
-  }
-  if (tid < KP) cn_s[tid] = tid < k ? cnorm[tid] : 0.0;
-  __syncthreads();
   if (warp == kTWarps) {  // ---- producer ----
     if (lane == 0) {
       prefetch_tmap(&tmX);
@@ -1788,7 +1783,14 @@ __global__ void __launch_bounds__((kTWarps + 1) * 32, 1)
     }
     return;
   }
-  // ---- consumers: thread tid = row tid of the block ----
+  // ---- consumers: stage the centres (overlapping the first tiles' loads), then one
+  // row per thread ----
+  for (int e = tid; e < KP * dch; e += kTR) {
+    const int q = e / dch, f = e % dch;
+    sts_f64(cbase + 8u * e, (q < k && f < d) ? __ldg(centers + static_cast<int64_t>(q) * d + f) : 0.0);
+  }
+  if (tid < KP) cn_s[tid] = tid < k ? cnorm[tid] : 0.0;
+  consumer_sync(kTR);
   unsigned ch = 0;
   double dot[KP];
   double xn = 0.0;
@@ -1856,13 +1858,13 @@ static bool try_assign_tma(const double* X, int64_t n, int64_t d, const double* 
   static const bool off = std::getenv("PKRR_ASSIGN_TMA") && std::atoi(std::getenv("PKRR_ASSIGN_TMA")) == 0;
   const int64_t dch = (d + kTF - 1) / kTF * kTF;
   const size_t smem = kTS * kTStage + sizeof(double) * KP * dch + 1024;
-  if (off || d % 2 || (reinterpret_cast<uintptr_t>(X) & 15) || smem > 200 * 1024) return false;
+  if (off || d % 2 || (reinterpret_cast<uintptr_t>(X) & 15) || smem > 80 * 1024) return false;
   CUtensorMap tm;
   if (!make_tmap(&tm, X, n, d, d)) return false;
   static std::atomic<uint64_t> attr{0};
-  smem_optin(attr, assign_tma_kernel<KP>, 200 * 1024);
+  smem_optin(attr, assign_tma_kernel<KP>, 80 * 1024);
   const int64_t nblk = (n - row0 + kTR - 1) / kTR;
-  const int64_t grid = nblk < g_sms ? nblk : g_sms;
+  const int64_t grid = nblk < kTBlocksPerSM * g_sms ? nblk : kTBlocksPerSM * g_sms;
   assign_tma_kernel<KP><<<static_cast<unsigned>(grid), (kTWarps + 1) * 32, smem, s>>>(
       tm, n, static_cast<int>(d), xnorm, centers, cnorm, k, row0, label, best_dist, changed);
   c.launched();
