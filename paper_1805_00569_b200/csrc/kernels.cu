@@ -1744,7 +1744,7 @@ template <int KP>
 __global__ void __launch_bounds__((kTWarps + 1) * 32, kTBlocksPerSM)
     assign_tma_kernel(const __grid_constant__ CUtensorMap tmX, int64_t n, int d, const double* __restrict__ xnorm,
                       const double* __restrict__ centers, const double* __restrict__ cnorm, int k, int64_t row0,
-                      int32_t* label, double* best_dist, unsigned long long* changed) {
+                      int32_t* label, double* best_dist, unsigned long long* changed, int probe) {
   extern __shared__ unsigned char tma_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(tma_smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -1815,8 +1815,9 @@ __global__ void __launch_bounds__((kTWarps + 1) * 32, kTBlocksPerSM)
     }
     const uint32_t st = sbase + s * kTStage;
     const uint32_t cc = cbase + 8u * (c * kTF);
+    // PKRR_ASSIGN_PROBE=1: skip the dot products (memory-side timing probe; labels wrong)
 #pragma unroll
-    for (int p = 0; p < kTF / 2; ++p) {
+    for (int p = 0; p < (probe ? 0 : kTF / 2); ++p) {
       const double2 x = lds_f64x2(st + swz128(tid, 2 * p));
 #pragma unroll
       for (int q = 0; q < KP; ++q) {
@@ -1851,11 +1852,114 @@ __global__ void __launch_bounds__((kTWarps + 1) * 32, kTBlocksPerSM)
   }
 }
 
+// Lloyd assign / routing (mode 0), register-streamed: one row per thread, the row read
+// with 16-byte global loads (L1-cached: a row's 720 bytes come in as whole lines, and the
+// next 16-feature chunk's loads are in flight while this chunk's dot products run), the
+// centres in shared memory read by broadcast.  Same arithmetic as assign_kernel.
+constexpr int kLRows = 128, kLChunk = 16;
+
+template <int KP>
+__global__ void __launch_bounds__(kLRows, 4)
+    assign_ldg_kernel(const double* __restrict__ X, int64_t n, int d, const double* __restrict__ xnorm,
+                      const double* __restrict__ centers, const double* __restrict__ cnorm, int k, int64_t row0,
+                      int32_t* label, double* best_dist, unsigned long long* changed) {
+  extern __shared__ __align__(16) double ldg_cs[];  // [KP][dch]
+  __shared__ double cn_s[KP];
+  const int tid = threadIdx.x;
+  const int nch = (d + kLChunk - 1) / kLChunk, dch = nch * kLChunk;
+  const uint32_t cbase = smem_u32(ldg_cs);
+  for (int e = tid; e < KP * dch; e += kLRows) {
+    const int q = e / dch, f = e % dch;
+    sts_f64(cbase + 8u * e, (q < k && f < d) ? __ldg(centers + static_cast<int64_t>(q) * d + f) : 0.0);
+  }
+  if (tid < KP) cn_s[tid] = tid < k ? cnorm[tid] : 0.0;
+  const int64_t i = row0 + static_cast<int64_t>(blockIdx.x) * kLRows + tid;
+  const bool valid = i < n;
+  const double2* xr = reinterpret_cast<const double2*>(X + (valid ? i : row0) * d);
+  const int dp2 = d / 2;  // d is even: the row is dp2 double2s
+  // two register buffers, unrolled by hand (no dynamic indexing: no local memory)
+  double2 ba[kLChunk / 2], bb[kLChunk / 2];
+  auto load = [&](double2 (&b)[kLChunk / 2], int c) {
+#pragma unroll
+    for (int p = 0; p < kLChunk / 2; ++p) {
+      const int g = c * (kLChunk / 2) + p;
+      b[p] = g < dp2 ? __ldg(xr + g) : make_double2(0.0, 0.0);
+    }
+  };
+  double dot[KP];
+#pragma unroll
+  for (int q = 0; q < KP; ++q) dot[q] = 0.0;
+  auto compute = [&](const double2 (&b)[kLChunk / 2], int c) {
+    const uint32_t cc = cbase + 8u * (c * kLChunk);
+#pragma unroll
+    for (int p = 0; p < kLChunk / 2; ++p) {
+      const double2 x = b[p];
+#pragma unroll
+      for (int q = 0; q < KP; ++q) {
+        const double2 cv = lds_f64x2(cc + 8u * (q * dch + 2 * p));
+        dot[q] = __dadd_rn(dot[q], __dmul_rn(x.x, cv.x));
+        dot[q] = __dadd_rn(dot[q], __dmul_rn(x.y, cv.y));
+      }
+    }
+  };
+  load(ba, 0);
+  const double xn = valid ? xnorm[i] : 0.0;
+  const int lab = valid ? label[i] : 0;
+  __syncthreads();
+  for (int c = 0; c < nch; c += 2) {
+    if (c + 1 < nch) load(bb, c + 1);  // the next chunk in flight during this one's arithmetic
+    compute(ba, c);
+    if (c + 1 < nch) {
+      if (c + 2 < nch) load(ba, c + 2);
+      compute(bb, c + 1);
+    }
+  }
+  unsigned ch = 0;
+  if (valid) {
+    double min_d = INFINITY;
+    int min_j = 0;
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      if (q >= k) break;
+      double dist = __dsub_rn(__dadd_rn(xn, cn_s[q]), __dmul_rn(2.0, dot[q]));
+      if (dist < 0.0) dist = 0.0;
+      if (dist < min_d) {
+        min_d = dist;
+        min_j = q;
+      }
+    }
+    if (lab != min_j) {
+      label[i] = min_j;
+      ch = 1;
+    }
+    if (best_dist) best_dist[i] = min_d;
+  }
+  if (changed) {
+    const unsigned w = __reduce_add_sync(0xffffffffu, ch);
+    if ((tid & 31) == 0 && w) atomicAdd(changed, static_cast<unsigned long long>(w));
+  }
+}
+
+template <int KP>
+static bool try_assign_ldg(const double* X, int64_t n, int64_t d, const double* xnorm, const double* centers,
+                           const double* cnorm, int k, int64_t row0, int32_t* label, double* best_dist,
+                           unsigned long long* changed, cudaStream_t s, Counter& c) {
+  const int64_t dch = (d + kLChunk - 1) / kLChunk * kLChunk;
+  const size_t smem = sizeof(double) * KP * dch;
+  if (d % 2 || (reinterpret_cast<uintptr_t>(X) & 15) || smem > 48 * 1024) return false;
+  const int64_t blocks = (n - row0 + kLRows - 1) / kLRows;
+  assign_ldg_kernel<KP><<<static_cast<unsigned>(blocks), kLRows, smem, s>>>(
+      X, n, static_cast<int>(d), xnorm, centers, cnorm, k, row0, label, best_dist, changed);
+  c.launched();
+  return true;
+}
+
 template <int KP>
 static bool try_assign_tma(const double* X, int64_t n, int64_t d, const double* xnorm, const double* centers,
                            const double* cnorm, int k, int64_t row0, int32_t* label, double* best_dist,
                            unsigned long long* changed, cudaStream_t s, Counter& c) {
   static const bool off = std::getenv("PKRR_ASSIGN_TMA") && std::atoi(std::getenv("PKRR_ASSIGN_TMA")) == 0;
+  static const bool probe = std::getenv("PKRR_ASSIGN_PROBE") != nullptr;
   const int64_t dch = (d + kTF - 1) / kTF * kTF;
   const size_t smem = kTS * kTStage + sizeof(double) * KP * dch + 1024;
   if (off || d % 2 || (reinterpret_cast<uintptr_t>(X) & 15) || smem > 80 * 1024) return false;
@@ -1866,7 +1970,7 @@ static bool try_assign_tma(const double* X, int64_t n, int64_t d, const double* 
   const int64_t nblk = (n - row0 + kTR - 1) / kTR;
   const int64_t grid = nblk < kTBlocksPerSM * g_sms ? nblk : kTBlocksPerSM * g_sms;
   assign_tma_kernel<KP><<<static_cast<unsigned>(grid), (kTWarps + 1) * 32, smem, s>>>(
-      tm, n, static_cast<int>(d), xnorm, centers, cnorm, k, row0, label, best_dist, changed);
+      tm, n, static_cast<int>(d), xnorm, centers, cnorm, k, row0, label, best_dist, changed, probe ? 1 : 0);
   c.launched();
   return true;
 }
@@ -1879,10 +1983,17 @@ void launch_assign(const double* X, int64_t n, int64_t d, const double* xnorm,
   if (rows <= 0) return;
   // mode 0 (Lloyd assign, routing): bulk-copy row streaming (k-balance rounds, mode 1, skip
   // whole blocks of settled rows and keep the per-chunk kernel below)
-  if (mode == 0 && k <= 8 &&
+  static const int variant = std::getenv("PKRR_ASSIGN") ? std::atoi(std::getenv("PKRR_ASSIGN")) : 1;
+  if (mode == 0 && variant == 1 && k <= 8 &&
+      try_assign_ldg<8>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
+    return;
+  if (mode == 0 && variant == 1 && k > 8 && k <= 16 &&
+      try_assign_ldg<16>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
+    return;
+  if (mode == 0 && variant == 2 && k <= 8 &&
       try_assign_tma<8>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
     return;
-  if (mode == 0 && k > 8 && k <= 16 &&
+  if (mode == 0 && variant == 2 && k > 8 && k <= 16 &&
       try_assign_tma<16>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
     return;
   const unsigned blocks = static_cast<unsigned>((rows + kAssignRows - 1) / kAssignRows);
