@@ -1954,6 +1954,165 @@ static bool try_assign_ldg(const double* X, int64_t n, int64_t d, const double* 
   return true;
 }
 
+// Lloyd assign / routing (mode 0) with a tensor-core distance SCREEN and an exact
+// recompute -- bitwise the reference's labels and distances:
+//  1. the CTA streams 64-row tiles of X by TMA (16-feature boxes, 128 B swizzle, zero
+//     fill past d) through a two-stage ring; each warp computes its 32 rows' dot
+//     products with all k centres by DMMA (m8n8k4 f64: ~1/8 of the FP64 issue of the
+//     non-FMA dot products);
+//  2. per row (one lane each): approximate distances a_q = max(0, (xn + cn_q) - 2 dot_q)
+//     and a bound e_q = (4 d + 16) 2^-53 (xn + cn_q) >= |a_q - exact_q| (the DMMA and the
+//     sequential dot each err by <= d u sum|x c| <= d u (xn + cn_q) / 2);
+//  3. candidates = {q : a_q - e_q <= min_j (a_j + e_j)} -- every index that can reach the
+//     exact minimum (ties included) and no other; their EXACT distances are recomputed
+//     in the reference's arithmetic (sequential __dmul_rn / __dadd_rn over the features,
+//     (xn + cn) - 2 dot, clamp) and the strict-< argmin in index order picks the winner.
+// Usually one candidate per row, so the FP64 pipe does ~1/8 of assign_kernel's work and
+// the kernel streams X at the memory rate.
+constexpr int kSRows = 64, kSStages = 2;
+
+template <int KP>
+__global__ void __launch_bounds__(kSRows, KP <= 16 ? 2 : 1)
+    assign_dmma_kernel(const __grid_constant__ CUtensorMap tmX, int64_t n, int d, const double* __restrict__ xnorm,
+                       const double* __restrict__ centers, const double* __restrict__ cnorm, int k, int64_t row0,
+                       int32_t* label, double* best_dist, unsigned long long* changed) {
+  extern __shared__ unsigned char sc_smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(sc_smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int nch = (d + 15) / 16, dch = nch * 16, cstr = dch + 2;  // centre row stride (bank spread)
+  const int stage_bytes = nch * 64 * 128;
+  double* cs = reinterpret_cast<double*>(smem + kSStages * stage_bytes);  // [KP][cstr]
+  double* dots = cs + KP * cstr;                                          // [kSRows][KP + 1]
+  __shared__ uint64_t full[kSStages];
+  __shared__ double cn_s[KP];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t rows = n - row0;
+  const int64_t ntiles = (rows + kSRows - 1) / kSRows;
+  auto issue = [&](int s, int64_t t) {
+    mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(stage_bytes));
+    for (int c = 0; c < nch; ++c)
+      tma_load_2d(smem + s * stage_bytes + c * 64 * 128, &tmX, c * 16, static_cast<int>(row0 + t * kSRows), &full[s]);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < kSStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    prefetch_tmap(&tmX);
+    for (int s = 0; s < kSStages; ++s)
+      if (blockIdx.x + static_cast<int64_t>(s) * gridDim.x < ntiles) issue(s, blockIdx.x + static_cast<int64_t>(s) * gridDim.x);
+  }
+  const uint32_t cbase = smem_u32(cs), dbase = smem_u32(dots);
+  for (int e = tid; e < KP * cstr; e += kSRows) {
+    const int q = e / cstr, f = e % cstr;
+    sts_f64(cbase + 8u * e, (q < k && f < d) ? __ldg(centers + static_cast<int64_t>(q) * d + f) : 0.0);
+  }
+  if (tid < KP) cn_s[tid] = tid < k ? cnorm[tid] : 0.0;
+  __syncthreads();
+  const int lr = lane >> 2, lk = lane & 3;
+  const double unit = 1.1102230246251565e-16;  // 2^-53
+  const double ebound = (4.0 * d + 16.0) * unit;
+  unsigned ch = 0;
+  int it = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int s = it % kSStages;
+    const int64_t i = row0 + t * kSRows + tid;  // this lane's row in the candidate phase
+    const double xn = i < n ? xnorm[i] : 0.0;
+    const int lab = i < n ? label[i] : 0;
+    mbar_wait(&full[s], static_cast<uint32_t>((it / kSStages) & 1));
+    const unsigned char* st = smem + s * stage_bytes;
+    // ---- 1. DMMA screen: rows warp*32 + mt*8 + lr, centres nt*8 + 2 lk + e ----
+    {
+      double acc[4][KP / 8][2];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < KP / 8; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+      for (int ks = 0; ks < dch / 4; ++ks) {
+        const int kk = ks * 4 + lk;
+        const unsigned char* chunk = st + (kk >> 4) * 64 * 128;
+        double af[4], bf[KP / 8];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) af[mt] = lds_f64(chunk, swz128(warp * 32 + mt * 8 + lr, kk & 15));
+#pragma unroll
+        for (int nt = 0; nt < KP / 8; ++nt) bf[nt] = lds_f64_at(cbase + 8u * ((nt * 8 + lr) * cstr + kk));
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < KP / 8; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
+      }
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < KP / 8; ++nt) {
+          const int r = warp * 32 + mt * 8 + lr, q = nt * 8 + 2 * lk;
+          sts_f64(dbase + 8u * (r * (KP + 1) + q), acc[mt][nt][0]);
+          sts_f64(dbase + 8u * (r * (KP + 1) + q + 1), acc[mt][nt][1]);
+        }
+    }
+    __syncwarp();
+    // ---- 2./3. candidates and their exact distances, one row per lane ----
+    if (i < n) {
+      double hi = INFINITY;
+      for (int q = 0; q < k; ++q) {
+        double a = (xn + cn_s[q]) - 2.0 * lds_f64_at(dbase + 8u * (tid * (KP + 1) + q));
+        a = a < 0.0 ? 0.0 : a;
+        const double e = ebound * (xn + cn_s[q]);
+        hi = fmin(hi, a + e);
+      }
+      double min_d = INFINITY;
+      int min_j = 0;
+      for (int q = 0; q < k; ++q) {
+        double a = (xn + cn_s[q]) - 2.0 * lds_f64_at(dbase + 8u * (tid * (KP + 1) + q));
+        a = a < 0.0 ? 0.0 : a;
+        const double e = ebound * (xn + cn_s[q]);
+        if (!(a - e <= hi)) continue;
+        double dot = 0.0;
+        for (int f = 0; f < d; ++f) {
+          const double x = lds_f64(st + (f >> 4) * 64 * 128, swz128(tid, f & 15));
+          dot = __dadd_rn(dot, __dmul_rn(x, lds_f64_at(cbase + 8u * (q * cstr + f))));
+        }
+        double dist = __dsub_rn(__dadd_rn(xn, cn_s[q]), __dmul_rn(2.0, dot));
+        if (dist < 0.0) dist = 0.0;
+        if (dist < min_d) {
+          min_d = dist;
+          min_j = q;
+        }
+      }
+      if (lab != min_j) {
+        label[i] = min_j;
+        ch += 1;
+      }
+      if (best_dist) best_dist[i] = min_d;
+    }
+    __syncthreads();  // stage s (and the dot scratch) consumed: refill
+    if (tid == 0 && t + static_cast<int64_t>(kSStages) * gridDim.x < ntiles)
+      issue(s, t + static_cast<int64_t>(kSStages) * gridDim.x);
+  }
+  if (changed) {
+    const unsigned w = __reduce_add_sync(0xffffffffu, ch);
+    if (lane == 0 && w) atomicAdd(changed, static_cast<unsigned long long>(w));
+  }
+}
+
+template <int KP>
+static bool try_assign_dmma(const double* X, int64_t n, int64_t d, const double* xnorm, const double* centers,
+                            const double* cnorm, int k, int64_t row0, int32_t* label, double* best_dist,
+                            unsigned long long* changed, cudaStream_t s, Counter& c) {
+  const int64_t nch = (d + 15) / 16, dch = nch * 16;
+  const size_t smem = kSStages * nch * 64 * 128 + sizeof(double) * (KP * (dch + 2) + kSRows * (KP + 1)) + 1024;
+  if (d % 2 || (reinterpret_cast<uintptr_t>(X) & 15) || smem > 200 * 1024) return false;
+  CUtensorMap tm;
+  if (!make_tmap(&tm, X, n, d, d)) return false;
+  static std::atomic<uint64_t> attr{0};
+  smem_optin(attr, assign_dmma_kernel<KP>, static_cast<int>(smem > 113 * 1024 ? smem : 113 * 1024));
+  const int64_t ntiles = (n - row0 + kSRows - 1) / kSRows;
+  const int per_sm = smem <= 113 * 1024 ? 2 : 1;
+  const int64_t grid = ntiles < per_sm * g_sms ? ntiles : per_sm * g_sms;
+  assign_dmma_kernel<KP><<<static_cast<unsigned>(grid), kSRows, smem, s>>>(
+      tm, n, static_cast<int>(d), xnorm, centers, cnorm, k, row0, label, best_dist, changed);
+  c.launched();
+  return true;
+}
+
 template <int KP>
 static bool try_assign_tma(const double* X, int64_t n, int64_t d, const double* xnorm, const double* centers,
                            const double* cnorm, int k, int64_t row0, int32_t* label, double* best_dist,
@@ -1983,7 +2142,20 @@ void launch_assign(const double* X, int64_t n, int64_t d, const double* xnorm,
   if (rows <= 0) return;
   // mode 0 (Lloyd assign, routing): bulk-copy row streaming (k-balance rounds, mode 1, skip
   // whole blocks of settled rows and keep the per-chunk kernel below)
-  static const int variant = std::getenv("PKRR_ASSIGN") ? std::atoi(std::getenv("PKRR_ASSIGN")) : 1;
+  static const int variant = std::getenv("PKRR_ASSIGN") ? std::atoi(std::getenv("PKRR_ASSIGN")) : 3;
+  if (mode == 0 && variant == 3) {
+    if (k <= 8 && try_assign_dmma<8>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
+      return;
+    if (k > 8 && k <= 16 &&
+        try_assign_dmma<16>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
+      return;
+    if (k > 16 && k <= 32 &&
+        try_assign_dmma<32>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
+      return;
+    if (k > 32 && k <= 64 &&
+        try_assign_dmma<64>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
+      return;
+  }
   if (mode == 0 && variant == 1 && k <= 8 &&
       try_assign_ldg<8>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
     return;
