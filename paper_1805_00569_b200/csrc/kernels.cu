@@ -1975,7 +1975,7 @@ template <int KP>
 __global__ void __launch_bounds__(kSRows, KP <= 16 ? 2 : 1)
     assign_dmma_kernel(const __grid_constant__ CUtensorMap tmX, int64_t n, int d, const double* __restrict__ xnorm,
                        const double* __restrict__ centers, const double* __restrict__ cnorm, int k, int64_t row0,
-                       int32_t* label, double* best_dist, unsigned long long* changed) {
+                       int32_t* label, double* best_dist, unsigned long long* changed, double* debug) {
   extern __shared__ unsigned char sc_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(sc_smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -2058,17 +2058,26 @@ __global__ void __launch_bounds__(kSRows, KP <= 16 ? 2 : 1)
         const double e = ebound * (xn + cn_s[q]);
         hi = fmin(hi, a + e);
       }
+      // candidates in index order, one per pass, every lane on its own next candidate
+      // (the passes are warp-uniform: usually exactly one)
       double min_d = INFINITY;
-      int min_j = 0;
-      for (int q = 0; q < k; ++q) {
-        double a = (xn + cn_s[q]) - 2.0 * lds_f64_at(dbase + 8u * (tid * (KP + 1) + q));
-        a = a < 0.0 ? 0.0 : a;
-        const double e = ebound * (xn + cn_s[q]);
-        if (!(a - e <= hi)) continue;
+      int min_j = 0, ncand = 0, q = -1;
+      auto next_cand = [&](int from) {
+        for (int r = from; r < k; ++r) {
+          double a = (xn + cn_s[r]) - 2.0 * lds_f64_at(dbase + 8u * (tid * (KP + 1) + r));
+          a = a < 0.0 ? 0.0 : a;
+          if (a - ebound * (xn + cn_s[r]) <= hi) return r;
+        }
+        return -1;
+      };
+      q = next_cand(0);
+      while (q >= 0) {
+        ++ncand;
         double dot = 0.0;
+        const uint32_t crow = cbase + 8u * (q * cstr);
         for (int f = 0; f < d; ++f) {
           const double x = lds_f64(st + (f >> 4) * 64 * 128, swz128(tid, f & 15));
-          dot = __dadd_rn(dot, __dmul_rn(x, lds_f64_at(cbase + 8u * (q * cstr + f))));
+          dot = __dadd_rn(dot, __dmul_rn(x, lds_f64_at(crow + 8u * f)));
         }
         double dist = __dsub_rn(__dadd_rn(xn, cn_s[q]), __dmul_rn(2.0, dot));
         if (dist < 0.0) dist = 0.0;
@@ -2076,12 +2085,19 @@ __global__ void __launch_bounds__(kSRows, KP <= 16 ? 2 : 1)
           min_d = dist;
           min_j = q;
         }
+        q = next_cand(q + 1);
       }
       if (lab != min_j) {
         label[i] = min_j;
         ch += 1;
       }
       if (best_dist) best_dist[i] = min_d;
+      if (debug) {  // PKRR_ASSIGN_DEBUG: candidates, the winner's screen error and bound
+        debug[3 * (i - row0)] = ncand;
+        const double a = (xn + cn_s[min_j]) - 2.0 * lds_f64_at(dbase + 8u * (tid * (KP + 1) + min_j));
+        debug[3 * (i - row0) + 1] = (a < 0.0 ? 0.0 : a) - min_d;
+        debug[3 * (i - row0) + 2] = ebound * (xn + cn_s[min_j]);
+      }
     }
     __syncthreads();  // stage s (and the dot scratch) consumed: refill
     if (tid == 0 && t + static_cast<int64_t>(kSStages) * gridDim.x < ntiles)
@@ -2107,9 +2123,23 @@ static bool try_assign_dmma(const double* X, int64_t n, int64_t d, const double*
   const int64_t ntiles = (n - row0 + kSRows - 1) / kSRows;
   const int per_sm = smem <= 113 * 1024 ? 2 : 1;
   const int64_t grid = ntiles < per_sm * g_sms ? ntiles : per_sm * g_sms;
+  static double* debug = nullptr;
+  static const bool dbg = std::getenv("PKRR_ASSIGN_DEBUG") != nullptr;
+  if (dbg && !debug) cudaMallocManaged(&debug, sizeof(double) * 3 * (n - row0));
   assign_dmma_kernel<KP><<<static_cast<unsigned>(grid), kSRows, smem, s>>>(
-      tm, n, static_cast<int>(d), xnorm, centers, cnorm, k, row0, label, best_dist, changed);
+      tm, n, static_cast<int>(d), xnorm, centers, cnorm, k, row0, label, best_dist, changed, debug);
   c.launched();
+  if (dbg) {
+    cudaStreamSynchronize(s);
+    double mx = 0, err = 0, bound = 0;
+    for (int64_t r = 0; r < n - row0; ++r) {
+      mx += debug[3 * r];
+      err = fmax(err, fabs(debug[3 * r + 1]));
+      bound = fmax(bound, debug[3 * r + 2]);
+    }
+    fprintf(stderr, "assign_dmma: %.3f candidates per row, max |screen - exact| %.3e, max bound %.3e\n",
+            mx / static_cast<double>(n - row0), err, bound);
+  }
   return true;
 }
 
