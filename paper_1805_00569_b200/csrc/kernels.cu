@@ -1729,104 +1729,74 @@ __global__ void __launch_bounds__(kAssignRows)
   }
 }
 
-// Lloyd assign / routing (mode 0), TMA-streamed: one persistent CTA per SM walks blocks of
-// 256 rows; a producer warp streams each block's 16-feature column chunks (256 x 16
-// doubles, 128 B swizzle, zero fill past d) through a 4-stage shared-memory ring, so
-// HBM reads run ahead of the dot products; 8 consumer warps, one row per thread, read
-// their row's chunk with conflict-free 16-byte loads and the centres by broadcast.
-// Arithmetic exactly assign_kernel's: sequential __dmul_rn / __dadd_rn in feature order
-// (the zero padding adds +0), (xn + cn) - 2 dot, clamp, strict < -- bitwise the
-// reference's labels (clustering.cpp:79-96, 182-195).
-constexpr int kTR = 128, kTS = 4, kTF = 16, kTWarps = kTR / 32, kTBlocksPerSM = 3;
-constexpr int kTStage = kTR * kTF * 8;  // 16 KB
+// Lloyd assign / routing (mode 0) with the rows streamed by the bulk-copy engine: a
+// persistent CTA of 64 threads (one row each) walks 64-row tiles of X, each tile one
+// contiguous cp.async.bulk (64 d doubles: rows are contiguous in row-major X) into a
+// two-stage shared-memory ring, so the next tile's HBM read overlaps this tile's dot
+// products.  Each thread reads its own row with 16-byte shared loads (row stride 8 d
+// bytes: conflict-free wavefronts) and the centres by broadcast.  Arithmetic exactly
+// assign_kernel's: sequential __dmul_rn / __dadd_rn in feature order, (xn + cn) - 2 dot,
+// clamp, strict < (bitwise the reference's labels, clustering.cpp:79-96, 182-195).
+constexpr int kBulkRows = 64, kBulkStages = 2;
 
 template <int KP>
-__global__ void __launch_bounds__((kTWarps + 1) * 32, kTBlocksPerSM)
-    assign_tma_kernel(const __grid_constant__ CUtensorMap tmX, int64_t n, int d, const double* __restrict__ xnorm,
-                      const double* __restrict__ centers, const double* __restrict__ cnorm, int k, int64_t row0,
-                      int32_t* label, double* best_dist, unsigned long long* changed, int probe) {
-  extern __shared__ unsigned char tma_smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(tma_smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  const int nch = (d + kTF - 1) / kTF, dch = nch * kTF;
-  double* cs = reinterpret_cast<double*>(smem + kTS * kTStage);  // [KP][dch], zero padded
-  __shared__ uint64_t full[kTS], empty[kTS];
+__global__ void __launch_bounds__(kBulkRows, 2)
+    assign_bulk_kernel(const double* __restrict__ X, int64_t n, int d, const double* __restrict__ xnorm,
+                       const double* __restrict__ centers, const double* __restrict__ cnorm, int k,
+                       int64_t row0, int32_t* label, double* best_dist, unsigned long long* changed) {
+  extern __shared__ __align__(16) unsigned char bulk_smem[];
+  double* tiles = reinterpret_cast<double*>(bulk_smem);
+  double* cs = tiles + kBulkStages * kBulkRows * d;  // [KP][d] centres (zero beyond k)
+  __shared__ uint64_t full[kBulkStages + 1];  // + the centres' barrier
   __shared__ double cn_s[KP];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x;
   const int64_t rows = n - row0;
-  const int64_t nblk = (rows + kTR - 1) / kTR;
-  const int64_t myblk = blockIdx.x < nblk ? (nblk - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t units = myblk * nch;
+  const int64_t ntiles = (rows + kBulkRows - 1) / kBulkRows;
+  auto tile_bytes = [&](int64_t t) {
+    const int64_t r = rows - t * kBulkRows;
+    return static_cast<uint32_t>((r < kBulkRows ? r : kBulkRows) * d * 8);
+  };
   if (tid == 0) {
-    for (int s = 0; s < kTS; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kTWarps);
-    }
+    for (int s = 0; s <= kBulkStages; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
-  }
-  __syncthreads();  // barriers initialised: the producer starts streaming at once
-  const uint32_t cbase = smem_u32(cs);  // explicit shared-window accesses (not generic)
-  if (warp == kTWarps) {  // ---- producer ----
-    if (lane == 0) {
-      prefetch_tmap(&tmX);
-      for (int64_t u = 0; u < units; ++u) {
-        const int s = static_cast<int>(u % kTS);
-        mbar_wait(&empty[s], static_cast<uint32_t>(((u / kTS) & 1) ^ 1));
-        mbar_arrive_expect_tx(&full[s], kTStage);
-        const int64_t blk = blockIdx.x + (u / nch) * gridDim.x;
-        const int c = static_cast<int>(u % nch);
-        unsigned char* dst = smem + s * kTStage;
-#pragma unroll
-        for (int h = 0; h < kTR / 64; ++h)
-          tma_load_2d(dst + h * 64 * 128, &tmX, c * kTF, static_cast<int>(row0 + blk * kTR + h * 64), &full[s]);
+    // the k centres (contiguous k d doubles) by one bulk copy, ahead of the first tile
+    mbar_arrive_expect_tx(&full[kBulkStages], static_cast<uint32_t>(k * d * 8));
+    bulk_load(cs, centers, static_cast<uint32_t>(k * d * 8), &full[kBulkStages]);
+    for (int s = 0; s < kBulkStages; ++s) {
+      const int64_t t = blockIdx.x + static_cast<int64_t>(s) * gridDim.x;
+      if (t < ntiles) {
+        mbar_arrive_expect_tx(&full[s], tile_bytes(t));
+        bulk_load(tiles + s * kBulkRows * d, X + (row0 + t * kBulkRows) * d, tile_bytes(t), &full[s]);
       }
     }
-    return;
   }
-  // ---- consumers: stage the centres (overlapping the first tiles' loads), then one
-  // row per thread ----
-  for (int e = tid; e < KP * dch; e += kTR) {
-    const int q = e / dch, f = e % dch;
-    sts_f64(cbase + 8u * e, (q < k && f < d) ? __ldg(centers + static_cast<int64_t>(q) * d + f) : 0.0);
-  }
+  for (int e = k * d + tid; e < KP * d; e += kBulkRows) cs[e] = 0.0;  // centres beyond k
   if (tid < KP) cn_s[tid] = tid < k ? cnorm[tid] : 0.0;
-  consumer_sync(kTR);
+  __syncthreads();
+  mbar_wait(&full[kBulkStages], 0);
   unsigned ch = 0;
-  double dot[KP];
-  double xn = 0.0;
-  int lab = 0;
-  const uint32_t sbase = smem_u32(smem);
-  for (int64_t u = 0; u < units; ++u) {
-    const int s = static_cast<int>(u % kTS);
-    const int c = static_cast<int>(u % nch);
-    const int64_t blk = blockIdx.x + (u / nch) * gridDim.x;
-    const int64_t i = row0 + blk * kTR + tid;
-    if (c == 0) {
+  int it = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int s = it % kBulkStages;
+    const int64_t i = row0 + t * kBulkRows + tid;
+    // the row's norm and label are read before waiting for its tile
+    const double xn = i < n ? xnorm[i] : 0.0;
+    const int lab = i < n ? label[i] : 0;
+    mbar_wait(&full[s], static_cast<uint32_t>((it / kBulkStages) & 1));
+    if (i < n) {
+      const double* xr = tiles + s * kBulkRows * d + tid * d;
+      double dot[KP];
 #pragma unroll
       for (int q = 0; q < KP; ++q) dot[q] = 0.0;
-      xn = i < n ? xnorm[i] : 0.0;
-      lab = i < n ? label[i] : 0;
-    }
-    mbar_wait(&full[s], static_cast<uint32_t>((u / kTS) & 1));
-    // deferred release of the previous stage (its loads are consumed by now)
-    if (u > 0) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[(u - 1) % kTS]);
-    }
-    const uint32_t st = sbase + s * kTStage;
-    const uint32_t cc = cbase + 8u * (c * kTF);
-    // PKRR_ASSIGN_PROBE=1: skip the dot products (memory-side timing probe; labels wrong)
+      for (int c = 0; c < d; c += 2) {
+        const double2 x = *reinterpret_cast<const double2*>(xr + c);
 #pragma unroll
-    for (int p = 0; p < (probe ? 0 : kTF / 2); ++p) {
-      const double2 x = lds_f64x2(st + swz128(tid, 2 * p));
-#pragma unroll
-      for (int q = 0; q < KP; ++q) {
-        const double2 cv = lds_f64x2(cc + 8u * (q * dch + 2 * p));
-        dot[q] = __dadd_rn(dot[q], __dmul_rn(x.x, cv.x));
-        dot[q] = __dadd_rn(dot[q], __dmul_rn(x.y, cv.y));
+        for (int q = 0; q < KP; ++q) {
+          const double2 cv = *reinterpret_cast<const double2*>(cs + q * d + c);
+          dot[q] = __dadd_rn(dot[q], __dmul_rn(x.x, cv.x));
+          dot[q] = __dadd_rn(dot[q], __dmul_rn(x.y, cv.y));
+        }
       }
-    }
-    if (c == nch - 1 && i < n) {
       double min_d = INFINITY;
       int min_j = 0;
 #pragma unroll
@@ -1845,94 +1815,14 @@ __global__ void __launch_bounds__((kTWarps + 1) * 32, kTBlocksPerSM)
       }
       if (best_dist) best_dist[i] = min_d;
     }
-  }
-  if (changed) {
-    const unsigned w = __reduce_add_sync(0xffffffffu, ch);
-    if (lane == 0 && w) atomicAdd(changed, static_cast<unsigned long long>(w));
-  }
-}
-
-// Lloyd assign / routing (mode 0), register-streamed: one row per thread, the row read
-// with 16-byte global loads (L1-cached: a row's 720 bytes come in as whole lines, and the
-// next 16-feature chunk's loads are in flight while this chunk's dot products run), the
-// centres in shared memory read by broadcast.  Same arithmetic as assign_kernel.
-constexpr int kLRows = 128, kLChunk = 16;
-
-template <int KP>
-__global__ void __launch_bounds__(kLRows, 4)
-    assign_ldg_kernel(const double* __restrict__ X, int64_t n, int d, const double* __restrict__ xnorm,
-                      const double* __restrict__ centers, const double* __restrict__ cnorm, int k, int64_t row0,
-                      int32_t* label, double* best_dist, unsigned long long* changed) {
-  extern __shared__ __align__(16) double ldg_cs[];  // [KP][dch]
-  __shared__ double cn_s[KP];
-  const int tid = threadIdx.x;
-  const int nch = (d + kLChunk - 1) / kLChunk, dch = nch * kLChunk;
-  const uint32_t cbase = smem_u32(ldg_cs);
-  for (int e = tid; e < KP * dch; e += kLRows) {
-    const int q = e / dch, f = e % dch;
-    sts_f64(cbase + 8u * e, (q < k && f < d) ? __ldg(centers + static_cast<int64_t>(q) * d + f) : 0.0);
-  }
-  if (tid < KP) cn_s[tid] = tid < k ? cnorm[tid] : 0.0;
-  const int64_t i = row0 + static_cast<int64_t>(blockIdx.x) * kLRows + tid;
-  const bool valid = i < n;
-  const double2* xr = reinterpret_cast<const double2*>(X + (valid ? i : row0) * d);
-  const int dp2 = d / 2;  // d is even: the row is dp2 double2s
-  // two register buffers, unrolled by hand (no dynamic indexing: no local memory)
-  double2 ba[kLChunk / 2], bb[kLChunk / 2];
-  auto load = [&](double2 (&b)[kLChunk / 2], int c) {
-#pragma unroll
-    for (int p = 0; p < kLChunk / 2; ++p) {
-      const int g = c * (kLChunk / 2) + p;
-      b[p] = g < dp2 ? __ldg(xr + g) : make_double2(0.0, 0.0);
-    }
-  };
-  double dot[KP];
-#pragma unroll
-  for (int q = 0; q < KP; ++q) dot[q] = 0.0;
-  auto compute = [&](const double2 (&b)[kLChunk / 2], int c) {
-    const uint32_t cc = cbase + 8u * (c * kLChunk);
-#pragma unroll
-    for (int p = 0; p < kLChunk / 2; ++p) {
-      const double2 x = b[p];
-#pragma unroll
-      for (int q = 0; q < KP; ++q) {
-        const double2 cv = lds_f64x2(cc + 8u * (q * dch + 2 * p));
-        dot[q] = __dadd_rn(dot[q], __dmul_rn(x.x, cv.x));
-        dot[q] = __dadd_rn(dot[q], __dmul_rn(x.y, cv.y));
+    __syncthreads();  // every row of stage s consumed: refill it
+    if (tid == 0) {
+      const int64_t tn = t + static_cast<int64_t>(kBulkStages) * gridDim.x;
+      if (tn < ntiles) {
+        mbar_arrive_expect_tx(&full[s], tile_bytes(tn));
+        bulk_load(tiles + s * kBulkRows * d, X + (row0 + tn * kBulkRows) * d, tile_bytes(tn), &full[s]);
       }
     }
-  };
-  load(ba, 0);
-  const double xn = valid ? xnorm[i] : 0.0;
-  const int lab = valid ? label[i] : 0;
-  __syncthreads();
-  for (int c = 0; c < nch; c += 2) {
-    if (c + 1 < nch) load(bb, c + 1);  // the next chunk in flight during this one's arithmetic
-    compute(ba, c);
-    if (c + 1 < nch) {
-      if (c + 2 < nch) load(ba, c + 2);
-      compute(bb, c + 1);
-    }
-  }
-  unsigned ch = 0;
-  if (valid) {
-    double min_d = INFINITY;
-    int min_j = 0;
-#pragma unroll
-    for (int q = 0; q < KP; ++q) {
-      if (q >= k) break;
-      double dist = __dsub_rn(__dadd_rn(xn, cn_s[q]), __dmul_rn(2.0, dot[q]));
-      if (dist < 0.0) dist = 0.0;
-      if (dist < min_d) {
-        min_d = dist;
-        min_j = q;
-      }
-    }
-    if (lab != min_j) {
-      label[i] = min_j;
-      ch = 1;
-    }
-    if (best_dist) best_dist[i] = min_d;
   }
   if (changed) {
     const unsigned w = __reduce_add_sync(0xffffffffu, ch);
@@ -1941,15 +1831,20 @@ __global__ void __launch_bounds__(kLRows, 4)
 }
 
 template <int KP>
-static bool try_assign_ldg(const double* X, int64_t n, int64_t d, const double* xnorm, const double* centers,
-                           const double* cnorm, int k, int64_t row0, int32_t* label, double* best_dist,
-                           unsigned long long* changed, cudaStream_t s, Counter& c) {
-  const int64_t dch = (d + kLChunk - 1) / kLChunk * kLChunk;
-  const size_t smem = sizeof(double) * KP * dch;
-  if (d % 2 || (reinterpret_cast<uintptr_t>(X) & 15) || smem > 48 * 1024) return false;
-  const int64_t blocks = (n - row0 + kLRows - 1) / kLRows;
-  assign_ldg_kernel<KP><<<static_cast<unsigned>(blocks), kLRows, smem, s>>>(
-      X, n, static_cast<int>(d), xnorm, centers, cnorm, k, row0, label, best_dist, changed);
+static bool try_assign_bulk(const double* X, int64_t n, int64_t d, const double* xnorm, const double* centers,
+                            const double* cnorm, int k, int64_t row0, int32_t* label, double* best_dist,
+                            unsigned long long* changed, cudaStream_t s, Counter& c) {
+  const size_t smem = sizeof(double) * (static_cast<size_t>(kBulkStages) * kBulkRows * d + KP * d);
+  if (d % 2 || (reinterpret_cast<uintptr_t>(X) & 15) || (reinterpret_cast<uintptr_t>(centers) & 15) ||
+      smem > 110 * 1024)
+    return false;
+  static std::atomic<uint64_t> attr{0};
+  smem_optin(attr, assign_bulk_kernel<KP>, 110 * 1024);
+  const int64_t ntiles = (n - row0 + kBulkRows - 1) / kBulkRows;
+  const int64_t grid = ntiles < 2 * g_sms ? ntiles : 2 * g_sms;
+  assign_bulk_kernel<KP><<<static_cast<unsigned>(grid), kBulkRows, smem, s>>>(X, n, static_cast<int>(d), xnorm,
+                                                                            centers, cnorm, k, row0, label,
+                                                                            best_dist, changed);
   c.launched();
   return true;
 }
@@ -2143,27 +2038,6 @@ static bool try_assign_dmma(const double* X, int64_t n, int64_t d, const double*
   return true;
 }
 
-template <int KP>
-static bool try_assign_tma(const double* X, int64_t n, int64_t d, const double* xnorm, const double* centers,
-                           const double* cnorm, int k, int64_t row0, int32_t* label, double* best_dist,
-                           unsigned long long* changed, cudaStream_t s, Counter& c) {
-  static const bool off = std::getenv("PKRR_ASSIGN_TMA") && std::atoi(std::getenv("PKRR_ASSIGN_TMA")) == 0;
-  static const bool probe = std::getenv("PKRR_ASSIGN_PROBE") != nullptr;
-  const int64_t dch = (d + kTF - 1) / kTF * kTF;
-  const size_t smem = kTS * kTStage + sizeof(double) * KP * dch + 1024;
-  if (off || d % 2 || (reinterpret_cast<uintptr_t>(X) & 15) || smem > 80 * 1024) return false;
-  CUtensorMap tm;
-  if (!make_tmap(&tm, X, n, d, d)) return false;
-  static std::atomic<uint64_t> attr{0};
-  smem_optin(attr, assign_tma_kernel<KP>, 80 * 1024);
-  const int64_t nblk = (n - row0 + kTR - 1) / kTR;
-  const int64_t grid = nblk < kTBlocksPerSM * g_sms ? nblk : kTBlocksPerSM * g_sms;
-  assign_tma_kernel<KP><<<static_cast<unsigned>(grid), (kTWarps + 1) * 32, smem, s>>>(
-      tm, n, static_cast<int>(d), xnorm, centers, cnorm, k, row0, label, best_dist, changed, probe ? 1 : 0);
-  c.launched();
-  return true;
-}
-
 void launch_assign(const double* X, int64_t n, int64_t d, const double* xnorm,
                    const double* centers, const double* cnorm, int k, int mode,
                    const uint8_t* open, int64_t row0, int32_t* label, double* best_dist,
@@ -2172,7 +2046,16 @@ void launch_assign(const double* X, int64_t n, int64_t d, const double* xnorm,
   if (rows <= 0) return;
   // mode 0 (Lloyd assign, routing): bulk-copy row streaming (k-balance rounds, mode 1, skip
   // whole blocks of settled rows and keep the per-chunk kernel below)
-  static const int variant = std::getenv("PKRR_ASSIGN") ? std::atoi(std::getenv("PKRR_ASSIGN")) : 3;
+  // 1 (default): bulk-copy streaming for k <= 16; 3: the DMMA screen (measured slower:
+  // DESIGN.md); 0: the chunked kernel below for every k
+  static const int variant = std::getenv("PKRR_ASSIGN") ? std::atoi(std::getenv("PKRR_ASSIGN")) : 1;
+  if (mode == 0 && variant == 1) {
+    if (k <= 8 && try_assign_bulk<8>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
+      return;
+    if (k > 8 && k <= 16 &&
+        try_assign_bulk<16>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
+      return;
+  }
   if (mode == 0 && variant == 3) {
     if (k <= 8 && try_assign_dmma<8>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
       return;
@@ -2186,18 +2069,6 @@ void launch_assign(const double* X, int64_t n, int64_t d, const double* xnorm,
         try_assign_dmma<64>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
       return;
   }
-  if (mode == 0 && variant == 1 && k <= 8 &&
-      try_assign_ldg<8>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
-    return;
-  if (mode == 0 && variant == 1 && k > 8 && k <= 16 &&
-      try_assign_ldg<16>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
-    return;
-  if (mode == 0 && variant == 2 && k <= 8 &&
-      try_assign_tma<8>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
-    return;
-  if (mode == 0 && variant == 2 && k > 8 && k <= 16 &&
-      try_assign_tma<16>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c))
-    return;
   const unsigned blocks = static_cast<unsigned>((rows + kAssignRows - 1) / kAssignRows);
   if (k <= 8)
     assign_kernel<8><<<blocks, kAssignRows, 0, s>>>(X, n, d, xnorm, centers, cnorm, k, mode, open,
