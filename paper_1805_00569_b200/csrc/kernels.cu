@@ -1610,17 +1610,31 @@ __global__ void combine_cells_kernel(const double* __restrict__ pp, int64_t P, i
   }
 }
 
-__global__ void mse_rows_kernel(const double* __restrict__ comb, const double* __restrict__ y, int64_t t,
-                                int64_t ncell, double* __restrict__ mse) {
-  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (c >= ncell) return;
+// One warp per cell: the lanes load 32 rows at a time (coalesced, the next 32 in flight)
+// and form (pred - y)^2 with explicit roundings; lane 0 adds them in row order -- the
+// reference's sequential sum, limited only by the dependent DADD latency.
+__global__ void __launch_bounds__(32) mse_rows_kernel(const double* __restrict__ comb, const double* __restrict__ y,
+                                                      int64_t t, double* __restrict__ mse) {
+  const int64_t c = blockIdx.x;
+  const int lane = threadIdx.x;
   const double* v = comb + c * t;
   double s = 0.0;
-  for (int64_t j = 0; j < t; ++j) {
+  auto sq = [&](int64_t j) {
+    if (j >= t) return 0.0;
     const double diff = __dsub_rn(v[j], y[j]);
-    s = __dadd_rn(s, __dmul_rn(diff, diff));
+    return __dmul_rn(diff, diff);
+  };
+  double cur = sq(lane);
+  for (int64_t base = 0; base < t; base += 32) {
+    const double nxt = sq(base + 32 + lane);
+    const int cnt = t - base < 32 ? static_cast<int>(t - base) : 32;
+    for (int r = 0; r < cnt; ++r) {
+      const double e = __shfl_sync(0xffffffffu, cur, r);
+      s = __dadd_rn(s, e);
+    }
+    cur = nxt;
   }
-  mse[c] = __ddiv_rn(s, static_cast<double>(t));
+  if (lane == 0) mse[c] = __ddiv_rn(s, static_cast<double>(t));
 }
 
 void launch_combine_cells(const double* pp, int64_t P, int64_t t, int64_t ncell, int predictor, const double* y,
@@ -1631,7 +1645,7 @@ void launch_combine_cells(const double* pp, int64_t P, int64_t t, int64_t ncell,
   combine_cells_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(pp, P, t, ncell, predictor, y, comb);
   c.launched();
   if (mse) {
-    mse_rows_kernel<<<static_cast<unsigned>((ncell + 31) / 32), 32, 0, s>>>(comb, y, t, ncell, mse);
+    mse_rows_kernel<<<static_cast<unsigned>(ncell), 32, 0, s>>>(comb, y, t, mse);
     c.launched();
   }
 }
