@@ -300,6 +300,18 @@ int pkrrgpu_multi_grid_search(pkrrgpu_multi* m, const pkrrgpu_grid_args* args, p
 int pkrrgpu_multi_train_krr(pkrrgpu_multi* m, const double* X, const double* y, int64_t n, int64_t d,
                             double sigma, double lambda, double* alpha, double* residual, int64_t* npd_pivot);
 
+/* Broadcast of a DEVICE buffer of `bytes` from rank `root` to every rank (e.g. an NCCL
+ * broadcast); called with the engine's stream synchronised; returns 0 on success. */
+typedef int (*pkrrgpu_bcast_fn)(void* user, void* dev_buf, int64_t bytes, int root);
+/* DKRR with one process per GPU: every rank calls it with the same inputs on its own
+ * context; rank r stores and updates the super-columns c with c mod world == r, the owner
+ * of each step broadcasts its factored panel (with the forward-substitution vector and
+ * its NPD status), the backward solve broadcasts each solved block.  alpha (n) and the
+ * residual on every rank; NPD as pkrrgpu_train_krr on every rank. */
+int pkrrgpu_dist_train_krr(pkrrgpu_ctx* ctx, int rank, int world, pkrrgpu_bcast_fn bcast, void* user,
+                           const double* X, const double* y, int64_t n, int64_t d, double sigma, double lambda,
+                           double* alpha, double* residual, int64_t* npd_pivot);
+
 /* ---- data preparation (dataset.hpp standardize, strategies.hpp auto_sigma_grid) */
 
 /* standardize -- dataset.cpp:199-232 (+ apply_feature_stats :178-197), dense rows:

@@ -58,6 +58,8 @@ class CudaError(RuntimeError):
 
 # pkrrgpu_allgather_fn: int (*)(void* user, void* dev_buf, int64_t bytes_per_rank)
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64)
+# pkrrgpu_bcast_fn: int (*)(void* user, void* dev_buf, int64_t bytes, int root)
+BCAST_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int)
 
 
 class GridArgs(C.Structure):
@@ -162,6 +164,9 @@ def load_library(path: str = LIB_PATH):
         "pkrrgpu_multi_grid_search": (C.c_int, [C.c_void_p, C.POINTER(GridArgs), C.POINTER(GridOut)]),
         "pkrrgpu_multi_train_krr": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_double,
                                               C.c_double, C.c_void_p, _d, _i64]),
+        "pkrrgpu_dist_train_krr": (C.c_int, [C.c_void_p, C.c_int, C.c_int, BCAST_FN, C.c_void_p, C.c_void_p,
+                                             C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_void_p,
+                                             _d, _i64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -495,6 +500,30 @@ class Engine:
                                       float(sigma), float(lam), C.byref(h), C.byref(fp), C.byref(piv))
         _check(rc, piv.value)
         return TrainedPartitions(self, h)
+
+    def dist_train_krr(self, X, y, sigma, lam, rank, world, bcast):
+        """DKRR with one process per GPU (pkrrgpu_dist_train_krr): every rank calls it with
+        the same inputs; bcast(dev_ptr, nbytes, root) broadcasts a device buffer (e.g.
+        sharding.torch_broadcast).  Returns (alpha, residual) on every rank."""
+        X = np.ascontiguousarray(X, np.float64)
+        y = np.ascontiguousarray(y, np.float64)
+        alpha = np.empty(X.shape[0])
+        res = C.c_double(0)
+        piv = C.c_int64(-1)
+
+        def _cb(user, buf, nbytes, root):
+            try:
+                bcast(int(buf), int(nbytes), int(root))
+                return 0
+            except Exception as exc:  # reported as a failed exchange by the engine
+                print(f"pkrr broadcast failed: {exc!r}", file=sys.stderr)
+                return 1
+        cb = BCAST_FN(_cb)
+        rc = _lib.pkrrgpu_dist_train_krr(self._h, int(rank), int(world), cb, None, X.ctypes.data, y.ctypes.data,
+                                         X.shape[0], X.shape[1], float(sigma), float(lam), alpha.ctypes.data,
+                                         C.byref(res), C.byref(piv))
+        _check(rc, piv.value)
+        return alpha, res.value
 
     def combine(self, strategy, p, pred, y, failed=None):
         """pkrrgpu_combine: cell combine + reference-order MSE + best cell over gathered

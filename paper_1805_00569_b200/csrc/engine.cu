@@ -716,6 +716,8 @@ const char* pkrrgpu_version(void) { return "pkrr-b200 0.1 (sm_100a, DMMA f64 + T
 const char* pkrrgpu_last_error(void) { return g_err.c_str(); }
 // internal (multi.cu): a worker thread's error reported on the calling thread
 void pkrrgpu_set_last_error_(const char* msg) { g_err = msg ? msg : ""; }
+// internal (dist.cu)
+int pkrrgpu_context_device_(const pkrrgpu_ctx* ctx) { return ctx ? ctx->device : 0; }
 // internal (dist.cu): launches made on a context's device outside its own calls
 void pkrrgpu_add_launches_(pkrrgpu_ctx* ctx, int64_t n) {
   if (ctx) ctx->counter.launches += n;

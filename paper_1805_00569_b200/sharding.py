@@ -92,3 +92,28 @@ def staged_allgather(dist, rank: int, world: int, device):
         full.copy_(torch.cat(parts).to(device))
         torch.cuda.synchronize(device)
     return fn
+
+
+# ---- DKRR panel broadcast (pkrrgpu_dist_train_krr) ------------------------------------
+def torch_broadcast(dist, device):
+    """bcast(ptr, nbytes, root) for Engine.dist_train_krr: one collective broadcast of the
+    device buffer on the process group's device (NCCL over NVLink)."""
+    import torch
+
+    def fn(ptr, nbytes, root):
+        dist.broadcast(_device_view(ptr, nbytes, device), src=root)
+        torch.cuda.current_stream(device).synchronize()
+    return fn
+
+
+def staged_broadcast(dist, device):
+    """The same broadcast through host memory (gloo process groups: the tests)."""
+    import torch
+
+    def fn(ptr, nbytes, root):
+        view = _device_view(ptr, nbytes, device)
+        host = view.cpu()
+        dist.broadcast(host, src=root)
+        view.copy_(host.to(device))
+        torch.cuda.synchronize(device)
+    return fn
