@@ -100,10 +100,11 @@ __global__ void __launch_bounds__(kSyrkThreads, 1)
             // C tile of this output block: wait until the previous tile's store drained
             mbar_wait(cempty, (it & 1) ^ 1);
             mbar_arrive_expect_tx(cfull, kCBytes);
+            const uint64_t pol = l2_policy_evict_first();  // C is streamed once per group
             for (int cb = 0; cb < 8; ++cb)
               for (int rb = 0; rb < 2; ++rb)
-                tma_load_2d(cbuf + ((cb * 2 + rb) << 13), &tmA, p.row0 + tn * 128 + cb * 16,
-                            p.row0 + tm * 128 + rb * 64, cfull);
+                tma_load_2d_hint(cbuf + ((cb * 2 + rb) << 13), &tmA, p.row0 + tn * 128 + cb * 16,
+                                 p.row0 + tm * 128 + rb * 64, cfull, pol);
           }
         }
       }
@@ -175,10 +176,11 @@ __global__ void __launch_bounds__(kSyrkThreads, 1)
     fence_proxy_async();
     consumer_sync(kConsumerWarps * 32);
     if (threadIdx.x == 128) {
+      const uint64_t pol = l2_policy_evict_first();
       for (int cb = 0; cb < 8; ++cb)
         for (int rb = 0; rb < 2; ++rb)
-          tma_store_2d(&tmA, p.row0 + tn * 128 + cb * 16, p.row0 + tm * 128 + rb * 64,
-                       cbuf + ((cb * 2 + rb) << 13));
+          tma_store_2d_hint(&tmA, p.row0 + tn * 128 + cb * 16, p.row0 + tm * 128 + rb * 64,
+                            cbuf + ((cb * 2 + rb) << 13), pol);
       bulk_commit();
       bulk_wait_read0();
       mbar_arrive(cempty);
