@@ -10,6 +10,10 @@
 #include <vector>
 #include <cstdlib>
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <queue>
+#include <tuple>
 
 #include "gemm_dmma.cuh"
 #include "syrk_persistent.cuh"
@@ -367,10 +371,11 @@ __device__ __forceinline__ void mma_row4_rn_lowB(double (&acc)[4][2], const doub
 // chain is LDS -> rsqrt -> multiply -> STS -> syncwarp.  After each column lane 0
 // arrives on cbar[j] (when given): the warps factoring the rows below the block
 // (warp_tall32) read the same slots without ever holding this warp up.
-__device__ __noinline__ int warp_potrf32(double* Sd, double* col, uint64_t* cbar, int lane) {
+template <int LS>
+__device__ __noinline__ int warp_potrf32_s(double* Sd, double* col, uint64_t* cbar, int lane) {
   double a[32];
 #pragma unroll
-  for (int c = 0; c < 32; ++c) a[c] = Sd[lane * kLS + c];
+  for (int c = 0; c < 32; ++c) a[c] = Sd[lane * LS + c];
   int bad = -1;
   if (lane == 0) col[32] = a[0];
   __syncwarp();
@@ -409,9 +414,12 @@ __device__ __noinline__ int warp_potrf32(double* Sd, double* col, uint64_t* cbar
   }
   if (bad < 0) {
 #pragma unroll
-    for (int c = 0; c < 32; ++c) Sd[lane * kLS + c] = c <= lane ? a[c] : 0.0;
+    for (int c = 0; c < 32; ++c) Sd[lane * LS + c] = c <= lane ? a[c] : 0.0;
   }
   return bad;
+}
+__device__ __forceinline__ int warp_potrf32(double* Sd, double* col, uint64_t* cbar, int lane) {
+  return warp_potrf32_s<kLS>(Sd, col, cbar, lane);
 }
 
 // The rows below the diagonal block, factored along with it (the panel TRSM of the
@@ -444,15 +452,16 @@ __device__ __noinline__ void warp_tall32(double* P, const double* pub, uint64_t*
 
 // inverse of the lower 32x32 block at Sd into Db (row-major, stride kBS);
 // lane c computes column c by forward substitution
-__device__ __noinline__ void warp_trtri32(const double* Sd, double* Db, int lane) {
-  const double rinv = 1.0 / Sd[lane * kLS + lane];  // lane i: 1 / L_ii, off the chain
+template <int LS, int DS>
+__device__ __noinline__ void warp_trtri32_s(const double* Sd, double* Db, int lane) {
+  const double rinv = 1.0 / Sd[lane * LS + lane];  // lane i: 1 / L_ii, off the chain
   double x[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
     double s0 = lane == i ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // 4 chains
 #pragma unroll
     for (int k = 0; k < i; ++k) {
-      const double t = Sd[i * kLS + k] * x[k];
+      const double t = Sd[i * LS + k] * x[k];
       if ((k & 3) == 0) s0 -= t;
       else if ((k & 3) == 1) s1 -= t;
       else if ((k & 3) == 2) s2 -= t;
@@ -462,7 +471,10 @@ __device__ __noinline__ void warp_trtri32(const double* Sd, double* Db, int lane
     x[i] = i >= lane ? ((s0 + s1) + (s2 + s3)) * ri : 0.0;
   }
 #pragma unroll
-  for (int i = 0; i < 32; ++i) Db[i * kBS + lane] = x[i];
+  for (int i = 0; i < 32; ++i) Db[i * DS + lane] = x[i];
+}
+__device__ __forceinline__ void warp_trtri32(const double* Sd, double* Db, int lane) {
+  warp_trtri32_s<kLS, kBS>(Sd, Db, lane);
 }
 
 #ifdef PKRR_LEAF_TRACE
@@ -668,6 +680,198 @@ __global__ void __launch_bounds__(kLeafThreads, 1)
 }
 
 
+}  // namespace pk
+#include "potrf_df.cuh"
+namespace pk {
+
+// ---------------------------------------------------------------------------
+// dataflow Cholesky (potrf_df.cuh): the static task list and the launcher
+// ---------------------------------------------------------------------------
+namespace {
+struct DfNode {
+  int type;  // -1 chain step, else DfType
+  int i, j, a, b, time, deadline;
+  std::vector<int> out;
+  int indeg;
+};
+}  // namespace
+
+// Topological order of the worker tasks of an nt-tile factorization, the chain steps as
+// virtual nodes processed as soon as they are ready (so every task a chain step waits
+// on precedes every task that waits on that step), ties by deadline: the step by which
+// the task's output is needed.
+std::vector<int4> df_build_tasks(int nt) {
+  std::vector<DfNode> nd;
+  auto add = [&](int type, int i, int j, int a, int b, int time) {
+    nd.push_back(DfNode{type, i, j, a, b, time, 0, {}, 0});
+    return static_cast<int>(nd.size()) - 1;
+  };
+  auto edge = [&](int from, int to) {
+    nd[from].out.push_back(to);
+    ++nd[to].indeg;
+  };
+  std::vector<int> chain(nt), trsm(static_cast<size_t>(nt) * nt, -1);
+  std::vector<std::vector<int>> items(static_cast<size_t>(nt) * nt);
+  for (int k = 0; k < nt; ++k) chain[k] = add(-1, k, k, 0, 0, k);
+  for (int i = 0; i < nt; ++i)
+    for (int j = 0; j <= i; ++j) {
+      const int e = i == j ? j - 1 : j;  // panels [0, e) applied by workers (the chain applies j-1 to (j,j))
+      if (e <= 0) continue;
+      const int s0 = std::max(0, e - kDfSingles);
+      std::vector<std::pair<int, int>> rng;
+      for (int a = 0; a < s0; a += kDfBatch) rng.push_back({a, std::min(a + kDfBatch, s0)});
+      for (int q = s0; q < e; ++q) rng.push_back({q, q + 1});
+      for (auto& r : rng) items[i * nt + j].push_back(add(DF_UPD, i, j, r.first, r.second, r.second - 1));
+    }
+  for (int k = 0; k < nt; ++k)
+    for (int i = k + 2; i < nt; ++i) trsm[i * nt + k] = add(DF_TRSM, i, k, 0, 0, k);
+  std::vector<int> inv;
+  for (int b = 0; b < nt / 2; ++b) inv.push_back(add(DF_INV, b, 0, 0, 0, 2 * b + 1));
+  auto lprod = [&](int row, int q) { return row == q + 1 ? chain[q] : trsm[row * nt + q]; };
+  for (int i = 0; i < nt; ++i)
+    for (int j = 0; j <= i; ++j) {
+      const std::vector<int>& it = items[i * nt + j];
+      for (size_t x = 0; x < it.size(); ++x) {
+        const int id = it[x];
+        if (x > 0) edge(it[x - 1], id);
+        const int q = nd[id].b - 1;
+        edge(lprod(i, q), id);
+        if (j != i) edge(lprod(j, q), id);
+        nd[id].deadline = x + 1 < it.size() ? nd[it[x + 1]].time : (i == j ? j - 1 : j);
+      }
+    }
+  for (int k = 0; k < nt; ++k)
+    for (int i = k + 2; i < nt; ++i) {
+      const int id = trsm[i * nt + k];
+      edge(chain[k], id);
+      if (!items[i * nt + k].empty()) edge(items[i * nt + k].back(), id);
+      nd[id].deadline = k + 1;
+    }
+  for (int k = 0; k < nt; ++k) {
+    if (k > 0) edge(chain[k - 1], chain[k]);
+    if (!items[k * nt + k].empty()) edge(items[k * nt + k].back(), chain[k]);
+    if (k + 1 < nt && !items[(k + 1) * nt + k].empty()) edge(items[(k + 1) * nt + k].back(), chain[k]);
+  }
+  for (int b = 0; b < nt / 2; ++b) {
+    edge(chain[2 * b + 1], inv[b]);
+    nd[inv[b]].deadline = nt + 1;
+  }
+  using Key = std::tuple<int, int, int, int, int, int>;  // deadline, time, type, i, j, id
+  std::priority_queue<Key, std::vector<Key>, std::greater<Key>> ready;
+  std::vector<int> chain_ready;
+  auto push = [&](int id) {
+    if (nd[id].type < 0)
+      chain_ready.push_back(id);
+    else
+      ready.push(Key{nd[id].deadline, nd[id].time, nd[id].type, nd[id].i, nd[id].j, id});
+  };
+  for (size_t id = 0; id < nd.size(); ++id)
+    if (nd[id].indeg == 0) push(static_cast<int>(id));
+  std::vector<int4> out;
+  size_t done = 0;
+  auto finish = [&](int id) {
+    ++done;
+    for (int o : nd[id].out)
+      if (--nd[o].indeg == 0) push(o);
+  };
+  while (true) {
+    while (!chain_ready.empty()) {
+      const int id = chain_ready.back();
+      chain_ready.pop_back();
+      finish(id);
+    }
+    if (ready.empty()) break;
+    const int id = std::get<5>(ready.top());
+    ready.pop();
+    const DfNode& n = nd[id];
+    out.push_back(make_int4(n.type, n.i, n.j, n.a | (n.b << 16)));
+    finish(id);
+  }
+  if (done != nd.size()) {
+    fprintf(stderr, "pkrr: dataflow task graph has a cycle (%zu of %zu)\n", done, nd.size());
+    abort();
+  }
+  return out;
+}
+
+// device copy of the task list per (device, nt), built once
+static const int4* df_tasks_device(int nt, int* ntasks) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, std::pair<int4*, int>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_pair(current_device(), nt);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    const std::vector<int4> h = df_build_tasks(nt);
+    int4* d = nullptr;
+    cudaMalloc(&d, sizeof(int4) * h.size());
+    cudaMemcpy(d, h.data(), sizeof(int4) * h.size(), cudaMemcpyHostToDevice);
+    it = cache.emplace(key, std::make_pair(d, static_cast<int>(h.size()))).first;
+  }
+  *ntasks = it->second.second;
+  return it->second.first;
+}
+
+static bool launch_potrf_df(double* A, const CUtensorMap& tmA, double* Linv, int64_t mp, int* status, cudaStream_t s,
+                            Counter& c, const FwdSolve* fs) {
+  static std::atomic<uint64_t> attr{0};
+  smem_optin(attr, potrf_df_kernel, kDfSmem);
+  const int nt = static_cast<int>(mp / kDfT);
+  DfParams p{};
+  p.tasks = df_tasks_device(nt, &p.ntasks);
+  const int64_t nflag = ((F_HEAD + static_cast<int64_t>(nt) * nt + nt + 2) + 31) / 32 * 32;
+  const size_t bytes = nflag * 4 + sizeof(double) * (static_cast<size_t>(nt) * 4096 + static_cast<size_t>(nt) * nt * 64);
+  // workspace: grow-only, one per (device, stream) -- calls on one stream are ordered,
+  // so its previous use has finished; a per-call cudaMallocAsync / cudaFreeAsync made the
+  // pool release and re-map the memory every call (~0.5 ms per C0 step)
+  void* ws = nullptr;
+  {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> pool;
+    std::lock_guard<std::mutex> lock(mu);
+    auto& e = pool[std::make_pair(current_device(), s)];
+    if (e.second < bytes) {
+      if (e.first) {
+        cudaStreamSynchronize(s);
+        cudaFree(e.first);
+      }
+      e.first = nullptr;
+      e.second = 0;
+      if (cudaMalloc(&e.first, bytes) == cudaSuccess) e.second = bytes;
+    }
+    ws = e.first;
+  }
+  cudaMemsetAsync(ws, 0, nflag * 4, s);
+  p.flags = static_cast<int*>(ws);
+  p.inv64 = reinterpret_cast<double*>(p.flags + nflag);
+  p.P = p.inv64 + static_cast<int64_t>(nt) * 4096;
+  p.status = status ? status : p.flags + nflag - 2;
+  p.A = A;
+  p.lda = mp;
+  p.nt = nt;
+  p.Linv = Linv;
+  p.y = fs ? fs->y : nullptr;
+  p.z = fs ? fs->z : nullptr;
+  CUtensorMap tmI;
+  if (!make_tmap(&tmI, p.inv64, static_cast<int64_t>(nt) * kDfT, kDfT, kDfT)) {
+    fprintf(stderr, "pkrr: tensor map for the dataflow Cholesky failed\n");
+    abort();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(g_sms));
+  cfg.blockDim = dim3(kDfThreads);
+  cfg.dynamicSmemBytes = kDfSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, potrf_df_kernel, tmA, tmI, p);
+  c.launched();
+  return fs != nullptr;
+}
+
 // Panel-grouped blocked right-looking Cholesky.  G consecutive 128-column panels
 // are factored with narrow column updates restricted to the group (leaf + DMMA
 // TRSM each), then ONE trailing SYRK with K = 128*G updates the rest: the
@@ -798,6 +1002,14 @@ bool launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
     }
     make_tmap(&sh.tmA, sh.A, mp, mp, mp);
     make_tmap(&sh.tmLinv, sh.Linv, mp, kNB, kNB);
+  }
+  // a lone small system: the dataflow kernel (potrf_df.cuh); PKRR_DF=0 keeps the
+  // stream-ordered panel chain below
+  {
+    static const bool df_on = !(std::getenv("PKRR_DF") && std::atoi(std::getenv("PKRR_DF")) == 0);
+    const bool int8_up = g_syrk_ozaki && slices && exps;
+    if (df_on && latency && mp / kNB < 64 && !shadow && !int8_up && g_panel_group == 0)
+      return launch_potrf_df(A, tmA, Linv, mp, status, s, c, fs);
   }
   // fused forward substitution (not with the shadow checker: its steps run twice)
   const bool fused = fs != nullptr && !shadow;

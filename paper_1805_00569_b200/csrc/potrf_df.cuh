@@ -1,0 +1,860 @@
+// potrf_df.cuh -- dataflow Cholesky for a system factorised ALONE (latency mode,
+// mp < 8192: BASELINE configs[0], pkrrgpu_cholesky / train_krr on one system).
+//
+// The stream-ordered blocked path (launch_potrf) runs one 128-column panel step as
+// leaf -> TRSM -> next-column update kernels; for a lone 4096-row system that chain
+// (≈ 57 µs per panel, the leaf alone 40 µs on a cold SM) and the K = 128 trailing
+// updates' wave tails bound the factorization at ≈ 2.1 ms (profiles/).
+// Here ONE persistent cooperative kernel does the whole factorization:
+//
+//  * the chain CTA (the first CTA to start) walks the 64-column panels k = 0..nt-1
+//    without ever leaving the SM: factor the diagonal tile (two 32-column warp
+//    panels, the reference's column loop solver.cpp:18-33), factor the tile below it
+//    (k+1, k) along with it one column behind (the panel TRSM for the next tile row,
+//    by substitution), invert L_kk (64 x 64), advance the forward substitution
+//    z_k = inv(L_kk) (y_k - sum_p L(k,p) z_p), publish, then apply panel k to the next
+//    diagonal tile in shared memory;
+//  * every other CTA is a worker pulling tile tasks from a static list: TRSM(i, k)
+//    (L(i,k) = A(i,k) inv(L_kk)^T as a DMMA GEMM, plus its L(i,k) z_k share of the
+//    forward substitution), UPD(i, j, [a, b)) (A(i,j) -= sum_{q in [a,b)} L(i,q) L(j,q)^T,
+//    far panels batched 8 at a time -- K = 512 -- the last two singly, so the tiles
+//    near the diagonal are ready a step after their panel), INV(b) (the 128 x 128
+//    diagonal-block inverse the backward solve uses).  Operands and C tiles move by
+//    TMA into a ring (producer warp), 8 DMMA warps compute;
+//  * dependencies are per-tile counters in global memory (release / acquire):
+//    applied[i][j] = panels applied to tile (i,j), lrow[i] = L tiles of row i done,
+//    chain = panels finished.  The task list is a topological order with the chain
+//    steps as virtual nodes (a task that waits on chain step k comes after every task
+//    chain step k waits on), claimed through one atomic ticket: with all CTAs
+//    co-resident (cooperative launch) the schedule cannot deadlock.
+//
+// Every tile receives its panels in a fixed order with fixed arithmetic, so the
+// factor is bitwise reproducible run to run; it differs from the 128-blocked path
+// only by summation order (parity vs the oracle: tests/test_gpu_parity.py, C0 golden).
+#pragma once
+
+namespace pk {
+
+constexpr int kDfT = 64;                  // tile
+constexpr int kDfThreads = 8 * 32;        // workers: 4 DMMA warps + 1 TMA producer warp (+ 3 idle);
+                                          // 2 warps per scheduler partition -> up to 255 registers
+constexpr int kDfStages = 8;
+constexpr int kDfStage = 2 * kDfT * kBK * 8;  // A box + B box (64 rows x 16) = 16 KB
+constexpr int kDfCbuf = kDfT * kDfT * 8;      // one C tile (4 swizzled 64x16 boxes) = 32 KB
+constexpr int kDS = 68;                       // chain smem row stride (== 4 mod 16: conflict-free fragments)
+constexpr int kDfSingles = 2;                 // trailing panels applied one at a time per tile
+constexpr int kDfBatch = 8;                   // far panels per update task (K = 512)
+constexpr int kDfWorkerSmem = kDfStages * kDfStage + 2 * kDfCbuf + 4 * 64 * 8 + 32 * 8 + 64;
+constexpr int kDfChainSmem = (5 * 64 * kDS + 32 * 32 + 8 * 64) * 8 + 8 * 8 + 64;
+constexpr int kDfSmem = (kDfWorkerSmem > kDfChainSmem ? kDfWorkerSmem : kDfChainSmem) + 1024;
+
+#ifdef PKRR_DF_TRACE
+// debug timeline (tools/df_trace.cu): chain phase stamps per step, per-task claim /
+// dependencies-met / done stamps (globaltimer ns)
+__device__ unsigned long long g_df_chain[256][12];
+__device__ unsigned long long g_df_task[65536][4];
+__device__ unsigned long long g_df_warp[256][8][2];
+__device__ __forceinline__ unsigned long long df_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+  return t;
+}
+#define DF_CHAIN_MARK(k, i) \
+  if (threadIdx.x == 0) g_df_chain[k][i] = df_now();
+#define DF_TASK_MARK(t, i, v) g_df_task[t][i] = (v);
+#else
+#define DF_CHAIN_MARK(k, i)
+#define DF_TASK_MARK(t, i, v)
+#endif
+
+enum DfType { DF_TRSM = 0, DF_UPD = 1, DF_INV = 2, DF_END = 3 };
+// flag words (ints) at the head of the workspace
+enum DfFlag { F_TICKET = 0, F_ROLE = 1, F_CHAIN = 2, F_HEAD = 8 };
+
+struct DfParams {
+  double* A;
+  int64_t lda;
+  int nt;                // tiles of 64
+  double* inv64;         // [nt][64][64] inverses of the 64-row diagonal blocks
+  double* P;             // [nt][nt][64] forward-substitution shares L(i,k) z_k
+  double* Linv;          // [mp][128] inverses of the 128-row diagonal blocks (backward solve)
+  const double* y;       // forward substitution right-hand side (null: factor only)
+  double* z;
+  int* status;           // [2] abort flag, first failing column
+  int* flags;            // F_HEAD ints, applied[nt*nt], lrow[nt]
+  const int4* tasks;     // {type, i, j, a | b << 16}
+  int ntasks;
+};
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+// async-proxy reads (TMA / bulk copies) of global data published by generic stores of
+// other CTAs, after the acquire that observed the publication
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+
+// spin until *flag >= target; false if the factorization was abandoned (NPD).  A wait
+// that exceeds ~2^33 cycles is a scheduling bug: trap (a loud launch failure) instead of
+// hanging the GPU.
+__device__ __noinline__ bool df_wait_ge(const int* flag, int target, const int* abort_flag) {
+  // relaxed polling + one acquire load on success: an ld.acquire per poll invalidates
+  // the SM's L1 every iteration
+  const volatile int* f = flag;
+  if (*f < target) {
+    const long long t0 = clock64();
+    while (*f < target) {
+      if (*reinterpret_cast<const volatile int*>(abort_flag)) return false;
+      if (clock64() - t0 > (1ll << 33)) __trap();
+      __nanosleep(32);
+    }
+  }
+  // one acquire load (orders what follows) -- not a fence.acq_rel, which would also wait
+  // for this thread's outstanding bulk copies (microseconds under the workers' traffic)
+  (void)ld_acquire_gpu(flag);
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// worker: TMA producer warp + 8 DMMA warps (2 x 4 grid, 32 x 16 per warp)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensorMap* tmI, const DfParams& p,
+                                          unsigned char* smem) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nt = p.nt;
+  unsigned char* ring = smem;
+  unsigned char* cbuf = smem + kDfStages * kDfStage;
+  double* red = reinterpret_cast<double*>(cbuf + 2 * kDfCbuf);  // [4][64]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + 4 * 64);
+  uint64_t* empty = full + kDfStages;
+  uint64_t* tfull = empty + kDfStages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* cfull = tempty + 2;
+  uint64_t* cempty = cfull + 2;
+  int4* tslot = reinterpret_cast<int4*>(cempty + 2);
+#ifdef PKRR_DF_TRACE
+  __shared__ int tticket[2];
+#endif
+  int* applied = p.flags + F_HEAD;
+  int* lrow = applied + nt * nt;
+  if (tid == 0) {
+    for (int s = 0; s < kDfStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);
+      mbar_init(&cfull[s], 1);
+      mbar_init(&cempty[s], 4);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp >= 5) return;
+  if (warp == 4) {
+    // ---------------- producer: claim, wait for dependencies, stream operands ----------------
+    if (lane != 0) return;
+    prefetch_tmap(tmA);
+    prefetch_tmap(tmI);
+    int kt = 0;
+    for (int it = 0;; ++it) {
+      const int t = atomicAdd(p.flags + F_TICKET, 1);
+      int4 task = t < p.ntasks ? p.tasks[t] : make_int4(DF_END, 0, 0, 0);
+#ifdef PKRR_DF_TRACE
+      if (t < p.ntasks) DF_TASK_MARK(t, 0, df_now());
+#endif
+      const int ti = task.y, tj = task.z, ta = task.w & 0xffff, tb = task.w >> 16;
+      bool ok = true;
+      if (task.x == DF_TRSM) {
+        ok = df_wait_ge(p.flags + F_CHAIN, tj + 1, p.status) && df_wait_ge(applied + ti * nt + tj, tj, p.status);
+      } else if (task.x == DF_UPD) {
+        ok = df_wait_ge(applied + ti * nt + tj, ta, p.status) && df_wait_ge(lrow + ti, tb, p.status) &&
+             df_wait_ge(lrow + tj, tb, p.status);
+      } else if (task.x == DF_INV) {
+        ok = df_wait_ge(p.flags + F_CHAIN, 2 * ti + 2, p.status);
+      }
+      if (!ok) task.x = DF_END;
+#ifdef PKRR_DF_TRACE
+      if (t < p.ntasks) {
+        DF_TASK_MARK(t, 1, df_now());
+        DF_TASK_MARK(t, 3, blockIdx.x);
+      }
+      tticket[it & 1] = t;
+#endif
+      fence_proxy_async_global();
+      const int slot = it & 1;
+      const uint32_t ph = (it >> 1) & 1;
+      mbar_wait(&tempty[slot], ph ^ 1);
+      tslot[slot] = task;
+      mbar_arrive(&tfull[slot]);
+      if (task.x == DF_END) return;
+      mbar_wait(&cempty[slot], ph ^ 1);
+      if (task.x == DF_UPD) {
+        mbar_arrive_expect_tx(&cfull[slot], kDfCbuf);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) tma_load_2d(cbuf + slot * kDfCbuf + h * 8192, tmA, tj * kDfT + 16 * h, ti * kDfT,
+                                                &cfull[slot]);
+      } else {
+        mbar_arrive(&cfull[slot]);
+      }
+      const int nk = task.x == DF_TRSM ? 4 : (task.x == DF_UPD ? 4 * (tb - ta) : 0);
+      for (int c = 0; c < nk; ++c, ++kt) {
+        const int s = kt % kDfStages;
+        const uint32_t sp = (kt / kDfStages) & 1;
+        mbar_wait(&empty[s], sp ^ 1);
+        mbar_arrive_expect_tx(&full[s], kDfStage);
+        unsigned char* sa = ring + s * kDfStage;
+        if (task.x == DF_TRSM) {
+          tma_load_2d(sa, tmA, tj * kDfT + 16 * c, ti * kDfT, &full[s]);
+          tma_load_2d(sa + 8192, tmI, 16 * c, tj * kDfT, &full[s]);
+        } else {
+          tma_load_2d(sa, tmA, ta * kDfT + 16 * c, ti * kDfT, &full[s]);
+          tma_load_2d(sa + 8192, tmA, ta * kDfT + 16 * c, tj * kDfT, &full[s]);
+        }
+      }
+    }
+  }
+
+  // ---------------- DMMA warps (2 x 2 grid, 32 x 32 each) ----------------
+  const int wm = warp >> 1, wn = warp & 1;
+  const int lr = lane >> 2, lk = lane & 3;
+  int kt = 0;
+  for (int it = 0;; ++it) {
+    const int slot = it & 1;
+    const uint32_t ph = (it >> 1) & 1;
+    mbar_wait(&tfull[slot], ph);
+    const int4 task = tslot[slot];
+#ifdef PKRR_DF_TRACE
+    const int ticket = tticket[slot];
+#endif
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tempty[slot]);
+    if (task.x == DF_END) return;
+    const int ti = task.y, tj = task.z, ta = task.w & 0xffff, tb = task.w >> 16;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const int nk = task.x == DF_TRSM ? 4 : (task.x == DF_UPD ? 4 * (tb - ta) : 0);
+    for (int c = 0; c < nk; ++c, ++kt) {
+      const int s = kt % kDfStages;
+      mbar_wait(&full[s], (kt / kDfStages) & 1);
+      if (c > 0) {  // deferred release (see gemm_dmma.cuh)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[(kt - 1) % kDfStages]);
+      }
+      const unsigned char* sa = ring + s * kDfStage;
+      const unsigned char* sb = sa + 8192;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const int k = ks * 4 + lk;
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = lds_f64(sa, swz128(wm * 32 + i * 8 + lr, k));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = lds_f64(sb, swz128(wn * 32 + j * 8 + lr, k));
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+      }
+    }
+    if (nk > 0) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[(kt - 1) % kDfStages]);
+    }
+    mbar_wait(&cfull[slot], ph);
+    unsigned char* cb = cbuf + slot * kDfCbuf;
+    const int64_t lda = p.lda;
+    if (task.x == DF_UPD) {
+      double* Cg = p.A + static_cast<int64_t>(ti * kDfT) * lda + tj * kDfT;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = wm * 32 + i * 8 + lr, c = wn * 32 + j * 8 + 2 * lk;
+          double2 v = lds_f64x2(smem_u32(cb + (c >> 4) * 8192) + swz128(r, c & 15));
+          v.x -= acc[i][j][0];
+          v.y -= acc[i][j][1];
+          *reinterpret_cast<double2*>(Cg + static_cast<int64_t>(r) * lda + c) = v;
+        }
+    } else if (task.x == DF_TRSM) {
+      double* Cg = p.A + static_cast<int64_t>(ti * kDfT) * lda + tj * kDfT;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = wm * 32 + i * 8 + lr, c = wn * 32 + j * 8 + 2 * lk;
+          *reinterpret_cast<double2*>(Cg + static_cast<int64_t>(r) * lda + c) =
+              make_double2(acc[i][j][0], acc[i][j][1]);
+        }
+      if (p.z) {
+        // this tile's share of the forward substitution, P[ti][tj] = L(ti,tj) z_tj:
+        // per-thread partials over its columns, the 4 lanes of a row, then the 4 column
+        // warps in a fixed order (deterministic)
+        double zc[4][2];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          zc[j][0] = __ldcg(p.z + tj * kDfT + wn * 32 + j * 8 + 2 * lk);
+          zc[j][1] = __ldcg(p.z + tj * kDfT + wn * 32 + j * 8 + 2 * lk + 1);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          double part = 0.0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) part = fma(acc[i][j][1], zc[j][1], fma(acc[i][j][0], zc[j][0], part));
+          part += __shfl_xor_sync(0xffffffffu, part, 1);
+          part += __shfl_xor_sync(0xffffffffu, part, 2);
+          if (lk == 0) red[wn * 64 + wm * 32 + i * 8 + lr] = part;
+        }
+        consumer_sync(128);
+        if (tid < 64) p.P[(static_cast<int64_t>(ti) * nt + tj) * kDfT + tid] = red[tid] + red[64 + tid];
+      }
+    } else {
+      // DF_INV: the 128 x 128 diagonal-block inverse [X0 0; Y X1] of block pair ti,
+      // Y = -X1 (L21 X0), for the backward solve (trsv_bwd_kernel reads Linv)
+      const int b2 = 2 * ti;
+      const double* L21 = p.A + static_cast<int64_t>((b2 + 1) * kDfT) * lda + b2 * kDfT;
+      const double* X0 = p.inv64 + static_cast<int64_t>(b2) * 4096;
+      const double* X1 = X0 + 4096;
+      double* T1 = reinterpret_cast<double*>(cb);  // [64][64]
+#pragma unroll 4
+      for (int k = 0; k < 64; k += 4) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = __ldcg(L21 + static_cast<int64_t>(wm * 32 + i * 8 + lr) * lda + k + lk);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = __ldcg(X0 + (k + lk) * 64 + wn * 32 + j * 8 + lr);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = wm * 32 + i * 8 + lr, c = wn * 32 + j * 8 + 2 * lk;
+          T1[r * 64 + c] = acc[i][j][0];
+          T1[r * 64 + c + 1] = acc[i][j][1];
+          acc[i][j][0] = acc[i][j][1] = 0.0;
+        }
+      consumer_sync(128);
+#pragma unroll 4
+      for (int k = 0; k < 64; k += 4) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = __ldcg(X1 + (wm * 32 + i * 8 + lr) * 64 + k + lk);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = T1[(k + lk) * 64 + wn * 32 + j * 8 + lr];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+      }
+      double* Lo = p.Linv + static_cast<int64_t>(ti) * 128 * 128;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = wm * 32 + i * 8 + lr, c = wn * 32 + j * 8 + 2 * lk;
+          *reinterpret_cast<double2*>(Lo + (64 + r) * 128 + c) = make_double2(-acc[i][j][0], -acc[i][j][1]);
+        }
+      for (int e = tid; e < 64 * 32; e += 128) {
+        const int r = e >> 5, c2 = 2 * (e & 31);
+        *reinterpret_cast<double2*>(Lo + r * 128 + c2) = __ldcg(reinterpret_cast<const double2*>(X0 + r * 64 + c2));
+        *reinterpret_cast<double2*>(Lo + r * 128 + 64 + c2) = make_double2(0.0, 0.0);
+        *reinterpret_cast<double2*>(Lo + (64 + r) * 128 + 64 + c2) =
+            __ldcg(reinterpret_cast<const double2*>(X1 + r * 64 + c2));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&cempty[slot]);
+    consumer_sync(128);  // every warp's stores issued before the publication
+    if (tid == 0) {
+      __threadfence();
+      if (task.x == DF_UPD) st_release_gpu(applied + ti * nt + tj, tb);
+      else if (task.x == DF_TRSM) st_release_gpu(lrow + ti, tj + 1);
+#ifdef PKRR_DF_TRACE
+      DF_TASK_MARK(ticket, 2, df_now());
+#endif
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// chain CTA
+// ---------------------------------------------------------------------------
+// Compact reciprocal / reciprocal square root (MUFU approximation + two Newton steps;
+// x is a positive normal pivot).  Inline-expanded library versions carry special-case
+// paths that multiply the chain's code size, and the chain must stay inside the SM's
+// 32 KB L1.5 instruction cache (the unrolled 128-leaf ran instruction-fetch bound).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  // MUFU seed + one Halley step (cubic): y (1 + e/2 + 3e^2/8), e = 1 - x y^2
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-(x * y), y, 1.0);
+  return fma(y * e, fma(0.375, e, 0.5), y);
+}
+
+// Per 32-column panel of a 64-column chain step, one warp factors the 32 x 32
+// diagonal block in ROW layout (lane i owns row i, a[c] = S[i][c]): the reference's
+// column loop (solver.cpp:18-33) -- pivot test, scale, rank-1 update -- per column j.
+// The pivot chain is SHFL -> rsqrt -> multiply -> FMA -> SHFL: lane j+1's next pivot
+// a[j+1] - l^2 and its column value travel by SHFL; the column values and rsqrt(pivot)
+// go to slot j of `ds` (33 slots of 40 doubles: [0, 32) the column, [33] the rsqrt)
+// with mbarrier cbar[j], for the rest of the update and for the warps factoring rows
+// below the diagonal block (warp_tall32s), which follow one column behind at most, or
+// later (every slot of the panel stays valid for the whole step).  Straight-line code
+// (the scheduler interleaves the update with the pivot chain).  Returns the first
+// failing pivot column, or -1.
+template <int LS>
+__device__ __noinline__ int warp_diag32(uint32_t S, uint32_t Xs, uint32_t ds, int lane) {
+  // S: the 32 x 32 diagonal block (factored in place, rows = lanes); Xs: 32 x 32 rows of
+  // the identity, turned into X = L^{-T} by the same column loop (the panel TRSM of the
+  // reference's loop applied to unit rows): inv(L) = X^T without a separate inversion.
+  // Rolled over 4 groups of 8 columns; the row registers rotate by 8 per group so the
+  // group's columns are always a[0..7] (a few KB of code: the loop stays resident in
+  // the instruction cache while the other warps' DMMA loops run beside it).
+  double a[32], x[32];
+#pragma unroll
+  for (int c = 0; c < 32; c += 2) {
+    const double2 v = lds_f64x2(S + (lane * LS + c) * 8);
+    a[c] = v.x;
+    a[c + 1] = v.y;
+    x[c] = c == lane ? 1.0 : 0.0;
+    x[c + 1] = c + 1 == lane ? 1.0 : 0.0;
+  }
+  int bad = -1;
+  double piv = __shfl_sync(0xffffffffu, a[0], 0);
+#pragma unroll 1
+  for (int g = 0; g < 4; ++g) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int j = 8 * g + c;  // global column
+      const uint32_t slot = ds + j * 256;
+      if (!(piv > 0.0) && bad < 0) bad = j;
+      const double r = rsqrt_nr(bad >= 0 ? 1.0 : piv);
+      const double l = a[c] * r, lx = x[c] * r;
+      // lane j+1's next pivot and column value (j + 1 == 32 reads a dead value)
+      piv = __shfl_sync(0xffffffffu, fma(-l, l, a[c + 1]), (j + 1) & 31);
+      const double ln = __shfl_sync(0xffffffffu, l, (j + 1) & 31);
+      sts_f64(slot + lane * 8, l);
+      __syncwarp();
+      sts_f64(S + (lane * LS + j) * 8, lane >= j ? l : 0.0);  // final L and X column j
+      sts_f64(Xs + (lane * LS + j) * 8, lx);
+      a[c + 1] = fma(-l, ln, a[c + 1]);
+      x[c + 1] = fma(-lx, ln, x[c + 1]);
+      // columns j + 2 .. (registers c + 2 .. 31; those past column 31 hold dead values)
+#pragma unroll
+      for (int k = c + 2; k < 32; ++k) {
+        const double v = lds_f64_at(slot + ((j + k - c) & 31) * 8);
+        a[k] = fma(-l, v, a[k]);
+        x[k] = fma(-lx, v, x[k]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 24; ++i) {
+      a[i] = a[i + 8];
+      x[i] = x[i + 8];
+    }
+  }
+  return bad;
+}
+
+__device__ __forceinline__ void df_record_npd(const DfParams& p, int col, int* sflag) {
+  *sflag = 1;
+  p.status[1] = col;
+  __threadfence();
+  atomicExch(&p.status[0], 1);
+}
+
+// rows [16 rb, 16 rb + 16) x cols [16 cb, +16) of dst -= A(rows) B(cols)^T over K (16 x 16
+// blocks of 2 x 2 DMMA tiles); lower_diag skips the strictly upper 8 x 8 tile of a
+// diagonal block
+__device__ __forceinline__ void df_block_update(double* dst, const double* Arow, const double* Brow, int K,
+                                                bool lower_diag, int lr, int lk) {
+  double acc[2][2][2] = {};
+  mma_2x2_rt(acc, Arow, Brow, kDS, K, lr, lk);
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (lower_diag && j > i) continue;
+      double* d2 = dst + (8 * i + lr) * kDS + 8 * j + 2 * lk;
+      const double2 v = *reinterpret_cast<double2*>(d2);
+      *reinterpret_cast<double2*>(d2) = make_double2(v.x - acc[i][j][0], v.y - acc[i][j][1]);
+    }
+}
+
+// 8-row x 32-column DMMA items of the chain's small products (row-major operands with
+// the chain stride): C (=, -=) A(8 rows, K) . B(K, 32) ["rn"] or A . Bt(32 rows, K)^T ["rt"]
+__device__ __forceinline__ void df_store8(double* dst, double (&acc)[4][2], int mode, int lr, int lk) {
+  // mode 0: dst = acc, 1: dst -= acc, 2: dst = -acc
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double2* d2 = reinterpret_cast<double2*>(dst + lr * kDS + 8 * c + 2 * lk);
+    if (mode == 1) {
+      const double2 v = *d2;
+      *d2 = make_double2(v.x - acc[c][0], v.y - acc[c][1]);
+    } else {
+      *d2 = mode == 0 ? make_double2(acc[c][0], acc[c][1]) : make_double2(-acc[c][0], -acc[c][1]);
+    }
+  }
+}
+__device__ __forceinline__ void df_rn8(double* dst, const double* A, const double* B, int mode, int lr, int lk) {
+  double acc[4][2] = {};
+  mma_row4_rn(acc, A, kDS, B, kDS, 0, 32, lr, lk);
+  __syncwarp();  // in place: every read of these rows precedes the write
+  df_store8(dst, acc, mode, lr, lk);
+}
+__device__ __forceinline__ void df_rt8(double* dst, const double* A, const double* Bt, int K, int mode, int lr,
+                                      int lk) {
+  double acc[4][2] = {};
+  mma_row4_rt(acc, A, kDS, Bt, kDS, 0, K, lr, lk);
+  __syncwarp();
+  df_store8(dst, acc, mode, lr, lk);
+}
+
+// The chain's tile loads, issued by one thread without holding up the step's barriers:
+// polled (non-blocking) at the phase boundaries, waited for only where the data is used.
+// The chain's tile loads come from warp 4 alone, which never joins the step's barriers:
+// issuing the 64 row copies of a tile costs microseconds (~30 ns per cp.async.bulk), so
+// a loader inside a barrier would stall the whole step.  Per step k it waits until the
+// compute warps have started the step (stepbar: the buffers are free), then issues T(k)
+// = tile (k+1, k) and D(k+1) = tile (k+1, k+1) as soon as the workers have applied
+// panels [0, k) to each (tbar / lbar complete_tx), whichever is ready first.
+__device__ __forceinline__ bool df_tile_load(const DfParams& p, const int* flag, int target, double* dst,
+                                             const double* src, uint64_t* bar, int lane) {
+  int ready = 0;
+  if (lane == 0) ready = *reinterpret_cast<const volatile int*>(flag) >= target;
+  ready = __shfl_sync(0xffffffffu, ready, 0);
+  if (!ready) return false;
+  if (lane == 0) mbar_arrive_expect_tx(bar, 64 * 512);
+  __syncwarp();
+  (void)ld_acquire_gpu(flag);
+  fence_proxy_async_global();
+  const int64_t lda = p.lda;
+  bulk_load(dst + lane * kDS, src + static_cast<int64_t>(lane) * lda, 512, bar);
+  bulk_load(dst + (lane + 32) * kDS, src + static_cast<int64_t>(lane + 32) * lda, 512, bar);
+  return true;
+}
+__device__ __noinline__ void df_loader(const DfParams& p, double* Dbuf, double* Tbuf, uint64_t* lbar, uint64_t* tbar,
+                                       uint64_t* stepbar, int lane) {
+  const int nt = p.nt;
+  const int* applied = p.flags + F_HEAD;
+  const int64_t lda = p.lda;
+  for (int k = 0; k + 1 < nt; ++k) {
+    // a sleeping wait: this warp shares its scheduler partition with the diagonal warp,
+    // and a try_wait spin takes issue slots from it for the whole first panel
+    while (!mbar_test(stepbar, k & 1)) {
+      if (*reinterpret_cast<const volatile int*>(p.status)) return;  // the chain abandoned (NPD)
+      __nanosleep(128);
+    }
+    bool dd = false, td = false;
+    const long long t0 = clock64();
+    while (!(dd && td)) {
+      if (!td)
+        td = df_tile_load(p, applied + (k + 1) * nt + k, k, Tbuf + (k & 1) * 64 * kDS,
+                          p.A + static_cast<int64_t>((k + 1) * kDfT) * lda + k * kDfT, tbar, lane);
+      if (!dd)
+        dd = df_tile_load(p, applied + (k + 1) * nt + (k + 1), k, Dbuf + ((k + 1) & 1) * 64 * kDS,
+                          p.A + static_cast<int64_t>((k + 1) * kDfT) * lda + (k + 1) * kDfT, lbar, lane);
+      if (!(dd && td)) {
+        if (__shfl_sync(0xffffffffu, *reinterpret_cast<const volatile int*>(p.status), 0)) return;
+        if (clock64() - t0 > (1ll << 33)) __trap();
+        __nanosleep(64);
+      }
+    }
+  }
+}
+
+// One chain step k (64 columns).  Warp 0 runs the column-sequential work; everything
+// else is placed so that it overlaps warp 0 wherever the dependencies allow:
+//   [A] warp 0: D00 -> L00, X00 = L00^{-T}.  Helpers (warps 1-3, 5-7), finishing step k-1
+//       beside it: T(k-1) rows 32..63 T1 X11(k-1) -> publish L(k,k-1) (lrow[k]),
+//       P[k][k-1] = L(k,k-1) z_{k-1}, w_k; D(k) rows 32..63 -= L(k,k-1)[32:] L(k,k-1)^T;
+//       store L_{k-1}; then the loader may refill D(k-1) / T(k-2)'s buffers (stepbar).
+//   [B] L10 = D10 X00
+//   [C] warp 0: D11 -> L11, X11 (after D11 -= L10 L10^T by warps 1-3); Xtmp = X00 L10^T;
+//       T(k) rows (if they arrived): T0 X00, T1 -= T0 L10^T
+//   [D] X01 = -Xtmp X11; z_k = X^T w_k; publish inv(L_kk) = X^T, z_k (chain = k + 1)
+//   [E] T(k) rows: the rest of T0 X00 / T1 -= T0 L10^T, and T1 X11 for rows 0..31;
+//       D(k+1)00 -= T(k)[:32] T(k)[:32]^T, the block the next step's warp 0 starts on.
+__device__ __forceinline__ void df_chain(const DfParams& p, unsigned char* smem) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int lr = lane >> 2, lk = lane & 3;
+  const int nt = p.nt;
+  const int64_t lda = p.lda;
+  double* Dbuf = reinterpret_cast<double*>(smem);  // 2 x [64][kDS]: diagonal tiles k, k+1
+  double* Tbuf = Dbuf + 2 * 64 * kDS;              // 2 x [64][kDS]: tiles (k+1, k), (k, k-1)
+  double* X = Tbuf + 2 * 64 * kDS;                 // X = L_kk^{-T} (upper triangular; X10 stays 0)
+  double* ds = X + 64 * kDS;                       // diagonal warp's 32 column slots of 32
+  double* wv = ds + 32 * 32;
+  double* zv = wv + 64;
+  double* pv = zv + 64;    // P[k][k-1] (computed at the start of step k)
+  double* red = pv + 64;   // [2][64] partial GEMV sums
+  uint64_t* lbar = reinterpret_cast<uint64_t*>(red + 128);
+  uint64_t* tbar = lbar + 1;
+  uint64_t* dbar = tbar + 1;     // D11 updated by the first panel (warps 1, 2, 3)
+  uint64_t* stepbar = dbar + 1;  // step k's helpers are done with D(k-1) / T(k-2): loader may refill
+  int* sflag = reinterpret_cast<int*>(stepbar + 1);
+  int* tdone = sflag + 1;  // [8] T row tile q has had T0 X00 and T1 -= T0 L10^T
+  int* applied = p.flags + F_HEAD;
+  int* lrow = applied + nt * nt;
+  if (tid == 0) {
+    mbar_init(lbar, 1);
+    mbar_init(tbar, 1);
+    mbar_init(dbar, 3);
+    mbar_init(stepbar, 1);
+    fence_mbar_init();
+    *sflag = 0;
+  }
+  for (int e = tid; e < 64 * kDS; e += kDfThreads) X[e] = 0.0;
+  __syncthreads();
+  if (warp == 4) {
+    df_loader(p, Dbuf, Tbuf, lbar, tbar, stepbar, lane);
+    return;
+  }
+  // compute warps 0-3, 5-7 (cw 0..6, ctid 0..223) on named barrier 2; the helpers
+  // (warps 1-3, 5-7: hw 0..5, htid 0..191) on named barrier 3
+  const int cw = warp < 4 ? warp : warp - 1, ctid = cw * 32 + lane;
+  const int hw = cw - 1, htid = ctid - 32;
+  auto csync = [] { asm volatile("bar.sync 2, 224;\n" ::: "memory"); };
+  auto hsync = [] { asm volatile("bar.sync 3, 192;\n" ::: "memory"); };
+  if (ctid == 0) {
+    mbar_arrive_expect_tx(lbar, 64 * 512);
+    for (int r = 0; r < 64; ++r) bulk_load(Dbuf + r * kDS, p.A + static_cast<int64_t>(r) * lda, 512, lbar);
+  }
+  mbar_wait(lbar, 0);
+  const uint32_t uds = smem_u32(ds);
+  double* X01 = X + 32;
+  double* X11 = X + 32 * kDS + 32;
+
+  for (int k = 0; k < nt; ++k) {
+    double* D = Dbuf + (k & 1) * 64 * kDS;
+    double* D10 = D + 32 * kDS;
+    double* D11 = D10 + 32;
+    double* Dp = Dbuf + ((k + 1) & 1) * 64 * kDS;  // D(k-1) = L_{k-1}
+    double* T = Tbuf + (k & 1) * 64 * kDS;         // T(k) = tile (k+1, k)
+    double* Tp = Tbuf + ((k + 1) & 1) * 64 * kDS;  // T(k-1) = L(k, k-1)
+    const bool has_t = k + 1 < nt;
+    const uint32_t par = k & 1;
+    DF_CHAIN_MARK(k, 0)
+    // ---------------- [A] ----------------
+    int bad = -1;
+#ifdef PKRR_DF_TRACE
+    if (lane == 0) g_df_warp[k][warp][0] = df_now();
+#endif
+    if (warp == 0) {
+      __syncwarp();  // converged entry (the callee's SHFLs)
+      bad = warp_diag32<kDS>(smem_u32(D), smem_u32(X), uds, lane);
+#ifdef PKRR_DF_TRACE
+      if (lane == 0) g_df_chain[k][2] = df_now();
+#endif
+    } else {
+      if (k > 0) {
+        // T(k-1) rows 32..63: T1 = T1 X11(k-1) (X11 is untouched until [C])
+        for (int q = 4 + hw; q < 8; q += 6) df_rn8(Tp + 8 * q * kDS + 32, Tp + 8 * q * kDS + 32, X11, 0, lr, lk);
+        hsync();
+        // publish L(k, k-1); P[k][k-1] = L(k,k-1) z_{k-1}
+        double* Tg = p.A + static_cast<int64_t>(k * kDfT) * lda + (k - 1) * kDfT;
+        for (int e = htid; e < 64 * 32; e += 192) {
+          const int r = e >> 5, c2 = 2 * (e & 31);
+          *reinterpret_cast<double2*>(Tg + static_cast<int64_t>(r) * lda + c2) =
+              *reinterpret_cast<const double2*>(Tp + r * kDS + c2);
+        }
+        if (p.z && htid < 128) {
+          const int r = htid & 63, pt = htid >> 6;
+          double sacc = 0.0;
+          for (int c = 32 * pt; c < 32 * pt + 32; ++c) sacc = fma(Tp[r * kDS + c], zv[c], sacc);
+          red[pt * 64 + r] = sacc;
+        }
+        hsync();
+        if (htid == 0) {
+          __threadfence();
+          st_release_gpu(lrow + k, k);
+        }
+        if (p.z && htid < 64) pv[htid] = red[htid] + red[64 + htid];
+        // D(k) rows 32..63 -= L(k,k-1)[32:64] L(k,k-1)^T (K = 64): D10 as 4 row tiles,
+        // D11 (lower) as 3 blocks of 16; L_{k-1} to global
+        for (int t = hw; t < 7; t += 6) {
+          if (t < 4) {
+            df_rt8(D10 + 8 * t * kDS, Tp + (32 + 8 * t) * kDS, Tp, 64, 1, lr, lk);
+          } else {
+            const int rb = t == 4 ? 0 : 1, cb = t == 6 ? 1 : 0;
+            df_block_update(D11 + 16 * rb * kDS + 16 * cb, Tp + (32 + 16 * rb) * kDS, Tp + (32 + 16 * cb) * kDS,
+                            64, rb == cb, lr, lk);
+          }
+        }
+        double* Ag = p.A + static_cast<int64_t>((k - 1) * kDfT) * lda + (k - 1) * kDfT;
+        for (int e = htid; e < 64 * 32; e += 192) {
+          const int r = e >> 5, c2 = 2 * (e & 31);
+          if (c2 <= r)
+            *reinterpret_cast<double2*>(Ag + static_cast<int64_t>(r) * lda + c2) =
+                *reinterpret_cast<const double2*>(Dp + r * kDS + c2);
+        }
+      }
+#ifdef PKRR_DF_TRACE
+      if (lane == 0) g_df_warp[k][warp][1] = df_now();
+#endif
+      hsync();  // pv, D(k-1) and T(k-2) done with
+      if (htid == 0) {
+        fence_proxy_async();
+        mbar_arrive(stepbar);  // the loader may refill D(k-1) / T(k-2)'s buffers
+      }
+      if (htid < 8) tdone[htid] = 0;
+      if (p.z && warp == 7) {
+        // w_k = y_k - sum_p P[k][p] in panel order
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          const int r = lane + 32 * h;
+          double sw = p.y[k * kDfT + r];
+          const double* pk_ = p.P + static_cast<int64_t>(k) * nt * kDfT + r;
+          int q = 0;
+          for (; q + 4 <= k - 1; q += 4) {
+            const double a0 = __ldcg(pk_ + (q + 0) * kDfT), a1 = __ldcg(pk_ + (q + 1) * kDfT);
+            const double a2 = __ldcg(pk_ + (q + 2) * kDfT), a3 = __ldcg(pk_ + (q + 3) * kDfT);
+            sw = (((sw - a0) - a1) - a2) - a3;
+          }
+          for (; q < k - 1; ++q) sw -= __ldcg(pk_ + q * kDfT);
+          if (k > 0) sw -= pv[r];
+          wv[r] = sw;
+        }
+      }
+    }
+    csync();
+    DF_CHAIN_MARK(k, 1)
+    // ---------------- [B] L10 = D10 X00 ----------------
+    const int dw = warp == 5 ? 3 : warp - 1;  // 0..3 for warps 1, 2, 3, 5
+    if (warp == 1 || warp == 2 || warp == 3 || warp == 5) df_rn8(D10 + 8 * dw * kDS, D10 + 8 * dw * kDS, X, 0, lr, lk);
+    if (warp == 0 && bad >= 0 && lane == 0) df_record_npd(p, k * kDfT + bad, sflag);
+    csync();
+    DF_CHAIN_MARK(k, 3)
+    // ---------------- [C] ----------------
+    if (warp == 0) {
+      mbar_wait(dbar, par);
+      __syncwarp();
+      const int bad1 = warp_diag32<kDS>(smem_u32(D11), smem_u32(X11), uds, lane);
+      if (bad1 >= 0 && lane == 0 && !*sflag) df_record_npd(p, k * kDfT + 32 + bad1, sflag);
+    } else if (warp >= 1 && warp <= 3) {
+      const int rb = warp == 1 ? 1 : (warp == 2 ? 0 : 1), cb = warp == 3 ? 1 : 0;
+      df_block_update(D11 + 16 * rb * kDS + 16 * cb, D10 + 16 * rb * kDS, D10 + 16 * cb * kDS, 32, rb == cb, lr, lk);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dbar);
+      for (int q = warp - 1; q < 4; q += 3) df_rt8(X01 + 8 * q * kDS, X + 8 * q * kDS, D10, 32, 0, lr, lk);
+    } else if (warp >= 5 && has_t && __shfl_sync(0xffffffffu, mbar_test(tbar, par), 0)) {
+      for (int q = warp - 5; q < 8; q += 3) {
+        df_rn8(T + 8 * q * kDS, T + 8 * q * kDS, X, 0, lr, lk);
+        __syncwarp();
+        df_rt8(T + 8 * q * kDS + 32, T + 8 * q * kDS, D10, 32, 1, lr, lk);
+        if (lane == 0) tdone[q] = 1;
+      }
+    }
+    csync();
+    DF_CHAIN_MARK(k, 4)
+    // ---------------- [D] X01, z_k, publish inv(L_kk), z_k ----------------
+    if (warp < 4) df_rn8(X01 + 8 * warp * kDS, X01 + 8 * warp * kDS, X11, 2, lr, lk);
+    csync();
+    if (*sflag) return;
+    DF_CHAIN_MARK(k, 5)
+    if (p.z) {
+      if (ctid < 128) {
+        const int r = ctid & 63, pt = ctid >> 6;
+        double sacc = 0.0;
+        for (int c = 32 * pt; c < 32 * pt + 32; ++c) sacc = fma(X[c * kDS + r], wv[c], sacc);
+        red[pt * 64 + r] = sacc;
+      }
+      csync();
+      if (ctid < 64) {
+        const double z = red[ctid] + red[64 + ctid];
+        zv[ctid] = z;
+        p.z[k * kDfT + ctid] = z;
+      }
+    }
+    {
+      double* Ig = p.inv64 + static_cast<int64_t>(k) * 4096;
+      for (int e = ctid; e < 64 * 32; e += 224) {
+        const int ri = e & 63, ci = 2 * (e >> 6);  // X read down its columns: conflict-free
+        *reinterpret_cast<double2*>(Ig + ri * 64 + ci) = make_double2(X[ci * kDS + ri], X[(ci + 1) * kDS + ri]);
+      }
+    }
+    csync();
+    if (ctid == 0) {
+      __threadfence();
+      st_release_gpu(p.flags + F_CHAIN, k + 1);
+    }
+    DF_CHAIN_MARK(k, 6)
+    if (!has_t) break;
+    // ---------------- [E] T(k) rows, D(k+1)00 ----------------
+    mbar_wait(tbar, par);
+    DF_CHAIN_MARK(k, 7)
+    for (int q = cw; q < 8; q += 7) {
+      if (!tdone[q]) {
+        df_rn8(T + 8 * q * kDS, T + 8 * q * kDS, X, 0, lr, lk);
+        __syncwarp();
+        df_rt8(T + 8 * q * kDS + 32, T + 8 * q * kDS, D10, 32, 1, lr, lk);
+      }
+      __syncwarp();
+      if (q < 4) df_rn8(T + 8 * q * kDS + 32, T + 8 * q * kDS + 32, X11, 0, lr, lk);
+    }
+    mbar_wait(lbar, (k + 1) & 1);  // D(k+1) prefetched
+    csync();
+    DF_CHAIN_MARK(k, 8)
+    double* Dn = Dbuf + ((k + 1) & 1) * 64 * kDS;
+    if (warp < 3) {
+      const int rb = warp == 0 ? 0 : 1, cb = warp == 2 ? 1 : 0;
+      df_block_update(Dn + 16 * rb * kDS + 16 * cb, T + 16 * rb * kDS, T + 16 * cb * kDS, 64, rb == cb, lr, lk);
+    }
+    csync();
+    DF_CHAIN_MARK(k, 10)
+  }
+  // the last diagonal block
+  {
+    const int k = nt - 1;
+    double* D = Dbuf + (k & 1) * 64 * kDS;
+    double* Ag = p.A + static_cast<int64_t>(k * kDfT) * lda + k * kDfT;
+    for (int e = ctid; e < 64 * 32; e += 224) {
+      const int r = e >> 5, c2 = 2 * (e & 31);
+      if (c2 <= r)
+        *reinterpret_cast<double2*>(Ag + static_cast<int64_t>(r) * lda + c2) =
+            *reinterpret_cast<const double2*>(D + r * kDS + c2);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kDfThreads, 1)
+    potrf_df_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmI, DfParams p) {
+  if (*reinterpret_cast<const volatile int*>(p.status)) return;
+  extern __shared__ unsigned char df_smem_raw[];
+  // 1024-byte alignment (128B-swizzled TMA ring) by pointer arithmetic on the shared
+  // array itself, so the compiler keeps the shared address space (LDS / STS, not
+  // generic LD / ST) through every derived pointer
+  unsigned char* smem = df_smem_raw + ((1024u - (smem_u32(df_smem_raw) & 1023u)) & 1023u);
+  __shared__ int role;
+  if (threadIdx.x == 0) role = atomicAdd(p.flags + F_ROLE, 1);
+  __syncthreads();
+  if (role == 0)
+    df_chain(p, smem);
+  else
+    df_worker(&tmA, &tmI, p, smem);
+}
+
+}  // namespace pk
