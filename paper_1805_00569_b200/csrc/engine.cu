@@ -2092,6 +2092,21 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
     hmark("batch enqueued");
   }
   pk::shadow_report();
+  // one GPU: every cell's combine + reference-order MSE goes on the stream now, behind
+  // the parts, so the host reads statuses, residuals and MSEs after a single sync (the
+  // failed cells are masked on the host afterwards) instead of a sync -> launch -> sync
+  // round trip at the end of the call
+  double *comb = nullptr, *dmse = nullptr, *comb_e = nullptr, *dmse_e = nullptr;
+  if (world == 1) {
+    comb = sc.alloc<double>(ncell * t);
+    dmse = sc.alloc<double>(ncell);
+    pk::launch_combine_cells(pred_t, pp_parts, t, ncell, predictor, dyt, comb, dmse, s, ctx->counter);
+    if (te) {
+      comb_e = sc.alloc<double>(ncell * te);
+      dmse_e = sc.alloc<double>(ncell);
+      pk::launch_combine_cells(pred_e, pp_parts, te, ncell, predictor, dye, comb_e, dmse_e, s, ctx->counter);
+    }
+  }
   ck(cudaEventRecord(t_all.b, s), "event");
   ck(cudaDeviceSynchronize(), "grid");
 
@@ -2196,14 +2211,21 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
         const double r = rs[(c * p + q) * 4 + 0];
         if (!pfail[c * p + q] && r > cres[c]) cres[c] = r;
       }
-    std::vector<double> cmse, cemse;
-    o->best_index = combine_cells(ctx, sc, predictor, pp_parts, t, ncell, pred_t, dyt, cfail, cmse, o->best_pred);
+    // best = first strict minimum over the non-failed cells (strategies.cpp:499-505)
+    std::vector<double> cmse = to_host(dmse, ncell, s), cemse;
+    int64_t best = -1;
+    for (int64_t c = 0; c < ncell; ++c) {
+      if (cfail[c]) {
+        cmse[c] = std::numeric_limits<double>::quiet_NaN();
+        continue;
+      }
+      if (best < 0 || cmse[c] < cmse[best]) best = c;
+    }
+    o->best_index = best;
+    if (best >= 0 && o->best_pred) copy_out(o->best_pred, comb + best * t, t, s);
     if (te) {
       // the eval set's predictions of the cell chosen on the selection set
-        double* comb_e = sc.alloc<double>(ncell * te);
-      double* dm = sc.alloc<double>(ncell);
-      pk::launch_combine_cells(pred_e, pp_parts, te, ncell, predictor, dye, comb_e, dm, s, ctx->counter);
-      cemse = to_host(dm, ncell, s);
+      cemse = to_host(dmse_e, ncell, s);
       for (int64_t c = 0; c < ncell; ++c)
         if (cfail[c]) cemse[c] = std::numeric_limits<double>::quiet_NaN();
       if (o->best_index >= 0 && o->best_eval_pred) copy_out(o->best_eval_pred, comb_e + o->best_index * te, te, s);
