@@ -719,7 +719,14 @@ std::vector<int4> df_build_tasks(int nt) {
       if (e <= 0) continue;
       const int s0 = std::max(0, e - kDfSingles);
       std::vector<std::pair<int, int>> rng;
-      for (int a = 0; a < s0; a += kDfBatch) rng.push_back({a, std::min(a + kDfBatch, s0)});
+      // batch boundaries staggered per tile: aligned ones made every far tile's batch
+      // come due on the same step (multiples of 8), queueing ~1000 K = 512 tasks ahead
+      // of the single updates that step's chain work needed
+      for (int a = 0; a < s0;) {
+        const int len = a == 0 ? 1 + (i + j) % kDfBatch : kDfBatch;
+        rng.push_back({a, std::min(a + len, s0)});
+        a += len;
+      }
       for (int q = s0; q < e; ++q) rng.push_back({q, q + 1});
       for (auto& r : rng) items[i * nt + j].push_back(add(DF_UPD, i, j, r.first, r.second, r.second - 1));
     }
