@@ -57,6 +57,8 @@ int main(int argc, char** argv) {
   static unsigned long long ch[256][12];
   static unsigned long long tk[65536][4];
   cudaMemcpyFromSymbol(ch, pk::g_df_chain, sizeof(ch));
+  for (int k = 0; k < 256; ++k)
+    for (int i = 0; i < 12; ++i) ch[k][i] = (unsigned long long)(ch[k][i] / 1.965);  // cycles -> ns
   cudaMemcpyFromSymbol(tk, pk::g_df_task, sizeof(tk));
   const unsigned long long t0 = ch[0][0];
   const char* names[] = {"start", "T ready", "diag0 done", "sub0", "syrk", "sub1", "inv", "fwd", "publish",
@@ -97,14 +99,20 @@ int main(int argc, char** argv) {
   printf("tasks %zu, span %.1f us, worker busy %.1f%%, mean dep wait %.2f us, mean task %.2f us\n", tasks.size(),
          (tend - t0) / 1e3, 100.0 * busy / (147.0 * (tend - t0)), wait / tasks.size() / 1e3,
          busy / tasks.size() / 1e3);
-  static unsigned long long wt[256][8][2];
+  static unsigned long long wt[256][8][8];
   cudaMemcpyFromSymbol(wt, pk::g_df_warp, sizeof(wt));
-  for (int k = 8; k < 12; ++k) {
-    printf("[A] step %d (us after step start):", k);
+  for (int k = 0; k < 256; ++k)
     for (int w = 0; w < 8; ++w)
-      printf(" w%d %.2f-%.2f", w, ((long long)wt[k][w][0] - (long long)ch[k][0]) / 1e3,
-             ((long long)wt[k][w][1] - (long long)ch[k][0]) / 1e3);
-    printf("  diag done %.2f\n", ((long long)ch[k][2] - (long long)ch[k][0]) / 1e3);
+      for (int i = 0; i < 8; ++i) wt[k][w][i] = (unsigned long long)(wt[k][w][i] / 1.965);
+  for (int k = 8; k < 11; ++k) {
+    const long long c0 = (long long)ch[k][0];
+    printf("step %d marks A %.2f B %.2f C %.2f D %.2f\n", k, ((long long)ch[k][1] - c0) / 1e3,
+           ((long long)ch[k][3] - c0) / 1e3, ((long long)ch[k][4] - c0) / 1e3, ((long long)ch[k][5] - c0) / 1e3);
+    for (int w = 0; w < 8; ++w)
+      printf("   w%d: A-start %.2f A-hsync %.2f B-done %.2f C-done %.2f D-done %.2f\n", w,
+             ((long long)wt[k][w][0] - c0) / 1e3, ((long long)wt[k][w][1] - c0) / 1e3,
+             ((long long)wt[k][w][2] - c0) / 1e3, ((long long)wt[k][w][3] - c0) / 1e3,
+             ((long long)wt[k][w][4] - c0) / 1e3);
   }
   if (argc > 2) {
     FILE* f = fopen(argv[2], "w");
