@@ -645,6 +645,11 @@ struct Timer {
   }
 };
 
+bool df_gram_fused() {
+  static const bool on = std::getenv("PKRR_DF_GRAM") && std::atoi(std::getenv("PKRR_DF_GRAM")) != 0;
+  return on;
+}
+
 double chol_flops(int64_t m) {
   const double mu = static_cast<double>(m);
   return mu * (mu + 1) * (2 * mu + 1) / 6.0;
@@ -2026,8 +2031,12 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
         const double m = static_cast<double>(pb.m);
         if (res_done[q]) ck(cudaStreamWaitEvent(ws, res_done[q], 0), "wait");  // K is rewritten
         cudaEvent_t g0 = ev_on(ws);
-        pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws, ctx->counter,
-                            false);
+        // PKRR_DF_GRAM=1: a lone system on the dataflow path forms K and A inside its
+        // factorization (first lambda of each sigma; pk::GramFuse) -- measured slower
+        // than the gram + assemble kernels at C0 (DF kernel +270 us vs 145 us saved)
+        if (!(p == 1 && df_gram_fused() && pk::potrf_df_eligible(pb.mp, true)))
+          pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws, ctx->counter,
+                              false);
         f_gram += static_cast<double>(d) * m * (m + 1);
         gram_iv.push_back({g0, ev_on(ws)});
         if (si == 0) part_ev[q][0] = g0, part_ev[q][1] = gram_iv.back().b;
@@ -2043,11 +2052,14 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
           int* st = dstatus + (cell * p + q) * 2;
           double* rs = dres + (cell * p + q) * 4;
           cudaEvent_t c0 = ev_on(ws);
-          pk::launch_assemble(pb.K, pb.A, pb.mp, shift, st, ws, ctx->counter, true);
+          const bool gram_fused = li == 0 && p == 1 && df_gram_fused() && pk::potrf_df_eligible(pb.mp, true);
+          const pk::GramFuse gf{pb.tmX, pb.norms, pb.K, pb.dp, pb.m, sigma, shift};
+          if (!gram_fused) pk::launch_assemble(pb.K, pb.A, pb.mp, shift, st, ws, ctx->counter, true);
           const pk::FwdSolve fs{pb.yp, pb.w, pb.z};
           // rank-independent schedule (p == 1): the same at any world size
           const bool fused = pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, st, ws, ctx->counter,
-                                              pb.slices, pb.exps, look_streams[sidx[q]], p == 1, &fs);
+                                              pb.slices, pb.exps, look_streams[sidx[q]], p == 1, &fs,
+                                              gram_fused ? &gf : nullptr);
           cudaEvent_t c1 = ev_on(ws);
           chol_iv.push_back({c0, c1});
           if (li == 0 && si == 0) part_end[q] = c1, part_ev[q][2] = c0, part_ev[q][3] = c1;

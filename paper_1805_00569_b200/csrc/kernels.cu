@@ -700,7 +700,7 @@ struct DfNode {
 // virtual nodes processed as soon as they are ready (so every task a chain step waits
 // on precedes every task that waits on that step), ties by deadline: the step by which
 // the task's output is needed.
-std::vector<int4> df_build_tasks(int nt) {
+std::vector<int4> df_build_tasks(int nt, bool gram) {
   std::vector<DfNode> nd;
   auto add = [&](int type, int i, int j, int a, int b, int time) {
     nd.push_back(DfNode{type, i, j, a, b, time, 0, {}, 0});
@@ -734,6 +734,11 @@ std::vector<int4> df_build_tasks(int nt) {
     for (int i = k + 2; i < nt; ++i) trsm[i * nt + k] = add(DF_TRSM, i, k, 0, 0, k);
   std::vector<int> inv;
   for (int b = 0; b < nt / 2; ++b) inv.push_back(add(DF_INV, b, 0, 0, 0, 2 * b + 1));
+  // fused kernel-matrix build: GRAM(i, j) precedes everything that touches tile (i, j)
+  std::vector<int> gramt(static_cast<size_t>(nt) * nt, -1);
+  if (gram)
+    for (int i = 0; i < nt; ++i)
+      for (int j = 0; j <= i; ++j) gramt[i * nt + j] = add(DF_GRAM, i, j, 0, 0, -1);
   auto lprod = [&](int row, int q) { return row == q + 1 ? chain[q] : trsm[row * nt + q]; };
   for (int i = 0; i < nt; ++i)
     for (int j = 0; j <= i; ++j) {
@@ -759,6 +764,24 @@ std::vector<int4> df_build_tasks(int nt) {
     if (!items[k * nt + k].empty()) edge(items[k * nt + k].back(), chain[k]);
     if (k + 1 < nt && !items[(k + 1) * nt + k].empty()) edge(items[(k + 1) * nt + k].back(), chain[k]);
   }
+  if (gram)
+    for (int i = 0; i < nt; ++i)
+      for (int j = 0; j <= i; ++j) {
+        const int g = gramt[i * nt + j];
+        const std::vector<int>& it = items[i * nt + j];
+        if (!it.empty()) {
+          // one step ahead of the tile's first update, not at its earliest start: early
+          // keys queued ~2000 tile builds ahead of the first steps' critical tasks
+          edge(g, it.front());
+          nd[g].deadline = nd[it.front()].deadline - 1;
+        } else if (i >= j + 2) {
+          edge(g, trsm[i * nt + j]);
+          nd[g].deadline = j;
+        } else {
+          edge(g, chain[j]);  // (j, j) or (j + 1, j): read by the chain at step j
+          nd[g].deadline = j - 1;
+        }
+      }
   for (int b = 0; b < nt / 2; ++b) {
     edge(chain[2 * b + 1], inv[b]);
     nd[inv[b]].deadline = nt + 1;
@@ -802,14 +825,14 @@ std::vector<int4> df_build_tasks(int nt) {
 }
 
 // device copy of the task list per (device, nt), built once
-static const int4* df_tasks_device(int nt, int* ntasks) {
+static const int4* df_tasks_device(int nt, bool gram, int* ntasks) {
   static std::mutex mu;
-  static std::map<std::pair<int, int>, std::pair<int4*, int>> cache;
+  static std::map<std::tuple<int, int, bool>, std::pair<int4*, int>> cache;
   std::lock_guard<std::mutex> lock(mu);
-  const auto key = std::make_pair(current_device(), nt);
+  const auto key = std::make_tuple(current_device(), nt, gram);
   auto it = cache.find(key);
   if (it == cache.end()) {
-    const std::vector<int4> h = df_build_tasks(nt);
+    const std::vector<int4> h = df_build_tasks(nt, gram);
     int4* d = nullptr;
     cudaMalloc(&d, sizeof(int4) * h.size());
     cudaMemcpy(d, h.data(), sizeof(int4) * h.size(), cudaMemcpyHostToDevice);
@@ -820,12 +843,12 @@ static const int4* df_tasks_device(int nt, int* ntasks) {
 }
 
 static bool launch_potrf_df(double* A, const CUtensorMap& tmA, double* Linv, int64_t mp, int* status, cudaStream_t s,
-                            Counter& c, const FwdSolve* fs) {
+                            Counter& c, const FwdSolve* fs, const GramFuse* gf) {
   static std::atomic<uint64_t> attr{0};
   smem_optin(attr, potrf_df_kernel, kDfSmem);
   const int nt = static_cast<int>(mp / kDfT);
   DfParams p{};
-  p.tasks = df_tasks_device(nt, &p.ntasks);
+  p.tasks = df_tasks_device(nt, gf != nullptr, &p.ntasks);
   const int64_t nflag = ((F_HEAD + static_cast<int64_t>(nt) * nt + nt + 2) + 31) / 32 * 32;
   const size_t bytes = nflag * 4 + sizeof(double) * (static_cast<size_t>(nt) * 4096 + static_cast<size_t>(nt) * nt * 64);
   // workspace: grow-only, one per (device, stream) -- calls on one stream are ordered,
@@ -850,6 +873,17 @@ static bool launch_potrf_df(double* A, const CUtensorMap& tmA, double* Linv, int
   }
   cudaMemsetAsync(ws, 0, nflag * 4, s);
   p.flags = static_cast<int*>(ws);
+  if (gf) {
+    // tiles not yet formed: applied = -1 until their GRAM task
+    cudaMemsetAsync(p.flags + F_HEAD, 0xff, sizeof(int) * static_cast<size_t>(nt) * nt, s);
+    p.gram = 1;
+    p.xk = static_cast<int>(gf->dp / kBK);
+    p.m_valid = static_cast<int>(gf->m_valid);
+    p.xnorm = gf->xnorm;
+    p.K = gf->K;
+    p.neg_inv_denom = -1.0 / ((2.0 * gf->sigma) * gf->sigma);
+    p.shift = gf->shift;
+  }
   p.inv64 = reinterpret_cast<double*>(p.flags + nflag);
   p.P = p.inv64 + static_cast<int64_t>(nt) * 4096;
   p.status = status ? status : p.flags + nflag - 2;
@@ -874,7 +908,8 @@ static bool launch_potrf_df(double* A, const CUtensorMap& tmA, double* Linv, int
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, potrf_df_kernel, tmA, tmI, p);
+  const CUtensorMap tmX = gf ? gf->tmX : tmA;
+  cudaLaunchKernelEx(&cfg, potrf_df_kernel, tmA, tmI, tmX, p);
   c.launched();
   return fs != nullptr;
 }
@@ -988,9 +1023,15 @@ struct FactorBufs {
 };
 }  // namespace
 
+bool potrf_df_eligible(int64_t mp, bool latency) {
+  static const bool df_on = !(std::getenv("PKRR_DF") && std::atoi(std::getenv("PKRR_DF")) == 0);
+  static const bool shadow = std::getenv("PKRR_SHADOW") != nullptr;
+  return df_on && latency && mp / kNB < 64 && !shadow && !g_syrk_ozaki && g_panel_group == 0;
+}
+
 bool launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, double* Linv,
                   int64_t mp, int64_t m_valid, int* status, cudaStream_t s, Counter& c, int8_t* slices,
-                  int* exps, cudaStream_t s2, bool latency, const FwdSolve* fs) {
+                  int* exps, cudaStream_t s2, bool latency, const FwdSolve* fs, const GramFuse* gf) {
   static std::atomic<uint64_t> attr_leaf{0}, attr_syrk{0}, attr_oz{0};
   smem_optin(attr_leaf, potrf_leaf_kernel, kLeafSmem);
   smem_optin(attr_syrk, dsyrk_persistent_kernel, kSyrkSmem);
@@ -1012,12 +1053,7 @@ bool launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, 
   }
   // a lone small system: the dataflow kernel (potrf_df.cuh); PKRR_DF=0 keeps the
   // stream-ordered panel chain below
-  {
-    static const bool df_on = !(std::getenv("PKRR_DF") && std::atoi(std::getenv("PKRR_DF")) == 0);
-    const bool int8_up = g_syrk_ozaki && slices && exps;
-    if (df_on && latency && mp / kNB < 64 && !shadow && !int8_up && g_panel_group == 0)
-      return launch_potrf_df(A, tmA, Linv, mp, status, s, c, fs);
-  }
+  if (potrf_df_eligible(mp, latency)) return launch_potrf_df(A, tmA, Linv, mp, status, s, c, fs, gf);
   // fused forward substitution (not with the shadow checker: its steps run twice)
   const bool fused = fs != nullptr && !shadow;
   if (fused) cudaMemcpyAsync(fs->w, fs->y, sizeof(double) * mp, cudaMemcpyDeviceToDevice, s);

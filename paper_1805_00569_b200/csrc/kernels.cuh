@@ -64,11 +64,28 @@ struct FwdSolve {
   double* w;
   double* z;
 };
+// Kernel-matrix build fused into the factorization (the dataflow path only): A and K
+// are formed tile by tile from the padded rows (tmX over Xp [mp x dp], norms) as
+// K = exp(-d^2 / ((2 sigma) sigma)), A = K + shift I, instead of gram + assemble kernels.
+struct GramFuse {
+  CUtensorMap tmX;
+  const double* xnorm;
+  double* K;
+  int64_t dp;
+  int64_t m_valid;
+  double sigma;
+  double shift;
+};
+// true when launch_potrf factors an mp x mp system with the dataflow kernel
+// (csrc/potrf_df.cuh): a system factorised alone (latency) with mp < 8192, default
+// schedule settings (PKRR_DF=0 disables it)
+bool potrf_df_eligible(int64_t mp, bool latency);
 // Returns true when the forward solve was fused (fs given and not in PKRR_SHADOW mode).
+// gf (eligible systems only, else ignored): A is built from gf instead of read.
 bool launch_potrf(double* A, const CUtensorMap& tmA, const CUtensorMap& tmLinv, double* Linv,
                   int64_t mp, int64_t m_valid, int* status, cudaStream_t s, Counter& c,
                   int8_t* slices = nullptr, int* exps = nullptr, cudaStream_t s2 = nullptr,
-                  bool latency = false, const FwdSolve* fs = nullptr);
+                  bool latency = false, const FwdSolve* fs = nullptr, const GramFuse* gf = nullptr);
 // s2 (optional): a second stream for lookahead -- the next panel's columns are
 // updated first on s and the rest of the trailing update runs on s2, overlapping the
 // next panel factorisation; the result is bitwise the same as without.

@@ -74,7 +74,7 @@ __device__ __forceinline__ unsigned long long df_clk() {
 #define DF_TASK_MARK(t, i, v)
 #endif
 
-enum DfType { DF_TRSM = 0, DF_UPD = 1, DF_INV = 2, DF_END = 3 };
+enum DfType { DF_TRSM = 0, DF_UPD = 1, DF_INV = 2, DF_END = 3, DF_GRAM = 4 };
 // flag words (ints) at the head of the workspace
 enum DfFlag { F_TICKET = 0, F_ROLE = 1, F_CHAIN = 2, F_HEAD = 8 };
 
@@ -91,6 +91,16 @@ struct DfParams {
   int* flags;            // F_HEAD ints, applied[nt*nt], lrow[nt]
   const int4* tasks;     // {type, i, j, a | b << 16}
   int ntasks;
+  // fused kernel-matrix build (gram != 0): GRAM(i, j) tasks form tile (i, j) of
+  // K = exp(-|x_i - x_j|^2 / ((2 s) s)) (kernel.cpp:52-56) from the padded rows X (tmX,
+  // xk 16-column chunks) and their norms, write it to K and K + shift I to A
+  int gram;
+  int xk;
+  int m_valid;
+  const double* xnorm;
+  double* K;
+  double neg_inv_denom;
+  double shift;
 };
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
@@ -131,7 +141,8 @@ __device__ __noinline__ bool df_wait_ge(const int* flag, int target, const int* 
 // ---------------------------------------------------------------------------
 // worker: TMA producer warp + 8 DMMA warps (2 x 4 grid, 32 x 16 per warp)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensorMap* tmI, const DfParams& p,
+__device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensorMap* tmI, const CUtensorMap* tmX,
+                                          const DfParams& p,
                                           unsigned char* smem) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nt = p.nt;
@@ -171,6 +182,7 @@ __device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensor
     if (lane != 0) return;
     prefetch_tmap(tmA);
     prefetch_tmap(tmI);
+    if (p.gram) prefetch_tmap(tmX);
     int kt = 0;
     for (int it = 0;; ++it) {
       const int t = atomicAdd(p.flags + F_TICKET, 1);
@@ -212,7 +224,8 @@ __device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensor
       } else {
         mbar_arrive(&cfull[slot]);
       }
-      const int nk = task.x == DF_TRSM ? 4 : (task.x == DF_UPD ? 4 * (tb - ta) : 0);
+      const int nk =
+          task.x == DF_TRSM ? 4 : (task.x == DF_UPD ? 4 * (tb - ta) : (task.x == DF_GRAM ? p.xk : 0));
       for (int c = 0; c < nk; ++c, ++kt) {
         const int s = kt % kDfStages;
         const uint32_t sp = (kt / kDfStages) & 1;
@@ -222,6 +235,9 @@ __device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensor
         if (task.x == DF_TRSM) {
           tma_load_2d(sa, tmA, tj * kDfT + 16 * c, ti * kDfT, &full[s]);
           tma_load_2d(sa + 8192, tmI, 16 * c, tj * kDfT, &full[s]);
+        } else if (task.x == DF_GRAM) {
+          tma_load_2d(sa, tmX, 16 * c, ti * kDfT, &full[s]);
+          tma_load_2d(sa + 8192, tmX, 16 * c, tj * kDfT, &full[s]);
         } else {
           tma_load_2d(sa, tmA, ta * kDfT + 16 * c, ti * kDfT, &full[s]);
           tma_load_2d(sa + 8192, tmA, ta * kDfT + 16 * c, tj * kDfT, &full[s]);
@@ -251,7 +267,8 @@ __device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensor
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    const int nk = task.x == DF_TRSM ? 4 : (task.x == DF_UPD ? 4 * (tb - ta) : 0);
+    const int nk =
+        task.x == DF_TRSM ? 4 : (task.x == DF_UPD ? 4 * (tb - ta) : (task.x == DF_GRAM ? p.xk : 0));
     for (int c = 0; c < nk; ++c, ++kt) {
       const int s = kt % kDfStages;
       mbar_wait(&full[s], (kt / kDfStages) & 1);
@@ -294,6 +311,46 @@ __device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensor
           v.y -= acc[i][j][1];
           *reinterpret_cast<double2*>(Cg + static_cast<int64_t>(r) * lda + c) = v;
         }
+    } else if (task.x == DF_GRAM) {
+      // the gram epilogue of dgemm_tn_kernel<G_GRAM_SYM> (kernel.cpp:52-56): dist2 =
+      // (n_i + n_j) - 2 x_i.x_j clamped at 0, exp(dist2 * -1/((2 s) s)); unit diagonal,
+      // padding rows / columns identity; A = K + shift I
+      double* Kg = p.K + static_cast<int64_t>(ti * kDfT) * lda + tj * kDfT;
+      double* Ag = p.A + static_cast<int64_t>(ti * kDfT) * lda + tj * kDfT;
+      double nb[4][2];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = wn * 32 + j * 8 + 2 * lk;
+        nb[j][0] = __ldg(p.xnorm + tj * kDfT + c);
+        nb[j][1] = __ldg(p.xnorm + tj * kDfT + c + 1);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = wm * 32 + i * 8 + lr, gi = ti * kDfT + r;
+        const double na = __ldg(p.xnorm + gi);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = wn * 32 + j * 8 + 2 * lk;
+          double v[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int gj = tj * kDfT + c + e;
+            if (gi >= p.m_valid || gj >= p.m_valid) {
+              v[e] = gi == gj ? 1.0 : 0.0;
+            } else if (gi == gj) {
+              v[e] = 1.0;
+            } else {
+              double dist2 = (na + nb[j][e]) - 2.0 * acc[i][j][e];
+              if (dist2 < 0.0) dist2 = 0.0;
+              v[e] = exp(dist2 * p.neg_inv_denom);
+            }
+          }
+          *reinterpret_cast<double2*>(Kg + static_cast<int64_t>(r) * lda + c) = make_double2(v[0], v[1]);
+          const int gj0 = tj * kDfT + c;
+          *reinterpret_cast<double2*>(Ag + static_cast<int64_t>(r) * lda + c) =
+              make_double2(gi == gj0 ? v[0] + p.shift : v[0], gi == gj0 + 1 ? v[1] + p.shift : v[1]);
+        }
+      }
     } else if (task.x == DF_TRSM) {
       double* Cg = p.A + static_cast<int64_t>(ti * kDfT) * lda + tj * kDfT;
 #pragma unroll
@@ -391,6 +448,7 @@ __device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensor
       __threadfence();
       if (task.x == DF_UPD) st_release_gpu(applied + ti * nt + tj, tb);
       else if (task.x == DF_TRSM) st_release_gpu(lrow + ti, tj + 1);
+      else if (task.x == DF_GRAM) st_release_gpu(applied + ti * nt + tj, 0);
 #ifdef PKRR_DF_TRACE
       DF_TASK_MARK(ticket, 2, df_now());
 #endif
@@ -712,6 +770,8 @@ __device__ __forceinline__ void df_chain(const DfParams& p, unsigned char* smem)
   auto csync = [] { asm volatile("bar.sync 2, 224;\n" ::: "memory"); };
   auto hsync = [] { asm volatile("bar.sync 3, 192;\n" ::: "memory"); };
   if (ctid == 0) {
+    df_wait_ge(applied, 0, p.status);  // tile (0, 0) formed (fused gram)
+    fence_proxy_async_global();
     mbar_arrive_expect_tx(lbar, 64 * 512);
     for (int r = 0; r < 64; ++r) bulk_load(Dbuf + r * kDS, p.A + static_cast<int64_t>(r) * lda, 512, lbar);
   }
@@ -922,7 +982,8 @@ __device__ __forceinline__ void df_chain(const DfParams& p, unsigned char* smem)
 }
 
 __global__ void __launch_bounds__(kDfThreads, 1)
-    potrf_df_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmI, DfParams p) {
+    potrf_df_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmI,
+                    const __grid_constant__ CUtensorMap tmX, DfParams p) {
   if (*reinterpret_cast<const volatile int*>(p.status)) return;
   extern __shared__ unsigned char df_smem_raw[];
   // 1024-byte alignment (128B-swizzled TMA ring) by pointer arithmetic on the shared
@@ -935,7 +996,7 @@ __global__ void __launch_bounds__(kDfThreads, 1)
   if (role == 0)
     df_chain(p, smem);
   else
-    df_worker(&tmA, &tmI, p, smem);
+    df_worker(&tmA, &tmI, &tmX, p, smem);
 }
 
 }  // namespace pk

@@ -62,3 +62,25 @@ def test_train_krr_alpha_matches_oracle(engine, oracle, m):
     alpha_ref, _ = oracle.train_krr(X, y, 2.0, 1e-4)
     assert np.linalg.norm(mod.alpha - alpha_ref) <= 1e-8 * np.linalg.norm(alpha_ref)
     assert mod.residual_ratio <= 1e-8
+
+
+def test_fused_gram_grid_matches_separate_kernels():
+    """PKRR_DF_GRAM=1 (opt-in): the dataflow kernel forms K and A = K + lambda m I tile by
+    tile; the grid result must match the default path (separate gram + assemble)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, '.'); import numpy as np, paper_1805_00569_b200 as pk;"
+        "from paper_1805_00569_b200 import datagen;"
+        "dd = datagen.make(1500, 0, 300, 12, 4, seed=5); e = pk.Engine(0);"
+        "g = e.grid_search('exact', dd['X_train'], dd['y_train'], dd['X_test'], dd['y_test'], 1,"
+        " [1e-4, 1e-2], [1.5, 3.0], 1);"
+        "print(repr(list(g.mse)))")
+    out = {}
+    for flag in ("0", "1"):
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, PKRR_DF_GRAM=flag),
+                           capture_output=True, text=True, cwd=os.path.dirname(os.path.dirname(__file__)))
+        assert r.returncode == 0, r.stderr
+        out[flag] = np.array(eval(r.stdout.strip().splitlines()[-1]))
+    assert np.all(np.abs(out["1"] - out["0"]) <= 1e-8 * np.abs(out["0"]))

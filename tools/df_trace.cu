@@ -53,7 +53,7 @@ int main(int argc, char** argv) {
   }
   printf("m %d: %.3f ms (%s)\n", m, ms, cudaGetErrorString(cudaGetLastError()));
   const int nt = mp / 64;
-  std::vector<int4> tasks = pk::df_build_tasks(nt);
+  std::vector<int4> tasks = pk::df_build_tasks(nt, false);
   static unsigned long long ch[256][12];
   static unsigned long long tk[65536][4];
   cudaMemcpyFromSymbol(ch, pk::g_df_chain, sizeof(ch));
