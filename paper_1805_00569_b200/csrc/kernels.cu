@@ -19,6 +19,7 @@
 #include "syrk_persistent.cuh"
 #include "ozaki_syrk.cuh"
 #include "predict_fused.cuh"
+#include "gram_pp.cuh"
 #include <string>
 #include "kernels.cuh"
 
@@ -244,6 +245,25 @@ void launch_gram_sym(const CUtensorMap& tmX, const double* norms, int64_t mp, in
   p.denom = (2.0 * sigma) * sigma;
   p.neg_inv_denom = -1.0 / p.denom;
   p.abort_flag = abort;
+  static const bool pp = !(std::getenv("PKRR_GRAM_PP") && std::atoi(std::getenv("PKRR_GRAM_PP")) == 0);
+  if (!mirror && pp) {
+    // the pipeline's K (lower tiles only): persistent ping-pong kernel (gram_pp.cuh)
+    GramPPParams q{};
+    q.T = T;
+    q.ktiles = p.ktiles;
+    q.K = K;
+    q.ldk = ldk;
+    q.norms = norms;
+    q.valid = static_cast<int>(m);
+    q.neg_inv_denom = p.neg_inv_denom;
+    q.abort_flag = abort;
+    static std::atomic<uint64_t> attr{0};
+    smem_optin(attr, gram_pp_kernel, kPPSmem);
+    const int nhalf = T * (T + 1);
+    launch_pdl(gram_pp_kernel, static_cast<unsigned>(nhalf < g_sms ? nhalf : g_sms), kPPThreads, kPPSmem, s, tmX, q);
+    c.launched();
+    return;
+  }
   gemm_launch<128, G_GRAM_SYM>(tmX, tmX, p, T * (T + 1) / 2, s, c);
 }
 
