@@ -2479,7 +2479,13 @@ void launch_group(const int32_t* label, int64_t n, int k, int64_t* sizes, int64_
 // order) stream through a double-buffered shared-memory ring via cp.async; warp
 // 0 keeps one strictly sequential accumulator per feature, so every centre
 // coordinate is the same chain of roundings as the reference's loop.
-constexpr int kMeansRows = 128, kMeansF = 32, kMeansThreads = 256, kMeansRing = 6;
+#ifndef PKRR_MEANS_F
+#define PKRR_MEANS_F 8
+#endif
+// kMeansF features per CTA: one chain per feature on the consumer warp.  Fewer features
+// per CTA = fewer gathered bytes per member row feeding each chain warp and more CTAs:
+// C1 per Lloyd iteration 157 us (32) -> 134 (16) -> 120 (8); 4 / 2 exceed one wave (190)
+constexpr int kMeansRows = 128, kMeansF = PKRR_MEANS_F, kMeansThreads = 256, kMeansRing = 6;
 constexpr int kMeansSmem = kMeansRing * kMeansRows * kMeansF * 8;
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -2522,17 +2528,18 @@ __global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __re
   __syncthreads();
   if (bulk && threadIdx.x >= 32) {
     // Even d, 16-byte aligned X: each member row's feature block is a run of 16-byte
-    // pieces.  Loader warp w handles rows 2(w-1) + {0,1} + 14 i of a chunk (lanes 0-15
-    // and 16-31 one row each, one piece per lane); the row indices of chunk c + 1 are
-    // loaded while chunk c is issued, so their latency is off the critical path.
+    // pieces.  A loader warp covers kRpw rows per step (kMeansF / 2 lanes per row, one
+    // piece per lane); the row indices of chunk c + 1 are loaded while chunk c is
+    // issued, so their latency is off the critical path.
+    constexpr int kPieces = kMeansF / 2, kRpw = 32 / kPieces, kRps = 7 * kRpw;
     const int w = (threadIdx.x >> 5) - 1, lane = threadIdx.x & 31;
-    const int half = lane >> 4, piece = lane & 15;
+    const int half = lane / kPieces, piece = lane % kPieces;
     const int npieces = fw >> 1;
-    constexpr int kSteps = (kMeansRows + 13) / 14;  // 5 rows per half-warp per chunk
+    constexpr int kSteps = (kMeansRows + kRps - 1) / kRps;
     auto load_idx = [&](int64_t c, int64_t (&ix)[kSteps]) {
 #pragma unroll
       for (int u = 0; u < kSteps; ++u) {
-        const int rr = 2 * w + half + 14 * u;
+        const int rr = kRpw * w + half + kRps * u;
         const int64_t r = c * kMeansRows + rr;
         ix[u] = (c < nchunks && rr < kMeansRows && r < sz) ? __ldg(members + st + r) : -1;
       }
@@ -2547,7 +2554,7 @@ __global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __re
       if (piece < npieces) {
 #pragma unroll
         for (int u = 0; u < kSteps; ++u) {
-          const int rr = 2 * w + half + 14 * u;
+          const int rr = kRpw * w + half + kRps * u;
           if (cur[u] >= 0)
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(b + rr * kMeansF + 2 * piece)),
                          "l"(X + cur[u] * d + f0 + 2 * piece)
@@ -2591,7 +2598,10 @@ __global__ void __launch_bounds__(kMeansThreads) means_kernel(const double* __re
   // (their operands -- the LDS results -- have arrived, so the reads are complete).
   double s = 0.0;
   const int64_t nfull = sz / kMeansRows;
-  auto slot_of = [&](int64_t c) { return smem_u32(mbuf + (c % kMeansRing) * kMeansRows * kMeansF + threadIdx.x); };
+  // lanes >= kMeansF run a duplicate chain (never stored) inside the slot
+  auto slot_of = [&](int64_t c) {
+    return smem_u32(mbuf + (c % kMeansRing) * kMeansRows * kMeansF + (threadIdx.x % kMeansF));
+  };
   auto wait_full = [&](int64_t c) {
     mbar_wait(&full[c % kMeansRing], static_cast<uint32_t>((c / kMeansRing) & 1));
   };
