@@ -118,6 +118,26 @@ struct pkrrgpu_ctx {
   double timings[8] = {0};
   std::vector<double> part_ms;  // last grid call: per-part Cholesky end, ms after the phase start
   std::vector<double> part_tl;  // last grid call, first cell: per part {gram0, gram1, chol0, chol1, pred1} ms after start
+  // timing events of the grid calls: pooled (created once, re-recorded every call) and
+  // turned into timings lazily -- at pkrrgpu_last_timings or the next call -- so a call
+  // spends no host time on event creation / destruction / elapsed-time queries
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_next = 0;
+  struct Pending {
+    bool on = false;
+    cudaEvent_t all_a, all_b, part_a, part_b;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gram, chol, pred;
+    std::vector<cudaEvent_t> part_end;
+    std::vector<std::array<cudaEvent_t, 5>> part_ev;
+  } pending;
+  cudaEvent_t pool_event() {
+    if (ev_next == ev_pool.size()) {
+      cudaEvent_t e;
+      ck(cudaEventCreate(&e), "event");
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_next++];
+  }
   void* pinned = nullptr;  // 64 KB pinned staging for small device->host reads
   double total_mem = 0.0;  // device HBM bytes
   std::multimap<size_t, void*> free_blocks;
@@ -220,6 +240,42 @@ std::vector<T> to_host(const T* dsrc, int64_t count, cudaStream_t s) {
   }
   return v;
 }
+
+// Result copies of a call batched through the context's pinned staging buffer: small
+// device -> host copies become async copies into pinned memory plus one sync and host
+// memcpys (a copy to pageable memory costs a synchronous staged transfer each); device
+// destinations and large copies go direct.
+struct D2HBatch {
+  void* pinned;
+  size_t cap;
+  cudaStream_t s;
+  struct Req {
+    void* dst;
+    const void* src;
+    size_t bytes;
+    size_t off;
+  };
+  std::vector<Req> staged;
+  size_t used = 0;
+  template <typename T>
+  void add(T* dst, const T* src, int64_t count) {
+    if (!dst || count <= 0) return;
+    const size_t bytes = sizeof(T) * static_cast<size_t>(count);
+    if (is_device_ptr(dst) || used + bytes > cap) {
+      ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s), "copy out");
+      return;
+    }
+    ck(cudaMemcpyAsync(static_cast<unsigned char*>(pinned) + used, src, bytes, cudaMemcpyDeviceToHost, s), "D2H");
+    staged.push_back({dst, src, bytes, used});
+    used = (used + bytes + 15) / 16 * 16;
+  }
+  void flush() {
+    ck(cudaStreamSynchronize(s), "sync");
+    for (const Req& r : staged) std::memcpy(r.dst, static_cast<unsigned char*>(pinned) + r.off, r.bytes);
+    staged.clear();
+    used = 0;
+  }
+};
 
 __global__ void set_diag_kernel(double* A, int64_t from, int64_t mp, double v) {
   const int64_t i = from + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -793,6 +849,7 @@ void pkrrgpu_destroy(pkrrgpu_ctx* ctx) {
   if (ctx->aux_main) cudaStreamDestroy(ctx->aux_main);
   cudaStreamDestroy(ctx->main);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   delete ctx;
 }
 
@@ -893,8 +950,78 @@ int pkrrgpu_fp64_peak(pkrrgpu_ctx* ctx, double* tflops) {
   API_END
 }
 
-int pkrrgpu_last_timings(const pkrrgpu_ctx* ctx, double* ms, int n) {
-  if (!ctx || !ms) return PKRRGPU_INVALID;
+namespace {
+// the last grid call's phase timings from its (completed) pooled events
+void finalize_timings(pkrrgpu_ctx* ctx) {
+  pkrrgpu_ctx::Pending& P = ctx->pending;
+  if (!P.on) return;
+  P.on = false;
+  // union of [start, end] intervals (ms after the call start)
+  auto union_ms = [&](const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& iv) {
+    std::vector<std::pair<float, float>> x;
+    for (const auto& v : iv) {
+      float a0 = 0, a1 = 0;
+      cudaEventElapsedTime(&a0, P.all_a, v.first);
+      cudaEventElapsedTime(&a1, P.all_a, v.second);
+      x.push_back({a0, a1});
+    }
+    std::sort(x.begin(), x.end());
+    double tot = 0, cs = -1, ce = -1;
+    for (auto& v : x) {
+      if (v.first > ce) {
+        if (ce > cs) tot += ce - cs;
+        cs = v.first;
+        ce = v.second;
+      } else if (v.second > ce) {
+        ce = v.second;
+      }
+    }
+    if (ce > cs) tot += ce - cs;
+    return tot;
+  };
+  const double ms_gram = union_ms(P.gram), ms_chol = union_ms(P.chol), ms_pred = union_ms(P.pred);
+  float chol0 = 1e30f;
+  for (const auto& v : P.chol) {
+    float a0 = 0;
+    cudaEventElapsedTime(&a0, P.all_a, v.first);
+    chol0 = std::min(chol0, a0);
+  }
+  float ms_part = 0, ms_all = 0;
+  cudaEventElapsedTime(&ms_part, P.part_a, P.part_b);
+  cudaEventElapsedTime(&ms_all, P.all_a, P.all_b);
+  ctx->timings[0] = ms_part;
+  ctx->timings[1] = ms_all - ms_part;
+  ctx->timings[2] = ms_pred;
+  ctx->timings[3] = ms_all;
+  ctx->timings[4] = ms_chol;
+  ctx->timings[5] = ms_gram;
+  const size_t p = P.part_end.size();
+  ctx->part_ms.assign(p, 0.0);
+  for (size_t q = 0; q < p; ++q)
+    if (P.part_end[q]) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, P.all_a, P.part_end[q]);
+      ctx->part_ms[q] = ms - chol0;
+    }
+  ctx->part_tl.assign(5 * p, 0.0);
+  for (size_t q = 0; q < p; ++q)
+    for (int j = 0; j < 5; ++j)
+      if (P.part_ev[q][j]) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, P.all_a, P.part_ev[q][j]);
+        ctx->part_tl[5 * q + j] = ms;
+      }
+  cudaGetLastError();
+}
+}  // namespace
+
+int pkrrgpu_last_timings(const pkrrgpu_ctx* cctx, double* ms, int n) {
+  if (!cctx || !ms) return PKRRGPU_INVALID;
+  pkrrgpu_ctx* ctx = const_cast<pkrrgpu_ctx*>(cctx);
+  if (ctx->pending.on) {
+    cudaSetDevice(ctx->device);
+    finalize_timings(ctx);
+  }
   for (int i = 0; i < n && i < 8; ++i) ms[i] = ctx->timings[i];
   // [8 ...]: per-part Cholesky completion (ms after the first Cholesky phase start)
   const int np = static_cast<int>(ctx->part_ms.size());
@@ -1811,7 +1938,11 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   const int predictor = predictor_of(a->strategy);
   Scope sc(ctx);
   cudaStream_t s = ctx->main;
-  Timer t_all, t_part;
+  finalize_timings(ctx);  // the previous call's pooled events are about to be re-recorded
+  ctx->ev_next = 0;
+  struct {
+    cudaEvent_t a, b;
+  } t_all{ctx->pool_event(), ctx->pool_event()}, t_part{ctx->pool_event(), ctx->pool_event()};
   ck(cudaEventRecord(t_all.a, s), "event");
   // PKRR_TRACE_HOST=1: host-side timestamps of the grid call's phases (stderr)
   static const bool htrace = std::getenv("PKRR_TRACE_HOST") != nullptr;
@@ -1906,7 +2037,16 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   const int64_t pp_parts = predictor == 2 || predictor == 0 ? 1 : p;
   double* pred_t = sc.zeros<double>(ncell * pp_parts * t, s);
   double* pred_e = te ? sc.zeros<double>(ncell * pp_parts * te, s) : nullptr;
-  ck(cudaStreamSynchronize(s), "sync");
+  double* comb = world == 1 ? sc.alloc<double>(ncell * t) : nullptr;
+  double* dmse = world == 1 ? sc.alloc<double>(ncell) : nullptr;
+  double* comb_e = world == 1 && te ? sc.alloc<double>(ncell * te) : nullptr;
+  double* dmse_e = world == 1 && te ? sc.alloc<double>(ncell) : nullptr;
+  // the part streams' first work (buffer memsets, row gathers from the partition's order
+  // array and the uploaded inputs) is ordered after everything enqueued on s so far by
+  // this event -- not by a host sync, which left the GPU idle while the host set up parts
+  cudaEvent_t e_pre;
+  ck(cudaEventCreateWithFlags(&e_pre, cudaEventDisableTiming), "event");
+  ck(cudaEventRecord(e_pre, s), "event");
   hmark("result slots ready");
 
   double f_chol = 0, f_gram = 0, f_other = 0;
@@ -1978,7 +2118,6 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
       used += b;
     }
   }
-  std::vector<cudaEvent_t> evs;
   struct Iv {
     cudaEvent_t a, b;
   };
@@ -1990,6 +2129,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
       for (int64_t q : batch) {
       PartBuf& pb = parts[q];
       cudaStream_t ws = streams[sidx[q]];
+      ck(cudaStreamWaitEvent(ws, e_pre, 0), "wait");
       part_alloc(bsc, pb, po.sizes[q], d, true, ws);
       part_load(ctx, pb, dX, dy, d, po.order + po.start[q], ws);
       query_alloc(bsc, qt[q], tcount[q], pb.dp, pb.mp);
@@ -2011,10 +2151,8 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
     // solves overlap the large part's Cholesky.  Phase times are the UNION of the
     // per-(part, cell) intervals, from events on the launching streams.
     auto ev_on = [&](cudaStream_t st) {
-      cudaEvent_t e;
-      ck(cudaEventCreate(&e), "event");
+      cudaEvent_t e = ctx->pool_event();
       ck(cudaEventRecord(e, st), "event");
-      evs.push_back(e);
       return e;
     };
     {
@@ -2101,6 +2239,14 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
       ck(cudaStreamWaitEvent(s, e, 0), "wait");
       if (res_done[q]) ck(cudaStreamWaitEvent(s, res_done[q], 0), "wait");
     }
+    if (world == 1 && &batch == &batches.back()) {
+      // every cell's combine + reference-order MSE, behind the last batch's parts and
+      // before the batch scope synchronises: the host reads statuses, residuals and MSEs
+      // after one sync (the failed cells are masked on the host afterwards)
+      pk::launch_combine_cells(pred_t, pp_parts, t, ncell, predictor, dyt, comb, dmse, s, ctx->counter);
+      if (te)
+        pk::launch_combine_cells(pred_e, pp_parts, te, ncell, predictor, dye, comb_e, dmse_e, s, ctx->counter);
+    }
     hmark("batch enqueued");
   }
   pk::shadow_report();
@@ -2108,80 +2254,56 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   // the parts, so the host reads statuses, residuals and MSEs after a single sync (the
   // failed cells are masked on the host afterwards) instead of a sync -> launch -> sync
   // round trip at the end of the call
-  double *comb = nullptr, *dmse = nullptr, *comb_e = nullptr, *dmse_e = nullptr;
-  if (world == 1) {
-    comb = sc.alloc<double>(ncell * t);
-    dmse = sc.alloc<double>(ncell);
-    pk::launch_combine_cells(pred_t, pp_parts, t, ncell, predictor, dyt, comb, dmse, s, ctx->counter);
-    if (te) {
-      comb_e = sc.alloc<double>(ncell * te);
-      dmse_e = sc.alloc<double>(ncell);
-      pk::launch_combine_cells(pred_e, pp_parts, te, ncell, predictor, dye, comb_e, dmse_e, s, ctx->counter);
-    }
-  }
   ck(cudaEventRecord(t_all.b, s), "event");
+  hmark("all enqueued");
   ck(cudaDeviceSynchronize(), "grid");
+  hmark("device synchronized");
+  cudaEventDestroy(e_pre);
 
-  // union of [start, end] intervals (ms after the call start)
-  auto union_ms = [&](const std::vector<Iv>& iv) {
-    std::vector<std::pair<float, float>> x;
-    for (const Iv& v : iv) {
-      float a0 = 0, a1 = 0;
-      cudaEventElapsedTime(&a0, t_all.a, v.a);
-      cudaEventElapsedTime(&a1, t_all.a, v.b);
-      x.push_back({a0, a1});
-    }
-    std::sort(x.begin(), x.end());
-    double tot = 0, cs = -1, ce = -1;
-    for (auto& v : x) {
-      if (v.first > ce) {
-        if (ce > cs) tot += ce - cs;
-        cs = v.first;
-        ce = v.second;
-      } else if (v.second > ce) {
-        ce = v.second;
-      }
-    }
-    if (ce > cs) tot += ce - cs;
-    return tot;
-  };
-  const double ms_gram = union_ms(gram_iv), ms_chol = union_ms(chol_iv), ms_pred = union_ms(pred_iv);
-  float chol0 = 1e30f;
-  for (const Iv& v : chol_iv) {
-    float a0 = 0;
-    cudaEventElapsedTime(&a0, t_all.a, v.a);
-    chol0 = std::min(chol0, a0);
-  }
   {
-    float ms_part = 0, ms_all = 0;
-    cudaEventElapsedTime(&ms_part, t_part.a, t_part.b);
-    cudaEventElapsedTime(&ms_all, t_all.a, t_all.b);
-    ctx->timings[0] = ms_part;
-    ctx->timings[1] = ms_all - ms_part;
-    ctx->timings[2] = ms_pred;
-    ctx->timings[3] = ms_all;
-    ctx->timings[4] = ms_chol;
-    ctx->timings[5] = ms_gram;
+    pkrrgpu_ctx::Pending& P = ctx->pending;
+    P.on = true;
+    P.all_a = t_all.a;
+    P.all_b = t_all.b;
+    P.part_a = t_part.a;
+    P.part_b = t_part.b;
+    P.gram.clear();
+    P.chol.clear();
+    P.pred.clear();
+    for (const Iv& v : gram_iv) P.gram.push_back({v.a, v.b});
+    for (const Iv& v : chol_iv) P.chol.push_back({v.a, v.b});
+    for (const Iv& v : pred_iv) P.pred.push_back({v.a, v.b});
+    P.part_end = part_end;
+    P.part_ev = part_ev;
   }
-  ctx->part_ms.assign(p, 0.0);
-  for (int64_t q = 0; q < p; ++q)
-    if (part_end[q]) {
-      float ms = 0;
-      cudaEventElapsedTime(&ms, t_all.a, part_end[q]);
-      ctx->part_ms[q] = ms - chol0;
-    }
-  ctx->part_tl.assign(5 * p, 0.0);
-  for (int64_t q = 0; q < p; ++q)
-    for (int j = 0; j < 5; ++j)
-      if (part_ev[q][j]) {
-        float ms = 0;
-        cudaEventElapsedTime(&ms, t_all.a, part_ev[q][j]);
-        ctx->part_tl[5 * q + j] = ms;
-      }
-  for (auto e : evs) cudaEventDestroy(e);
 
-  const std::vector<int> st = to_host(dstatus, ncell * p * 2, s);
-  const std::vector<double> rs = to_host(dres, ncell * p * 4, s);
+  // the call's small results in one D2H pass through the pinned staging buffer (one
+  // sync instead of one per array)
+  std::vector<int> st(ncell * p * 2);
+  std::vector<double> rs(ncell * p * 4), cmse_h(world == 1 ? ncell : 0), cemse_h(world == 1 && te ? ncell : 0);
+  {
+    const size_t b_st = sizeof(int) * st.size(), b_rs = sizeof(double) * rs.size();
+    const size_t b_m = sizeof(double) * cmse_h.size(), b_e = sizeof(double) * cemse_h.size();
+    const size_t o_rs = (b_st + 15) / 16 * 16, o_m = o_rs + b_rs, o_e = o_m + b_m;
+    if (o_e + b_e <= 64 * 1024) {
+      auto* pin = static_cast<unsigned char*>(ctx->pinned);
+      ck(cudaMemcpyAsync(pin, dstatus, b_st, cudaMemcpyDeviceToHost, s), "D2H");
+      ck(cudaMemcpyAsync(pin + o_rs, dres, b_rs, cudaMemcpyDeviceToHost, s), "D2H");
+      if (b_m) ck(cudaMemcpyAsync(pin + o_m, dmse, b_m, cudaMemcpyDeviceToHost, s), "D2H");
+      if (b_e) ck(cudaMemcpyAsync(pin + o_e, dmse_e, b_e, cudaMemcpyDeviceToHost, s), "D2H");
+      ck(cudaStreamSynchronize(s), "sync");
+      std::memcpy(st.data(), pin, b_st);
+      std::memcpy(rs.data(), pin + o_rs, b_rs);
+      if (b_m) std::memcpy(cmse_h.data(), pin + o_m, b_m);
+      if (b_e) std::memcpy(cemse_h.data(), pin + o_e, b_e);
+    } else {
+      st = to_host(dstatus, ncell * p * 2, s);
+      rs = to_host(dres, ncell * p * 4, s);
+      if (b_m) cmse_h = to_host(dmse, ncell, s);
+      if (b_e) cemse_h = to_host(dmse_e, ncell, s);
+    }
+  }
+  hmark("small results read");
   std::vector<uint8_t> pfail(ncell * p, 0);
   for (int64_t c = 0; c < ncell; ++c)
     for (int64_t q : owned) pfail[c * p + q] = st[(c * p + q) * 2] ? 1 : 0;
@@ -2203,8 +2325,9 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   o->flops_chol = f_chol;
   o->flops_gram = f_gram;
   o->flops_other = f_other;
-  if (o->part_of) copy_out(o->part_of, po.part_of, n, s);
-  if (o->centers && po.centers) copy_out(o->centers, po.centers, p * d, s);
+  D2HBatch outb{ctx->pinned, 64 * 1024, s, {}};
+  if (o->part_of) outb.add(o->part_of, po.part_of, n);
+  if (o->centers && po.centers) outb.add(o->centers, po.centers, p * d);
   if (o->part_sizes)
     for (int64_t q = 0; q < p; ++q) o->part_sizes[q] = po.sizes[q];
 
@@ -2212,8 +2335,8 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
   o->pred_rows = pp_parts;
   // this rank's predictions (rows / part slices it does not own are zero): the
   // multi-rank caller sums them over ranks (exact: disjoint) and runs pkrrgpu_combine
-  if (o->cell_pred) copy_out(o->cell_pred, pred_t, ncell * pp_parts * t, s);
-  if (o->cell_eval_pred && te) copy_out(o->cell_eval_pred, pred_e, ncell * pp_parts * te, s);
+  if (o->cell_pred) outb.add(o->cell_pred, pred_t, ncell * pp_parts * t);
+  if (o->cell_eval_pred && te) outb.add(o->cell_eval_pred, pred_e, ncell * pp_parts * te);
   if (world == 1) {
     std::vector<uint8_t> cfail(ncell, 0);
     std::vector<double> cres(ncell, 0.0);
@@ -2224,7 +2347,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
         if (!pfail[c * p + q] && r > cres[c]) cres[c] = r;
       }
     // best = first strict minimum over the non-failed cells (strategies.cpp:499-505)
-    std::vector<double> cmse = to_host(dmse, ncell, s), cemse;
+    std::vector<double> cmse = cmse_h, cemse;
     int64_t best = -1;
     for (int64_t c = 0; c < ncell; ++c) {
       if (cfail[c]) {
@@ -2234,20 +2357,21 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
       if (best < 0 || cmse[c] < cmse[best]) best = c;
     }
     o->best_index = best;
-    if (best >= 0 && o->best_pred) copy_out(o->best_pred, comb + best * t, t, s);
+    if (best >= 0 && o->best_pred) outb.add(o->best_pred, comb + best * t, t);
     if (te) {
       // the eval set's predictions of the cell chosen on the selection set
-      cemse = to_host(dmse_e, ncell, s);
+      cemse = cemse_h;
       for (int64_t c = 0; c < ncell; ++c)
         if (cfail[c]) cemse[c] = std::numeric_limits<double>::quiet_NaN();
-      if (o->best_index >= 0 && o->best_eval_pred) copy_out(o->best_eval_pred, comb_e + o->best_index * te, te, s);
+      if (o->best_index >= 0 && o->best_eval_pred) outb.add(o->best_eval_pred, comb_e + o->best_index * te, te);
     }
     if (o->cell_mse) std::memcpy(o->cell_mse, cmse.data(), sizeof(double) * ncell);
     if (o->cell_failed) std::memcpy(o->cell_failed, cfail.data(), ncell);
     if (o->cell_residual) std::memcpy(o->cell_residual, cres.data(), sizeof(double) * ncell);
     if (o->cell_eval_mse && te) std::memcpy(o->cell_eval_mse, cemse.data(), sizeof(double) * ncell);
   }
-  ck(cudaStreamSynchronize(s), "sync");
+  outb.flush();
+  hmark("results copied out");
   API_END
 }
 
