@@ -582,7 +582,8 @@ def main():
         return 2
     if os.environ.get("PKRR_BENCH_DRYRUN"):  # launcher test: report the rank layout only
         rank, world, local = dist_env()
-        print(json.dumps({"rank": rank, "world": world, "local_rank": local, "config": args.config}), flush=True)
+        # one write(2) per line: the ranks share the launcher's stdout pipe
+        os.write(1, (json.dumps({"rank": rank, "world": world, "local_rank": local, "config": args.config}) + "\n").encode())
         return 0
     if args.update == "int8":  # read by the library at context creation
         os.environ["PKRR_SYRK"] = "ozaki"
