@@ -616,13 +616,45 @@ __device__ __forceinline__ void df_record_npd(const DfParams& p, int col, int* s
   atomicExch(&p.status[0], 1);
 }
 
+// The chain's small products are dependent-DMMA-latency bound (one accumulator chain of
+// K / 4 steps per 8 x 8 tile), so K is split SPLIT ways into independent chains that are
+// summed at the end in a fixed order (kDfSplit k-ranges of K / kDfSplit).
+#ifndef PKRR_DF_SPLIT
+#define PKRR_DF_SPLIT 0
+#endif
 // rows [16 rb, 16 rb + 16) x cols [16 cb, +16) of dst -= A(rows) B(cols)^T over K (16 x 16
 // blocks of 2 x 2 DMMA tiles); lower_diag skips the strictly upper 8 x 8 tile of a
 // diagonal block
 __device__ __forceinline__ void df_block_update(double* dst, const double* Arow, const double* Brow, int K,
                                                 bool lower_diag, int lr, int lk) {
+#if PKRR_DF_SPLIT
+  double part[4][2][2][2] = {};
+  const int KS = K >> 2;
+#pragma unroll 2
+  for (int k = 0; k < KS; k += 4) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int kk = s * KS + k + lk;
+      const double a0 = Arow[lr * kDS + kk], a1 = Arow[(8 + lr) * kDS + kk];
+      const double b0 = Brow[lr * kDS + kk], b1 = Brow[(8 + lr) * kDS + kk];
+      dmma(part[s][0][0], a0, b0);
+      dmma(part[s][0][1], a0, b1);
+      dmma(part[s][1][0], a1, b0);
+      dmma(part[s][1][1], a1, b1);
+    }
+  }
+  double acc[2][2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        acc[i][j][e] = (part[0][i][j][e] + part[1][i][j][e]) + (part[2][i][j][e] + part[3][i][j][e]);
+#else
   double acc[2][2][2] = {};
   mma_2x2_rt(acc, Arow, Brow, kDS, K, lr, lk);
+#endif
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -651,16 +683,79 @@ __device__ __forceinline__ void df_store8(double* dst, double (&acc)[4][2], int 
 }
 __device__ __forceinline__ void df_rn8(double* dst, const double* A, const double* B, int mode, int lr, int lk) {
   double acc[4][2] = {};
+#if PKRR_DF_SPLIT
+  double p1[4][2] = {};  // K = 32 as two chains of 4 steps
+#pragma unroll 2
+  for (int k = 0; k < 16; k += 4) {
+    const double a0 = A[lr * kDS + k + lk], a1 = A[lr * kDS + 16 + k + lk];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dmma(acc[c], a0, B[(k + lk) * kDS + 8 * c + lr]);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dmma(p1[c], a1, B[(16 + k + lk) * kDS + 8 * c + lr]);
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    acc[c][0] += p1[c][0];
+    acc[c][1] += p1[c][1];
+  }
+#else
   mma_row4_rn(acc, A, kDS, B, kDS, 0, 32, lr, lk);
+#endif
   __syncwarp();  // in place: every read of these rows precedes the write
   df_store8(dst, acc, mode, lr, lk);
 }
 __device__ __forceinline__ void df_rt8(double* dst, const double* A, const double* Bt, int K, int mode, int lr,
                                       int lk) {
   double acc[4][2] = {};
+#if PKRR_DF_SPLIT
+  double p1[4][2] = {};  // two chains of K / 8 steps
+  const int KS = K >> 1;
+#pragma unroll 2
+  for (int k = 0; k < KS; k += 4) {
+    const double a0 = A[lr * kDS + k + lk], a1 = A[lr * kDS + KS + k + lk];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dmma(acc[c], a0, Bt[(8 * c + lr) * kDS + k + lk]);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dmma(p1[c], a1, Bt[(8 * c + lr) * kDS + KS + k + lk]);
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    acc[c][0] += p1[c][0];
+    acc[c][1] += p1[c][1];
+  }
+#else
   mma_row4_rt(acc, A, kDS, Bt, kDS, 0, K, lr, lk);
+#endif
   __syncwarp();
   df_store8(dst, acc, mode, lr, lk);
+}
+
+// dst8 (8 x 32) -= A8 (8 rows, K = 64) . Bt(32 rows)^T  and  the lower 16 x 16 block
+// dst16 -= S(16 rows) . S^T, in one k loop
+__device__ __forceinline__ void df_rt8_block11(double* dst8, double* dst16, const double* A8, const double* Bt,
+                                               const double* S, int lr, int lk) {
+  double acc[4][2] = {}, b00[2] = {}, b10[2] = {}, b11[2] = {};
+#pragma unroll 4
+  for (int k = 0; k < 64; k += 4) {
+    const double a = A8[lr * kDS + k + lk];
+    const double s0 = S[lr * kDS + k + lk], s1 = S[(8 + lr) * kDS + k + lk];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dmma(acc[c], a, Bt[(8 * c + lr) * kDS + k + lk]);
+    dmma(b00, s0, s0);
+    dmma(b10, s1, s0);
+    dmma(b11, s1, s1);
+  }
+  __syncwarp();
+  df_store8(dst8, acc, 1, lr, lk);
+  double2* d = reinterpret_cast<double2*>(dst16 + lr * kDS + 2 * lk);
+  double2 v = *d;
+  *d = make_double2(v.x - b00[0], v.y - b00[1]);
+  d = reinterpret_cast<double2*>(dst16 + (8 + lr) * kDS + 2 * lk);
+  v = *d;
+  *d = make_double2(v.x - b10[0], v.y - b10[1]);
+  d = reinterpret_cast<double2*>(dst16 + (8 + lr) * kDS + 8 + 2 * lk);
+  v = *d;
+  *d = make_double2(v.x - b11[0], v.y - b11[1]);
 }
 
 // The chain's tile loads, issued by one thread without holding up the step's barriers:
@@ -827,7 +922,11 @@ __device__ __forceinline__ void df_chain(const DfParams& p, unsigned char* smem)
         if (p.z && htid < 64) pv[htid] = red[htid] + red[64 + htid];
         // D(k) rows 32..63 -= L(k,k-1)[32:64] L(k,k-1)^T (K = 64): D10 as 4 row tiles,
         // D11 (lower) as 3 blocks of 16; L_{k-1} to global
-        for (int t = hw; t < 7; t += 6) {
+        if (hw == 0) {
+          // this warp's two items (D10 row tile 0, D11 block (1,1)) as one loop: 7
+          // independent DMMA chains instead of two latency-bound passes
+          df_rt8_block11(D10, D11 + 16 * kDS + 16, Tp + 32 * kDS, Tp, Tp + 48 * kDS, lr, lk);
+        } else for (int t = hw; t < 6; t += 6) {
           if (t < 4) {
             df_rt8(D10 + 8 * t * kDS, Tp + (32 + 8 * t) * kDS, Tp, 64, 1, lr, lk);
           } else {
@@ -853,25 +952,10 @@ __device__ __forceinline__ void df_chain(const DfParams& p, unsigned char* smem)
         mbar_arrive(stepbar);  // the loader may refill D(k-1) / T(k-2)'s buffers
       }
       if (htid < 8) tdone[htid] = 0;
-      if (p.z && warp == 7) {
-        // w_k = y_k - sum_p P[k][p] in panel order
-#pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-          const int r = lane + 32 * h;
-          double sw = p.y[k * kDfT + r];
-          const double* pk_ = p.P + static_cast<int64_t>(k) * nt * kDfT + r;
-          int q = 0;
-          for (; q + 4 <= k - 1; q += 4) {
-            const double a0 = __ldcg(pk_ + (q + 0) * kDfT), a1 = __ldcg(pk_ + (q + 1) * kDfT);
-            const double a2 = __ldcg(pk_ + (q + 2) * kDfT), a3 = __ldcg(pk_ + (q + 3) * kDfT);
-            sw = (((sw - a0) - a1) - a2) - a3;
-          }
-          for (; q < k - 1; ++q) sw -= __ldcg(pk_ + q * kDfT);
-          if (k > 0) sw -= pv[r];
-          wv[r] = sw;
-        }
-      }
     }
+#ifdef PKRR_DF_TRACE
+    if (lane == 0) g_df_warp[k][warp][5] = df_clk();
+#endif
     csync();
     DF_CHAIN_MARK(k, 1)
     // ---------------- [B] L10 = D10 X00 ----------------
@@ -895,12 +979,33 @@ __device__ __forceinline__ void df_chain(const DfParams& p, unsigned char* smem)
       __syncwarp();
       if (lane == 0) mbar_arrive(dbar);
       for (int q = warp - 1; q < 4; q += 3) df_rt8(X01 + 8 * q * kDS, X + 8 * q * kDS, D10, 32, 0, lr, lk);
-    } else if (warp >= 5 && has_t && __shfl_sync(0xffffffffu, mbar_test(tbar, par), 0)) {
-      for (int q = warp - 5; q < 8; q += 3) {
-        df_rn8(T + 8 * q * kDS, T + 8 * q * kDS, X, 0, lr, lk);
-        __syncwarp();
-        df_rt8(T + 8 * q * kDS + 32, T + 8 * q * kDS, D10, 32, 1, lr, lk);
-        if (lane == 0) tdone[q] = 1;
+    } else if (warp >= 5) {
+      if (p.z && warp >= 6) {
+        // w_k = y_k - sum_p P[k][p] in panel order (P[k][k-1] = pv from [A]); the P loads are
+        // L2 round trips, so they run here, beside the second diagonal panel, not on the
+        // way to a barrier of the chain
+        const int r = lane + 32 * (warp - 6);
+        double sw = p.y[k * kDfT + r];
+        const double* pk_ = p.P + static_cast<int64_t>(k) * nt * kDfT + r;
+        int q = 0;
+        for (; q + 8 <= k - 1; q += 8) {
+          double a[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) a[u] = __ldcg(pk_ + (q + u) * kDfT);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) sw -= a[u];
+        }
+        for (; q < k - 1; ++q) sw -= __ldcg(pk_ + q * kDfT);
+        if (k > 0) sw -= pv[r];
+        wv[r] = sw;
+      }
+      if (has_t && __shfl_sync(0xffffffffu, mbar_test(tbar, par), 0)) {
+        for (int q = warp - 5; q < 8; q += 3) {
+          df_rn8(T + 8 * q * kDS, T + 8 * q * kDS, X, 0, lr, lk);
+          __syncwarp();
+          df_rt8(T + 8 * q * kDS + 32, T + 8 * q * kDS, D10, 32, 1, lr, lk);
+          if (lane == 0) tdone[q] = 1;
+        }
       }
     }
 #ifdef PKRR_DF_TRACE
@@ -916,38 +1021,13 @@ __device__ __forceinline__ void df_chain(const DfParams& p, unsigned char* smem)
     csync();
     if (*sflag) return;
     DF_CHAIN_MARK(k, 5)
-    if (p.z) {
-      if (ctid < 128) {
-        const int r = ctid & 63, pt = ctid >> 6;
-        double sacc = 0.0;
-        for (int c = 32 * pt; c < 32 * pt + 32; ++c) sacc = fma(X[c * kDS + r], wv[c], sacc);
-        red[pt * 64 + r] = sacc;
-      }
-      csync();
-      if (ctid < 64) {
-        const double z = red[ctid] + red[64 + ctid];
-        zv[ctid] = z;
-        p.z[k * kDfT + ctid] = z;
-      }
-    }
-    {
-      double* Ig = p.inv64 + static_cast<int64_t>(k) * 4096;
-      for (int e = ctid; e < 64 * 32; e += 224) {
-        const int ri = e & 63, ci = 2 * (e >> 6);  // X read down its columns: conflict-free
-        *reinterpret_cast<double2*>(Ig + ri * 64 + ci) = make_double2(X[ci * kDS + ri], X[(ci + 1) * kDS + ri]);
-      }
-    }
-    csync();
-    if (ctid == 0) {
-      __threadfence();
-      st_release_gpu(p.flags + F_CHAIN, k + 1);
-    }
-    DF_CHAIN_MARK(k, 6)
-    if (!has_t) break;
-    // ---------------- [E] T(k) rows, D(k+1)00 ----------------
-    mbar_wait(tbar, par);
-    DF_CHAIN_MARK(k, 7)
-    for (int q = cw; q < 8; q += 7) {
+    // ---------------- [E] ----------------
+    // critical (warps 0-3): rows 0..31 of T(k) (all three products) and then D(k+1)00, the
+    // block the next step's diagonal warp starts on.  Background (warps 5-7), beside it:
+    // z_k = X^T w_k, publish inv(L_kk) = X^T and z_k (chain = k + 1: the fence's L2 round
+    // trip is off the critical warps), then rows 32..55 of T(k) (two products now, T1 X11 in
+    // the next step's [A]); rows 56..63 go to warp 3 beside the D(k+1)00 update.
+    auto trow = [&](int q) {
       if (!tdone[q]) {
         df_rn8(T + 8 * q * kDS, T + 8 * q * kDS, X, 0, lr, lk);
         __syncwarp();
@@ -955,16 +1035,60 @@ __device__ __forceinline__ void df_chain(const DfParams& p, unsigned char* smem)
       }
       __syncwarp();
       if (q < 4) df_rn8(T + 8 * q * kDS + 32, T + 8 * q * kDS + 32, X11, 0, lr, lk);
+    };
+    if (warp >= 5) {
+      const int bt = (warp - 5) * 32 + lane;
+      if (p.z && bt < 64) {
+        double s0 = 0.0, s1 = 0.0;  // the two half sums, then their sum (fixed order)
+#pragma unroll 8
+        for (int c = 0; c < 32; ++c) {
+          s0 = fma(X[c * kDS + bt], wv[c], s0);
+          s1 = fma(X[(c + 32) * kDS + bt], wv[c + 32], s1);
+        }
+        const double z = s0 + s1;
+        zv[bt] = z;
+        p.z[k * kDfT + bt] = z;
+      }
+      double* Ig = p.inv64 + static_cast<int64_t>(k) * 4096;
+      for (int e = bt; e < 64 * 32; e += 96) {
+        const int ri = e & 63, ci = 2 * (e >> 6);  // X read down its columns: conflict-free
+        *reinterpret_cast<double2*>(Ig + ri * 64 + ci) = make_double2(X[ci * kDS + ri], X[(ci + 1) * kDS + ri]);
+      }
+      asm volatile("bar.sync 5, 96;\n" ::: "memory");
+      if (bt == 0) {
+        __threadfence();
+        st_release_gpu(p.flags + F_CHAIN, k + 1);
+      }
+#ifdef PKRR_DF_TRACE
+      if (lane == 0) g_df_warp[k][warp][6] = df_clk();
+#endif
+      if (has_t) {
+        mbar_wait(tbar, par);
+        trow(warp - 1);
+      }
+#ifdef PKRR_DF_TRACE
+      if (lane == 0) g_df_warp[k][warp][7] = df_clk();
+#endif
+    } else if (has_t) {
+      mbar_wait(tbar, par);
+      DF_CHAIN_MARK(k, 7)
+      trow(warp);
+#ifdef PKRR_DF_TRACE
+      if (lane == 0) g_df_warp[k][warp][7] = df_clk();
+#endif
+      mbar_wait(lbar, (k + 1) & 1);  // D(k+1) prefetched
+      asm volatile("bar.sync 4, 128;\n" ::: "memory");
+      DF_CHAIN_MARK(k, 8)
+      if (warp < 3) {
+        double* Dn = Dbuf + ((k + 1) & 1) * 64 * kDS;
+        const int rb = warp == 0 ? 0 : 1, cb = warp == 2 ? 1 : 0;
+        df_block_update(Dn + 16 * rb * kDS + 16 * cb, T + 16 * rb * kDS, T + 16 * cb * kDS, 64, rb == cb, lr, lk);
+      } else {
+        trow(7);
+      }
     }
-    mbar_wait(lbar, (k + 1) & 1);  // D(k+1) prefetched
     csync();
-    DF_CHAIN_MARK(k, 8)
-    double* Dn = Dbuf + ((k + 1) & 1) * 64 * kDS;
-    if (warp < 3) {
-      const int rb = warp == 0 ? 0 : 1, cb = warp == 2 ? 1 : 0;
-      df_block_update(Dn + 16 * rb * kDS + 16 * cb, T + 16 * rb * kDS, T + 16 * cb * kDS, 64, rb == cb, lr, lk);
-    }
-    csync();
+    if (!has_t) break;
     DF_CHAIN_MARK(k, 10)
   }
   // the last diagonal block

@@ -73,7 +73,7 @@ int main(int argc, char** argv) {
   for (int k = 0; k + 1 < nt; ++k) printf(" %.1f", (ch[k + 1][0] - ch[k][0]) / 1e3);
   printf("\n");
   // critical worker tasks: TRSM(k+1, k-1) and UPD(k+1, k, {k-1}) per step
-  for (int k = 2; k < std::min(nt - 1, 12); ++k) {
+  for (int k = 40; k < std::min(nt - 1, 43); ++k) {
     printf("step %d: start %.1f, publish(k-1) %.1f", k, (ch[k][0] - t0) / 1e3, (ch[k - 1][8] - t0) / 1e3);
     for (size_t t = 0; t < tasks.size(); ++t) {
       const int4 q = tasks[t];
@@ -104,15 +104,19 @@ int main(int argc, char** argv) {
   for (int k = 0; k < 256; ++k)
     for (int w = 0; w < 8; ++w)
       for (int i = 0; i < 8; ++i) wt[k][w][i] = (unsigned long long)(wt[k][w][i] / 1.965);
-  for (int k = 8; k < 11; ++k) {
+  for (int k : {8, 40, 41}) {
     const long long c0 = (long long)ch[k][0];
-    printf("step %d marks A %.2f B %.2f C %.2f D %.2f\n", k, ((long long)ch[k][1] - c0) / 1e3,
-           ((long long)ch[k][3] - c0) / 1e3, ((long long)ch[k][4] - c0) / 1e3, ((long long)ch[k][5] - c0) / 1e3);
-    for (int w = 0; w < 8; ++w)
-      printf("   w%d: A-start %.2f A-hsync %.2f B-done %.2f C-done %.2f D-done %.2f\n", w,
+    printf("step %d chain marks (us):", k);
+    for (int i = 1; i <= 10; ++i) printf(" m%d %.2f", i, ((long long)ch[k][i] - c0) / 1e3);
+    printf("  next-start %.2f\n", ((long long)ch[k + 1][0] - c0) / 1e3);
+    for (int w = 0; w < 8; ++w) {
+      if (w == 4) continue;
+      printf("   w%d: A-start %.2f A-work %.2f pre-csync1 %.2f B-work %.2f C-work %.2f D-work %.2f zpub %.2f Trows %.2f\n", w,
              ((long long)wt[k][w][0] - c0) / 1e3, ((long long)wt[k][w][1] - c0) / 1e3,
-             ((long long)wt[k][w][2] - c0) / 1e3, ((long long)wt[k][w][3] - c0) / 1e3,
-             ((long long)wt[k][w][4] - c0) / 1e3);
+             ((long long)wt[k][w][5] - c0) / 1e3, ((long long)wt[k][w][2] - c0) / 1e3,
+             ((long long)wt[k][w][3] - c0) / 1e3, ((long long)wt[k][w][4] - c0) / 1e3,
+             ((long long)wt[k][w][6] - c0) / 1e3, ((long long)wt[k][w][7] - c0) / 1e3);
+    }
   }
   if (argc > 2) {
     FILE* f = fopen(argv[2], "w");
