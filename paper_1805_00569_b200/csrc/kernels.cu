@@ -720,6 +720,10 @@ struct DfNode {
 // virtual nodes processed as soon as they are ready (so every task a chain step waits
 // on precedes every task that waits on that step), ties by deadline: the step by which
 // the task's output is needed.
+int df_band() {
+  static const int d = std::getenv("PKRR_DF_BAND") ? std::atoi(std::getenv("PKRR_DF_BAND")) : 1 << 20;
+  return d;
+}
 std::vector<int4> df_build_tasks(int nt, bool gram) {
   std::vector<DfNode> nd;
   auto add = [&](int type, int i, int j, int a, int b, int time) {
@@ -737,7 +741,9 @@ std::vector<int4> df_build_tasks(int nt, bool gram) {
     for (int j = 0; j <= i; ++j) {
       const int e = i == j ? j - 1 : j;  // panels [0, e) applied by workers (the chain applies j-1 to (j,j))
       if (e <= 0) continue;
-      const int s0 = std::max(0, e - kDfSingles);
+      // the last kDfSingles panels singly (ready a step after their panel) only within
+      // df_band() tile rows of the diagonal; farther tiles take the remainder as one batch
+      const int s0 = std::max(0, e - (i - j <= df_band() ? kDfSingles : 0));
       std::vector<std::pair<int, int>> rng;
       // batch boundaries staggered per tile: aligned ones made every far tile's batch
       // come due on the same step (multiples of 8), queueing ~1000 K = 512 tasks ahead

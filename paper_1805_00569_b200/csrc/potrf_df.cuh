@@ -445,7 +445,8 @@ __device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensor
     if (lane == 0) mbar_arrive(&cempty[slot]);
     consumer_sync(128);  // every warp's stores issued before the publication
     if (tid == 0) {
-      __threadfence();
+      // st.release.gpu is the fence (MEMBAR.ALL.GPU); a __threadfence() before it added a
+      // MEMBAR.SC.GPU + L1 invalidate per task
       if (task.x == DF_UPD) st_release_gpu(applied + ti * nt + tj, tb);
       else if (task.x == DF_TRSM) st_release_gpu(lrow + ti, tj + 1);
       else if (task.x == DF_GRAM) st_release_gpu(applied + ti * nt + tj, 0);
@@ -885,6 +886,9 @@ __device__ __forceinline__ void df_chain(const DfParams& p, unsigned char* smem)
     const bool has_t = k + 1 < nt;
     const uint32_t par = k & 1;
     DF_CHAIN_MARK(k, 0)
+#ifdef PKRR_DF_TRACE
+    if (threadIdx.x == 0) g_df_chain[k][11] = df_now();
+#endif
     // ---------------- [A] ----------------
     int bad = -1;
 #ifdef PKRR_DF_TRACE
@@ -916,8 +920,10 @@ __device__ __forceinline__ void df_chain(const DfParams& p, unsigned char* smem)
         }
         hsync();
         if (htid == 0) {
-          __threadfence();
           st_release_gpu(lrow + k, k);
+#ifdef PKRR_DF_TRACE
+          g_df_warp[k][4][0] = df_now();
+#endif
         }
         if (p.z && htid < 64) pv[htid] = red[htid] + red[64 + htid];
         // D(k) rows 32..63 -= L(k,k-1)[32:64] L(k,k-1)^T (K = 64): D10 as 4 row tiles,
@@ -1056,8 +1062,10 @@ __device__ __forceinline__ void df_chain(const DfParams& p, unsigned char* smem)
       }
       asm volatile("bar.sync 5, 96;\n" ::: "memory");
       if (bt == 0) {
-        __threadfence();
         st_release_gpu(p.flags + F_CHAIN, k + 1);
+#ifdef PKRR_DF_TRACE
+        g_df_chain[k][9] = df_now();
+#endif
       }
 #ifdef PKRR_DF_TRACE
       if (lane == 0) g_df_warp[k][warp][6] = df_clk();

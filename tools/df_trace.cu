@@ -58,7 +58,7 @@ int main(int argc, char** argv) {
   static unsigned long long tk[65536][4];
   cudaMemcpyFromSymbol(ch, pk::g_df_chain, sizeof(ch));
   for (int k = 0; k < 256; ++k)
-    for (int i = 0; i < 12; ++i) ch[k][i] = (unsigned long long)(ch[k][i] / 1.965);  // cycles -> ns
+    for (int i = 0; i < 12; ++i) if (i != 9 && i != 11) ch[k][i] = (unsigned long long)(ch[k][i] / 1.965);  // cycles -> ns
   cudaMemcpyFromSymbol(tk, pk::g_df_task, sizeof(tk));
   const unsigned long long t0 = ch[0][0];
   const char* names[] = {"start", "T ready", "diag0 done", "sub0", "syrk", "sub1", "inv", "fwd", "publish",
@@ -72,9 +72,16 @@ int main(int argc, char** argv) {
   printf("\nstep length (us):");
   for (int k = 0; k + 1 < nt; ++k) printf(" %.1f", (ch[k + 1][0] - ch[k][0]) / 1e3);
   printf("\n");
-  // critical worker tasks: TRSM(k+1, k-1) and UPD(k+1, k, {k-1}) per step
-  for (int k = 40; k < std::min(nt - 1, 43); ++k) {
-    printf("step %d: start %.1f, publish(k-1) %.1f", k, (ch[k][0] - t0) / 1e3, (ch[k - 1][8] - t0) / 1e3);
+  // critical worker tasks per step k (globaltimer us after the step's start): TRSM(k+1, k-1)
+  // -> UPD(k+1, k, {k-1}) -> T(k), UPD(k+1, k+1, {k-1}) -> D(k+1)
+  static unsigned long long wt0[256][8][8];
+  cudaMemcpyFromSymbol(wt0, pk::g_df_warp, sizeof(wt0));
+  for (int k : {4, 12, 14, 16, 20, 24, 40, 41}) {
+    if (k >= nt - 1) continue;
+    const long long s0 = (long long)ch[k][11];
+    printf("step %d (len %.1f): publish(k-1) %.1f, L(k,k-1) out %.1f, publish(k) %.1f", k,
+           ((long long)ch[k + 1][11] - s0) / 1e3, ((long long)ch[k - 1][9] - s0) / 1e3,
+           ((long long)wt0[k][4][0] - s0) / 1e3, ((long long)ch[k][9] - s0) / 1e3);
     for (size_t t = 0; t < tasks.size(); ++t) {
       const int4 q = tasks[t];
       const int a = q.w & 0xffff, b = q.w >> 16;
@@ -82,8 +89,8 @@ int main(int argc, char** argv) {
           (q.x == pk::DF_UPD && q.y == k + 1 && q.z == k && b == k) ||
           (q.x == pk::DF_UPD && q.y == k + 1 && q.z == k + 1 && b == k))
         printf("  [%s %d,%d %d-%d #%zu: claim %.1f ready %.1f done %.1f cta %llu]", q.x == pk::DF_TRSM ? "TRSM" : "UPD",
-               q.y, q.z, a, b, t, ((long long)tk[t][0] - (long long)t0) / 1e3,
-               ((long long)tk[t][1] - (long long)t0) / 1e3, ((long long)tk[t][2] - (long long)t0) / 1e3, tk[t][3]);
+               q.y, q.z, a, b, t, ((long long)tk[t][0] - s0) / 1e3, ((long long)tk[t][1] - s0) / 1e3,
+               ((long long)tk[t][2] - s0) / 1e3, tk[t][3]);
     }
     printf("\n");
   }
