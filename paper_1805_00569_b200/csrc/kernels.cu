@@ -1516,7 +1516,6 @@ __global__ void __launch_bounds__(256) trsv_fwd_kernel(const double* __restrict_
     const double sum = warp_sum(fma(m[rr].w, v.w, fma(m[rr].z, v.z, fma(m[rr].y, v.y, m[rr].x * v.x))));
     if (lane == 0) z[I * kNB + w * 16 + rr] = sum;
   }
-  __threadfence();
   __syncthreads();
   if (tid == 0) st_release(&flags[I], 1);
 }
@@ -1537,7 +1536,15 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(const double* __restrict_
   if (tid == 0) sI = ihi - 1 - atomicAdd(ticket, 1);
   __syncthreads();
   const int I = sI;
-  prefetch_l2_block(Linv + static_cast<int64_t>(I) * kNB * kNB, kNB, tid);
+  // this thread's 16 x 4 piece of inv(L_II), parked in shared memory now (the same thread
+  // reads it back): loading it after the last flag put an L2 round trip on every chain step
+  extern __shared__ double4 sLinv[];
+  {
+    double4 m[16];
+    load_block16(Linv + (static_cast<int64_t>(I) * kNB + w * 16) * kNB + lane * 4, kNB, m);
+#pragma unroll
+    for (int rr = 0; rr < 16; ++rr) sLinv[rr * 256 + tid] = m[rr];
+  }
   const double zI = tid < kNB ? __ldg(z + I * kNB + tid) : 0.0;  // z is final (previous kernel): load now
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // columns 4l..4l+3, partial over this warp's rows
   for (int K = nb - 1; K > I; --K) {
@@ -1564,16 +1571,15 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(const double* __restrict_
   }
   __syncthreads();
   // x_I = Linv_I^T sv: column sums over this warp's 16 rows, then across warps
-  double4 m[16];
-  load_block16(Linv + (static_cast<int64_t>(I) * kNB + w * 16) * kNB + lane * 4, kNB, m);
   a0 = a1 = a2 = a3 = 0.0;
 #pragma unroll
   for (int rr = 0; rr < 16; ++rr) {
     const double v = sv[w * 16 + rr];
-    a0 = fma(m[rr].x, v, a0);
-    a1 = fma(m[rr].y, v, a1);
-    a2 = fma(m[rr].z, v, a2);
-    a3 = fma(m[rr].w, v, a3);
+    const double4 m = sLinv[rr * 256 + tid];
+    a0 = fma(m.x, v, a0);
+    a1 = fma(m.y, v, a1);
+    a2 = fma(m.z, v, a2);
+    a3 = fma(m.w, v, a3);
   }
   __syncthreads();
   *reinterpret_cast<double4*>(&red[w][lane * 4]) = make_double4(a0, a1, a2, a3);
@@ -1584,16 +1590,22 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(const double* __restrict_
     for (int q = 0; q < 8; ++q) sum += red[q][tid];
     x[I * kNB + tid] = sum;
   }
-  __threadfence();
   __syncthreads();
-  if (tid == 0) st_release(&flags[I], 1);
+  if (tid == 0) st_release(&flags[I], 1);  // st.release.gpu is the fence (no __threadfence before it)
+}
+
+constexpr int kTrsvBwdSmem = 16 * 256 * 32;  // 128 KB: inv(L_II) in the threads' own slots
+static void trsv_bwd_optin() {
+  static std::atomic<uint64_t> attr{0};
+  smem_optin(attr, trsv_bwd_kernel, kTrsvBwdSmem);
 }
 
 void launch_trsv_bwd(const double* L, const double* Linv, int64_t mp, const double* z, double* x,
                      int* scratch, const int* abort, cudaStream_t s, Counter& c) {
   const int nb = static_cast<int>(mp / kNB);
   cudaMemsetAsync(scratch, 0, sizeof(int) * (2 * nb + 2), s);
-  trsv_bwd_kernel<<<nb, 256, 0, s>>>(L, mp, Linv, z, x, nb, scratch + 1, scratch + 2 + nb, abort, nb);
+  trsv_bwd_optin();
+  trsv_bwd_kernel<<<nb, 256, kTrsvBwdSmem, s>>>(L, mp, Linv, z, x, nb, scratch + 1, scratch + 2 + nb, abort, nb);
   c.launched();
 }
 
@@ -1601,8 +1613,9 @@ void launch_trsv(const double* L, const double* Linv, int64_t mp, const double* 
                  double* x, int* scratch, const int* abort, cudaStream_t s, Counter& c) {
   const int nb = static_cast<int>(mp / kNB);
   cudaMemsetAsync(scratch, 0, sizeof(int) * (2 * nb + 2), s);
+  trsv_bwd_optin();
   trsv_fwd_kernel<<<nb, 256, 0, s>>>(L, mp, Linv, b, z, nb, scratch, scratch + 2, abort);
-  trsv_bwd_kernel<<<nb, 256, 0, s>>>(L, mp, Linv, z, x, nb, scratch + 1, scratch + 2 + nb, abort, nb);
+  trsv_bwd_kernel<<<nb, 256, kTrsvBwdSmem, s>>>(L, mp, Linv, z, x, nb, scratch + 1, scratch + 2 + nb, abort, nb);
   c.launched(2);
 }
 
@@ -3101,7 +3114,8 @@ void launch_trsv_bwd_range(const double* L_shifted, int64_t ld, const double* Li
   // scratch: [0] ticket, [1 ..] flags: the blocks >= ihi are final (x from later super-columns)
   cudaMemsetAsync(scratch, 0, sizeof(int), s);
   fill_flags_kernel<<<(nb + 255) / 256, 256, 0, s>>>(scratch + 1, nb, ilo, ihi);
-  trsv_bwd_kernel<<<ihi - ilo, 256, 0, s>>>(L_shifted, ld, Linv, z, x, nb, scratch, scratch + 1, abort, ihi);
+  trsv_bwd_optin();
+  trsv_bwd_kernel<<<ihi - ilo, 256, kTrsvBwdSmem, s>>>(L_shifted, ld, Linv, z, x, nb, scratch, scratch + 1, abort, ihi);
   c.launched(2);
 }
 
