@@ -338,7 +338,7 @@ void part_alloc(Scope& sc, PartBuf& pb, int64_t m, int64_t d, bool need_K, cudaS
   pb.w = sc.alloc<double>(pb.mp);
   pb.alpha = sc.alloc<double>(pb.mp);
   pb.Ka = sc.alloc<double>(pb.mp * pk::kSymvSplit);
-  pb.scratch = sc.alloc<int>(2 * (pb.mp / kNB) + 2);
+  pb.scratch = sc.alloc<int>(pk::trsv_scratch_ints(pb.mp));
   if (pk::syrk_ozaki()) {
     pb.slices = sc.alloc<int8_t>(2 * 8 * pb.mp * 512);  // two buffers: lookahead alternates them
     pb.exps = sc.alloc<int>(2 * pb.mp);
@@ -2093,7 +2093,7 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
       const int64_t qp = round_up(cnt > 0 ? cnt : 1, 64);
       return qp * dp + 2 * qp + qp * mp;
     };
-    return 8.0 * static_cast<double>(mp * dp + 8 * mp + 2 * mp * mp + mp * kNB + qbytes(tcount[q]) +
+    return 8.0 * static_cast<double>(mp * dp + 12 * mp + 2 * mp * mp + mp * kNB + qbytes(tcount[q]) +
                                      (te ? qbytes(ecount[q]) : 0)) +
            (pk::syrk_ozaki() ? 2.0 * 8.0 * 512.0 * static_cast<double>(mp) : 0.0);
   };

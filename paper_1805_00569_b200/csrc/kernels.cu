@@ -1525,7 +1525,12 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(const double* __restrict_
                                                        const double* __restrict__ Linv,
                                                        const double* __restrict__ z, double* x,
                                                        int nb, int* ticket, int* flags,
-                                                       const int* abort, int ihi) {
+                                                       const int* abort, int ihi, unsigned long long* xt) {
+  // xt != null: x blocks travel as tagged words (two 8-byte {32 data bits, tag} halves per
+  // value, the tag set by the same store as the data: readers poll the data itself -- one
+  // L2 round trip per chain step instead of flag, then data, and no fence before a flag);
+  // xt == null: release / acquire flags (the distributed solve, whose later blocks are
+  // final before the launch)
   if (abort && *reinterpret_cast<const volatile int*>(abort)) return;
   __shared__ double red[8][kNB];
   __shared__ double sv[kNB];
@@ -1550,8 +1555,20 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(const double* __restrict_
   for (int K = nb - 1; K > I; --K) {
     double4 m[16];
     load_block16(L + (static_cast<int64_t>(K) * kNB + w * 16) * ld + I * kNB + lane * 4, ld, m);
-    wait_flag(&flags[K], lane);
-    const double xv = lane < 16 ? __ldcg(x + K * kNB + w * 16 + lane) : 0.0;
+    double xv = 0.0;
+    if (xt) {
+      const unsigned long long* src = xt + 2 * static_cast<int64_t>(K * kNB + w * 16 + (lane & 15));
+      for (;;) {
+        unsigned long long lo, hi;
+        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(lo), "=l"(hi) : "l"(src) : "memory");
+        const bool ok = (lo >> 32) == 1ull && (hi >> 32) == 1ull;
+        xv = __hiloint2double(static_cast<int>(hi & 0xffffffffull), static_cast<int>(lo & 0xffffffffull));
+        if (__all_sync(0xffffffffu, ok)) break;
+      }
+    } else {
+      wait_flag(&flags[K], lane);
+      xv = lane < 16 ? __ldcg(x + K * kNB + w * 16 + lane) : 0.0;
+    }
 #pragma unroll
     for (int rr = 0; rr < 16; ++rr) {
       const double v = __shfl_sync(0xffffffffu, xv, rr);
@@ -1589,11 +1606,25 @@ __global__ void __launch_bounds__(256) trsv_bwd_kernel(const double* __restrict_
 #pragma unroll
     for (int q = 0; q < 8; ++q) sum += red[q][tid];
     x[I * kNB + tid] = sum;
+    if (xt) {
+      const unsigned long long lo = static_cast<unsigned int>(__double2loint(sum)) | (1ull << 32);
+      const unsigned long long hi = static_cast<unsigned int>(__double2hiint(sum)) | (1ull << 32);
+      asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};\n" ::"l"(xt + 2 * static_cast<int64_t>(I * kNB + tid)),
+                   "l"(lo), "l"(hi)
+                   : "memory");
+    }
   }
+  if (xt) return;
   __syncthreads();
   if (tid == 0) st_release(&flags[I], 1);  // st.release.gpu is the fence (no __threadfence before it)
 }
 
+// scratch of the solves: [2 nb + 2] tickets / flags, then (16-byte aligned) the tagged
+// x words of the backward solve, 4 ints per row
+size_t trsv_scratch_ints(int64_t mp) { return static_cast<size_t>((2 * (mp / kNB) + 2 + 3) / 4 * 4 + 4 * mp); }
+static unsigned long long* trsv_tagged(int* scratch, int nb) {
+  return reinterpret_cast<unsigned long long*>(scratch + (2 * nb + 2 + 3) / 4 * 4);
+}
 constexpr int kTrsvBwdSmem = 16 * 256 * 32;  // 128 KB: inv(L_II) in the threads' own slots
 static void trsv_bwd_optin() {
   static std::atomic<uint64_t> attr{0};
@@ -1603,19 +1634,21 @@ static void trsv_bwd_optin() {
 void launch_trsv_bwd(const double* L, const double* Linv, int64_t mp, const double* z, double* x,
                      int* scratch, const int* abort, cudaStream_t s, Counter& c) {
   const int nb = static_cast<int>(mp / kNB);
-  cudaMemsetAsync(scratch, 0, sizeof(int) * (2 * nb + 2), s);
+  cudaMemsetAsync(scratch, 0, sizeof(int) * trsv_scratch_ints(mp), s);
   trsv_bwd_optin();
-  trsv_bwd_kernel<<<nb, 256, kTrsvBwdSmem, s>>>(L, mp, Linv, z, x, nb, scratch + 1, scratch + 2 + nb, abort, nb);
+  trsv_bwd_kernel<<<nb, 256, kTrsvBwdSmem, s>>>(L, mp, Linv, z, x, nb, scratch + 1, scratch + 2 + nb, abort, nb,
+                                                trsv_tagged(scratch, nb));
   c.launched();
 }
 
 void launch_trsv(const double* L, const double* Linv, int64_t mp, const double* b, double* z,
                  double* x, int* scratch, const int* abort, cudaStream_t s, Counter& c) {
   const int nb = static_cast<int>(mp / kNB);
-  cudaMemsetAsync(scratch, 0, sizeof(int) * (2 * nb + 2), s);
+  cudaMemsetAsync(scratch, 0, sizeof(int) * trsv_scratch_ints(mp), s);
   trsv_bwd_optin();
   trsv_fwd_kernel<<<nb, 256, 0, s>>>(L, mp, Linv, b, z, nb, scratch, scratch + 2, abort);
-  trsv_bwd_kernel<<<nb, 256, kTrsvBwdSmem, s>>>(L, mp, Linv, z, x, nb, scratch + 1, scratch + 2 + nb, abort, nb);
+  trsv_bwd_kernel<<<nb, 256, kTrsvBwdSmem, s>>>(L, mp, Linv, z, x, nb, scratch + 1, scratch + 2 + nb, abort, nb,
+                                                trsv_tagged(scratch, nb));
   c.launched(2);
 }
 
@@ -3115,7 +3148,8 @@ void launch_trsv_bwd_range(const double* L_shifted, int64_t ld, const double* Li
   cudaMemsetAsync(scratch, 0, sizeof(int), s);
   fill_flags_kernel<<<(nb + 255) / 256, 256, 0, s>>>(scratch + 1, nb, ilo, ihi);
   trsv_bwd_optin();
-  trsv_bwd_kernel<<<ihi - ilo, 256, kTrsvBwdSmem, s>>>(L_shifted, ld, Linv, z, x, nb, scratch, scratch + 1, abort, ihi);
+  trsv_bwd_kernel<<<ihi - ilo, 256, kTrsvBwdSmem, s>>>(L_shifted, ld, Linv, z, x, nb, scratch, scratch + 1, abort, ihi,
+                                                       nullptr);
   c.launched(2);
 }
 

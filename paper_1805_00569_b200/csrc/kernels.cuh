@@ -110,6 +110,7 @@ void launch_zero_upper(double* A, int64_t mp, cudaStream_t s, Counter& c);
 
 // ---- triangular solves (L L^T x = b) on the blocked factor ----------------
 // scratch: 2*nb + 2 ints (tickets + flags), zeroed by the launcher
+size_t trsv_scratch_ints(int64_t mp);  // ints of the solves' scratch (tickets, flags, tagged x words)
 void launch_trsv(const double* L, const double* Linv, int64_t mp, const double* b, double* z,
                  double* x, int* scratch, const int* abort, cudaStream_t s, Counter& c);
 // backward half only (z from a fused forward substitution)
