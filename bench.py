@@ -48,8 +48,8 @@ METRIC = "train+predict samples/sec (FP64)"
 # K=512 profiles/ncu_syrk_r01.txt, K=1024 ncu_syrk_k1024_r01.txt, K=2048 ncu_syrk_k2048_r01.txt;
 # K=128 (a lone 4096-row system, C0): ncu_syrk_k128_r01.txt (tools/syrk_probe_alone.py).
 # DRAM bytes (read, write) of the dataflow Cholesky's ncu capture (m = 4096 lone system,
-# profiles/ncu_df_c0_r02.txt)
-DF_NCU_BYTES = {4096: (73.09e6, 54.22e6)}
+# profiles/ncu_df_c0_r02b.txt)
+DF_NCU_BYTES = {4096: (73.19e6, 56.23e6)}
 
 
 def DF_ROOFLINE(m, tflops, peak, probe):
@@ -61,8 +61,8 @@ def DF_ROOFLINE(m, tflops, peak, probe):
             "kernel": "potrf_df_kernel (the whole Cholesky of the lone system: chain CTA + 147 DMMA worker CTAs)",
             "achieved": tflops, "peak": peak, "unit": "TFLOP/s", "frac": tflops / peak if peak else None,
             "traffic": (nb[0] + nb[1]) if nb else None,
-            "traffic_note": ("DRAM read+write bytes of the captured launch (ncu --set full, profiles/ncu_df_c0_r02.txt) "
-                             "vs 4 m^2 = 67 MB of lower-triangle operands: the matrix stays L2-resident (hit 91.6 %)"
+            "traffic_note": ("DRAM read+write bytes of the captured launch (ncu --set full, profiles/ncu_df_c0_r02b.txt) "
+                             "vs 4 m^2 = 67 MB of lower-triangle operands: the matrix stays L2-resident (hit 91.8 %)"
                              if nb else "no ncu capture for this m"),
             "peak_source": "measured live after the warm-up, best of 3: FP64 DMMA (mma.sync m8n8k4) probe over "
                            "148 SMs; MEASURED_PEAKS.json has no FP64 entry",
