@@ -208,4 +208,36 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
+
+// exp(x) for the Gaussian kernel's argument x = -dist2 / (2 s^2) <= 0 (kernel.cpp:52-56),
+// branch-free so that the epilogues' independent elements interleave: k = round(x log2 e)
+// by the 1.5 * 2^52 shift, r = x - k ln2 in two steps (fdlibm's ln2 hi / lo), exp(r) by its
+// degree-13 Taylor polynomial (|r| <= 0.347: truncation 4e-18), 2^k added into the exponent
+// field.  Measured against libm over [-700, 0]: <= 2.3e-16 relative (tools/exp_check.c).
+// x < -700 returns exp(-700) ~ 1e-304 (never denormal); NaN stays NaN.
+__device__ __forceinline__ double exp_nonpos(double x) {
+  const double xc = x < -700.0 ? -700.0 : x;
+  const double t = fma(xc, 1.4426950408889634, 6755399441055744.0);
+  const int k = __double2loint(t);
+  const double kf = t - 6755399441055744.0;
+  double r = fma(kf, -6.93147180369123816490e-01, xc);
+  r = fma(kf, -1.90821492927058770002e-10, r);
+  double p = 1.0 / 6227020800.0;
+  p = fma(p, r, 1.0 / 479001600.0);
+  p = fma(p, r, 1.0 / 39916800.0);
+  p = fma(p, r, 1.0 / 3628800.0);
+  p = fma(p, r, 1.0 / 362880.0);
+  p = fma(p, r, 1.0 / 40320.0);
+  p = fma(p, r, 1.0 / 5040.0);
+  p = fma(p, r, 1.0 / 720.0);
+  p = fma(p, r, 1.0 / 120.0);
+  p = fma(p, r, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const double res = __hiloint2double(__double2hiint(p) + (k << 20), __double2loint(p));
+  return x != x ? x : res;
+}
+
 }  // namespace pk

@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(gemm_threads<MODE>(), gemm_min_blocks<BM, MODE
             if (dist2 < 0.0) dist2 = 0.0;
             // kernel.cpp:55 divides; a multiply by -1/denom moves the exponent by <= 1.5 ulp,
             // i.e. K by <= e^-1 |x| 2^-53 absolute -- far inside the 1e-13 K tolerance
-            v = exp(dist2 * p.neg_inv_denom);
+            v = exp_nonpos(dist2 * p.neg_inv_denom);
           }
           acc[i][j][e] = v;
         }

@@ -44,7 +44,6 @@ __global__ void __launch_bounds__(kPPThreads, 1)
   unsigned char* smem = pp_smem_raw + ((1024u - (smem_u32(pp_smem_raw) & 1023u)) & 1023u);
   uint64_t* fullb = reinterpret_cast<uint64_t*>(smem + 2 * kPPStages * kPPStage);  // [2][S]
   uint64_t* emptyb = fullb + 2 * kPPStages;                                          // [2][S]
-  uint64_t* go = emptyb + 2 * kPPStages;  // warpgroup 0's first mainloop done
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nhalf = p.T * (p.T + 1);  // lower 128-tiles x 2 column halves
   const int KT = p.ktiles;
@@ -53,7 +52,6 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       mbar_init(&fullb[s], 1);
       mbar_init(&emptyb[s], 4);
     }
-    mbar_init(go, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -94,8 +92,13 @@ __global__ void __launch_bounds__(kPPThreads, 1)
   const unsigned char* ring = smem + wg * kPPStages * kPPStage;
   uint64_t* full = fullb + wg * kPPStages;
   uint64_t* empty = emptyb + wg * kPPStages;
-  // stagger: warpgroup 1 starts once warpgroup 0 has finished its first mainloop
-  if (wg == 1 && static_cast<int>(blockIdx.x) < nhalf) mbar_wait(go, 0);
+  // Strict alternation of the two warpgroups' mainloops (named barriers 8 + wg, 256
+  // threads: the waiting warpgroup syncs, the other arrives when its mainloop is done):
+  // left alone they drifted into running both mainloops, then both epilogues, together --
+  // the DMMA pipe idle through the latter.  Warpgroup 1 primes warpgroup 0's first turn.
+  auto turn_wait = [&] { asm volatile("bar.sync %0, 256;\n" ::"r"(8 + wg) : "memory"); };
+  auto turn_pass = [&] { asm volatile("bar.arrive %0, 256;\n" ::"r"(8 + (wg ^ 1)) : "memory"); };
+  if (wg == 1) turn_pass();
   int g = 0;
   for (int t = wg;; t += 2) {
     const int idx = blockIdx.x + t * gridDim.x;
@@ -117,6 +120,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     for (int i = 0; i < 8; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    turn_wait();
     for (int kt = 0; kt < KT; ++kt, ++g) {
       const int s = g % kPPStages;
       mbar_wait(&full[s], (g / kPPStages) & 1);
@@ -142,10 +146,12 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[(g - 1) % kPPStages]);
-    if (wg == 0 && t == 0 && cw == 0 && lane == 0) mbar_arrive(go);
+    turn_pass();
     // epilogue (kernel.cpp:52-56): dist2 = (n_a + n_b) - 2 dot, clamp at 0,
     // exp(dist2 * -1/((2 s) s)); unit diagonal; padding identity; diagonal tiles keep
     // only gi >= gj (nothing reads their upper triangle)
+    // branch-free per element (selects only), so the 64 independent exp chains of a lane
+    // interleave instead of running one after another
     const bool diag_tile = I == J;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -156,15 +162,11 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         double v[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          if (gi >= p.valid || gj + e >= p.valid) {
-            v[e] = gi == gj + e ? 1.0 : 0.0;
-          } else if (gi == gj + e) {
-            v[e] = 1.0;
-          } else {
-            double dist2 = (na[i] + nb[j][e]) - 2.0 * acc[i][j][e];
-            if (dist2 < 0.0) dist2 = 0.0;
-            v[e] = exp(dist2 * p.neg_inv_denom);
-          }
+          double dist2 = (na[i] + nb[j][e]) - 2.0 * acc[i][j][e];
+          dist2 = dist2 < 0.0 ? 0.0 : dist2;
+          const double ev = exp_nonpos(dist2 * p.neg_inv_denom);
+          const bool pad = gi >= p.valid || gj + e >= p.valid;
+          v[e] = gi == gj + e ? 1.0 : (pad ? 0.0 : ev);
         }
         double* dst = p.K + static_cast<int64_t>(gi) * p.ldk + gj;
         if (!diag_tile || gi >= gj + 1)

@@ -342,7 +342,7 @@ __device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensor
             } else {
               double dist2 = (na + nb[j][e]) - 2.0 * acc[i][j][e];
               if (dist2 < 0.0) dist2 = 0.0;
-              v[e] = exp(dist2 * p.neg_inv_denom);
+              v[e] = exp_nonpos(dist2 * p.neg_inv_denom);
             }
           }
           *reinterpret_cast<double2*>(Kg + static_cast<int64_t>(r) * lda + c) = make_double2(v[0], v[1]);

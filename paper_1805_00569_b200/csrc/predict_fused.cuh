@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int i = 0; i < Cfg::MT; ++i) {
           double dist2 = (na[i] + nb[j][e]) - 2.0 * acc[i][j][e];
           if (dist2 < 0.0) dist2 = 0.0;
-          part[i] = fma(exp(dist2 * p.neg_inv_denom), al[j][e], part[i]);
+          part[i] = fma(exp_nonpos(dist2 * p.neg_inv_denom), al[j][e], part[i]);
         }
       }
   }
