@@ -240,4 +240,38 @@ __device__ __forceinline__ double exp_nonpos(double x) {
   return x != x ? x : res;
 }
 
+__constant__ double kExpTaylor[14] = {1.0 / 6227020800.0, 1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0,
+                                      1.0 / 362880.0,     1.0 / 40320.0,     1.0 / 5040.0,     1.0 / 720.0,
+                                      1.0 / 120.0,        1.0 / 24.0,        1.0 / 6.0,        0.5,
+                                      1.0,                1.0};
+// The same function over N independent arguments, written stage by stage so that the N
+// dependent chains reach the instruction stream interleaved (in place: x[u] = exp(x[u])).
+// 2^k is applied as a product, so a NaN argument stays NaN without a select.
+template <int N>
+__device__ __forceinline__ void exp_nonpos_n(double (&x)[N]) {
+  double r[N], kf[N], p[N];
+  int k[N];
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    const double xc = x[u] < -700.0 ? -700.0 : x[u];
+    const double t = fma(xc, 1.4426950408889634, 6755399441055744.0);
+    k[u] = __double2loint(t);
+    kf[u] = t - 6755399441055744.0;
+    r[u] = xc;
+  }
+#pragma unroll
+  for (int u = 0; u < N; ++u) r[u] = fma(kf[u], -6.93147180369123816490e-01, r[u]);
+#pragma unroll
+  for (int u = 0; u < N; ++u) r[u] = fma(kf[u], -1.90821492927058770002e-10, r[u]);
+  // coefficients from the constant bank (as DFMA operands): as literals they took 26 registers
+#pragma unroll
+  for (int u = 0; u < N; ++u) p[u] = kExpTaylor[0];
+#pragma unroll
+  for (int q = 1; q < 14; ++q)
+#pragma unroll
+    for (int u = 0; u < N; ++u) p[u] = fma(p[u], r[u], kExpTaylor[q]);
+#pragma unroll
+  for (int u = 0; u < N; ++u) x[u] = p[u] * __hiloint2double((k[u] + 1023) << 20, 0);
+}
+
 }  // namespace pk

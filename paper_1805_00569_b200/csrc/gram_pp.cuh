@@ -14,6 +14,8 @@
 // arithmetic per element as G_GRAM_SYM (bitwise the same K).
 #pragma once
 
+#include <type_traits>
+
 #include "gemm_dmma.cuh"
 
 namespace pk {
@@ -150,31 +152,51 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     // epilogue (kernel.cpp:52-56): dist2 = (n_a + n_b) - 2 dot, clamp at 0,
     // exp(dist2 * -1/((2 s) s)); unit diagonal; padding identity; diagonal tiles keep
     // only gi >= gj (nothing reads their upper triangle)
-    // branch-free per element (selects only), so the 64 independent exp chains of a lane
-    // interleave instead of running one after another
-    const bool diag_tile = I == J;
+    // Branch-free per element (selects only) and, off the diagonal tiles, no branch around
+    // the stores either: a row's 8 exp chains sit in one basic block and interleave.  (With
+    // two chains per block every dependent DFMA queued behind a 16-cycle DMMA of the other
+    // warpgroup's mainloop on the shared FP64 datapath: the epilogue, not the mainloop, set
+    // the alternation period.)
+    auto epilogue = [&](auto diag_c) {
+      constexpr bool kDiag = decltype(diag_c)::value;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int gi = row0 + wm * 64 + i * 8 + lr;
+      for (int i = 0; i < 8; ++i) {
+        const int gi = row0 + wm * 64 + i * 8 + lr;
+        double v[4][2];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int gj = col0 + wn * 32 + j * 8 + 2 * lk;
-        double v[2];
+        for (int h = 0; h < 2; ++h) {  // 4 chains at a time (register budget: 128 accumulator registers)
+          double ex[4];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          double dist2 = (na[i] + nb[j][e]) - 2.0 * acc[i][j][e];
-          dist2 = dist2 < 0.0 ? 0.0 : dist2;
-          const double ev = exp_nonpos(dist2 * p.neg_inv_denom);
-          const bool pad = gi >= p.valid || gj + e >= p.valid;
-          v[e] = gi == gj + e ? 1.0 : (pad ? 0.0 : ev);
+          for (int u = 0; u < 4; ++u) {
+            const int j = 2 * h + (u >> 1), e = u & 1;
+            double dist2 = (na[i] + nb[j][e]) - 2.0 * acc[i][j][e];
+            dist2 = dist2 < 0.0 ? 0.0 : dist2;
+            ex[u] = dist2 * p.neg_inv_denom;
+          }
+          exp_nonpos_n<4>(ex);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = 2 * h + (u >> 1), e = u & 1;
+            const int gj = col0 + wn * 32 + j * 8 + 2 * lk + e;
+            const bool pad = gi >= p.valid || gj >= p.valid;
+            v[j][e] = gi == gj ? 1.0 : (pad ? 0.0 : ex[u]);
+          }
         }
-        double* dst = p.K + static_cast<int64_t>(gi) * p.ldk + gj;
-        if (!diag_tile || gi >= gj + 1)
-          *reinterpret_cast<double2*>(dst) = make_double2(v[0], v[1]);
-        else if (gi == gj)
-          dst[0] = v[0];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int gj = col0 + wn * 32 + j * 8 + 2 * lk;
+          double* dst = p.K + static_cast<int64_t>(gi) * p.ldk + gj;
+          if (!kDiag || gi >= gj + 1)
+            *reinterpret_cast<double2*>(dst) = make_double2(v[j][0], v[j][1]);
+          else if (gi == gj)
+            dst[0] = v[j][0];
+        }
       }
-    }
+    };
+    if (I == J)
+      epilogue(std::true_type{});
+    else
+      epilogue(std::false_type{});
   }
 }
 
