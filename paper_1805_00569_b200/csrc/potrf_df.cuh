@@ -902,10 +902,8 @@ __device__ __forceinline__ void df_chain(const DfParams& p, unsigned char* smem)
 #endif
     } else {
       if (k > 0) {
-        // T(k-1) rows 32..63: T1 = T1 X11(k-1) (X11 is untouched until [C])
-        for (int q = 4 + hw; q < 8; q += 6) df_rn8(Tp + 8 * q * kDS + 32, Tp + 8 * q * kDS + 32, X11, 0, lr, lk);
-        hsync();
-        // publish L(k, k-1); P[k][k-1] = L(k,k-1) z_{k-1}
+        // publish L(k, k-1) (finished in step k-1's [E]) first: the worker update of tile
+        // (k+1, k) that the chain reloads as T(k) waits for it; P[k][k-1] = L(k,k-1) z_{k-1}
         double* Tg = p.A + static_cast<int64_t>(k * kDfT) * lda + (k - 1) * kDfT;
         for (int e = htid; e < 64 * 32; e += 192) {
           const int r = e >> 5, c2 = 2 * (e & 31);
@@ -1031,8 +1029,9 @@ __device__ __forceinline__ void df_chain(const DfParams& p, unsigned char* smem)
     // critical (warps 0-3): rows 0..31 of T(k) (all three products) and then D(k+1)00, the
     // block the next step's diagonal warp starts on.  Background (warps 5-7), beside it:
     // z_k = X^T w_k, publish inv(L_kk) = X^T and z_k (chain = k + 1: the fence's L2 round
-    // trip is off the critical warps), then rows 32..55 of T(k) (two products now, T1 X11 in
-    // the next step's [A]); rows 56..63 go to warp 3 beside the D(k+1)00 update.
+    // trip is off the critical warps), then rows 32..55 of T(k); rows 56..63 go to warp 3
+    // beside the D(k+1)00 update.  T(k) = L(k+1, k) is complete at the end of the step, so
+    // the next step's [A] publishes it at once.
     auto trow = [&](int q) {
       if (!tdone[q]) {
         df_rn8(T + 8 * q * kDS, T + 8 * q * kDS, X, 0, lr, lk);
@@ -1040,7 +1039,7 @@ __device__ __forceinline__ void df_chain(const DfParams& p, unsigned char* smem)
         df_rt8(T + 8 * q * kDS + 32, T + 8 * q * kDS, D10, 32, 1, lr, lk);
       }
       __syncwarp();
-      if (q < 4) df_rn8(T + 8 * q * kDS + 32, T + 8 * q * kDS + 32, X11, 0, lr, lk);
+      df_rn8(T + 8 * q * kDS + 32, T + 8 * q * kDS + 32, X11, 0, lr, lk);
     };
     if (warp >= 5) {
       const int bt = (warp - 5) * 32 + lane;

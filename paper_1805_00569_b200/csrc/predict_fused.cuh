@@ -131,12 +131,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         if (gj0 + j * 8 + e >= p.valid_x) continue;
+        double ex[Cfg::MT];  // the column's MT exp chains, interleaved stage by stage
 #pragma unroll
         for (int i = 0; i < Cfg::MT; ++i) {
           double dist2 = (na[i] + nb[j][e]) - 2.0 * acc[i][j][e];
-          if (dist2 < 0.0) dist2 = 0.0;
-          part[i] = fma(exp_nonpos(dist2 * p.neg_inv_denom), al[j][e], part[i]);
+          dist2 = dist2 < 0.0 ? 0.0 : dist2;
+          ex[i] = dist2 * p.neg_inv_denom;
         }
+        exp_nonpos_n<Cfg::MT>(ex);
+#pragma unroll
+        for (int i = 0; i < Cfg::MT; ++i) part[i] = fma(ex[i], al[j][e], part[i]);
       }
   }
   // rows: 4 lanes (lk) x 4 warps (wn) hold partials of the same row; fixed-order sums

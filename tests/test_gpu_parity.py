@@ -51,6 +51,26 @@ def test_gram_cross_matches_oracle(engine, oracle):
     assert np.max(np.abs(K - oracle.gram_cross(A, B, 1.7))) <= 1e-13
 
 
+def test_gaussian_exp_accuracy_and_underflow(engine, oracle):
+    """The epilogues' inline exp (common.cuh exp_nonpos; libm in kernel.cpp:55): relative
+    accuracy over the whole argument range on exact arguments (row 0: point 0, so
+    dist2 = (0 + n_b) - 0 exactly), and the underflow range, where the reference's libm
+    returns 0 and exp_nonpos returns exp(-700) ~ 1e-304 (never a denormal, never NaN)."""
+    dist = np.array([0.0, 1e-4, 0.01, 0.3, 0.5, 1.0, 2.0, 3.0, 5.0, 7.0, 12.0, 20.0, 30.0, 36.0, 37.0, 37.4, 38.0,
+                     45.0, 100.0])
+    P = dist[:, None]
+    K = engine.gram(P, P, 1.0)
+    assert np.all(np.isfinite(K)) and np.all(K > 0) and np.all(K <= 1.0)
+    ref = np.exp(-dist ** 2 / 2.0)
+    ok = ref >= 1e-300
+    rel = np.abs(K[0, ok] - ref[ok]) / ref[ok]
+    print("exp_nonpos max relative difference vs libm on exact arguments:", rel.max())
+    assert rel.max() <= 1e-15, rel
+    assert np.all(K[0, ~ok] <= 1e-300)  # libm: 0 or denormal; here exp(-700)
+    # every pair against the reference's own formula (n_a + n_b - 2 a.b, kernel.cpp:52-56)
+    assert np.max(np.abs(K - oracle.gram_sym(P, 1.0))) <= 1e-13
+
+
 def test_gram_known_answers(engine):
     # test_kernel.cpp:34-39: distance 2, sigma 1 -> exp(-2)
     K = engine.gram(np.array([[0.0], [2.0]]), np.array([[0.0], [2.0]]), 1.0)
