@@ -2080,17 +2080,26 @@ __global__ void __launch_bounds__(kAssignRows)
 // clamp, strict < (bitwise the reference's labels, clustering.cpp:79-96, 182-195).
 constexpr int kBulkRows = 64, kBulkStages = 2;
 
-template <int KP>
-__global__ void __launch_bounds__(kBulkRows, 2)
+// TPR threads per row: with 2, warps 0-1 take the first KP / 2 centres of the tile's 64 rows
+// and warps 2-3 the rest (8 warps per SM instead of 4: one warp per scheduler left every
+// barrier wait and LDS latency exposed); the halves' minima meet through shared memory,
+// the lower half winning ties -- the sequential scan's strict < (clustering.cpp:79-96).
+template <int KP, int TPR>
+__global__ void __launch_bounds__(kBulkRows * TPR, 2)
     assign_bulk_kernel(const double* __restrict__ X, int64_t n, int d, const double* __restrict__ xnorm,
                        const double* __restrict__ centers, const double* __restrict__ cnorm, int k,
                        int64_t row0, int32_t* label, double* best_dist, unsigned long long* changed) {
+  constexpr int KH = KP / TPR;  // centres per thread
   extern __shared__ __align__(16) unsigned char bulk_smem[];
   double* tiles = reinterpret_cast<double*>(bulk_smem);
   double* cs = tiles + kBulkStages * kBulkRows * d;  // [KP][d] centres (zero beyond k)
   __shared__ uint64_t full[kBulkStages + 1];  // + the centres' barrier
   __shared__ double cn_s[KP];
+  __shared__ double hmin_d[kBulkRows];
+  __shared__ int hmin_j[kBulkRows];
   const int tid = threadIdx.x;
+  const int row = tid % kBulkRows, half = tid / kBulkRows;
+  const int q0 = half * KH;
   const int64_t rows = n - row0;
   const int64_t ntiles = (rows + kBulkRows - 1) / kBulkRows;
   auto tile_bytes = [&](int64_t t) {
@@ -2111,7 +2120,7 @@ __global__ void __launch_bounds__(kBulkRows, 2)
       }
     }
   }
-  for (int e = k * d + tid; e < KP * d; e += kBulkRows) cs[e] = 0.0;  // centres beyond k
+  for (int e = k * d + tid; e < KP * d; e += kBulkRows * TPR) cs[e] = 0.0;  // centres beyond k
   if (tid < KP) cn_s[tid] = tid < k ? cnorm[tid] : 0.0;
   __syncthreads();
   mbar_wait(&full[kBulkStages], 0);
@@ -2119,37 +2128,50 @@ __global__ void __launch_bounds__(kBulkRows, 2)
   int it = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
     const int s = it % kBulkStages;
-    const int64_t i = row0 + t * kBulkRows + tid;
+    const int64_t i = row0 + t * kBulkRows + row;
     // the row's norm and label are read before waiting for its tile
     const double xn = i < n ? xnorm[i] : 0.0;
-    const int lab = i < n ? label[i] : 0;
+    const int lab = i < n && half == 0 ? label[i] : 0;
     mbar_wait(&full[s], static_cast<uint32_t>((it / kBulkStages) & 1));
+    double min_d = INFINITY;
+    int min_j = 0;
     if (i < n) {
-      const double* xr = tiles + s * kBulkRows * d + tid * d;
-      double dot[KP];
+      const double* xr = tiles + s * kBulkRows * d + row * d;
+      double dot[KH];
 #pragma unroll
-      for (int q = 0; q < KP; ++q) dot[q] = 0.0;
+      for (int q = 0; q < KH; ++q) dot[q] = 0.0;
       for (int c = 0; c < d; c += 2) {
         const double2 x = *reinterpret_cast<const double2*>(xr + c);
 #pragma unroll
-        for (int q = 0; q < KP; ++q) {
-          const double2 cv = *reinterpret_cast<const double2*>(cs + q * d + c);
+        for (int q = 0; q < KH; ++q) {
+          const double2 cv = *reinterpret_cast<const double2*>(cs + (q0 + q) * d + c);
           dot[q] = __dadd_rn(dot[q], __dmul_rn(x.x, cv.x));
           dot[q] = __dadd_rn(dot[q], __dmul_rn(x.y, cv.y));
         }
       }
-      double min_d = INFINITY;
-      int min_j = 0;
 #pragma unroll
-      for (int q = 0; q < KP; ++q) {
-        if (q >= k) break;
-        double dist = __dsub_rn(__dadd_rn(xn, cn_s[q]), __dmul_rn(2.0, dot[q]));
+      for (int q = 0; q < KH; ++q) {
+        if (q0 + q >= k) break;
+        double dist = __dsub_rn(__dadd_rn(xn, cn_s[q0 + q]), __dmul_rn(2.0, dot[q]));
         if (dist < 0.0) dist = 0.0;
         if (dist < min_d) {
           min_d = dist;
-          min_j = q;
+          min_j = q0 + q;
         }
       }
+    }
+    if (TPR > 1) {
+      if (half == 1) {
+        hmin_d[row] = min_d;
+        hmin_j[row] = min_j;
+      }
+      __syncthreads();
+      if (half == 0 && hmin_d[row] < min_d) {  // strict: the lower centre index keeps a tie
+        min_d = hmin_d[row];
+        min_j = hmin_j[row];
+      }
+    }
+    if (i < n && half == 0) {
       if (lab != min_j) {
         label[i] = min_j;
         ch += 1;
@@ -2171,23 +2193,33 @@ __global__ void __launch_bounds__(kBulkRows, 2)
   }
 }
 
-template <int KP>
-static bool try_assign_bulk(const double* X, int64_t n, int64_t d, const double* xnorm, const double* centers,
-                            const double* cnorm, int k, int64_t row0, int32_t* label, double* best_dist,
-                            unsigned long long* changed, cudaStream_t s, Counter& c) {
+template <int KP, int TPR>
+static bool try_assign_bulk_t(const double* X, int64_t n, int64_t d, const double* xnorm, const double* centers,
+                              const double* cnorm, int k, int64_t row0, int32_t* label, double* best_dist,
+                              unsigned long long* changed, cudaStream_t s, Counter& c) {
   const size_t smem = sizeof(double) * (static_cast<size_t>(kBulkStages) * kBulkRows * d + KP * d);
   if (d % 2 || (reinterpret_cast<uintptr_t>(X) & 15) || (reinterpret_cast<uintptr_t>(centers) & 15) ||
       smem > 110 * 1024)
     return false;
   static std::atomic<uint64_t> attr{0};
-  smem_optin(attr, assign_bulk_kernel<KP>, 110 * 1024);
+  smem_optin(attr, assign_bulk_kernel<KP, TPR>, 110 * 1024);
   const int64_t ntiles = (n - row0 + kBulkRows - 1) / kBulkRows;
   const int64_t grid = ntiles < 2 * g_sms ? ntiles : 2 * g_sms;
-  assign_bulk_kernel<KP><<<static_cast<unsigned>(grid), kBulkRows, smem, s>>>(X, n, static_cast<int>(d), xnorm,
-                                                                            centers, cnorm, k, row0, label,
-                                                                            best_dist, changed);
+  assign_bulk_kernel<KP, TPR><<<static_cast<unsigned>(grid), kBulkRows * TPR, smem, s>>>(
+      X, n, static_cast<int>(d), xnorm, centers, cnorm, k, row0, label, best_dist, changed);
   c.launched();
   return true;
+}
+template <int KP>
+static bool try_assign_bulk(const double* X, int64_t n, int64_t d, const double* xnorm, const double* centers,
+                            const double* cnorm, int k, int64_t row0, int32_t* label, double* best_dist,
+                            unsigned long long* changed, cudaStream_t s, Counter& c) {
+  // two threads per row from 8 centres (PKRR_ASSIGN_TPR=1: one)
+  static const int tpr = std::getenv("PKRR_ASSIGN_TPR") ? std::atoi(std::getenv("PKRR_ASSIGN_TPR")) : 2;
+  if (KP >= 8 && tpr == 2)
+    return try_assign_bulk_t<KP, (KP >= 8 ? 2 : 1)>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed,
+                                                   s, c);
+  return try_assign_bulk_t<KP, 1>(X, n, d, xnorm, centers, cnorm, k, row0, label, best_dist, changed, s, c);
 }
 
 // Lloyd assign / routing (mode 0) with a tensor-core distance SCREEN and an exact

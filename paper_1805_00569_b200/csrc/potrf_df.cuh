@@ -191,9 +191,14 @@ __device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensor
       if (t < p.ntasks) DF_TASK_MARK(t, 0, df_now());
 #endif
       const int ti = task.y, tj = task.z, ta = task.w & 0xffff, tb = task.w >> 16;
+      // TRSMs and single updates (K = 64, the tasks the chain's next steps wait for) stream
+      // each operand as soon as ITS producer is done instead of after the last dependency:
+      // the C tile / A rows are in flight while the task still waits for the chain's
+      // publication, and only the B rows' TMA latency follows it
+      const bool split = task.x == DF_TRSM || (task.x == DF_UPD && tb - ta == 1);
       bool ok = true;
-      if (task.x == DF_TRSM) {
-        ok = df_wait_ge(p.flags + F_CHAIN, tj + 1, p.status) && df_wait_ge(applied + ti * nt + tj, tj, p.status);
+      if (split) {
+        ok = df_wait_ge(applied + ti * nt + tj, task.x == DF_TRSM ? tj : ta, p.status);
       } else if (task.x == DF_UPD) {
         ok = df_wait_ge(applied + ti * nt + tj, ta, p.status) && df_wait_ge(lrow + ti, tb, p.status) &&
              df_wait_ge(lrow + tj, tb, p.status);
@@ -203,7 +208,7 @@ __device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensor
       if (!ok) task.x = DF_END;
 #ifdef PKRR_DF_TRACE
       if (t < p.ntasks) {
-        DF_TASK_MARK(t, 1, df_now());
+        if (!split) DF_TASK_MARK(t, 1, df_now());
         DF_TASK_MARK(t, 3, blockIdx.x);
       }
       tticket[it & 1] = t;
@@ -224,18 +229,41 @@ __device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensor
       } else {
         mbar_arrive(&cfull[slot]);
       }
-      const int nk =
-          task.x == DF_TRSM ? 4 : (task.x == DF_UPD ? 4 * (tb - ta) : (task.x == DF_GRAM ? p.xk : 0));
+      if (split) {
+        // (an abandoned factorization -- a wait returning false -- still issues every load:
+        // the consumers are already waiting on these stages; the next claim ends the worker)
+        const bool trsm = task.x == DF_TRSM;
+        if (!trsm) {
+          (void)df_wait_ge(lrow + ti, tb, p.status);
+          fence_proxy_async_global();
+        }
+        for (int c = 0; c < 4; ++c) {
+          const int s = (kt + c) % kDfStages;
+          mbar_wait(&empty[s], (((kt + c) / kDfStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[s], kDfStage);
+          tma_load_2d(ring + s * kDfStage, tmA, (trsm ? tj : ta) * kDfT + 16 * c, ti * kDfT, &full[s]);
+        }
+        (void)df_wait_ge(trsm ? p.flags + F_CHAIN : lrow + tj, trsm ? tj + 1 : tb, p.status);
+        fence_proxy_async_global();
+#ifdef PKRR_DF_TRACE
+        DF_TASK_MARK(t, 1, df_now());
+#endif
+        for (int c = 0; c < 4; ++c) {
+          unsigned char* sb = ring + ((kt + c) % kDfStages) * kDfStage + 8192;
+          if (trsm) tma_load_2d(sb, tmI, 16 * c, tj * kDfT, &full[(kt + c) % kDfStages]);
+          else tma_load_2d(sb, tmA, ta * kDfT + 16 * c, tj * kDfT, &full[(kt + c) % kDfStages]);
+        }
+        kt += 4;
+        continue;
+      }
+      const int nk = task.x == DF_UPD ? 4 * (tb - ta) : (task.x == DF_GRAM ? p.xk : 0);
       for (int c = 0; c < nk; ++c, ++kt) {
         const int s = kt % kDfStages;
         const uint32_t sp = (kt / kDfStages) & 1;
         mbar_wait(&empty[s], sp ^ 1);
         mbar_arrive_expect_tx(&full[s], kDfStage);
         unsigned char* sa = ring + s * kDfStage;
-        if (task.x == DF_TRSM) {
-          tma_load_2d(sa, tmA, tj * kDfT + 16 * c, ti * kDfT, &full[s]);
-          tma_load_2d(sa + 8192, tmI, 16 * c, tj * kDfT, &full[s]);
-        } else if (task.x == DF_GRAM) {
+        if (task.x == DF_GRAM) {
           tma_load_2d(sa, tmX, 16 * c, ti * kDfT, &full[s]);
           tma_load_2d(sa + 8192, tmX, 16 * c, tj * kDfT, &full[s]);
         } else {
