@@ -318,6 +318,7 @@ struct PartBuf {
   double* w = nullptr;      // fused forward-substitution accumulator (mp)
   double* alpha = nullptr;
   double* Ka = nullptr;
+  bool assembled = false;   // A already holds K + lambda_0 m I (written by the gram's epilogue)
   int* scratch = nullptr;   // trsv tickets/flags
   int8_t* slices = nullptr; // Ozaki SYRK scratch: 2 x int8 [8 x mp x 512]
   int* exps = nullptr;      // [mp]
@@ -674,9 +675,9 @@ void part_load(pkrrgpu_ctx* ctx, PartBuf& pb, const double* dX, const double* dy
 }
 
 void part_solve(pkrrgpu_ctx* ctx, PartBuf& pb, double lambda, int* status, double* res_out,
-                cudaStream_t s, cudaStream_t s2, bool alone) {
+                cudaStream_t s, cudaStream_t s2, bool alone, bool assembled = false) {
   const double shift = lambda * static_cast<double>(pb.m);
-  pk::launch_assemble(pb.K, pb.A, pb.mp, shift, status, s, ctx->counter, /*lower_only=*/true);
+  if (!assembled) pk::launch_assemble(pb.K, pb.A, pb.mp, shift, status, s, ctx->counter, /*lower_only=*/true);
   const pk::FwdSolve fs{pb.yp, pb.w, pb.z};
   if (pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, status, s, ctx->counter, pb.slices,
                        pb.exps, s2, alone, &fs))
@@ -1449,10 +1450,11 @@ int pkrrgpu_train_krr(pkrrgpu_ctx* ctx, const double* X, const double* y, int64_
   iota_kernel<<<blocks_for(m), 256, 0, s>>>(idx, m);
   ctx->counter.launched();
   part_load(ctx, pb, dX, dy, d, idx, s);
-  pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, m, sigma, pb.K, pb.mp, nullptr, s, ctx->counter, false);
+  const bool assembled = pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, m, sigma, pb.K, pb.mp, nullptr, s,
+                                             ctx->counter, false, pb.A, lambda * static_cast<double>(m));
   int* status = sc.zeros<int>(2, s);
   double* res = sc.zeros<double>(2, s);
-  part_solve(ctx, pb, lambda, status, res, s, ctx->aux_main, true);
+  part_solve(ctx, pb, lambda, status, res, s, ctx->aux_main, true, assembled);
   std::vector<int> st = to_host(status, 2, s);
   if (st[0]) {
     if (npd_pivot) *npd_pivot = st[1];
@@ -1617,8 +1619,9 @@ pkrrgpu_models* train_models(pkrrgpu_ctx* ctx, Scope& sc, const double* dX, cons
     PartBuf& pb = parts[t];
     part_alloc(sc, pb, po.sizes[t], d, true, ws);
     part_load(ctx, pb, dX, dy, d, po.order + po.start[t], ws);
-    pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws, ctx->counter, false);
-    part_solve(ctx, pb, lambda, status + 2 * t, res + 2 * t, ws, ctx->aux[i % S], po.p == 1);
+    const bool assembled = pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws,
+                                               ctx->counter, false, pb.A, lambda * static_cast<double>(pb.m));
+    part_solve(ctx, pb, lambda, status + 2 * t, res + 2 * t, ws, ctx->aux[i % S], po.p == 1, assembled);
   }
   ck(cudaEventDestroy(ready), "event");
   ck(cudaDeviceSynchronize(), "train");
@@ -2172,9 +2175,10 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
         // PKRR_DF_GRAM=1: a lone system on the dataflow path forms K and A inside its
         // factorization (first lambda of each sigma; pk::GramFuse) -- measured slower
         // than the gram + assemble kernels at C0 (DF kernel +270 us vs 145 us saved)
+        // the first lambda's system A = K + lambda m I leaves the gram's epilogue with K
         if (!(p == 1 && df_gram_fused() && pk::potrf_df_eligible(pb.mp, true)))
-          pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws, ctx->counter,
-                              false);
+          pb.assembled = pk::launch_gram_sym(pb.tmX, pb.norms, pb.mp, pb.dp, pb.m, sigma, pb.K, pb.mp, nullptr, ws,
+                                             ctx->counter, false, pb.A, a->lambdas[0] * m);
         f_gram += static_cast<double>(d) * m * (m + 1);
         gram_iv.push_back({g0, ev_on(ws)});
         if (si == 0) part_ev[q][0] = g0, part_ev[q][1] = gram_iv.back().b;
@@ -2192,7 +2196,8 @@ int pkrrgpu_grid_search_ex(pkrrgpu_ctx* ctx, const pkrrgpu_grid_args* a, pkrrgpu
           cudaEvent_t c0 = ev_on(ws);
           const bool gram_fused = li == 0 && p == 1 && df_gram_fused() && pk::potrf_df_eligible(pb.mp, true);
           const pk::GramFuse gf{pb.tmX, pb.norms, pb.K, pb.dp, pb.m, sigma, shift};
-          if (!gram_fused) pk::launch_assemble(pb.K, pb.A, pb.mp, shift, st, ws, ctx->counter, true);
+          if (!gram_fused && !(li == 0 && pb.assembled))
+            pk::launch_assemble(pb.K, pb.A, pb.mp, shift, st, ws, ctx->counter, true);
           const pk::FwdSolve fs{pb.yp, pb.w, pb.z};
           // rank-independent schedule (p == 1): the same at any world size
           const bool fused = pk::launch_potrf(pb.A, pb.tmA, pb.tmLinv, pb.Linv, pb.mp, pb.m, st, ws, ctx->counter,

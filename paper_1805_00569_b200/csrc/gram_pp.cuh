@@ -36,6 +36,8 @@ struct GramPPParams {
   int valid;      // rows >= valid are padding (identity)
   double neg_inv_denom;
   const int* abort_flag;
+  double* A;      // != null: also A = K + shift I (the first lambda's system: no assemble pass)
+  double shift;
 };
 
 __global__ void __launch_bounds__(kPPThreads, 1)
@@ -190,6 +192,14 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             *reinterpret_cast<double2*>(dst) = make_double2(v[j][0], v[j][1]);
           else if (gi == gj)
             dst[0] = v[j][0];
+          if (p.A) {
+            double* da = p.A + static_cast<int64_t>(gi) * p.ldk + gj;
+            if (!kDiag || gi >= gj + 1)
+              *reinterpret_cast<double2*>(da) =
+                  make_double2(kDiag && gi == gj ? v[j][0] + p.shift : v[j][0], kDiag && gi == gj + 1 ? v[j][1] + p.shift : v[j][1]);
+            else if (gi == gj)
+              da[0] = v[j][0] + p.shift;
+          }
         }
       }
     };

@@ -227,9 +227,9 @@ static void gemm_launch(const CUtensorMap& a, const CUtensorMap& b, const GemmPa
   c.launched();
 }
 
-void launch_gram_sym(const CUtensorMap& tmX, const double* norms, int64_t mp, int64_t dp,
+bool launch_gram_sym(const CUtensorMap& tmX, const double* norms, int64_t mp, int64_t dp,
                      int64_t m, double sigma, double* K, int64_t ldk, const int* abort,
-                     cudaStream_t s, Counter& c, bool mirror) {
+                     cudaStream_t s, Counter& c, bool mirror, double* A, double shift) {
   GemmParams p{};
   p.mirror = mirror ? 1 : 0;
   p.a_row0 = p.b_row0 = 0;
@@ -257,14 +257,17 @@ void launch_gram_sym(const CUtensorMap& tmX, const double* norms, int64_t mp, in
     q.valid = static_cast<int>(m);
     q.neg_inv_denom = p.neg_inv_denom;
     q.abort_flag = abort;
+    q.A = A;
+    q.shift = shift;
     static std::atomic<uint64_t> attr{0};
     smem_optin(attr, gram_pp_kernel, kPPSmem);
     const int nhalf = T * (T + 1);
     launch_pdl(gram_pp_kernel, static_cast<unsigned>(nhalf < g_sms ? nhalf : g_sms), kPPThreads, kPPSmem, s, tmX, q);
     c.launched();
-    return;
+    return A != nullptr;
   }
   gemm_launch<128, G_GRAM_SYM>(tmX, tmX, p, T * (T + 1) / 2, s, c);
+  return false;
 }
 
 void launch_gram_cross(const CUtensorMap& tmQ, const CUtensorMap& tmX, const double* qnorms,

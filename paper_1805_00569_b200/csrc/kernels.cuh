@@ -44,9 +44,12 @@ void launch_gather_vec(const double* y, const int64_t* idx, int64_t cnt, double*
 
 // ---- DMMA GEMM family (gemm_dmma.cuh) -------------------------------------
 // K (ldk x ldk, padded mp) = gaussian gram of Xp (mp x dp) ; valid = m
-void launch_gram_sym(const CUtensorMap& tmX, const double* norms, int64_t mp, int64_t dp,
+// With A != null the lower tiles of A = K + shift I (strategies.cpp:296-303, the first lambda's
+// system) are written by the same epilogue when the ping-pong kernel runs; returns whether A
+// was written (otherwise launch_assemble forms it).
+bool launch_gram_sym(const CUtensorMap& tmX, const double* norms, int64_t mp, int64_t dp,
                      int64_t m, double sigma, double* K, int64_t ldk, const int* abort,
-                     cudaStream_t s, Counter& c, bool mirror = true);
+                     cudaStream_t s, Counter& c, bool mirror = true, double* A = nullptr, double shift = 0.0);
 // Kc (qp x mp) = k(Q_q, X_i); valid rows q, valid cols m
 void launch_gram_cross(const CUtensorMap& tmQ, const CUtensorMap& tmX, const double* qnorms,
                        const double* xnorms, int64_t qp, int64_t q, int64_t mp, int64_t m,
