@@ -158,7 +158,10 @@ __device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensor
   int4* tslot = reinterpret_cast<int4*>(cempty + 2);
 #ifdef PKRR_DF_TRACE
   __shared__ int tticket[2];
+  __shared__ int pticket[2];
 #endif
+  __shared__ uint64_t pubfull[2], pubempty[2];
+  __shared__ int4 ptask[2];
   int* applied = p.flags + F_HEAD;
   int* lrow = applied + nt * nt;
   if (tid == 0) {
@@ -171,12 +174,37 @@ __device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensor
       mbar_init(&tempty[s], 4);
       mbar_init(&cfull[s], 1);
       mbar_init(&cempty[s], 4);
+      mbar_init(&pubfull[s], 4);
+      mbar_init(&pubempty[s], 1);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp >= 5) return;
+  if (warp >= 6) return;
+  if (warp == 5) {
+    // ---------------- publisher: the tasks' release stores ----------------
+    // st.release.gpu waits (MEMBAR.ALL.GPU, ~0.7 us under the workers' traffic) for the
+    // CTA's stores to be visible; on a DMMA warp that wait was added to every task (the
+    // other three warps met it again at the next task's barrier).  The four DMMA warps
+    // arrive on pubfull[slot] when their stores are issued; this thread publishes.
+    if (lane != 0) return;
+    for (int it = 0;; ++it) {
+      const int slot = it & 1;
+      const uint32_t ph = (it >> 1) & 1;
+      mbar_wait(&pubfull[slot], ph);
+      const int4 task = ptask[slot];
+      if (task.x == DF_END) return;
+      const int ti = task.y, tj = task.z, tb = task.w >> 16;
+      if (task.x == DF_UPD) st_release_gpu(applied + ti * nt + tj, tb);
+      else if (task.x == DF_TRSM) st_release_gpu(lrow + ti, tj + 1);
+      else if (task.x == DF_GRAM) st_release_gpu(applied + ti * nt + tj, 0);
+#ifdef PKRR_DF_TRACE
+      DF_TASK_MARK(pticket[slot], 2, df_now());
+#endif
+      mbar_arrive(&pubempty[slot]);
+    }
+  }
   if (warp == 4) {
     // ---------------- producer: claim, wait for dependencies, stream operands ----------------
     if (lane != 0) return;
@@ -288,7 +316,18 @@ __device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensor
 #endif
     __syncwarp();
     if (lane == 0) mbar_arrive(&tempty[slot]);
-    if (task.x == DF_END) return;
+    if (tid == 0) {  // the publisher's copy (its slot is free once task it - 2 is published)
+      mbar_wait(&pubempty[slot], ph ^ 1);
+      ptask[slot] = task;
+#ifdef PKRR_DF_TRACE
+      pticket[slot] = ticket;
+#endif
+    }
+    if (task.x == DF_END) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pubfull[slot]);
+      return;
+    }
     const int ti = task.y, tj = task.z, ta = task.w & 0xffff, tb = task.w >> 16;
     double acc[4][4][2];
 #pragma unroll
@@ -410,6 +449,7 @@ __device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensor
         }
         consumer_sync(128);
         if (tid < 64) p.P[(static_cast<int64_t>(ti) * nt + tj) * kDfT + tid] = red[tid] + red[64 + tid];
+        consumer_sync(128);  // red is read: the next TRSM may overwrite it
       }
     } else {
       // DF_INV: the 128 x 128 diagonal-block inverse [X0 0; Y X1] of block pair ti,
@@ -470,17 +510,9 @@ __device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensor
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&cempty[slot]);
-    consumer_sync(128);  // every warp's stores issued before the publication
-    if (tid == 0) {
-      // st.release.gpu is the fence (MEMBAR.ALL.GPU); a __threadfence() before it added a
-      // MEMBAR.SC.GPU + L1 invalidate per task
-      if (task.x == DF_UPD) st_release_gpu(applied + ti * nt + tj, tb);
-      else if (task.x == DF_TRSM) st_release_gpu(lrow + ti, tj + 1);
-      else if (task.x == DF_GRAM) st_release_gpu(applied + ti * nt + tj, 0);
-#ifdef PKRR_DF_TRACE
-      DF_TASK_MARK(ticket, 2, df_now());
-#endif
+    if (lane == 0) {
+      mbar_arrive(&cempty[slot]);
+      mbar_arrive(&pubfull[slot]);  // this warp's stores are issued: the publisher releases the task
     }
   }
 }
