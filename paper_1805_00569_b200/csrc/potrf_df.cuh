@@ -20,7 +20,9 @@
 //    far panels batched 8 at a time -- K = 512 -- the last two singly, so the tiles
 //    near the diagonal are ready a step after their panel), INV(b) (the 128 x 128
 //    diagonal-block inverse the backward solve uses).  Operands and C tiles move by
-//    TMA into a ring (producer warp), 8 DMMA warps compute;
+//    TMA into a ring (producer warp; TRSMs and single updates stream each operand as soon
+//    as its own producer is done), 4 DMMA warps (32 x 32 each) compute, a publisher warp
+//    issues the tasks' release stores;
 //  * dependencies are per-tile counters in global memory (release / acquire):
 //    applied[i][j] = panels applied to tile (i,j), lrow[i] = L tiles of row i done,
 //    chain = panels finished.  The task list is a topological order with the chain
@@ -36,7 +38,7 @@
 namespace pk {
 
 constexpr int kDfT = 64;                  // tile
-constexpr int kDfThreads = 8 * 32;        // workers: 4 DMMA warps + 1 TMA producer warp (+ 3 idle);
+constexpr int kDfThreads = 8 * 32;        // workers: 4 DMMA warps + TMA producer warp + publisher warp (+ 2 idle);
                                           // 2 warps per scheduler partition -> up to 255 registers
 constexpr int kDfStages = 8;
 constexpr int kDfStage = 2 * kDfT * kBK * 8;  // A box + B box (64 rows x 16) = 16 KB
@@ -139,7 +141,7 @@ __device__ __noinline__ bool df_wait_ge(const int* flag, int target, const int* 
 }
 
 // ---------------------------------------------------------------------------
-// worker: TMA producer warp + 8 DMMA warps (2 x 4 grid, 32 x 16 per warp)
+// worker: TMA producer warp + 4 DMMA warps (2 x 2 grid, 32 x 32 per warp) + publisher warp
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void df_worker(const CUtensorMap* tmA, const CUtensorMap* tmI, const CUtensorMap* tmX,
                                           const DfParams& p,
