@@ -418,7 +418,9 @@ def run_ours(args):
     # leave no clock sample: keep the same step running, untimed, until ~1 s has passed
     extended = 0
     t_clk = time.perf_counter()
-    while time.perf_counter() - t_wall0 < 1.0 and time.perf_counter() - t_clk < 1.5:
+    # (one rank only: with several ranks a time-based loop would run different numbers of
+    # steps -- and of their collectives -- on different ranks; those runs are longer than 1 s)
+    while world == 1 and time.perf_counter() - t_wall0 < 1.0 and time.perf_counter() - t_clk < 1.5:
         with torch.cuda.stream(stream):
             step(g)
         torch.cuda.synchronize(dev)
