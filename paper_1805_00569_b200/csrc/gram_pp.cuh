@@ -38,6 +38,7 @@ struct GramPPParams {
   const int* abort_flag;
   double* A;      // != null: also A = K + shift I (the first lambda's system: no assemble pass)
   double shift;
+  int turns;      // strict alternation of the warpgroups' mainloops (short mainloops: small d)
 };
 
 __global__ void __launch_bounds__(kPPThreads, 1)
@@ -102,7 +103,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
   // the DMMA pipe idle through the latter.  Warpgroup 1 primes warpgroup 0's first turn.
   auto turn_wait = [&] { asm volatile("bar.sync %0, 256;\n" ::"r"(8 + wg) : "memory"); };
   auto turn_pass = [&] { asm volatile("bar.arrive %0, 256;\n" ::"r"(8 + (wg ^ 1)) : "memory"); };
-  if (wg == 1) turn_pass();
+  const bool turns = p.turns != 0;
+  if (turns && wg == 1) turn_pass();
   int g = 0;
   for (int t = wg;; t += 2) {
     const int idx = blockIdx.x + t * gridDim.x;
@@ -124,7 +126,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     for (int i = 0; i < 8; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    turn_wait();
+    if (turns) turn_wait();
     for (int kt = 0; kt < KT; ++kt, ++g) {
       const int s = g % kPPStages;
       mbar_wait(&full[s], (g / kPPStages) & 1);
@@ -150,7 +152,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[(g - 1) % kPPStages]);
-    turn_pass();
+    if (turns) turn_pass();
     // epilogue (kernel.cpp:52-56): dist2 = (n_a + n_b) - 2 dot, clamp at 0,
     // exp(dist2 * -1/((2 s) s)); unit diagonal; padding identity; diagonal tiles keep
     // only gi >= gj (nothing reads their upper triangle)

@@ -259,6 +259,11 @@ bool launch_gram_sym(const CUtensorMap& tmX, const double* norms, int64_t mp, in
     q.abort_flag = abort;
     q.A = A;
     q.shift = shift;
+    // alternate the warpgroups' mainloops strictly while the epilogue is comparable to the
+    // mainloop (dp <= 256); with long mainloops (C4: dp = 784) two concurrent mainloops hide
+    // each other's latencies better than one at a time
+    static const int turn_max = std::getenv("PKRR_GRAM_TURNS") ? std::atoi(std::getenv("PKRR_GRAM_TURNS")) : 16;
+    q.turns = q.ktiles <= turn_max ? 1 : 0;
     static std::atomic<uint64_t> attr{0};
     smem_optin(attr, gram_pp_kernel, kPPSmem);
     const int nhalf = T * (T + 1);
