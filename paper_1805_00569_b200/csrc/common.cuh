@@ -236,7 +236,7 @@ __device__ __forceinline__ double exp_nonpos(double x) {
   p = fma(p, r, 0.5);
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
-  const double res = __hiloint2double(__double2hiint(p) + (k << 20), __double2loint(p));
+  const double res = __hiloint2double(__double2hiint(p) + k * (1 << 20), __double2loint(p));  // k < 0: no shift of a negative
   return x != x ? x : res;
 }
 
