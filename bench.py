@@ -45,7 +45,8 @@ sys.path.insert(0, ROOT)
 METRIC = "train+predict samples/sec (FP64)"
 # DRAM bytes (read, write) and 128x128 tiles of one trailing-SYRK launch per K, from the
 # committed ncu --set full captures of the m = 20544 factorization probe:
-# K=512 profiles/ncu_syrk_r01.txt, K=1024 ncu_syrk_k1024_r01.txt, K=2048 ncu_syrk_k2048_r01.txt;
+# K=2048 profiles/ncu_syrk_k2048_r02.txt (banded tile order, round 2; K=1024 / K=512 from the
+# metrics-only pass noted there);
 # K=128 (a lone 4096-row system, C0): ncu_syrk_k128_r01.txt (tools/syrk_probe_alone.py).
 # DRAM bytes (read, write) of the dataflow Cholesky's ncu capture (m = 4096 lone system,
 # profiles/ncu_df_c0_r02b.txt)
@@ -70,8 +71,8 @@ def DF_ROOFLINE(m, tflops, peak, probe):
                            f"({probe['total_ms']:.3f} ms, standalone factorization)"}
 
 
-SYRK_NCU_LAUNCH = {128: (351, 49.44e6, 1.77e6), 512: (8911, 2.98e9, 1.14e9), 1024: (11781, 9.87e9, 1.53e9),
-                   2048: (10585, 16.05e9, 1.38e9)}
+SYRK_NCU_LAUNCH = {128: (351, 49.44e6, 1.77e6), 512: (11781, 2.26e9, 1.51e9), 1024: (11781, 3.18e9, 1.53e9),
+                   2048: (10585, 5.01e9, 1.38e9)}
 UNIT = "samples/s"
 
 
@@ -87,9 +88,9 @@ def syrk_traffic_note(k):
     no_reuse = tiles * (2 * 128 * k * 8 + 2 * 128 * 128 * 8)
     return (f"DRAM read+write bytes of the captured K={k} launch ({tiles} tiles of 128x128, ncu --set full, "
             f"profiles/): {(rd + wr) / compulsory:.1f}x its compulsory {compulsory:.3e} B (each lower C tile read and "
-            f"written once, the panel once) and {(rd + wr) / no_reuse:.2f}x the no-reuse {no_reuse:.3e} B: panel "
-            "operands that fall out of L2 between tile rows are re-fetched; the launch is DMMA-bound "
-            "(tensor pipe 88-94 % in the captures), not HBM-bound")
+            f"written once, the panel once) and {(rd + wr) / no_reuse:.2f}x the no-reuse {no_reuse:.3e} B (tiles run in "
+            "bands of 8 tile rows, so the panel rows in flight stay in L2; row-major order took 5.7x the compulsory "
+            "bytes at K=2048); the launch is DMMA-bound (tensor pipe 88-94 % in the captures), not HBM-bound")
 
 # BASELINE.json configs (per GPU for the weak-scaled ones).  km_iters 20 = exactly
 # 20 Lloyd iterations (threshold -1); 0 = the reference defaults (0.01 / 100).
