@@ -72,7 +72,7 @@ def DF_ROOFLINE(m, tflops, peak, probe):
 
 
 SYRK_NCU_LAUNCH = {128: (351, 49.44e6, 1.77e6), 512: (11781, 2.26e9, 1.51e9), 1024: (11781, 3.18e9, 1.53e9),
-                   2048: (10585, 5.01e9, 1.38e9)}
+                   2048: (10585, 6.10e9, 1.38e9)}
 UNIT = "samples/s"
 
 
@@ -89,7 +89,7 @@ def syrk_traffic_note(k):
     return (f"DRAM read+write bytes of the captured K={k} launch ({tiles} tiles of 128x128, ncu --set full, "
             f"profiles/): {(rd + wr) / compulsory:.1f}x its compulsory {compulsory:.3e} B (each lower C tile read and "
             f"written once, the panel once) and {(rd + wr) / no_reuse:.2f}x the no-reuse {no_reuse:.3e} B (tiles run in "
-            "bands of 8 tile rows, so the panel rows in flight stay in L2; row-major order took 5.7x the compulsory "
+            "bands of 8 tile rows and blocks of 8 tile columns, so the panel rows in flight stay in L2; row-major order took 5.7x the compulsory "
             "bytes at K=2048); the launch is DMMA-bound (tensor pipe 88-94 % in the captures), not HBM-bound")
 
 # BASELINE.json configs (per GPU for the weak-scaled ones).  km_iters 20 = exactly

@@ -67,29 +67,32 @@ __global__ void __launch_bounds__(kSyrkThreads, 1)
   auto coords = [&](int b, int& tm, int& tn) {
     const int tri = p.narrow * (p.narrow + 1) / 2;
     if (p.narrow <= 0) {
-      // Bands of kBand tile rows, column-major inside a band: the ~148 tiles in flight span 8
-      // A-panel rows and ~18 B-panel rows (2 MB each at K = 2048: L2-resident) instead of one
-      // tile row and every B panel -- in row-major order each tile row re-streamed all the B
-      // panels from HBM (17.4 GB per launch at T = 145 against 3.1 GB compulsory).
+      // Bands of kBand tile rows; inside a band, blocks of kBand tile columns, row-major in a
+      // block: the ~148 tiles in flight span 8 A-panel rows and ~19 B-panel rows (2 MB each at
+      // K = 2048: L2-resident) instead of one tile row and every B panel -- in plain row-major
+      // order each tile row re-streamed all the B panels from HBM (17.4 GB per launch at T = 145
+      // against 3.1 GB compulsory) -- and consecutive tiles are neighbours in a row of C.
       constexpr int kBand = 8;
       int r, c;
       lower_tile_coords(b, r, c);
       const int R0 = r / kBand * kBand;
       const int nrows = p.T - R0 < kBand ? p.T - R0 : kBand;
-      int q = b - R0 * (R0 + 1) / 2;  // index inside the band
-      const int nfull = (R0 + 1) * nrows;  // columns 0 .. R0: every row of the band
-      if (q < nfull) {
-        tn = q / nrows;
-        tm = R0 + q % nrows;
+      int q = b - R0 * (R0 + 1) / 2;            // index inside the band
+      const int nblk = R0 / kBand;              // full blocks: columns [0, R0)
+      if (q < nblk * kBand * nrows) {
+        const int blk = q / (kBand * nrows), rq = q % (kBand * nrows);
+        tm = R0 + rq / kBand;
+        tn = blk * kBand + rq % kBand;
       } else {
-        q -= nfull;
-        int j = 1;
-        while (q >= nrows - j) {
-          q -= nrows - j;
-          ++j;
+        // the band's own triangle: columns R0 .. R0 + nrows - 1, rows >= column (row-major)
+        q -= nblk * kBand * nrows;
+        int i = 0;
+        while (q > i) {
+          q -= i + 1;
+          ++i;
         }
-        tn = R0 + j;
-        tm = R0 + j + q;
+        tm = R0 + i;
+        tn = R0 + q;
       }
     } else if (b < tri) {
       lower_tile_coords(b, tm, tn);
